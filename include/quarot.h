@@ -1,0 +1,142 @@
+/* quarot.h — C ABI of the B200 (sm_100a) QuaRot online quantized-linear hot path.
+ *
+ * QuaRot: Outlier-Free 4-Bit Inference in Rotated LLMs (arXiv 2404.00456).
+ * Citations: P:<n> = line n of the paper's LaTeX source.
+ *
+ * The library implements, as hand-written CUDA kernels for sm_100a:
+ *   quarot_hadamard_quant   online Hadamard (FULL / ACROSS_HEADS / NONE) fused with
+ *                           per-token symmetric INT4 RTN and nibble packing
+ *                           (P:182-185 Stage 1b, P:204-208 Stage 1c, P:232-233 Stage 2b)
+ *   quarot_int4_linear      INT4 x INT4 GEMM (tcgen05 kind::i8, int32 accumulators in
+ *                           TMEM) with the fused dequantizing epilogue
+ *   quarot_int4_matmul_s32  the same mainloop exporting the raw int32 accumulators
+ *                           (parity only)
+ *   quarot_kv_quant         KV-cache "Init": per-head Hadamard on K (and optionally Q, in
+ *                           place) + asymmetric INT4 group quantization
+ *                           (P:210-225 Stage 1d, P:236-237 Stage 2c)
+ *
+ * Conventions (all entry points)
+ *  - Tensor pointers are CUDA DEVICE pointers owned by the caller.  The library never
+ *    allocates device memory for tensors; its only state is immutable per-device tables
+ *    of the stored Hadamard matrices H_28 and H_172 (built and verified H H^T = m I on
+ *    first use).
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  All work is enqueued
+ *    on it; no entry point synchronizes the host.  Calls are reentrant across streams.
+ *  - Arguments are validated before any launch; a failing call launches nothing and
+ *    leaves outputs untouched.  Launch failures map to QUAROT_ERR_CUDA; asynchronous
+ *    faults surface at the caller's next synchronization.  Nothing throws.
+ *  - Outputs must not alias inputs (except q in quarot_kv_quant, rotated in place).
+ *  - Results are bitwise deterministic for identical inputs and independent of how
+ *    rows are split across calls or GPUs (no atomics in any reduction).
+ *  - INT4 signed codes are stored two per byte, two's complement nibbles, LOW nibble =
+ *    EVEN index: byte j = (c[2j] & 0xF) | (c[2j+1] << 4)   (the "sub-byte format").
+ */
+#ifndef QUAROT_H_
+#define QUAROT_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QUAROT_ABI_VERSION 1
+
+typedef enum {
+  QUAROT_OK = 0,
+  QUAROT_ERR_NULL = 1,             /* a required pointer is NULL                        */
+  QUAROT_ERR_DIM = 2,              /* non-positive / inconsistent dimension, ld < width */
+  QUAROT_ERR_UNSUPPORTED_SIZE = 3, /* K not 2^n * m with m in {1, 28, 172}; heads not 2^n */
+  QUAROT_ERR_ALIGN = 4,            /* pointer / leading dimension misaligned (16 B) or a
+                                      width not a multiple of the kernel granularity    */
+  QUAROT_ERR_ARG = 5,              /* clip ratio outside (0, 1], bad mode or flags       */
+  QUAROT_ERR_CUDA = 6              /* CUDA runtime error at launch                       */
+} quarot_status;
+
+typedef enum {
+  /* QKV / gate-up input: quantize only (the global rotation Q is fused into W). */
+  QUAROT_HAD_NONE = 0,
+  /* down_proj input: y = H^_K x, H^_K = (H_{2^n} (x) H_m) / sqrt(K), K = 2^n m,
+   * m in {1, 28, 172}.  Element i = a*m + b: H_m acts on the contiguous index b,
+   * H_{2^n} (Sylvester / natural order, Eq. 1) on a.  y_i = sum_j H^_ij x_j. */
+  QUAROT_HAD_FULL = 1,
+  /* out_proj input, "Hadamard heads" (Eq. 9): y = (H_{n_h} (x) I_{d_h}) z / sqrt(n_h),
+   * n_h = K / head_dim; n_h and head_dim powers of two. */
+  QUAROT_HAD_ACROSS_HEADS = 2
+} quarot_had_mode;
+
+/* Rows a1|a2 + a3 of the hot path: online Hadamard + per-token symmetric INT4 RTN + pack.
+ *
+ *   x      fp16 [M][ld_x] row-major (K used); 16-B aligned; ld_x % 8 == 0.
+ *   M      tokens (>= 0; M == 0 is a no-op).      K  width (even; see mode).
+ *   mode   quarot_had_mode.  head_dim: used by ACROSS_HEADS only (power of two).
+ *   clip_ratio  in (0, 1]; the paper uses 0.9.
+ *   q      uint8 [M][ld_q] (K/2 bytes used), 16-B aligned; ld_q % 16 == 0.
+ *   scale  fp32 [M].
+ * Per row, with y the transformed (normalized) row (fp32 arithmetic on fp16 input):
+ *   a = max_k |y_k|;  a == 0 -> scale 1, codes 0;  a not finite -> scale NaN, codes 0;
+ *   else scale = fp32(clip * a / 7), code_k = clamp(round_half_even(y_k / scale), -7, 7)
+ *   ("dividing the maximum absolute value of each token by 7 ... round the
+ *   result to its nearest integer").  x^ = code * scale approximates y.
+ * Granularity: K % 16 == 0 (NONE); K % 32 == 0 and K / head_dim a power of two
+ * (ACROSS_HEADS, head_dim % 2 == 0); K = 2^n m with 2^n >= 2 (FULL).            */
+quarot_status quarot_hadamard_quant(const void* x, int64_t M, int64_t K, int64_t ld_x,
+                                    int32_t mode, int32_t head_dim, float clip_ratio,
+                                    uint8_t* q, int64_t ld_q, float* scale, void* stream);
+
+/* Rows a4 + a5: y[m][n] = fp16_rn( (fp32)acc[m][n] * x_scale[m] * w_scale[n] ),
+ *   acc[m][n] = sum_k cx[m][k] * cw[n][k]   (exact int32).
+ *   xq     uint8 [M][ld_xq] packed INT4 activations (output of quarot_hadamard_quant).
+ *   wq     uint8 [N][ld_wq] packed INT4 weights, nn.Linear [out][in] orientation (same
+ *          nibble layout along K), pre-rotated offline to pair with the online mode.
+ *   x_scale fp32 [M], w_scale fp32 [N] (per output channel, "per-column").
+ *   y      fp16 [M][ld_y].
+ * Requirements: K % 128 == 0; N % 8 == 0; ld_xq, ld_wq % 16 == 0; ld_y % 8 == 0; all
+ * pointers 16-B aligned.  Ragged M and N tails are handled. */
+quarot_status quarot_int4_linear(const uint8_t* xq, const float* x_scale, int64_t M, int64_t K,
+                                 int64_t ld_xq, const uint8_t* wq, const float* w_scale,
+                                 int64_t N, int64_t ld_wq, void* y, int64_t ld_y, void* stream);
+
+/* Parity only: the same tcgen05 mainloop, raw accumulators acc int32 [M][ld_acc]
+ * (ld_acc % 4 == 0).  Same requirements as quarot_int4_linear. */
+quarot_status quarot_int4_matmul_s32(const uint8_t* xq, int64_t M, int64_t K, int64_t ld_xq,
+                                     const uint8_t* wq, int64_t N, int64_t ld_wq,
+                                     int32_t* acc, int64_t ld_acc, void* stream);
+
+/* Rows a6 + a7, KV-cache Init (P:858 routine "Init").
+ *   k, v   fp16 [T][ld_k] / [T][ld_v]: token t's heads at k + t*ld_k, [n_kv][head_dim]
+ *          contiguous (post-RoPE keys, values).  ld_* are in elements, >= n*head_dim,
+ *          multiples of 8 — so K, V and Q can be read straight out of a fused QKV output.
+ *   q      optional fp16 [T][ld_q] ([n_q][head_dim] per token), rotated IN PLACE
+ *          q_h <- H^ q_h (Eq. 13), rounded to fp16; NULL or n_q == 0 skips it.
+ *   flags  bit0: rotate K (Eq. 14; default set), bit1: rotate V (the paper fuses
+ *          V's rotation into W_v, so bit1 is for tests only).  Other bits: ERR_ARG.
+ *   clip_ratio in (0, 1]; the paper uses 0.95.  Group = head_dim (128 in the paper).
+ *   *_codes uint8 [T][n_kv][head_dim/2] unsigned nibbles (low = even index);
+ *   *_scale fp32 [T][n_kv]; *_zero uint8 [T][n_kv].
+ * Per group g (after the optional rotation H^ = H_{head_dim} / sqrt(head_dim)):
+ *   lo = clip * min(min g, 0), hi = clip * max(max g, 0);  hi == lo -> scale 1, zero 0,
+ *   codes 0;  else scale = fp32((hi - lo) / 15), zero = clamp(rne(-lo / scale), 0, 15),
+ *   code = clamp(rne(g / scale) + zero, 0, 15);  x^ = (code - zero) * scale.
+ * Requirements: head_dim in {64, 128, 256}; T >= 0; n_kv >= 1; 16-B aligned pointers. */
+quarot_status quarot_kv_quant(const void* k, int64_t ld_k, const void* v, int64_t ld_v, int64_t T,
+                              int32_t n_kv, int32_t head_dim, void* q, int64_t ld_q, int32_t n_q,
+                              uint32_t flags,
+                              float clip_ratio, uint8_t* k_codes, float* k_scale,
+                              uint8_t* k_zero, uint8_t* v_codes, float* v_scale,
+                              uint8_t* v_zero, void* stream);
+
+/* Host-side utilities (no GPU work). */
+const char* quarot_status_string(int32_t status);
+int32_t quarot_abi_version(void);
+/* Copies the library's stored base Hadamard H_m (m in {28, 172}) as int8 +-1, row-major,
+ * into host buffer out[m*m].  Lets tests compare the library's independently built table
+ * with the oracle's.  Returns QUAROT_ERR_UNSUPPORTED_SIZE for other m. */
+quarot_status quarot_base_hadamard(int32_t m, int8_t* out);
+/* Number of kernels the last successful entry point on this host thread enqueued. */
+int32_t quarot_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QUAROT_H_ */

@@ -1,0 +1,445 @@
+// hadamard_quant.cu — rows a1/a2 + a3 of the QuaRot hot path on sm_100a.
+//
+// Online Hadamard transform of fp16 activation rows (FP32 arithmetic), fused with
+// per-token symmetric INT4 round-to-nearest (clip 0.9 P:249) and nibble packing
+// (the "sub-byte format").  One read of x, one write of the packed codes + scale.
+//
+//   NONE          quantize only (QKV / gate-up inputs; global Q fused into W)
+//   ACROSS_HEADS  y = (H_{n_h} (x) I_{d_h}) z   ("Hadamard heads", Eq. 9)
+//   FULL          y = (H_{2^n} (x) H_m) x, m in {1, 28, 172}   (down_proj input)
+//
+// The orthonormal factor 1/sqrt(size) (reading Z5) is folded into the per-row scale: codes
+// are invariant to positive scaling of y, so the kernels transform unnormalized and scale
+// once per row in double precision.
+#include "common.cuh"
+#include "quarot_internal.h"
+
+namespace qr {
+namespace hq {
+
+// RNE code in [-7, 7] of v * inv (inv = 1 / scale, or 0 for a zero / non-finite row)
+QR_DEVICE int code_of(float v, float inv) {
+  int c = __float2int_rn(v * inv);
+  c = c > 7 ? 7 : c;
+  c = c < -7 ? -7 : c;
+  return c;
+}
+QR_DEVICE uint32_t nib(int c) { return (uint32_t)c & 0xFu; }
+
+// Per-row scale from the unnormalized amax: scale = fp32(clip * amax * norm / 7);
+// returns inv = norm / scale so that code = rne(y_unnorm * inv).  Zero row -> scale 1,
+// inv 0 (all codes 0); non-finite -> scale NaN, inv 0.
+QR_DEVICE void row_scale(float amax_u, double norm, float clip, float& scale, float& inv) {
+  if (amax_u == 0.f) {
+    scale = 1.f;
+    inv = 0.f;
+  } else if (!isfinite(amax_u)) {
+    scale = __int_as_float(0x7fc00000);
+    inv = 0.f;
+  } else {
+    const double s = (double)clip * (double)amax_u * norm / 7.0;
+    scale = (float)s;
+    inv = (float)(norm / (double)scale);
+  }
+}
+
+template <int NWARPS>
+QR_DEVICE float block_max(float v, float* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax_nan(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  float r = red[0];
+#pragma unroll
+  for (int w = 1; w < NWARPS; ++w) r = fmax_nan(r, red[w]);
+  return r;
+}
+
+// ------------------------------------------------------------------ NONE
+// One row per 128-thread CTA; each thread owns CPT 8-element chunks held in registers.
+template <int CPT>
+__global__ void __launch_bounds__(128) hq_none_kernel(const __half* __restrict__ x, int64_t K, int64_t ld_x,
+                                                      float clip, uint8_t* __restrict__ q, int64_t ld_q,
+                                                      float* __restrict__ scale) {
+  __shared__ float red[4];
+  const int64_t row = blockIdx.x;
+  const int nchunk = (int)(K >> 3);
+  const __half* xr = x + row * ld_x;
+  uint4 v[CPT];
+  float amax = 0.f;
+#pragma unroll
+  for (int i = 0; i < CPT; ++i) {
+    const int c = threadIdx.x + i * 128;
+    if (c < nchunk) {
+      v[i] = ldg_nc_v4(xr + (int64_t)c * 8);
+      const __half2* h = reinterpret_cast<const __half2*>(&v[i]);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __half22float2(h[e]);
+        amax = fmax_nan(amax, fmax_nan(fabsf(f.x), fabsf(f.y)));
+      }
+    }
+  }
+  amax = block_max<4>(amax, red);
+  float s, inv;
+  row_scale(amax, 1.0, clip, s, inv);
+  if (threadIdx.x == 0) scale[row] = s;
+  uint8_t* qr = q + row * ld_q;
+#pragma unroll
+  for (int i = 0; i < CPT; ++i) {
+    const int c = threadIdx.x + i * 128;
+    if (c < nchunk) {
+      const __half2* h = reinterpret_cast<const __half2*>(&v[i]);
+      uint32_t packed = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __half22float2(h[e]);
+        packed |= (nib(code_of(f.x, inv)) | (nib(code_of(f.y, inv)) << 4)) << (8 * e);
+      }
+      *reinterpret_cast<uint32_t*>(qr + (int64_t)c * 4) = packed;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ ACROSS_HEADS
+// Thread (p, g): column pair j = 2p, 2p+1 of head_dim, heads h = g*HPT + r, r < HPT.
+// Lane = g + G * p_lo: the FWHT over r runs in registers, over g with warp shuffles.
+template <int HPT, int G>
+__global__ void hq_heads_kernel(const __half* __restrict__ x, int64_t K, int64_t ld_x, int head_dim, float clip,
+                                uint8_t* __restrict__ q, int64_t ld_q, float* __restrict__ scale) {
+  extern __shared__ uint8_t sh_bytes[];  // K/2 packed bytes + reduction scratch
+  float* red = reinterpret_cast<float*>(sh_bytes + (K >> 1));
+  const int64_t row = blockIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int g = lane % G;
+  const int p = (threadIdx.x / 32) * (32 / G) + lane / G;  // column pair index
+  const int P2 = head_dim >> 1;
+  const __half* xr = x + row * ld_x;
+  float v0[HPT], v1[HPT];
+  const bool active = p < P2;
+#pragma unroll
+  for (int r = 0; r < HPT; ++r) {
+    const int h = g * HPT + r;
+    float2 f = make_float2(0.f, 0.f);
+    if (active) f = __half22float2(*reinterpret_cast<const __half2*>(xr + (int64_t)h * head_dim + 2 * p));
+    v0[r] = f.x;
+    v1[r] = f.y;
+  }
+  // in-register butterflies over r (low bits of h)
+#pragma unroll
+  for (int st = 1; st < HPT; st <<= 1) {
+#pragma unroll
+    for (int r = 0; r < HPT; ++r) {
+      if (!(r & st)) {
+        const float a0 = v0[r], b0 = v0[r + st], a1 = v1[r], b1 = v1[r + st];
+        v0[r] = a0 + b0;
+        v0[r + st] = a0 - b0;
+        v1[r] = a1 + b1;
+        v1[r + st] = a1 - b1;
+      }
+    }
+  }
+  // shuffle butterflies over g (high bits of h)
+#pragma unroll
+  for (int st = 1; st < G; st <<= 1) {
+    const bool upper = (g & st) != 0;
+#pragma unroll
+    for (int r = 0; r < HPT; ++r) {
+      const float o0 = __shfl_xor_sync(0xffffffffu, v0[r], st);
+      const float o1 = __shfl_xor_sync(0xffffffffu, v1[r], st);
+      v0[r] = upper ? (o0 - v0[r]) : (v0[r] + o0);
+      v1[r] = upper ? (o1 - v1[r]) : (v1[r] + o1);
+    }
+  }
+  float amax = 0.f;
+#pragma unroll
+  for (int r = 0; r < HPT; ++r) amax = fmax_nan(amax, fmax_nan(fabsf(v0[r]), fabsf(v1[r])));
+  // block reduce (variable warp count)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) amax = fmax_nan(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  const int nwarps = blockDim.x >> 5;
+  if (lane == 0) red[threadIdx.x >> 5] = amax;
+  __syncthreads();
+  amax = red[0];
+  for (int w = 1; w < nwarps; ++w) amax = fmax_nan(amax, red[w]);
+  const int n_h = (int)(K / head_dim);
+  float s, inv;
+  row_scale(amax, rsqrt((double)n_h), clip, s, inv);
+  if (threadIdx.x == 0) scale[row] = s;
+  if (active) {
+#pragma unroll
+    for (int r = 0; r < HPT; ++r) {
+      const int h = g * HPT + r;
+      sh_bytes[h * P2 + p] = (uint8_t)(nib(code_of(v0[r], inv)) | (nib(code_of(v1[r], inv)) << 4));
+    }
+  }
+  __syncthreads();
+  const int nvec = (int)(K >> 5);  // 16-byte vectors of packed output
+  uint8_t* qr = q + row * ld_q;
+  for (int i = threadIdx.x; i < nvec; i += blockDim.x)
+    *reinterpret_cast<uint4*>(qr + (int64_t)i * 16) = reinterpret_cast<const uint4*>(sh_bytes)[i];
+}
+
+// ------------------------------------------------------------------ FULL
+// One row per CTA, staged in shared memory: X (fp16, K) and Z (fp32, K).
+//  1) copy x -> X (m > 1) or -> Z (m == 1);
+//  2) m > 1: Z[a][:] = H_m X[a][:] for every chunk a with mma.sync.m16n8k16 (fp16 in, exact
+//     +-1 products, fp32 accumulation) on 16-chunk groups;
+//  3) H_{2^n} along a (stride m): radix-2^r passes, 2^r values per thread in registers;
+//     the last pass also tracks amax;
+//  4) scale, RNE codes, pack 8 codes per 32-bit store.
+template <int MB>
+struct BaseDims {
+  static constexpr int KS = (MB + 15) / 16;
+  static constexpr int NT = (MB + 7) / 8;
+};
+
+QR_DEVICE void mma_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <int MB>
+QR_DEVICE void base_transform(const uint32_t* __restrict__ X32, float* __restrict__ Z, int P,
+                              const uint32_t* __restrict__ bfrag) {
+  constexpr int KS = BaseDims<MB>::KS;
+  constexpr int NT = BaseDims<MB>::NT;
+  constexpr int MW = MB / 2;  // 32-bit words per chunk
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  const int gq = lane >> 2, t = lane & 3;
+  const int ngroups = (P + 15) / 16;
+  for (int grp = warp; grp < ngroups; grp += nwarps) {
+    const int a_lo = grp * 16 + gq, a_hi = a_lo + 8;
+    uint32_t afr[KS][4];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int w0 = ks * 8 + t, w1 = w0 + 4;  // word index within the chunk
+      afr[ks][0] = (a_lo < P && w0 < MW) ? X32[a_lo * MW + w0] : 0u;
+      afr[ks][1] = (a_hi < P && w0 < MW) ? X32[a_hi * MW + w0] : 0u;
+      afr[ks][2] = (a_lo < P && w1 < MW) ? X32[a_lo * MW + w1] : 0u;
+      afr[ks][3] = (a_hi < P && w1 < MW) ? X32[a_hi * MW + w1] : 0u;
+    }
+#pragma unroll 1
+    for (int nt = 0; nt < NT; ++nt) {
+      float d[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const uint2 b = __ldg(reinterpret_cast<const uint2*>(bfrag) + ((ks * NT + nt) * 32 + lane));
+        mma_16816(d, afr[ks], b.x, b.y);
+      }
+      const int b = nt * 8 + 2 * t;
+      if (b < MB) {
+        if (a_lo < P) *reinterpret_cast<float2*>(Z + a_lo * MB + b) = make_float2(d[0], d[1]);
+        if (a_hi < P) *reinterpret_cast<float2*>(Z + a_hi * MB + b) = make_float2(d[2], d[3]);
+      }
+    }
+  }
+}
+
+// One radix-R pass of the Walsh-Hadamard transform along a (stride m) on bits
+// [sh, sh + log2 R) of a.  Returns the thread's running amax if kAmax.
+template <int R, bool kAmax>
+QR_DEVICE float fwht_pass(float* __restrict__ Z, int P, int m, int sh) {
+  const int items = (P / R) * m;
+  float amax = 0.f;
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    const int b = it % m;
+    const int rest = it / m;
+    const int lo = rest & ((1 << sh) - 1);
+    const int hi = rest >> sh;
+    const int a0 = hi * (R << sh) + lo;
+    float v[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) v[j] = Z[(a0 + (j << sh)) * m + b];
+#pragma unroll
+    for (int st = 1; st < R; st <<= 1) {
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        if (!(j & st)) {
+          const float x0 = v[j], x1 = v[j + st];
+          v[j] = x0 + x1;
+          v[j + st] = x0 - x1;
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      Z[(a0 + (j << sh)) * m + b] = v[j];
+      if (kAmax) amax = fmax_nan(amax, fabsf(v[j]));
+    }
+  }
+  return amax;
+}
+
+template <bool kAmax>
+QR_DEVICE float fwht_pass_dyn(int r, float* Z, int P, int m, int sh) {
+  switch (r) {
+    case 1: return fwht_pass<2, kAmax>(Z, P, m, sh);
+    case 2: return fwht_pass<4, kAmax>(Z, P, m, sh);
+    case 3: return fwht_pass<8, kAmax>(Z, P, m, sh);
+    case 4: return fwht_pass<16, kAmax>(Z, P, m, sh);
+    default: return fwht_pass<32, kAmax>(Z, P, m, sh);
+  }
+}
+
+template <int MB>
+__global__ void hq_full_kernel(const __half* __restrict__ x, int64_t ld_x, int P, float clip,
+                               uint8_t* __restrict__ q, int64_t ld_q, float* __restrict__ scale,
+                               const uint32_t* __restrict__ bfrag) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int m = MB;
+  const int K = P * m;
+  float* Z = reinterpret_cast<float*>(smem);
+  uint32_t* X32 = reinterpret_cast<uint32_t*>(smem + (size_t)K * 4);
+  float* red = reinterpret_cast<float*>(smem + (size_t)K * 4 + (MB > 1 ? (size_t)K * 2 : 0));
+  const int64_t row = blockIdx.x;
+  const __half* xr = x + row * ld_x;
+
+  // 1) stage the row
+  const int nvec = K >> 3;
+  for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
+    const uint4 v = ldg_nc_v4(xr + (int64_t)i * 8);
+    if (MB > 1) {
+      reinterpret_cast<uint4*>(X32)[i] = v;
+    } else {
+      const __half2* h = reinterpret_cast<const __half2*>(&v);
+      float4 f0, f1;
+      float2 t0 = __half22float2(h[0]), t1 = __half22float2(h[1]), t2 = __half22float2(h[2]),
+             t3 = __half22float2(h[3]);
+      f0 = make_float4(t0.x, t0.y, t1.x, t1.y);
+      f1 = make_float4(t2.x, t2.y, t3.x, t3.y);
+      reinterpret_cast<float4*>(Z)[2 * i] = f0;
+      reinterpret_cast<float4*>(Z)[2 * i + 1] = f1;
+    }
+  }
+  __syncthreads();
+  // 2) H_m on tensor cores
+  if (MB > 1) {
+    base_transform<MB>(X32, Z, P, bfrag);
+    __syncthreads();
+  }
+  // 3) H_{2^n} along a
+  int nbits = 0;
+  while ((1 << nbits) < P) ++nbits;
+  const int npass = (nbits + 4) / 5;
+  float amax = 0.f;
+  int sh = 0;
+  for (int ps = 0; ps < npass; ++ps) {
+    const int r = (nbits - sh + (npass - ps) - 1) / (npass - ps);  // balanced split
+    if (ps == npass - 1) amax = fwht_pass_dyn<true>(r, Z, P, m, sh);
+    else fwht_pass_dyn<false>(r, Z, P, m, sh);
+    sh += r;
+    __syncthreads();
+  }
+  if (npass == 0) {  // P == 1: amax over the base transform output
+    for (int i = threadIdx.x; i < K; i += blockDim.x) amax = fmax_nan(amax, fabsf(Z[i]));
+  }
+  // 4) scale + codes
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) amax = fmax_nan(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = amax;
+  __syncthreads();
+  amax = red[0];
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) amax = fmax_nan(amax, red[w]);
+  float s, inv;
+  row_scale(amax, rsqrt((double)K), clip, s, inv);
+  if (threadIdx.x == 0) scale[row] = s;
+  uint8_t* qr = q + row * ld_q;
+  for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
+    const float4 f0 = reinterpret_cast<const float4*>(Z)[2 * i];
+    const float4 f1 = reinterpret_cast<const float4*>(Z)[2 * i + 1];
+    const uint32_t packed = nib(code_of(f0.x, inv)) | (nib(code_of(f0.y, inv)) << 4) |
+                            (nib(code_of(f0.z, inv)) << 8) | (nib(code_of(f0.w, inv)) << 12) |
+                            (nib(code_of(f1.x, inv)) << 16) | (nib(code_of(f1.y, inv)) << 20) |
+                            (nib(code_of(f1.z, inv)) << 24) | (nib(code_of(f1.w, inv)) << 28);
+    *reinterpret_cast<uint32_t*>(qr + (int64_t)i * 4) = packed;
+  }
+}
+
+}  // namespace hq
+
+// ------------------------------------------------------------------ launchers
+
+cudaError_t launch_hq_none(const void* x, int64_t M, int64_t K, int64_t ld_x, float clip, uint8_t* q,
+                           int64_t ld_q, float* scale, cudaStream_t stream) {
+  const int64_t nchunk = K / 8;
+  const int cpt = (int)((nchunk + 127) / 128);
+  const dim3 grid((unsigned)M);
+  const __half* xh = static_cast<const __half*>(x);
+#define QR_NONE(C) hq::hq_none_kernel<C><<<grid, 128, 0, stream>>>(xh, K, ld_x, clip, q, ld_q, scale)
+  if (cpt <= 1) QR_NONE(1);
+  else if (cpt <= 2) QR_NONE(2);
+  else if (cpt <= 4) QR_NONE(4);
+  else if (cpt <= 8) QR_NONE(8);
+  else if (cpt <= 16) QR_NONE(16);
+  else QR_NONE(32);
+#undef QR_NONE
+  return cudaPeekAtLastError();
+}
+
+cudaError_t launch_hq_heads(const void* x, int64_t M, int64_t K, int64_t ld_x, int head_dim, float clip,
+                            uint8_t* q, int64_t ld_q, float* scale, cudaStream_t stream) {
+  const int n_h = (int)(K / head_dim);
+  const int P2 = head_dim / 2;
+  const __half* xh = static_cast<const __half*>(x);
+  // G groups of heads per column pair; HPT = n_h / G heads per thread (<= 16 in registers)
+  int G = n_h > 16 ? n_h / 16 : 1;
+  if (G > 32) return cudaErrorInvalidValue;
+  const int HPT = n_h / G;
+  int threads = P2 * G;
+  threads = ((threads + 31) / 32) * 32;
+  const size_t smem = (size_t)(K / 2) + 64 * sizeof(float);
+  const dim3 grid((unsigned)M);
+#define QR_HEADS(H, GG) \
+  hq::hq_heads_kernel<H, GG><<<grid, threads, smem, stream>>>(xh, K, ld_x, head_dim, clip, q, ld_q, scale)
+  switch (G) {
+    case 1:
+      switch (HPT) {
+        case 1: QR_HEADS(1, 1); break;
+        case 2: QR_HEADS(2, 1); break;
+        case 4: QR_HEADS(4, 1); break;
+        case 8: QR_HEADS(8, 1); break;
+        default: QR_HEADS(16, 1); break;
+      }
+      break;
+    case 2: QR_HEADS(16, 2); break;
+    case 4: QR_HEADS(16, 4); break;
+    case 8: QR_HEADS(16, 8); break;
+    case 16: QR_HEADS(16, 16); break;
+    default: QR_HEADS(16, 32); break;
+  }
+#undef QR_HEADS
+  return cudaPeekAtLastError();
+}
+
+cudaError_t launch_hq_full(const void* x, int64_t M, int64_t K, int64_t ld_x, int pow2, int m, float clip,
+                           uint8_t* q, int64_t ld_q, float* scale, cudaStream_t stream) {
+  const __half* xh = static_cast<const __half*>(x);
+  const int threads = K >= 16384 ? 512 : 256;
+  const size_t smem = (size_t)K * 4 + (m > 1 ? (size_t)K * 2 : 0) + 32 * sizeof(float);
+  const dim3 grid((unsigned)M);
+  cudaError_t e;
+  if (m == 1) {
+    e = cudaFuncSetAttribute(hq::hq_full_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    hq::hq_full_kernel<1><<<grid, threads, smem, stream>>>(xh, ld_x, pow2, clip, q, ld_q, scale, nullptr);
+  } else if (m == 28) {
+    e = cudaFuncSetAttribute(hq::hq_full_kernel<28>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    hq::hq_full_kernel<28><<<grid, threads, smem, stream>>>(xh, ld_x, pow2, clip, q, ld_q, scale,
+                                                           device_bfrag_table(28));
+  } else {
+    e = cudaFuncSetAttribute(hq::hq_full_kernel<172>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    hq::hq_full_kernel<172><<<grid, threads, smem, stream>>>(xh, ld_x, pow2, clip, q, ld_q, scale,
+                                                            device_bfrag_table(172));
+  }
+  return cudaPeekAtLastError();
+}
+
+}  // namespace qr

@@ -1,0 +1,175 @@
+// hadamard_tables.cu — the stored small Hadamard matrices H_m of P:67 ("a Kronecker
+// construction H_d = H_{2^n} (x) H_m ... m is the size of a known Hadamard matrix").
+//
+// Built on the host from classical constructions (reading Z3), written
+// independently of the oracle:
+//   H_28  Paley II, q = 13:  S = [[0, 1^T], [1, Q]], Q_ij = chi(j - i) (quadratic character
+//         of GF(13)),  H = S (x) [[1,1],[1,-1]] + I_14 (x) [[1,-1],[-1,-1]].
+//   H_172 Williamson array [[A,B,C,D],[-B,A,-D,C],[-C,D,A,-B],[-D,-C,B,A]] over symmetric
+//         circulants of order 43 whose first rows are -1 exactly on unions of cyclotomic
+//         classes C_i = {3^(7k+i) mod 43} selected by bit masks (7, 25, 44, 50) with
+//         diagonals (+1, +1, +1, -1).
+// Each matrix is verified H H^T = m I before use; a failure disables FULL mode for that m.
+//
+// The device copy is laid out as mma.sync.m16n8k16 B fragments (B[k][n] = H_m[n][k], so
+// D = X_chunks . H_m^T computes y_b = sum_b' H_m[b][b'] x_b' for every chunk), zero-padded
+// to multiples of 16 (k) and 8 (n).
+#include <cuda_fp16.h>
+
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "quarot_internal.h"
+
+namespace qr {
+
+namespace {
+
+constexpr int KS28 = 2, NT28 = 4;     // pad 28 -> 32 (k), 32 (n)
+constexpr int KS172 = 11, NT172 = 22; // pad 172 -> 176
+
+__device__ uint32_t g_bfrag28[KS28 * NT28 * 64];
+__device__ uint32_t g_bfrag172[KS172 * NT172 * 64];
+
+std::vector<int8_t> build_h28() {
+  const int q = 13;
+  int chi[13];
+  chi[0] = 0;
+  for (int x = 1; x < q; ++x) chi[x] = -1;
+  for (int x = 1; x < q; ++x) chi[(x * x) % q] = 1;
+  int S[14][14];
+  for (int i = 0; i < 14; ++i)
+    for (int j = 0; j < 14; ++j) {
+      if (i == 0 && j == 0) S[i][j] = 0;
+      else if (i == 0 || j == 0) S[i][j] = 1;
+      else S[i][j] = chi[((j - 1) - (i - 1) + q) % q];
+    }
+  const int A[2][2] = {{1, 1}, {1, -1}};
+  const int B[2][2] = {{1, -1}, {-1, -1}};
+  std::vector<int8_t> h(28 * 28);
+  for (int i = 0; i < 14; ++i)
+    for (int j = 0; j < 14; ++j)
+      for (int u = 0; u < 2; ++u)
+        for (int v = 0; v < 2; ++v)
+          h[(2 * i + u) * 28 + (2 * j + v)] = (int8_t)(S[i][j] * A[u][v] + (i == j ? B[u][v] : 0));
+  return h;
+}
+
+std::vector<int8_t> build_h172() {
+  const int p = 43;
+  // cyclotomic class index of every non-zero residue: 3^e mod 43 lies in class e mod 7
+  int cls[43];
+  cls[0] = -1;
+  int x = 1;
+  for (int e = 0; e < p - 1; ++e) {
+    cls[x] = e % 7;
+    x = (x * 3) % p;
+  }
+  const int masks[4] = {7, 25, 44, 50};
+  const int diag[4] = {1, 1, 1, -1};
+  int row[4][43];
+  for (int w = 0; w < 4; ++w) {
+    row[w][0] = diag[w];
+    for (int j = 1; j < p; ++j) row[w][j] = ((masks[w] >> cls[j]) & 1) ? -1 : 1;
+  }
+  auto circ = [&](int w, int i, int j) { return row[w][((j - i) % p + p) % p]; };
+  // block (R, C) of the Williamson array: sign * matrix index
+  const int blk_w[4][4] = {{0, 1, 2, 3}, {1, 0, 3, 2}, {2, 3, 0, 1}, {3, 2, 1, 0}};
+  const int blk_s[4][4] = {{1, 1, 1, 1}, {-1, 1, -1, 1}, {-1, 1, 1, -1}, {-1, -1, 1, 1}};
+  std::vector<int8_t> h(172 * 172);
+  for (int R = 0; R < 4; ++R)
+    for (int C = 0; C < 4; ++C)
+      for (int i = 0; i < p; ++i)
+        for (int j = 0; j < p; ++j)
+          h[(R * p + i) * 172 + (C * p + j)] = (int8_t)(blk_s[R][C] * circ(blk_w[R][C], i, j));
+  return h;
+}
+
+bool is_hadamard(const std::vector<int8_t>& h, int m) {
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < m; ++j) {
+      int s = 0;
+      for (int k = 0; k < m; ++k) s += h[i * m + k] * h[j * m + k];
+      if (s != (i == j ? m : 0)) return false;
+    }
+  return true;
+}
+
+struct Tables {
+  std::vector<int8_t> h28, h172;
+  bool ok28 = false, ok172 = false;
+};
+
+Tables& tables() {
+  static Tables t;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    t.h28 = build_h28();
+    t.h172 = build_h172();
+    t.ok28 = is_hadamard(t.h28, 28);
+    t.ok172 = is_hadamard(t.h172, 172);
+  });
+  return t;
+}
+
+uint16_t half_bits(int v) { return v > 0 ? 0x3C00 : (v < 0 ? 0xBC00 : 0); }
+
+std::vector<uint32_t> bfrag(const std::vector<int8_t>& h, int m, int KS, int NT) {
+  std::vector<uint32_t> out((size_t)KS * NT * 64);
+  auto H = [&](int n, int k) -> int { return (n < m && k < m) ? h[n * m + k] : 0; };
+  for (int ks = 0; ks < KS; ++ks)
+    for (int nt = 0; nt < NT; ++nt)
+      for (int lane = 0; lane < 32; ++lane) {
+        const int g = lane >> 2, t = lane & 3;
+        const int n = 8 * nt + g;
+        const int k0 = 16 * ks + 2 * t;
+        const uint32_t r0 = half_bits(H(n, k0)) | ((uint32_t)half_bits(H(n, k0 + 1)) << 16);
+        const uint32_t r1 = half_bits(H(n, k0 + 8)) | ((uint32_t)half_bits(H(n, k0 + 9)) << 16);
+        out[((size_t)(ks * NT + nt) * 32 + lane) * 2 + 0] = r0;
+        out[((size_t)(ks * NT + nt) * 32 + lane) * 2 + 1] = r1;
+      }
+  return out;
+}
+
+std::mutex g_dev_mu;
+bool g_dev_ready[64];
+
+}  // namespace
+
+const int8_t* base_hadamard_host(int m) {
+  Tables& t = tables();
+  if (m == 28) return t.ok28 ? t.h28.data() : nullptr;
+  if (m == 172) return t.ok172 ? t.h172.data() : nullptr;
+  return nullptr;
+}
+
+cudaError_t ensure_device_tables() {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  if (g_dev_ready[dev & 63]) return cudaSuccess;
+  Tables& t = tables();
+  if (t.ok28) {
+    auto f = bfrag(t.h28, 28, KS28, NT28);
+    e = cudaMemcpyToSymbol(g_bfrag28, f.data(), f.size() * sizeof(uint32_t));
+    if (e != cudaSuccess) return e;
+  }
+  if (t.ok172) {
+    auto f = bfrag(t.h172, 172, KS172, NT172);
+    e = cudaMemcpyToSymbol(g_bfrag172, f.data(), f.size() * sizeof(uint32_t));
+    if (e != cudaSuccess) return e;
+  }
+  g_dev_ready[dev & 63] = true;
+  return cudaSuccess;
+}
+
+const uint32_t* device_bfrag_table(int m) {
+  void* p = nullptr;
+  if (m == 28) cudaGetSymbolAddress(&p, g_bfrag28);
+  else if (m == 172) cudaGetSymbolAddress(&p, g_bfrag172);
+  return static_cast<const uint32_t*>(p);
+}
+
+}  // namespace qr

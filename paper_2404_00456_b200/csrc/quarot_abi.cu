@@ -1,0 +1,166 @@
+// quarot_abi.cu — the extern "C" boundary (include/quarot.h): argument validation and
+// dispatch to the sm_100a kernels.  No torch types, no allocation, no host synchronization.
+#include <cstring>
+
+#include "../../include/quarot.h"
+#include "quarot_internal.h"
+
+namespace {
+
+thread_local int32_t g_last_launches = 0;
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+bool pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+bool clip_ok(float c) { return c > 0.f && c <= 1.f; }  // NaN fails both
+
+// K = 2^n * m with m in {1, 28, 172}; smallest admissible m (largest power of two).
+bool factorize(int64_t K, int64_t& p, int& m) {
+  const int cands[3] = {1, 28, 172};
+  for (int c : cands) {
+    if (K % c == 0 && pow2(K / c)) {
+      p = K / c;
+      m = c;
+      return true;
+    }
+  }
+  return false;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* quarot_status_string(int32_t s) {
+  switch (s) {
+    case QUAROT_OK: return "ok";
+    case QUAROT_ERR_NULL: return "null pointer argument";
+    case QUAROT_ERR_DIM: return "dimension error (non-positive, odd, inconsistent or ld < width)";
+    case QUAROT_ERR_UNSUPPORTED_SIZE:
+      return "unsupported size: FULL needs K = 2^n * m with m in {1, 28, 172} and 2^n >= 2; "
+             "ACROSS_HEADS needs K / head_dim and head_dim powers of two (head_dim >= 64); "
+             "KV needs head_dim in {64, 128, 256}";
+    case QUAROT_ERR_ALIGN: return "alignment error (16-byte pointers / leading dimensions, width granularity)";
+    case QUAROT_ERR_ARG: return "bad argument (clip ratio outside (0, 1], unknown mode or flags)";
+    case QUAROT_ERR_CUDA: return "CUDA launch error";
+    default: return "unknown status";
+  }
+}
+
+int32_t quarot_abi_version(void) { return QUAROT_ABI_VERSION; }
+
+int32_t quarot_last_launch_count(void) { return g_last_launches; }
+
+quarot_status quarot_base_hadamard(int32_t m, int8_t* out) {
+  if (!out) return QUAROT_ERR_NULL;
+  const int8_t* h = qr::base_hadamard_host(m);
+  if (!h) return QUAROT_ERR_UNSUPPORTED_SIZE;
+  std::memcpy(out, h, (size_t)m * m);
+  return QUAROT_OK;
+}
+
+quarot_status quarot_hadamard_quant(const void* x, int64_t M, int64_t K, int64_t ld_x, int32_t mode,
+                                    int32_t head_dim, float clip_ratio, uint8_t* q, int64_t ld_q, float* scale,
+                                    void* stream) {
+  g_last_launches = 0;
+  if (mode < QUAROT_HAD_NONE || mode > QUAROT_HAD_ACROSS_HEADS) return QUAROT_ERR_ARG;
+  if (!clip_ok(clip_ratio)) return QUAROT_ERR_ARG;
+  if (M < 0 || K <= 0 || (K & 1) || ld_x < K || ld_q < K / 2) return QUAROT_ERR_DIM;
+  if (M > 0x7fffffffLL) return QUAROT_ERR_DIM;
+  if (M == 0) return QUAROT_OK;
+  if (!x || !q || !scale) return QUAROT_ERR_NULL;
+  if (!aligned16(x) || !aligned16(q) || (ld_x % 8) || (ld_q % 16)) return QUAROT_ERR_ALIGN;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  if (mode == QUAROT_HAD_NONE) {
+    if (K % 16) return QUAROT_ERR_ALIGN;
+    if (K > 32768) return QUAROT_ERR_UNSUPPORTED_SIZE;
+    e = qr::launch_hq_none(x, M, K, ld_x, clip_ratio, q, ld_q, scale, st);
+  } else if (mode == QUAROT_HAD_ACROSS_HEADS) {
+    if (head_dim <= 0 || K % head_dim) return QUAROT_ERR_DIM;
+    if (!pow2(head_dim) || head_dim < 64 || !pow2(K / head_dim) || K / head_dim > 512)
+      return QUAROT_ERR_UNSUPPORTED_SIZE;
+    if (K % 32) return QUAROT_ERR_ALIGN;
+    e = qr::launch_hq_heads(x, M, K, ld_x, head_dim, clip_ratio, q, ld_q, scale, st);
+  } else {
+    int64_t p = 0;
+    int m = 0;
+    if (!factorize(K, p, m) || p < 2 || K > 32768) return QUAROT_ERR_UNSUPPORTED_SIZE;
+    if (K % 16) return QUAROT_ERR_ALIGN;
+    if (m > 1) {
+      if (!qr::base_hadamard_host(m)) return QUAROT_ERR_UNSUPPORTED_SIZE;
+      e = qr::ensure_device_tables();
+      if (e != cudaSuccess) return QUAROT_ERR_CUDA;
+    }
+    e = qr::launch_hq_full(x, M, K, ld_x, (int)p, m, clip_ratio, q, ld_q, scale, st);
+  }
+  if (e != cudaSuccess) return QUAROT_ERR_CUDA;
+  g_last_launches = 1;
+  return QUAROT_OK;
+}
+
+static quarot_status check_gemm(const uint8_t* xq, int64_t M, int64_t K, int64_t ld_xq, const uint8_t* wq,
+                                int64_t N, int64_t ld_wq, const void* out, int64_t ld_out, int64_t out_elems_align) {
+  if (M < 0 || N <= 0 || K <= 0 || ld_xq < K / 2 || ld_wq < K / 2 || ld_out < N) return QUAROT_ERR_DIM;
+  if (M > 0x7fffffffLL || N > 0x7fffffffLL) return QUAROT_ERR_DIM;
+  if (M == 0) return QUAROT_OK;
+  if (!xq || !wq || !out) return QUAROT_ERR_NULL;
+  if (K % 128 || N % 8 || ld_xq % 16 || ld_wq % 16 || ld_out % out_elems_align) return QUAROT_ERR_ALIGN;
+  if (!aligned16(xq) || !aligned16(wq) || !aligned16(out)) return QUAROT_ERR_ALIGN;
+  if (K > 171196) return QUAROT_ERR_UNSUPPORTED_SIZE;  // 256 * 49 * K must fit int32
+  return QUAROT_OK;
+}
+
+quarot_status quarot_int4_linear(const uint8_t* xq, const float* x_scale, int64_t M, int64_t K, int64_t ld_xq,
+                                 const uint8_t* wq, const float* w_scale, int64_t N, int64_t ld_wq, void* y,
+                                 int64_t ld_y, void* stream) {
+  g_last_launches = 0;
+  quarot_status s = check_gemm(xq, M, K, ld_xq, wq, N, ld_wq, y, ld_y, 8);
+  if (s != QUAROT_OK || M == 0) return s;
+  if (!x_scale || !w_scale) return QUAROT_ERR_NULL;
+  if (!aligned16(w_scale)) return QUAROT_ERR_ALIGN;
+  cudaError_t e = qr::launch_int4_gemm(xq, x_scale, M, K, ld_xq, wq, w_scale, N, ld_wq, y, ld_y,
+                                       static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return QUAROT_ERR_CUDA;
+  g_last_launches = 1;
+  return QUAROT_OK;
+}
+
+quarot_status quarot_int4_matmul_s32(const uint8_t* xq, int64_t M, int64_t K, int64_t ld_xq, const uint8_t* wq,
+                                     int64_t N, int64_t ld_wq, int32_t* acc, int64_t ld_acc, void* stream) {
+  g_last_launches = 0;
+  quarot_status s = check_gemm(xq, M, K, ld_xq, wq, N, ld_wq, acc, ld_acc, 4);
+  if (s != QUAROT_OK || M == 0) return s;
+  cudaError_t e =
+      qr::launch_int4_gemm_s32(xq, M, K, ld_xq, wq, N, ld_wq, acc, ld_acc, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return QUAROT_ERR_CUDA;
+  g_last_launches = 1;
+  return QUAROT_OK;
+}
+
+quarot_status quarot_kv_quant(const void* k, int64_t ld_k, const void* v, int64_t ld_v, int64_t T, int32_t n_kv,
+                              int32_t head_dim, void* q, int64_t ld_q, int32_t n_q, uint32_t flags, float clip_ratio,
+                              uint8_t* k_codes, float* k_scale, uint8_t* k_zero, uint8_t* v_codes, float* v_scale,
+                              uint8_t* v_zero, void* stream) {
+  g_last_launches = 0;
+  if (flags & ~3u) return QUAROT_ERR_ARG;
+  if (!clip_ok(clip_ratio)) return QUAROT_ERR_ARG;
+  if (T < 0 || n_kv <= 0 || n_q < 0 || head_dim <= 0) return QUAROT_ERR_DIM;
+  if (!(head_dim == 64 || head_dim == 128 || head_dim == 256)) return QUAROT_ERR_UNSUPPORTED_SIZE;
+  const bool has_q = q != nullptr && n_q > 0;
+  if (ld_k < (int64_t)n_kv * head_dim || ld_v < (int64_t)n_kv * head_dim ||
+      (has_q && ld_q < (int64_t)n_q * head_dim))
+    return QUAROT_ERR_DIM;
+  if (T == 0) return QUAROT_OK;
+  if (!k || !v || !k_codes || !k_scale || !k_zero || !v_codes || !v_scale || !v_zero) return QUAROT_ERR_NULL;
+  if (!aligned16(k) || !aligned16(v) || (has_q && !aligned16(q)) || !aligned16(k_codes) || !aligned16(v_codes))
+    return QUAROT_ERR_ALIGN;
+  if ((ld_k % 8) || (ld_v % 8) || (has_q && (ld_q % 8))) return QUAROT_ERR_ALIGN;
+  cudaError_t e = qr::launch_kv_quant(k, ld_k, v, ld_v, T, n_kv, head_dim, has_q ? q : nullptr, ld_q,
+                                      has_q ? n_q : 0, flags, clip_ratio, k_codes, k_scale, k_zero, v_codes,
+                                      v_scale, v_zero, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return QUAROT_ERR_CUDA;
+  g_last_launches = 1;
+  return QUAROT_OK;
+}
+
+}  // extern "C"

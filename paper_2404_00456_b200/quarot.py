@@ -1,0 +1,179 @@
+"""Thin Python binding of libquarot.so (include/quarot.h): argument marshalling only.
+
+Every step of the hot path runs in the library's sm_100a kernels; this module only
+allocates outputs with ``torch.empty`` (PyTorch is the device-memory / stream plumbing),
+passes raw device pointers and the current CUDA stream, and raises on a non-OK status.
+There is no fallback: if the shared library or a GPU is missing, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libquarot.so")
+
+NONE, FULL, ACROSS_HEADS = 0, 1, 2
+MODES = {"none": NONE, "full": FULL, "across_heads": ACROSS_HEADS}
+KV_ROTATE_K, KV_ROTATE_V = 1, 2
+
+_c_i64, _c_i32, _c_u32, _c_f32, _vp = ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32, ctypes.c_float, ctypes.c_void_p
+
+_SIGS = {
+    "quarot_hadamard_quant": [_vp, _c_i64, _c_i64, _c_i64, _c_i32, _c_i32, _c_f32, _vp, _c_i64, _vp, _vp],
+    "quarot_int4_linear": [_vp, _vp, _c_i64, _c_i64, _c_i64, _vp, _vp, _c_i64, _c_i64, _vp, _c_i64, _vp],
+    "quarot_int4_matmul_s32": [_vp, _c_i64, _c_i64, _c_i64, _vp, _c_i64, _c_i64, _vp, _c_i64, _vp],
+    "quarot_kv_quant": [_vp, _c_i64, _vp, _c_i64, _c_i64, _c_i32, _c_i32, _vp, _c_i64, _c_i32, _c_u32,
+                        _c_f32, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "quarot_status_string": [_c_i32],
+    "quarot_abi_version": [],
+    "quarot_base_hadamard": [_c_i32, _vp],
+    "quarot_last_launch_count": [],
+}
+EXPORTS = tuple(_SIGS)
+
+
+class QuarotError(RuntimeError):
+    def __init__(self, fn: str, status: int, msg: str):
+        super().__init__(f"{fn}: status {status}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libquarot.so (built in-tree by __graft_entry__.build()).  Raises if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2404_00456_b200.build`")
+        h = ctypes.CDLL(LIB_PATH)
+        for name, args in _SIGS.items():
+            f = getattr(h, name)
+            f.argtypes = args
+            f.restype = ctypes.c_char_p if name == "quarot_status_string" else ctypes.c_int32
+        _lib = h
+    return _lib
+
+
+def _check(fn: str, status: int):
+    if status != 0:
+        raise QuarotError(fn, status, lib().quarot_status_string(status).decode())
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _dev(t: torch.Tensor, name: str, dtype=None):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if t.dim() >= 1 and t.stride(-1) != 1:
+        raise ValueError(f"{name} must have unit stride in its last dimension")
+    return t.data_ptr()
+
+
+def abi_version() -> int:
+    return lib().quarot_abi_version()
+
+
+def last_launch_count() -> int:
+    return lib().quarot_last_launch_count()
+
+
+def base_hadamard(m: int) -> torch.Tensor:
+    """The library's stored H_m (host int8), for cross-checking against the oracle."""
+    out = torch.empty(m * m, dtype=torch.int8)
+    _check("quarot_base_hadamard", lib().quarot_base_hadamard(m, out.data_ptr()))
+    return out.view(m, m)
+
+
+def hadamard_quant(x: torch.Tensor, mode="none", head_dim: int = 128, clip_ratio: float = 0.9,
+                   q: torch.Tensor | None = None, scale: torch.Tensor | None = None, stream=None):
+    """quarot_hadamard_quant: fp16 x [M, K] -> (packed uint8 q [M, K/2], fp32 scale [M])."""
+    mode_i = MODES[mode] if isinstance(mode, str) else int(mode)
+    M, K = x.shape
+    if q is None:
+        q = torch.empty(M, K // 2, dtype=torch.uint8, device=x.device)
+    if scale is None:
+        scale = torch.empty(M, dtype=torch.float32, device=x.device)
+    st = lib().quarot_hadamard_quant(_dev(x, "x", torch.float16), M, K, x.stride(0), mode_i, head_dim,
+                                     clip_ratio, _dev(q, "q", torch.uint8), q.stride(0),
+                                     _dev(scale, "scale", torch.float32), None, _stream(stream))
+    _check("quarot_hadamard_quant", st)
+    return q, scale
+
+
+def int4_linear(xq: torch.Tensor, x_scale: torch.Tensor, wq: torch.Tensor, w_scale: torch.Tensor,
+                y: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """quarot_int4_linear: y fp16 [M, N] = fp16(acc * s_x * s_w)."""
+    M, Kh = xq.shape
+    N = wq.shape[0]
+    if y is None:
+        y = torch.empty(M, N, dtype=torch.float16, device=xq.device)
+    st = lib().quarot_int4_linear(_dev(xq, "xq", torch.uint8), _dev(x_scale, "x_scale", torch.float32), M, 2 * Kh,
+                                  xq.stride(0), _dev(wq, "wq", torch.uint8), _dev(w_scale, "w_scale", torch.float32),
+                                  N, wq.stride(0), _dev(y, "y", torch.float16), y.stride(0), _stream(stream))
+    _check("quarot_int4_linear", st)
+    return y
+
+
+def int4_matmul_s32(xq: torch.Tensor, wq: torch.Tensor, acc: torch.Tensor | None = None,
+                    stream=None) -> torch.Tensor:
+    """quarot_int4_matmul_s32: raw int32 accumulators [M, N] (parity only)."""
+    M, Kh = xq.shape
+    N = wq.shape[0]
+    if acc is None:
+        acc = torch.empty(M, N, dtype=torch.int32, device=xq.device)
+    st = lib().quarot_int4_matmul_s32(_dev(xq, "xq", torch.uint8), M, 2 * Kh, xq.stride(0),
+                                      _dev(wq, "wq", torch.uint8), N, wq.stride(0),
+                                      _dev(acc, "acc", torch.int32), acc.stride(0), _stream(stream))
+    _check("quarot_int4_matmul_s32", st)
+    return acc
+
+
+def kv_quant(k: torch.Tensor, v: torch.Tensor, q: torch.Tensor | None = None, flags: int = KV_ROTATE_K,
+             clip_ratio: float = 0.95, out: dict | None = None, stream=None) -> dict:
+    """quarot_kv_quant (KV-cache Init): k, v fp16 [T, n_kv, d] (heads contiguous per token,
+    any token stride — e.g. views into a fused QKV output); q optional fp16 [T, n_q, d]
+    rotated in place.  Returns dict of codes / scales / zeros for K and V."""
+    T, n_kv, d = k.shape
+    if v.shape != k.shape:
+        raise ValueError("k and v shapes differ")
+    for name, t in (("k", k), ("v", v), ("q", q)):
+        if t is not None and (t.stride(2) != 1 or t.stride(1) != d):
+            raise ValueError(f"{name}: heads of a token must be contiguous [n, d]")
+    dev = k.device
+    if out is None:
+        out = {
+            "k_codes": torch.empty(T, n_kv, d // 2, dtype=torch.uint8, device=dev),
+            "k_scale": torch.empty(T, n_kv, dtype=torch.float32, device=dev),
+            "k_zero": torch.empty(T, n_kv, dtype=torch.uint8, device=dev),
+            "v_codes": torch.empty(T, n_kv, d // 2, dtype=torch.uint8, device=dev),
+            "v_scale": torch.empty(T, n_kv, dtype=torch.float32, device=dev),
+            "v_zero": torch.empty(T, n_kv, dtype=torch.uint8, device=dev),
+        }
+    n_q = 0 if q is None else q.shape[1]
+    st = lib().quarot_kv_quant(_dev(k, "k", torch.float16), k.stride(0), _dev(v, "v", torch.float16), v.stride(0),
+                               T, n_kv, d, None if q is None else _dev(q, "q", torch.float16),
+                               0 if q is None else q.stride(0), n_q, flags, clip_ratio,
+                               out["k_codes"].data_ptr(), out["k_scale"].data_ptr(), out["k_zero"].data_ptr(),
+                               out["v_codes"].data_ptr(), out["v_scale"].data_ptr(), out["v_zero"].data_ptr(),
+                               _stream(stream))
+    _check("quarot_kv_quant", st)
+    return out
+
+
+def quarot_linear(x: torch.Tensor, wq: torch.Tensor, w_scale: torch.Tensor, mode="none", head_dim: int = 128,
+                  clip_ratio: float = 0.9, y: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """The 4-bit linear layer of P:860: optional online Hadamard + quantize, INT4 GEMM,
+    dequantize to fp16 — two kernel launches."""
+    xq, xs = hadamard_quant(x, mode, head_dim, clip_ratio, stream=stream)
+    return int4_linear(xq, xs, wq, w_scale, y=y, stream=stream)

@@ -1,0 +1,115 @@
+"""C-ABI library checks that need no GPU: it loads, exports every symbol include/quarot.h
+declares, validates arguments before touching CUDA, and its independently built Hadamard
+tables agree with the oracle's."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import hadamard as had
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "quarot.h")
+
+
+@pytest.fixture(scope="module")
+def q():
+    from paper_2404_00456_b200 import build
+    build.build()
+    from paper_2404_00456_b200 import quarot
+    quarot.lib()
+    return quarot
+
+
+def declared_symbols():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(quarot_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_declares_north_star_calls():
+    syms = declared_symbols()
+    for name in ("quarot_hadamard_quant", "quarot_int4_linear", "quarot_kv_quant"):
+        assert name in syms
+
+
+def test_library_exports_every_declared_symbol(q):
+    lib = ctypes.CDLL(q.LIB_PATH)
+    for name in declared_symbols():
+        assert hasattr(lib, name), f"{name} declared in quarot.h but not exported"
+    assert set(declared_symbols()) == set(q.EXPORTS)
+
+
+def test_abi_version_and_status_strings(q):
+    assert q.abi_version() == 1
+    for s in range(7):
+        assert q.lib().quarot_status_string(s)
+
+
+@pytest.mark.parametrize("m", [28, 172])
+def test_library_tables_match_oracle(m):
+    # two independent constructions of the same instance (reading Z3) must agree exactly
+    from paper_2404_00456_b200 import quarot
+    got = quarot.base_hadamard(m).numpy().astype(np.int64)
+    assert np.array_equal(got, had.base_matrix(m))
+
+
+def test_unsupported_base_size(q):
+    with pytest.raises(q.QuarotError):
+        q.base_hadamard(12)
+
+
+def _hq(q, x=16, M=4, K=256, ld_x=256, mode=0, hd=128, clip=0.9, qp=32, ld_q=128, sp=48):
+    return q.lib().quarot_hadamard_quant(x, M, K, ld_x, mode, hd, clip, qp, ld_q, sp, None)
+
+
+def test_hadamard_quant_validation_without_gpu(q):
+    # All of these are rejected before any CUDA call (dummy non-null pointers are fine).
+    assert _hq(q, mode=3) == 5 and _hq(q, mode=-1) == 5              # ERR_ARG
+    assert _hq(q, clip=0.0) == 5 and _hq(q, clip=1.5) == 5 and _hq(q, clip=float("nan")) == 5
+    assert _hq(q, K=255) == 2 and _hq(q, ld_x=100) == 2 and _hq(q, ld_q=64) == 2  # ERR_DIM
+    assert _hq(q, M=-1) == 2
+    assert _hq(q, M=0) == 0                                            # no-op
+    assert _hq(q, x=None) == 1 and _hq(q, qp=None) == 1 and _hq(q, sp=None) == 1  # ERR_NULL
+    assert _hq(q, x=16 * 7 + 2) == 4                                   # misaligned pointer
+    assert _hq(q, mode=1, K=12 * 16, ld_x=12 * 16, ld_q=96) == 3       # 192 = 2^4 * 12: no H_12
+    assert _hq(q, mode=2, K=256, hd=48, ld_q=128) == 2                 # K % head_dim
+    assert _hq(q, mode=2, K=384, ld_x=384, hd=128, ld_q=192) == 3      # 3 heads: not 2^n
+    assert _hq(q, mode=2, K=256, hd=32) == 3                           # head_dim < 64
+
+
+def _lin(q, M=128, K=256, N=256, ld_xq=128, ld_wq=128, ld_y=256, xp=16, wp=16, yp=16):
+    return q.lib().quarot_int4_linear(xp, 16, M, K, ld_xq, wp, 16, N, ld_wq, yp, ld_y, None)
+
+
+def test_gemm_validation_without_gpu(q):
+    assert _lin(q, M=0) == 0
+    assert _lin(q, K=192, ld_xq=96, ld_wq=96) == 4      # K % 128
+    assert _lin(q, N=250, ld_y=256) == 4                # N % 8
+    assert _lin(q, ld_y=100) == 2
+    assert _lin(q, xp=None) == 1
+    assert _lin(q, xp=8) == 4
+    assert q.lib().quarot_int4_matmul_s32(16, 4, 256, 128, 16, 256, 128, 16, 258, None) == 4
+
+
+def test_kv_validation_without_gpu(q):
+    f = q.lib().quarot_kv_quant
+    # k, ld_k, v, ld_v, T, n_kv, hd, q, ld_q, n_q, flags, clip, 6 outputs, stream
+    args = [16, 1024, 16, 1024, 4, 8, 128, None, 0, 0, 1, 0.95, 16, 16, 16, 16, 16, 16, None]
+    # pointers are dummies: only argument sets rejected before any CUDA call are used
+    bad = list(args); bad[10] = 4
+    assert f(*bad) == 5                                 # unknown flag bit
+    bad = list(args); bad[11] = 0.0
+    assert f(*bad) == 5
+    bad = list(args); bad[6] = 96
+    assert f(*bad) == 3                                 # head_dim unsupported
+    bad = list(args); bad[4] = 0
+    assert f(*bad) == 0                                 # T == 0: no-op
+    bad = list(args); bad[0] = None
+    assert f(*bad) == 1
+    bad = list(args); bad[1] = 1000
+    assert f(*bad) == 2                                 # ld_k < n_kv * head_dim
+    bad = list(args); bad[1] = 1028
+    assert f(*bad) == 4                                 # ld_k % 8

@@ -1,0 +1,208 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element
+on seeded inputs.  Bars (BASELINE.json north_star): int32 accumulators bit-exact; INT4
+codes within one step on <= 1e-4 of elements; fp16 outputs within 1e-2 relative Frobenius;
+scales within 1e-5 relative."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import gemm as ogemm
+from oracle import kv as okv
+from oracle import layer as olayer
+from oracle import quant as oquant
+from tests import _parity as P
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def q():
+    from paper_2404_00456_b200 import quarot
+    quarot.lib()
+    assert torch.cuda.is_available()
+    return quarot
+
+
+DEV = "cuda"
+
+
+def _adversarial_rows(k: int) -> np.ndarray:
+    """Edge rows: zero, exact ties at clip 1 scale, one huge outlier, fp16 extremes,
+    subnormals, alternating signs."""
+    rows = []
+    rows.append(np.zeros(k))
+    r = np.zeros(k); r[0] = 7.0; r[1:8] = [0.5, 1.5, 2.5, -0.5, -1.5, -2.5, 3.5]; rows.append(r)
+    r = np.random.default_rng(0).standard_normal(k) * 0.01; r[k // 3] = 1000.0; rows.append(r)
+    r = np.full(k, 65504.0); r[::2] = -65504.0; rows.append(r)
+    r = np.full(k, 6e-8); r[1::3] = -6e-8; rows.append(r)
+    r = np.ones(k); r[1::2] = -1; rows.append(r)
+    return np.stack(rows).astype(np.float16)
+
+
+def _hq_compare(q, x16: torch.Tensor, mode: str, head_dim: int = 128, clip=0.9, rows=None):
+    xq, xs = q.hadamard_quant(x16, mode, head_dim, clip)
+    torch.cuda.synchronize()
+    sel = slice(None) if rows is None else torch.as_tensor(rows, device=x16.device)
+    xh = x16[sel].float().cpu().numpy().astype(np.float64)
+    ref_codes, _, ref_scale = olayer.hadamard_quant(xh, mode, head_dim, clip)
+    got_codes = P.unpack_signed(xq[sel].cpu().numpy())
+    st = P.assert_codes(got_codes, ref_codes, f"{mode} K={x16.shape[1]}")
+    P.assert_scales(xs[sel].cpu().numpy(), ref_scale, f"{mode} K={x16.shape[1]}")
+    # no code -8 is ever produced (symmetric range [-7, 7], Z8)
+    assert not np.any(got_codes == -8)
+    return xq, xs, st
+
+
+@pytest.mark.parametrize("mode,K,hd", [
+    ("none", 256, 128), ("none", 4096, 128), ("none", 8192, 128), ("none", 11008, 128),
+    ("full", 256, 128), ("full", 448, 128), ("full", 688, 128), ("full", 4096, 128),
+    ("full", 11008, 128), ("full", 28672, 128),
+    ("across_heads", 512, 128), ("across_heads", 4096, 128), ("across_heads", 8192, 128),
+    ("across_heads", 8192, 64),
+])
+def test_hadamard_quant_parity(q, mode, K, hd):
+    M = 37  # ragged
+    x = synth.activations(M, K, "outlier", seed=K + len(mode), device=DEV)
+    x = torch.cat([x, torch.from_numpy(_adversarial_rows(K)).to(DEV)], 0).contiguous()
+    _hq_compare(q, x, mode, hd)
+
+
+def test_hadamard_quant_nonfinite_rows(q):
+    K = 4096
+    x = synth.activations(4, K, "normal", seed=1, device=DEV)
+    x[1, 5] = float("nan")
+    x[2, 7] = float("inf")
+    for mode in ("none", "full", "across_heads"):
+        xq, xs = q.hadamard_quant(x, mode)
+        s = xs.cpu().numpy()
+        assert np.isfinite(s[0]) and np.isnan(s[1]) and np.isnan(s[2]) and np.isfinite(s[3])
+        codes = P.unpack_signed(xq.cpu().numpy())
+        assert np.all(codes[1] == 0) and np.all(codes[2] == 0)
+
+
+def test_hadamard_quant_strided_and_split_invariance(q):
+    # leading dimensions > width, and row splits give bitwise identical results
+    K, M = 4096, 64
+    big = synth.activations(M, K + 64, "outlier", seed=3, device=DEV)
+    x = big[:, :K]
+    for mode in ("none", "full", "across_heads"):
+        xq, xs = q.hadamard_quant(x, mode)
+        xq2, xs2 = q.hadamard_quant(x.contiguous(), mode)
+        a1, s1 = q.hadamard_quant(x[:20], mode)
+        a2, s2 = q.hadamard_quant(x[20:], mode)
+        assert torch.equal(xq, xq2) and torch.equal(xs, xs2)
+        assert torch.equal(torch.cat([a1, a2]), xq) and torch.equal(torch.cat([s1, s2]), xs)
+
+
+def _rand_codes_packed(rows, k, seed):
+    return synth.packed_weight_codes(rows, k, seed, device=DEV)
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 128), (1, 256, 256), (300, 776, 512), (129, 264, 4096),
+                                   (257, 512, 11008), (64, 256, 28672), (600, 1024, 8192)])
+def test_int4_gemm_s32_bit_exact(q, M, N, K):
+    xq = _rand_codes_packed(M, K, seed=M)
+    wq = _rand_codes_packed(N, K, seed=N + 1)
+    acc = q.int4_matmul_s32(xq, wq)
+    torch.cuda.synchronize()
+    cx = P.unpack_signed(xq.cpu().numpy())
+    cw = P.unpack_signed(wq.cpu().numpy())
+    ref = ogemm.int_matmul_exact_f64(cx, cw) if K > 4096 else ogemm.int_matmul(cx, cw)
+    assert np.array_equal(acc.cpu().numpy().astype(np.int64), ref)
+
+
+def test_int4_gemm_extreme_codes_bit_exact(q):
+    # all +-7: the largest accumulators (|acc| = 49 K); checks the x256 scaling path
+    M, N, K = 130, 264, 28672
+    xq = torch.full((M, K // 2), 0x77, dtype=torch.uint8, device=DEV)
+    wq = torch.full((N, K // 2), 0x99, dtype=torch.uint8, device=DEV)  # -7, -7
+    wq[::2] = 0x77
+    acc = q.int4_matmul_s32(xq, wq).cpu().numpy()
+    assert np.all(acc[:, 0::2] == 49 * K) and np.all(acc[:, 1::2] == -49 * K)
+
+
+@pytest.mark.parametrize("M,N,K", [(200, 264, 256), (129, 1024, 4096), (300, 512, 28672)])
+def test_int4_linear_epilogue(q, M, N, K):
+    xq = _rand_codes_packed(M, K, seed=7)
+    wq = _rand_codes_packed(N, K, seed=8)
+    xs = torch.rand(M, device=DEV) * 0.1 + 0.01
+    ws = synth.weight_scales(N, seed=9, device=DEV)
+    y = q.int4_linear(xq, xs, wq, ws)
+    torch.cuda.synchronize()
+    cx = P.unpack_signed(xq.cpu().numpy())
+    cw = P.unpack_signed(wq.cpu().numpy())
+    acc = ogemm.int_matmul_exact_f64(cx, cw)
+    ref = ogemm.dequant_epilogue(acc, xs.cpu().numpy(), ws.cpu().numpy())
+    got = y.cpu().numpy()
+    assert P.frob_rel(got, ref) <= P.FROB_REL
+    assert P.max_fp16_ulp(got, ref) <= 2
+
+
+def test_tiny_config_end_to_end(q):
+    # BASELINE config 0: 16 tokens x 256 -> 256, power-of-two Hadamard, RTN weights
+    x = synth.activations(16, 256, "outlier", seed=0, device="cpu", n_outliers=1)
+    w = synth.dense_weight(256, 256, seed=1).double().numpy()
+    cw, pw, sw = olayer.quantize_weight(w, "full")
+    y = q.quarot_linear(x.to(DEV), torch.from_numpy(pw).to(DEV), torch.from_numpy(sw).to(DEV), "full")
+    ref = olayer.quarot_linear(x.double().numpy(), cw, sw, "full")
+    assert P.frob_rel(y.cpu().numpy(), ref) <= P.FROB_REL
+    # and close to the full-precision product (QuaRot W4A4 on a rotated layer)
+    fp = x.double().numpy() @ w.T
+    assert P.frob_rel(y.cpu().numpy(), fp) < 0.2
+
+
+@pytest.mark.parametrize("T,n_kv,n_q,hd,flags", [(37, 8, 64, 128, 1), (5, 2, 0, 128, 1), (9, 4, 4, 64, 3),
+                                                 (3, 2, 2, 256, 1), (11, 8, 8, 128, 0)])
+def test_kv_quant_parity(q, T, n_kv, n_q, hd, flags):
+    k, v, qq = synth.kv_inputs(T, n_kv, n_q, hd, seed=T, device=DEV)
+    k[0, 0] = 0  # degenerate group
+    q_dev = None if qq is None else qq.clone()
+    out = q.kv_quant(k, v, q_dev, flags=flags)
+    torch.cuda.synchronize()
+    ref = okv.kv_init(k.cpu().numpy(), v.cpu().numpy(), None if qq is None else qq.cpu().numpy(),
+                      rotate_k=bool(flags & 1), rotate_v=bool(flags & 2))
+    for t in ("k", "v"):
+        P.assert_codes(P.unpack_unsigned(out[f"{t}_codes"].cpu().numpy()),
+                       P.unpack_unsigned(ref[f"{t}_codes"]), f"{t} codes")
+        P.assert_codes(out[f"{t}_zero"].cpu().numpy(), ref[f"{t}_zero"], f"{t} zero")
+        P.assert_scales(out[f"{t}_scale"].cpu().numpy(), ref[f"{t}_scale"], f"{t} scale")
+    assert out["k_scale"][0, 0].item() == 1.0 and out["k_zero"][0, 0].item() == 0
+    if qq is not None:
+        assert P.max_fp16_ulp(q_dev.cpu().numpy(), ref["q_rot"]) <= 1
+
+
+def test_deterministic_repeat(q):
+    x = synth.activations(512, 28672, "swiglu", seed=5, device=DEV)
+    a = q.hadamard_quant(x, "full")
+    b = q.hadamard_quant(x, "full")
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+    wq = _rand_codes_packed(512, 28672, seed=6)
+    ws = synth.weight_scales(512, seed=6, device=DEV)
+    y1 = q.int4_linear(a[0], a[1], wq, ws)
+    y2 = q.int4_linear(a[0], a[1], wq, ws)
+    assert torch.equal(y1, y2)
+
+
+def test_errors_raise_without_launch(q):
+    x = torch.zeros(4, 192, dtype=torch.float16, device=DEV)
+    with pytest.raises(q.QuarotError):
+        q.hadamard_quant(x, "full")  # 192 = 2^4 * 12 unsupported
+    assert q.last_launch_count() == 0
+
+
+def test_kv_quant_from_fused_qkv_views(q):
+    # K, V, Q read straight out of a fused QKV output [T, (n_q + 2 n_kv) d] (strided views)
+    T, n_q, n_kv, d = 33, 8, 2, 128
+    fused = synth.activations(T, (n_q + 2 * n_kv) * d, "normal", seed=2, device=DEV)
+    qv = fused[:, : n_q * d].view(T, n_q, d)
+    kv_ = fused[:, n_q * d:(n_q + n_kv) * d].view(T, n_kv, d)
+    vv = fused[:, (n_q + n_kv) * d:].view(T, n_kv, d)
+    k_ref, v_ref, q_ref = (t.cpu().numpy().copy() for t in (kv_, vv, qv))
+    out = q.kv_quant(kv_, vv, qv)
+    ref = okv.kv_init(k_ref, v_ref, q_ref)
+    P.assert_codes(P.unpack_unsigned(out["k_codes"].cpu().numpy()), P.unpack_unsigned(ref["k_codes"]), "k")
+    P.assert_codes(P.unpack_unsigned(out["v_codes"].cpu().numpy()), P.unpack_unsigned(ref["v_codes"]), "v")
+    assert P.max_fp16_ulp(qv.cpu().numpy(), ref["q_rot"]) <= 1
+    # K and V regions of the fused buffer are untouched
+    assert np.array_equal(kv_.cpu().numpy(), k_ref) and np.array_equal(vv.cpu().numpy(), v_ref)
