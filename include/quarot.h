@@ -71,7 +71,8 @@ typedef enum {
  *   M      tokens (>= 0; M == 0 is a no-op).      K  width (even; see mode).
  *   mode   quarot_had_mode.  head_dim: used by ACROSS_HEADS only (power of two).
  *   clip_ratio  in (0, 1]; the paper uses 0.9.
- *   q      uint8 [M][ld_q] (K/2 bytes used), 16-B aligned; ld_q % 16 == 0.
+ *   q      uint8 [M][ld_q] (K/2 bytes used), 16-B aligned; ld_q % 4 == 0 (% 16 for
+ *          ACROSS_HEADS).
  *   scale  fp32 [M].
  * Per row, with y the transformed (normalized) row (fp32 arithmetic on fp16 input):
  *   a = max_k |y_k|;  a == 0 -> scale 1, codes 0;  a not finite -> scale NaN, codes 0;

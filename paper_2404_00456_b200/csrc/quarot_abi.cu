@@ -68,7 +68,8 @@ quarot_status quarot_hadamard_quant(const void* x, int64_t M, int64_t K, int64_t
   if (M > 0x7fffffffLL) return QUAROT_ERR_DIM;
   if (M == 0) return QUAROT_OK;
   if (!x || !q || !scale) return QUAROT_ERR_NULL;
-  if (!aligned16(x) || !aligned16(q) || (ld_x % 8) || (ld_q % 16)) return QUAROT_ERR_ALIGN;
+  if (!aligned16(x) || !aligned16(q) || (ld_x % 8) || (ld_q % (mode == QUAROT_HAD_ACROSS_HEADS ? 16 : 4)))
+    return QUAROT_ERR_ALIGN;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e;
   if (mode == QUAROT_HAD_NONE) {
