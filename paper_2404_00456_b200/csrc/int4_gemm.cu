@@ -4,59 +4,72 @@
 // INT32"), y = fp16(acc * s_x[m] * s_w[n]) (P:233 dequantization with row and column
 // scales), fused in the epilogue instead of the paper's separate kernel.
 //
-// sm_100 tcgen05 has no s4 kind, so packed INT4 operands are widened to INT8 on the way
-// into shared memory and multiplied with tcgen05.mma kind::i8 into TMEM int32 accumulators.
+// sm_100 tcgen05 has no s4 kind, so the packed INT4 operands are widened to INT8 on chip and
+// multiplied with tcgen05.mma kind::i8 into TMEM int32 accumulators.
 //
-// Design:
-//  * persistent CTAs (one per SM), grouped-M tile raster for L2 reuse, tile 128 x 256,
-//    k-block 128 (one 128-byte SWIZZLE_128B atom row per operand row), 4-stage smem ring;
-//  * 8 producer warps: LDG.128 the packed tiles straight into registers (one k-block of
-//    prefetch), widen with the "x16 nibble trick" (int8 = code*16 = byte & 0xF0 for the
-//    high nibble, (byte << 4) & 0xF0 for the low nibble: 3 ALU ops per 8 codes, no sign
-//    extension), STS.128 into the canonical K-major SW128 layout.  Each 32-code packed chunk
-//    becomes [16 low-nibble codes | 16 high-nibble codes]: the SAME permutation of k for A
-//    and B, so the dot product is unchanged.  The MMA accumulates 256*acc (|256*acc| <=
-//    256*49*K < 2^31 for K <= 171196), the epilogue shifts right by 8 exactly;
-//  * 1 MMA warp: a single thread issues 4 x tcgen05.mma (M128 N256 K32) per k-block and
-//    tcgen05.commit's the stage back to the producers;
-//  * 4 epilogue warps: tcgen05.ld 32x32b.x32 from TMEM (double-buffered 2 x 256 columns so
-//    the next tile's mainloop overlaps this tile's epilogue), scale, round to fp16, store.
+// Design — a CTA pair (cluster 2x1) computes a 256 x 256 output tile with
+// tcgen05.mma.cta_group::2 (M256 N256 K32); CTA r owns A rows [128r, 128r+128) and B rows
+// [128r, 128r+128) of the tile:
+//  * TMA warp: cp.async.bulk.tensor loads the PACKED A and B k-blocks (128 rows x 64 B each,
+//    SWIZZLE_64B) into an 8-stage staging ring — asynchronous, no registers in flight;
+//  * 4 A-widen warps (thread = row): LDS the row's 64 packed bytes, widen to 128 int8 with the
+//    "x16 nibble trick" (int8 = code*16 = byte & 0xF0 for the high nibble, (byte << 4) & 0xF0
+//    for the low nibble), tcgen05.st them into a TMEM A stage: the MMA takes A from TMEM
+//    (TS form), so widened A never goes back through shared memory;
+//  * 4 B-widen warps: LDS packed B, widen, STS.128 into a 4-stage K-major SWIZZLE_128B ring;
+//  * every packed 32-code chunk becomes [16 low-nibble codes | 16 high-nibble codes]: the
+//    SAME permutation of k for A and B, so the dot product is unchanged.  The MMA
+//    accumulates 256*acc (|256*acc| <= 256*49*K < 2^31 for K <= 171196); the epilogue shifts
+//    right by 8, exactly;
+//  * MMA warp (leader CTA, one thread): 4 x tcgen05.mma per k-block; tcgen05.commit
+//    multicasts the stage release to both CTAs;
+//  * 4 epilogue warps per CTA: tcgen05.ld 32x32b.x32, scale, round to fp16, store.
+// Shared-memory traffic per CTA per k-block: 16 KB TMA + 16 KB LDS + 16 KB STS + 16 KB MMA
+// read = 64 KB per 512 MMA cycles (125 B/clk at the full tensor rate, vs ~128 B/clk).
+// No thread ever holds a global load in flight across the proxy fence (whose MEMBAR would
+// wait for it), which is what capped the register-prefetch design at ~40% of peak.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
 #include "common.cuh"
 #include "quarot_internal.h"
 
 namespace qr {
 namespace gemm {
 
-constexpr int BM = 128;
-constexpr int BN = 256;
-constexpr int BK = 128;           // int8 elements per k-block
-constexpr int BKP = BK / 2;       // packed bytes per row per k-block
-constexpr int STAGES = 4;
-constexpr int A_BYTES = BM * BK;  // 16 KB
-constexpr int B_BYTES = BN * BK;  // 32 KB
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int BM = 256;            // pair tile rows (128 per CTA)
+constexpr int BMC = 128;
+constexpr int BN = 256;            // pair tile cols (128 B rows per CTA)
+constexpr int BNC = 128;
+constexpr int BK = 128;            // int8 elements per k-block
+constexpr int BKP = BK / 2;        // packed bytes per row per k-block
+constexpr int SSTAGES = 8;         // packed staging ring (TMA destination)
+constexpr int OSTAGES = 4;         // widened operand ring (TMEM A + smem B)
+constexpr int SA_BYTES = BMC * BKP;                 // 8 KB packed A
+constexpr int SB_BYTES = BNC * BKP;                 // 8 KB packed B
+constexpr int SSTAGE_BYTES = SA_BYTES + SB_BYTES;   // 16 KB
+constexpr int OB_BYTES = BNC * BK;                  // 16 KB widened B (SW128 K-major)
 constexpr int NUM_EPI_WARPS = 4;
-constexpr int NUM_PROD_WARPS = 8;
-constexpr int PROD_THREADS = NUM_PROD_WARPS * 32;
-constexpr int MMA_WARP = NUM_EPI_WARPS + NUM_PROD_WARPS;  // warp 12
-constexpr int NUM_THREADS = (MMA_WARP + 1) * 32;          // 416
-constexpr int CHUNKS = (BM + BN) * (BKP / 16);            // 1536 x 16-byte packed chunks
-constexpr int CPT = CHUNKS / PROD_THREADS;                // 6 per producer thread
-constexpr int TMEM_COLS = 512;                            // 2 accumulators x 256 columns
-constexpr int GROUP_M = 16;
+constexpr int A_WARP0 = 4;                          // warps 4..7
+constexpr int B_WARP0 = 8;                          // warps 8..11
+constexpr int TMA_WARP = 12;
+constexpr int MMA_WARP = 13;
+constexpr int NUM_THREADS = 14 * 32;
+constexpr int TMEM_COLS = 512;
+constexpr int ACC_COL = 0;                          // accumulator: columns [0, 256)
+constexpr int A_COL0 = 256;                         // A stages: 32 columns each
+constexpr int GROUP_M = 8;                          // pair-rows per raster group
 constexpr uint32_t IDESC = idesc_i8(BM, BN);
-constexpr size_t SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-
-static_assert(CHUNKS % PROD_THREADS == 0, "chunk split");
+constexpr size_t SMEM_BYTES = SSTAGES * SSTAGE_BYTES + OSTAGES * OB_BYTES + 1024 + 512;
 
 struct Params {
-  const uint8_t* xq;
-  const uint8_t* wq;
   const float* x_scale;
   const float* w_scale;
   void* out;  // fp16 y or int32 acc
-  int64_t M, N, K, ld_xq, ld_wq, ld_out;
-  int num_m, num_n, num_kb, num_tiles;
+  int64_t M, N, K, ld_out;
+  int num_m, num_n, num_kb, num_tiles;  // num_m in 256-row pair tiles
 };
 
 QR_DEVICE void tile_coords(const Params& p, int t, int& mb, int& nb) {
@@ -72,152 +85,252 @@ QR_DEVICE void tile_coords(const Params& p, int t, int& mb, int& nb) {
 QR_DEVICE uint32_t lo_nib16(uint32_t w) { return (w << 4) & 0xF0F0F0F0u; }
 QR_DEVICE uint32_t hi_nib16(uint32_t w) { return w & 0xF0F0F0F0u; }
 
+QR_DEVICE uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+QR_DEVICE void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+QR_DEVICE uint32_t map_to_rank(const void* local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(local)), "r"(rank));
+  return r;
+}
+// Arrive on a barrier by shared::cluster address (default .release.cta, as CUTLASS's
+// ClusterBarrier::arrive(cta_id)).
+QR_DEVICE void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+QR_DEVICE void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+QR_DEVICE void tma_load_2d(uint32_t dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+QR_DEVICE uint4 lds_v4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+// D[tmem] (+)= A[tmem] * B[smem]^T, kind::i8, CTA pair
+QR_DEVICE void mma_i8_ts_2sm(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], [%1], %2, %3, p;\n\t}"
+      ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(acc));
+}
+QR_DEVICE void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+#define QR_TMEM_ST32(taddr, r)                                                                             \
+  asm volatile(                                                                                            \
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16," \
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),                     \
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),     \
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),          \
+      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),         \
+      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])                      \
+      : "memory")
+
 template <bool kS32>
-__global__ void __launch_bounds__(NUM_THREADS, 1) int4_gemm_kernel(const Params p) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    int4_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* full_bar = bars;                       // [STAGES] producers -> MMA
-  uint64_t* empty_bar = bars + STAGES;             // [STAGES] MMA commit -> producers
-  uint64_t* tfull_bar = bars + 2 * STAGES;         // [2] MMA commit -> epilogue
-  uint64_t* tempty_bar = bars + 2 * STAGES + 2;    // [2] epilogue -> MMA
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+  uint8_t* stage_smem = smem;                                  // [SSTAGES][A 8 KB | B 8 KB]
+  uint8_t* opb_smem = smem + SSTAGES * SSTAGE_BYTES;           // [OSTAGES][16 KB]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(opb_smem + OSTAGES * OB_BYTES);
+  uint64_t* st_full = bars;                          // [SSTAGES] TMA -> widen warps
+  uint64_t* st_empty = st_full + SSTAGES;            // [SSTAGES] widen warps -> TMA (8 warps)
+  uint64_t* op_full = st_empty + SSTAGES;            // [OSTAGES] widen warps of both CTAs -> leader MMA
+  uint64_t* op_empty = op_full + OSTAGES;            // [OSTAGES] MMA commit -> widen warps
+  uint64_t* t_full = op_empty + OSTAGES;             // MMA commit -> epilogue
+  uint64_t* t_empty = t_full + 1;                    // epilogues of both CTAs -> leader MMA
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(t_empty + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int pair = (int)blockIdx.x >> 1;
+  const int num_pairs = (int)gridDim.x >> 1;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full_bar[s], NUM_PROD_WARPS);
-      mbar_init(&empty_bar[s], 1);
+    for (int s = 0; s < SSTAGES; ++s) {
+      mbar_init(&st_full[s], 1);
+      mbar_init(&st_empty[s], 8);
     }
-    for (int a = 0; a < 2; ++a) {
-      mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], NUM_EPI_WARPS);
+    for (int s = 0; s < OSTAGES; ++s) {
+      mbar_init(&op_full[s], 2 * 8);
+      mbar_init(&op_empty[s], 1);
     }
+    mbar_init(t_full, 1);
+    mbar_init(t_empty, 2 * NUM_EPI_WARPS);
     fence_barrier_init();
   }
   if (warp == MMA_WARP) {
-    tmem_alloc(tmem_holder, TMEM_COLS);
-    tmem_relinquish();
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  if (warp == TMA_WARP && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
   }
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
-  const int my_tiles = (p.num_tiles > (int)blockIdx.x)
-                           ? (p.num_tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1
-                           : 0;
+  const int my_tiles = (p.num_tiles > pair) ? (p.num_tiles - 1 - pair) / num_pairs + 1 : 0;
+  const int total = my_tiles * p.num_kb;
 
-  if (warp >= NUM_EPI_WARPS && warp < MMA_WARP) {
-    // ===================== producers: LDG packed -> widen -> STS =====================
-    const int pt = threadIdx.x - NUM_EPI_WARPS * 32;
-    const int total = my_tiles * p.num_kb;
-    uint4 nxt[CPT];
-    auto load = [&](int it, uint4 (&dst)[CPT]) {
-      const int tl = it / p.num_kb;
-      const int kb = it - tl * p.num_kb;
-      int mb, nb;
-      tile_coords(p, (int)blockIdx.x + tl * (int)gridDim.x, mb, nb);
-#pragma unroll
-      for (int i = 0; i < CPT; ++i) {
-        const int c = pt + i * PROD_THREADS;
-        const int r = c >> 2;
-        const int q = c & 3;
-        const uint8_t* src;
-        bool ok;
-        if (r < BM) {
-          const int64_t row = (int64_t)mb * BM + r;
-          ok = row < p.M;
-          src = p.xq + row * p.ld_xq + (int64_t)kb * BKP + q * 16;
-        } else {
-          const int64_t row = (int64_t)nb * BN + (r - BM);
-          ok = row < p.N;
-          src = p.wq + row * p.ld_wq + (int64_t)kb * BKP + q * 16;
-        }
-        dst[i] = ok ? ldg_nc_v4(src) : make_uint4(0, 0, 0, 0);
+  if (warp == TMA_WARP) {
+    // ===================== TMA producer: packed k-blocks -> staging ring =====================
+    if (lane == 0) {
+      for (int it = 0; it < total; ++it) {
+        const int tl = it / p.num_kb;
+        const int kb = it - tl * p.num_kb;
+        int mb, nb;
+        tile_coords(p, pair + tl * num_pairs, mb, nb);
+        const int s = it % SSTAGES;
+        mbar_wait(&st_empty[s], ((it / SSTAGES) & 1) ^ 1);
+        mbar_expect_tx(&st_full[s], SSTAGE_BYTES);
+        const uint32_t dst = smem_u32(stage_smem + s * SSTAGE_BYTES);
+        tma_load_2d(dst, &tmA, kb * BKP, mb * BM + (int)rank * BMC, &st_full[s]);
+        tma_load_2d(dst + SA_BYTES, &tmB, kb * BKP, nb * BN + (int)rank * BNC, &st_full[s]);
       }
-    };
-    if (total > 0) load(0, nxt);
+    }
+  } else if (warp >= A_WARP0 && warp < A_WARP0 + 4) {
+    // ===================== A widen: thread = row, packed smem -> int8 TMEM =====================
+    const int row = (warp - A_WARP0) * 32 + lane;            // == TMEM lane (warp % 4 quarter)
+    const uint32_t sw = (uint32_t)((row >> 1) & 3);           // TMA SWIZZLE_64B chunk xor
+    const uint32_t opfull_leader = map_to_rank(&op_full[0], 0);
+    const uint32_t tlane = (uint32_t)((warp - A_WARP0) * 32) << 16;
     for (int it = 0; it < total; ++it) {
-      const int stage = it % STAGES;
-      const uint32_t phase = (it / STAGES) & 1;
-      uint4 cur[CPT];
+      const int s = it % SSTAGES;
+      const int o = it % OSTAGES;
+      mbar_wait(&st_full[s], (it / SSTAGES) & 1);
+      const uint32_t src = smem_u32(stage_smem + s * SSTAGE_BYTES) + (uint32_t)row * BKP;
+      uint4 w[4];
 #pragma unroll
-      for (int i = 0; i < CPT; ++i) cur[i] = nxt[i];
-      if (it + 1 < total) load(it + 1, nxt);
-      mbar_wait(&empty_bar[stage], phase ^ 1);
-      const uint32_t sbase = smem_u32(smem + stage * STAGE_BYTES);
+      for (int c = 0; c < 4; ++c) w[c] = lds_v4(src + (((uint32_t)c ^ sw) << 4));
+      uint32_t r[32];
 #pragma unroll
-      for (int i = 0; i < CPT; ++i) {
-        const int c = pt + i * PROD_THREADS;
-        const int r = c >> 2;
-        const int q = c & 3;
-        const uint32_t obase = (r < BM) ? sbase + (uint32_t)(r >> 3) * 1024u + (uint32_t)(r & 7) * 128u
-                                        : sbase + A_BYTES + (uint32_t)((r - BM) >> 3) * 1024u +
-                                              (uint32_t)((r - BM) & 7) * 128u;
-        const uint32_t sw = (uint32_t)(r & 7);  // (r - BM) & 7 == r & 7 since BM % 8 == 0
-        const uint4 w = cur[i];
-        const uint4 lo = make_uint4(lo_nib16(w.x), lo_nib16(w.y), lo_nib16(w.z), lo_nib16(w.w));
-        const uint4 hi = make_uint4(hi_nib16(w.x), hi_nib16(w.y), hi_nib16(w.z), hi_nib16(w.w));
-        sts_v4(obase + ((((uint32_t)(2 * q)) ^ sw) << 4), lo);
-        sts_v4(obase + ((((uint32_t)(2 * q + 1)) ^ sw) << 4), hi);
+      for (int c = 0; c < 4; ++c) {  // packed chunk c -> MMA k-step c: [16 lo | 16 hi] int8
+        r[8 * c + 0] = lo_nib16(w[c].x);
+        r[8 * c + 1] = lo_nib16(w[c].y);
+        r[8 * c + 2] = lo_nib16(w[c].z);
+        r[8 * c + 3] = lo_nib16(w[c].w);
+        r[8 * c + 4] = hi_nib16(w[c].x);
+        r[8 * c + 5] = hi_nib16(w[c].y);
+        r[8 * c + 6] = hi_nib16(w[c].z);
+        r[8 * c + 7] = hi_nib16(w[c].w);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&st_empty[s]);
+      mbar_wait(&op_empty[o], ((it / OSTAGES) & 1) ^ 1);
+      tc_fence_after();
+      QR_TMEM_ST32(tmem_base + tlane + (uint32_t)(A_COL0 + 32 * o), r);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(opfull_leader + (uint32_t)o * 8u);
+    }
+  } else if (warp >= B_WARP0 && warp < B_WARP0 + 4) {
+    // ===================== B widen: packed smem -> int8 SW128 smem =====================
+    const int t = threadIdx.x - B_WARP0 * 32;  // 0..127
+    const uint32_t opfull_leader = map_to_rank(&op_full[0], 0);
+    for (int it = 0; it < total; ++it) {
+      const int s = it % SSTAGES;
+      const int o = it % OSTAGES;
+      mbar_wait(&st_full[s], (it / SSTAGES) & 1);
+      const uint32_t src = smem_u32(stage_smem + s * SSTAGE_BYTES) + SA_BYTES;
+      uint4 w[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int c = t + 128 * i;
+        const int rr = c >> 2, q = c & 3;
+        w[i] = lds_v4(src + (uint32_t)rr * BKP + ((((uint32_t)q) ^ (uint32_t)((rr >> 1) & 3)) << 4));
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&st_empty[s]);
+      mbar_wait(&op_empty[o], ((it / OSTAGES) & 1) ^ 1);
+      const uint32_t dbase = smem_u32(opb_smem + o * OB_BYTES);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int c = t + 128 * i;
+        const int rr = c >> 2, q = c & 3;
+        const uint32_t rowb = dbase + (uint32_t)(rr >> 3) * 1024u + (uint32_t)(rr & 7) * 128u;
+        const uint32_t swz = (uint32_t)(rr & 7);
+        sts_v4(rowb + ((((uint32_t)(2 * q)) ^ swz) << 4),
+               make_uint4(lo_nib16(w[i].x), lo_nib16(w[i].y), lo_nib16(w[i].z), lo_nib16(w[i].w)));
+        sts_v4(rowb + ((((uint32_t)(2 * q + 1)) ^ swz) << 4),
+               make_uint4(hi_nib16(w[i].x), hi_nib16(w[i].y), hi_nib16(w[i].z), hi_nib16(w[i].w)));
       }
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&full_bar[stage]);
+      if (lane == 0) mbar_arrive_cluster(opfull_leader + (uint32_t)o * 8u);
     }
   } else if (warp == MMA_WARP) {
-    // ===================== MMA issuer (one thread) =====================
-    if (lane == 0) {
+    // ===================== MMA issuer (leader CTA, one thread) =====================
+    if (rank == 0 && lane == 0) {
       int it = 0;
       for (int tl = 0; tl < my_tiles; ++tl) {
-        const int acc = tl & 1;
-        const uint32_t acc_phase = (tl >> 1) & 1;
-        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        mbar_wait(t_empty, (tl & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+        const uint32_t d_tmem = tmem_base + ACC_COL;
         for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
-          const int stage = it % STAGES;
-          const uint32_t phase = (it / STAGES) & 1;
-          mbar_wait(&full_bar[stage], phase);
+          const int o = it % OSTAGES;
+          mbar_wait(&op_full[o], (it / OSTAGES) & 1);
           tc_fence_after();
-          const uint32_t a_addr = smem_u32(smem + stage * STAGE_BYTES);
-          const uint64_t a_desc = umma_desc_sw128(a_addr);
-          const uint64_t b_desc = umma_desc_sw128(a_addr + A_BYTES);
+          const uint64_t b_desc = umma_desc_sw128(smem_u32(opb_smem + o * OB_BYTES));
+          const uint32_t a_tmem = tmem_base + (uint32_t)(A_COL0 + 32 * o);
 #pragma unroll
-          for (int k = 0; k < BK / 32; ++k) {
-            // advance 32 bytes along K inside the 128-byte swizzle atom: +2 in 16-byte units
-            mma_i8_ss(d_tmem, a_desc + (uint64_t)(2 * k), b_desc + (uint64_t)(2 * k), IDESC,
-                      (kb | k) != 0 ? 1u : 0u);
-          }
-          mma_commit(&empty_bar[stage]);
+          for (int k = 0; k < BK / 32; ++k)
+            mma_i8_ts_2sm(d_tmem, a_tmem + (uint32_t)(8 * k), b_desc + (uint64_t)(2 * k), IDESC,
+                          (kb | k) != 0 ? 1u : 0u);
+          mma_commit_pair(&op_empty[o]);
         }
-        mma_commit(&tfull_bar[acc]);
+        mma_commit_pair(t_full);
       }
     }
     __syncwarp();
   } else {
-    // ===================== epilogue warps 0..3 =====================
-    const int row_in_tile = warp * 32 + lane;
+    // ===================== epilogue warps 0..3 (each CTA: its 128 rows) =====================
+    const uint32_t tempty_leader = map_to_rank(t_empty, 0);
+    const int row_in_tile = (int)rank * BMC + warp * 32 + lane;
     for (int tl = 0; tl < my_tiles; ++tl) {
-      const int acc = tl & 1;
-      const uint32_t acc_phase = (tl >> 1) & 1;
       int mb, nb;
-      tile_coords(p, (int)blockIdx.x + tl * (int)gridDim.x, mb, nb);
-      mbar_wait(&tfull_bar[acc], acc_phase);
+      tile_coords(p, pair + tl * num_pairs, mb, nb);
+      mbar_wait(t_full, tl & 1);
       tc_fence_after();
       const int64_t m = (int64_t)mb * BM + row_in_tile;
       const bool row_ok = m < p.M;
       float sx = 0.f;
       if (!kS32 && row_ok) sx = __ldg(p.x_scale + m);
-      const uint32_t taddr = tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)(acc * BN);
+      const uint32_t taddr = tmem_base + ((uint32_t)(warp * 32) << 16) + ACC_COL;
 #pragma unroll 1
       for (int cc = 0; cc < BN / 32; ++cc) {
         uint32_t r[32];
         QR_TMEM_LD32(taddr + (uint32_t)(cc * 32), r);
         tmem_ld_wait();
+        if (cc == BN / 32 - 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(tempty_leader);
+        }
         const int64_t n0 = (int64_t)nb * BN + cc * 32;
         if (row_ok) {
           if constexpr (kS32) {
@@ -237,12 +350,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) int4_gemm_kernel(const Params 
               if (n0 + g * 8 < p.N) {
                 const float4 s0 = __ldg(reinterpret_cast<const float4*>(p.w_scale + n0 + g * 8));
                 const float4 s1 = __ldg(reinterpret_cast<const float4*>(p.w_scale + n0 + g * 8 + 4));
-                const float sw[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+                const float swv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
                 uint32_t h[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                  const float v0 = ((float)((int32_t)r[8 * g + 2 * e] >> 8) * sx) * sw[2 * e];
-                  const float v1 = ((float)((int32_t)r[8 * g + 2 * e + 1] >> 8) * sx) * sw[2 * e + 1];
+                  const float v0 = ((float)((int32_t)r[8 * g + 2 * e] >> 8) * sx) * swv[2 * e];
+                  const float v1 = ((float)((int32_t)r[8 * g + 2 * e + 1] >> 8) * sx) * swv[2 * e + 1];
                   __half2 hv = __floats2half2_rn(v0, v1);
                   h[e] = *reinterpret_cast<uint32_t*>(&hv);
                 }
@@ -252,25 +365,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) int4_gemm_kernel(const Params 
           }
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
     }
   }
 
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();
   if (warp == MMA_WARP) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, TMEM_COLS);
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
   }
 }
 
 }  // namespace gemm
 
-static int g_num_sms[64];
+namespace {
 
-static int num_sms_current() {
+int g_num_sms[64];
+
+int num_sms_current() {
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) dev = 0;
@@ -281,6 +393,37 @@ static int num_sms_current() {
   }
   return g_num_sms[dev];
 }
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D map over packed INT4 rows: [rows][K/2 bytes] with row pitch ld bytes; box 64 B x 128
+// rows, SWIZZLE_64B (16-byte chunk c of row r lands at chunk c ^ ((r >> 1) & 3)); rows past
+// the end are zero-filled.
+bool make_packed_map(CUtensorMap* map, const uint8_t* base, int64_t rows, int64_t kbytes, int64_t ld) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)kbytes, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld};
+  cuuint32_t box[2] = {(cuuint32_t)gemm::BKP, 128u};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace
 
 template <bool kS32>
 static cudaError_t launch_gemm_impl(const uint8_t* xq, const float* xs, int64_t M, int64_t K, int64_t ld_xq,
@@ -296,24 +439,24 @@ static cudaError_t launch_gemm_impl(const uint8_t* xq, const float* xs, int64_t 
     if (e != cudaSuccess) return e;
     attr_set[dev & 63] = true;
   }
+  CUtensorMap ma, mb;
+  if (!make_packed_map(&ma, xq, M, K / 2, ld_xq) || !make_packed_map(&mb, wq, N, K / 2, ld_wq))
+    return cudaErrorInvalidValue;
   Params p;
-  p.xq = xq;
-  p.wq = wq;
   p.x_scale = xs;
   p.w_scale = ws;
   p.out = out;
   p.M = M;
   p.N = N;
   p.K = K;
-  p.ld_xq = ld_xq;
-  p.ld_wq = ld_wq;
   p.ld_out = ld_out;
   p.num_m = (int)((M + BM - 1) / BM);
   p.num_n = (int)((N + BN - 1) / BN);
   p.num_kb = (int)(K / BK);
   p.num_tiles = p.num_m * p.num_n;
-  const int grid = p.num_tiles < num_sms_current() ? p.num_tiles : num_sms_current();
-  int4_gemm_kernel<kS32><<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(p);
+  const int max_pairs = num_sms_current() / 2;
+  const int pairs = p.num_tiles < max_pairs ? p.num_tiles : max_pairs;
+  int4_gemm_kernel<kS32><<<2 * pairs, NUM_THREADS, SMEM_BYTES, stream>>>(ma, mb, p);
   return cudaPeekAtLastError();
 }
 

@@ -1,0 +1,80 @@
+"""Kernel micro-benchmarks (CUDA events, warm, inputs > L2) for fast iteration on the GPU box.
+
+  python scripts/kbench.py [gemm] [hq] [kv] [--tokens 131072]
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+import paper_2404_00456_b200 as q  # noqa: E402
+
+
+def timeit(fn, iters=10, warm=3):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(iters):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / iters
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("what", nargs="*", default=["gemm", "hq", "kv"])
+    ap.add_argument("--tokens", type=int, default=131072)
+    ap.add_argument("--iters", type=int, default=10)
+    a = ap.parse_args()
+    M = a.tokens
+    dev = "cuda"
+    res = {}
+    if "gemm" in a.what:
+        xq_big = synth.packed_weight_codes(M, 28672, 1, dev)
+        for name, N, K in (("qkv", 10240, 8192), ("o", 8192, 8192), ("gate_up", 57344, 8192), ("down", 8192, 28672)):
+            xq = xq_big[:, : K // 2]
+            wq = synth.packed_weight_codes(N, K, 2, dev)
+            xs = torch.rand(M, device=dev) + 0.5
+            ws = synth.weight_scales(N, 3, dev)
+            y = torch.empty(M, N, dtype=torch.float16, device=dev)
+            ms = timeit(lambda: q.int4_linear(xq, xs, wq, ws, y=y), a.iters)
+            tops = 2 * M * N * K / ms / 1e9
+            res[f"gemm_{name}"] = {"ms": ms, "tops": tops, "frac_int8_2x_bf16_sustained": tops / 2765.6}
+            print(name, json.dumps(res[f"gemm_{name}"]), flush=True)
+            del wq, y
+        del xq_big
+    if "hq" in a.what:
+        for mode, K in (("none", 8192), ("across_heads", 8192), ("full", 28672), ("full", 11008), ("none", 4096)):
+            x = synth.activations(M, K, "outlier", 5, dev)
+            qb = torch.empty(M, K // 2, dtype=torch.uint8, device=dev)
+            sb = torch.empty(M, dtype=torch.float32, device=dev)
+            ms = timeit(lambda: q.hadamard_quant(x, mode, 128, 0.9, q=qb, scale=sb), a.iters)
+            gbs = M * (2.5 * K + 4) / ms / 1e6
+            res[f"hq_{mode}_{K}"] = {"ms": ms, "gbs": gbs, "frac_hbm": gbs / 6536}
+            print(mode, K, json.dumps(res[f"hq_{mode}_{K}"]), flush=True)
+            del x
+    if "kv" in a.what:
+        fused = synth.activations(M, 10240, "normal", 6, dev)
+        T, d = M, 128
+        qv = fused[:, :8192].view(T, 64, d)
+        kv_ = fused[:, 8192:9216].view(T, 8, d)
+        vv = fused[:, 9216:].view(T, 8, d)
+        out = q.kv_quant(kv_, vv, qv)
+        ms = timeit(lambda: q.kv_quant(kv_, vv, qv, out=out), a.iters)
+        byts = 2 * T * 8 * (2 * d + d // 2 + 5) + T * 64 * d * 4
+        res["kv"] = {"ms": ms, "gbs": byts / ms / 1e6, "frac_hbm": byts / ms / 1e6 / 6536}
+        print("kv", json.dumps(res["kv"]), flush=True)
+    print(json.dumps(res))
+
+
+if __name__ == "__main__":
+    main()
