@@ -361,6 +361,227 @@ __global__ void hq_full_kernel(const __half* __restrict__ x, int64_t ld_x, int P
   }
 }
 
+
+// ------------------------------------------------------------------ FULL, K = 1024 x 28
+// The bench / 70B down_proj width, K = 28672: i = a*28 + b, a = a_hi*32 + a_lo (reading Z2),
+// y = (H_32[a_hi] (x) H_32[a_lo] (x) H_28[b]) x   (Sylvester H_1024 = H_32 (x) H_32, Eq. 1).
+// Persistent CTAs (one per SM, 512 threads); per row:
+//  0) cp.async.bulk copies the fp16 row (57 KB) into smem; the copy of the NEXT row is in
+//     flight during phase 2 of this one;
+//  1) warp w takes slabs a_hi = w, w + 16 (32 x 28 contiguous elements): H_28 on tensor cores
+//     (mma.sync m16n8k16, A = H_28 padded to 32, B = slab^T: exact +-1 x fp16 products, fp32
+//     accumulation), then H_32 over a_lo on the fp32 fragments: 3 butterfly stages in
+//     registers (a_lo bits 0, 3, 4) + 2 with warp shuffles (bits 1, 2); results to smem Z
+//     in natural order (conflict-free: word stride 56 across t, 1 across g);
+//  2) thread t < 448 owns (a_lo = t / 14, b = 2(t % 14), +1) for all 32 a_hi: 32 LDS.64,
+//     H_32 over a_hi with packed fp32x2 butterflies (FADD2), row amax (block reduce), RNE
+//     codes via the magic-number add, one packed byte per a_hi at byte a_hi*448 + t — staged
+//     in smem and written out with 16-byte stores.
+namespace f28 {
+constexpr int MB = 28, P = 1024, K = MB * P, NT = 512;  // (M is the row count)
+constexpr int XS_BYTES = K * 2;      // 57344
+constexpr int Z_BYTES = K * 4;       // 114688
+constexpr int OUT_BYTES = K / 2;     // 14336 (aliases Z after phase 2 has read it)
+constexpr size_t SMEM = XS_BYTES + Z_BYTES + 256;
+}  // namespace f28
+
+QR_DEVICE float2 f2add(float2 a, float2 b) {
+  float2 r;
+  asm("{\n\t.reg .b64 ra, rb, rc;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
+      "add.rn.f32x2 rc, ra, rb;\n\tmov.b64 {%0,%1}, rc;\n\t}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+QR_DEVICE float2 f2sub(float2 a, float2 b) {
+  float2 r;
+  asm("{\n\t.reg .b64 ra, rb, rc;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
+      "sub.rn.f32x2 rc, ra, rb;\n\tmov.b64 {%0,%1}, rc;\n\t}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+QR_DEVICE float2 f2mul(float2 a, float2 b) {
+  float2 r;
+  asm("{\n\t.reg .b64 ra, rb, rc;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
+      "mul.rn.f32x2 rc, ra, rb;\n\tmov.b64 {%0,%1}, rc;\n\t}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+// byte = nib(rne(clamp(v.x * inv))) | nib(rne(clamp(v.y * inv))) << 4; RNE via 1.5 * 2^23
+QR_DEVICE uint32_t quant_pair(float2 v, float inv) {
+  float2 m = f2mul(v, make_float2(inv, inv));
+  m.x = fminf(fmaxf(m.x, -7.f), 7.f);
+  m.y = fminf(fmaxf(m.y, -7.f), 7.f);
+  m = f2add(m, make_float2(12582912.f, 12582912.f));
+  return (__float_as_uint(m.x) & 0xFu) | ((__float_as_uint(m.y) & 0xFu) << 4);
+}
+
+__global__ void __launch_bounds__(f28::NT, 1)
+    hq_full28_kernel(const __half* __restrict__ x, int64_t M, int64_t ld_x, float clip, uint8_t* __restrict__ q,
+                     int64_t ld_q, float* __restrict__ scale, const uint32_t* __restrict__ afrag) {
+  using namespace f28;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* xs = smem;                                        // fp16 row
+  float* Z = reinterpret_cast<float*>(smem + XS_BYTES);     // fp32 after phase 1
+  uint8_t* out = smem + XS_BYTES;                            // packed bytes, aliases Z
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + XS_BYTES + Z_BYTES);
+  float* red = reinterpret_cast<float*>(smem + XS_BYTES + Z_BYTES + 64);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue_row = [&](int64_t row) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(XS_BYTES)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(xs)),
+        "l"(x + row * ld_x), "r"(XS_BYTES), "r"(smem_u32(bar))
+        : "memory");
+  };
+  int64_t row = blockIdx.x;
+  if (threadIdx.x == 0 && row < M) issue_row(row);
+  uint32_t phase = 0;
+  const uint32_t* xw = reinterpret_cast<const uint32_t*>(xs);
+  for (; row < M; row += gridDim.x, phase ^= 1) {
+    // H_28 A fragments (2 m-tiles x 2 k-steps x 4 regs; L1-resident, reloaded per row so they
+    // do not occupy registers during phase 2)
+    uint32_t ha[2][2][4];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(afrag) + ((mt * 2 + ks) * 32 + lane));
+        ha[mt][ks][0] = v.x;
+        ha[mt][ks][1] = v.y;
+        ha[mt][ks][2] = v.z;
+        ha[mt][ks][3] = v.w;
+      }
+    mbar_wait(bar, phase);
+    // ---------------- phase 1: H_28 (tensor cores) + H_32 over a_lo, per slab
+#pragma unroll 1
+    for (int si = 0; si < 2; ++si) {
+      const int a_hi = warp + 16 * si;
+      float d[2][4][4];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const int a = a_hi * 32 + nt * 8 + g;  // B column n = g -> a_lo = 8 nt + g
+        const int wbase = a * (MB / 2);        // 14 words per chunk
+        uint32_t b[2][2];
+        b[0][0] = xw[wbase + t];
+        b[0][1] = xw[wbase + 4 + t];
+        b[1][0] = xw[wbase + 8 + t];
+        b[1][1] = (t < 2) ? xw[wbase + 12 + t] : 0u;
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          d[mt][nt][0] = d[mt][nt][1] = d[mt][nt][2] = d[mt][nt][3] = 0.f;
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks) mma_16816(d[mt][nt], ha[mt][ks], b[ks][0], b[ks][1]);
+        }
+      }
+      // d[mt][nt][e + 2h] = D1[b = 16 mt + g + 8 h][a_lo = 8 nt + 2 t + e]
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {  // a_lo bit 0 (register pair)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const float u = d[mt][nt][2 * h], v = d[mt][nt][2 * h + 1];
+            d[mt][nt][2 * h] = u + v;
+            d[mt][nt][2 * h + 1] = u - v;
+          }
+        }
+#pragma unroll
+        for (int st = 1; st < 4; st <<= 1) {  // a_lo bits 3, 4 (n-tile index)
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) {
+            if (!(nt & st)) {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float u = d[mt][nt][e], v = d[mt][nt + st][e];
+                d[mt][nt][e] = u + v;
+                d[mt][nt + st][e] = u - v;
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int st = 1; st < 4; st <<= 1) {  // a_lo bits 1, 2 (lane bits of t)
+          const float sg = (t & st) ? -1.f : 1.f;
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float o = __shfl_xor_sync(0xffffffffu, d[mt][nt][e], st);
+              d[mt][nt][e] = fmaf(sg, d[mt][nt][e], o);  // lower: v + o, upper: o - v
+            }
+        }
+        // store D1 rows b < 28 to Z in natural order
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int bb = 16 * mt + g + 8 * (e >> 1);
+            const int a = a_hi * 32 + nt * 8 + 2 * t + (e & 1);
+            if (bb < MB) Z[a * MB + bb] = d[mt][nt][e];
+          }
+      }
+    }
+    __syncthreads();
+    // xs is free: start the next row's copy while this one finishes
+    if (threadIdx.x == 0 && row + gridDim.x < M) issue_row(row + gridDim.x);
+    // ---------------- phase 2: H_32 over a_hi (packed fp32x2), amax, codes
+    const bool active = threadIdx.x < 448;
+    float2 v[32];
+    float amax = 0.f;
+    if (active) {
+      const float2* zp = reinterpret_cast<const float2*>(Z) + threadIdx.x;  // (a_lo*28 + 2j) / 2 == t
+#pragma unroll
+      for (int ah = 0; ah < 32; ++ah) v[ah] = zp[ah * 448];
+#pragma unroll
+      for (int st = 1; st < 32; st <<= 1) {
+#pragma unroll
+        for (int ah = 0; ah < 32; ++ah) {
+          if (!(ah & st)) {
+            const float2 u = v[ah], w = v[ah + st];
+            v[ah] = f2add(u, w);
+            v[ah + st] = f2sub(u, w);
+          }
+        }
+      }
+#pragma unroll
+      for (int ah = 0; ah < 32; ++ah) amax = fmax_nan(amax, fmax_nan(fabsf(v[ah].x), fabsf(v[ah].y)));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) amax = fmax_nan(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    if (lane == 0) red[warp] = amax;
+    __syncthreads();  // also: every thread has read its Z values -> Z may be overwritten
+    amax = red[0];
+#pragma unroll
+    for (int w = 1; w < NT / 32; ++w) amax = fmax_nan(amax, red[w]);
+    float s, inv;
+    row_scale(amax, rsqrt((double)K), clip, s, inv);
+    if (threadIdx.x == 0) scale[row] = s;
+    if (active) {
+      if (inv != 0.f) {
+#pragma unroll
+        for (int ah = 0; ah < 32; ++ah) out[ah * 448 + threadIdx.x] = (uint8_t)quant_pair(v[ah], inv);
+      } else {
+#pragma unroll
+        for (int ah = 0; ah < 32; ++ah) out[ah * 448 + threadIdx.x] = 0;
+      }
+    }
+    __syncthreads();
+    uint8_t* qr = q + row * ld_q;
+    for (int i = threadIdx.x; i < OUT_BYTES / 16; i += NT)
+      *reinterpret_cast<uint4*>(qr + i * 16) = reinterpret_cast<const uint4*>(out)[i];
+    __syncthreads();  // out (= Z) is rewritten by the next row's phase 1
+  }
+}
+
 }  // namespace hq
 
 // ------------------------------------------------------------------ launchers
@@ -428,6 +649,21 @@ cudaError_t launch_hq_full(const void* x, int64_t M, int64_t K, int64_t ld_x, in
     e = cudaFuncSetAttribute(hq::hq_full_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     hq::hq_full_kernel<1><<<grid, threads, smem, stream>>>(xh, ld_x, pow2, clip, q, ld_q, scale, nullptr);
+  } else if (m == 28 && pow2 == 1024) {
+    static bool attr[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!attr[dev & 63]) {
+      e = cudaFuncSetAttribute(hq::hq_full28_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)hq::f28::SMEM);
+      if (e != cudaSuccess) return e;
+      attr[dev & 63] = true;
+    }
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = (int)(M < nsm ? M : nsm);
+    hq::hq_full28_kernel<<<grid, hq::f28::NT, hq::f28::SMEM, stream>>>(xh, M, ld_x, clip, q, ld_q, scale,
+                                                                      device_afrag28());
   } else if (m == 28) {
     e = cudaFuncSetAttribute(hq::hq_full_kernel<28>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

@@ -31,6 +31,7 @@ constexpr int KS172 = 11, NT172 = 22; // pad 172 -> 176
 
 __device__ uint32_t g_bfrag28[KS28 * NT28 * 64];
 __device__ uint32_t g_bfrag172[KS172 * NT172 * 64];
+__device__ uint32_t g_afrag28[2 * 2 * 32 * 4];
 
 std::vector<int8_t> build_h28() {
   const int q = 13;
@@ -132,6 +133,28 @@ std::vector<uint32_t> bfrag(const std::vector<int8_t>& h, int m, int KS, int NT)
   return out;
 }
 
+// A operand (row-major 16x16 per (mt, ks)): a0 = (r = g, c = 2t..2t+1), a1 = (r = g+8, same c),
+// a2 = (r = g, c + 8), a3 = (r = g+8, c + 8), with A[r][c] = H_28[16 mt + r][16 ks + c].
+std::vector<uint32_t> afrag28(const std::vector<int8_t>& h) {
+  std::vector<uint32_t> out(2 * 2 * 32 * 4);
+  auto H = [&](int r, int c) -> int { return (r < 28 && c < 28) ? h[r * 28 + c] : 0; };
+  for (int mt = 0; mt < 2; ++mt)
+    for (int ks = 0; ks < 2; ++ks)
+      for (int lane = 0; lane < 32; ++lane) {
+        const int g = lane >> 2, t = lane & 3;
+        const int r0 = 16 * mt + g, c0 = 16 * ks + 2 * t;
+        auto pair = [&](int r, int c) {
+          return (uint32_t)half_bits(H(r, c)) | ((uint32_t)half_bits(H(r, c + 1)) << 16);
+        };
+        uint32_t* o = &out[((mt * 2 + ks) * 32 + lane) * 4];
+        o[0] = pair(r0, c0);
+        o[1] = pair(r0 + 8, c0);
+        o[2] = pair(r0, c0 + 8);
+        o[3] = pair(r0 + 8, c0 + 8);
+      }
+  return out;
+}
+
 std::mutex g_dev_mu;
 bool g_dev_ready[64];
 
@@ -155,6 +178,9 @@ cudaError_t ensure_device_tables() {
     auto f = bfrag(t.h28, 28, KS28, NT28);
     e = cudaMemcpyToSymbol(g_bfrag28, f.data(), f.size() * sizeof(uint32_t));
     if (e != cudaSuccess) return e;
+    auto a = afrag28(t.h28);
+    e = cudaMemcpyToSymbol(g_afrag28, a.data(), a.size() * sizeof(uint32_t));
+    if (e != cudaSuccess) return e;
   }
   if (t.ok172) {
     auto f = bfrag(t.h172, 172, KS172, NT172);
@@ -163,6 +189,12 @@ cudaError_t ensure_device_tables() {
   }
   g_dev_ready[dev & 63] = true;
   return cudaSuccess;
+}
+
+const uint32_t* device_afrag28() {
+  void* p = nullptr;
+  cudaGetSymbolAddress(&p, g_afrag28);
+  return static_cast<const uint32_t*>(p);
 }
 
 const uint32_t* device_bfrag_table(int m) {

@@ -23,7 +23,8 @@
 //    right by 8, exactly;
 //  * MMA warp (leader CTA, one thread): 4 x tcgen05.mma per k-block; tcgen05.commit
 //    multicasts the stage release to both CTAs;
-//  * 4 epilogue warps per CTA: tcgen05.ld 32x32b.x32, scale, round to fp16, store.
+//  * 8 epilogue warps per CTA (2 per TMEM lane quarter, one column half each): tcgen05.ld
+//    32x32b.x32 (next chunk in flight while the current one is stored), scale, fp16, store.
 // Shared-memory traffic per CTA per k-block: 16 KB TMA + 16 KB LDS + 16 KB STS + 16 KB MMA
 // read = 64 KB per 512 MMA cycles (125 B/clk at the full tensor rate, vs ~128 B/clk).
 // No thread ever holds a global load in flight across the proxy fence (whose MEMBAR would
@@ -51,12 +52,12 @@ constexpr int SA_BYTES = BMC * BKP;                 // 8 KB packed A
 constexpr int SB_BYTES = BNC * BKP;                 // 8 KB packed B
 constexpr int SSTAGE_BYTES = SA_BYTES + SB_BYTES;   // 16 KB
 constexpr int OB_BYTES = BNC * BK;                  // 16 KB widened B (SW128 K-major)
-constexpr int NUM_EPI_WARPS = 4;
-constexpr int A_WARP0 = 4;                          // warps 4..7
-constexpr int B_WARP0 = 8;                          // warps 8..11
-constexpr int TMA_WARP = 12;
-constexpr int MMA_WARP = 13;
-constexpr int NUM_THREADS = 14 * 32;
+constexpr int NUM_EPI_WARPS = 8;                    // warps 0..7: TMEM lane quarter w % 4, column half w / 4
+constexpr int A_WARP0 = 8;                          // warps 8..11
+constexpr int B_WARP0 = 12;                         // warps 12..15
+constexpr int TMA_WARP = 16;
+constexpr int MMA_WARP = 17;
+constexpr int NUM_THREADS = 18 * 32;
 constexpr int TMEM_COLS = 512;
 constexpr int ACC_COL = 0;                          // accumulator: columns [0, 256)
 constexpr int A_COL0 = 256;                         // A stages: 32 columns each
@@ -308,9 +309,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     }
     __syncwarp();
   } else {
-    // ===================== epilogue warps 0..3 (each CTA: its 128 rows) =====================
+    // ===================== epilogue warps 0..7 (each CTA: its 128 rows) =====================
+    // warp w reads TMEM lanes 32 (w % 4) .. +31 (its rows) and columns 128 (w / 4) .. +127;
+    // the next 32-column chunk is loaded while the current one is converted and stored.
     const uint32_t tempty_leader = map_to_rank(t_empty, 0);
-    const int row_in_tile = (int)rank * BMC + warp * 32 + lane;
+    const int quarter = warp & 3, chalf = warp >> 2;
+    const int row_in_tile = (int)rank * BMC + quarter * 32 + lane;
     for (int tl = 0; tl < my_tiles; ++tl) {
       int mb, nb;
       tile_coords(p, pair + tl * num_pairs, mb, nb);
@@ -320,26 +324,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       const bool row_ok = m < p.M;
       float sx = 0.f;
       if (!kS32 && row_ok) sx = __ldg(p.x_scale + m);
-      const uint32_t taddr = tmem_base + ((uint32_t)(warp * 32) << 16) + ACC_COL;
-#pragma unroll 1
-      for (int cc = 0; cc < BN / 32; ++cc) {
-        uint32_t r[32];
-        QR_TMEM_LD32(taddr + (uint32_t)(cc * 32), r);
+      const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + ACC_COL + (uint32_t)(chalf * 128);
+      uint32_t r[2][32];
+      QR_TMEM_LD32(taddr, r[0]);
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
         tmem_ld_wait();
-        if (cc == BN / 32 - 1) {
+        if (cc + 1 < 4) {
+          QR_TMEM_LD32(taddr + (uint32_t)((cc + 1) * 32), r[(cc + 1) & 1]);
+        } else {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(tempty_leader);
         }
-        const int64_t n0 = (int64_t)nb * BN + cc * 32;
+        const uint32_t* rc = r[cc & 1];
+        const int64_t n0 = (int64_t)nb * BN + chalf * 128 + cc * 32;
         if (row_ok) {
           if constexpr (kS32) {
             int32_t* dst = reinterpret_cast<int32_t*>(p.out) + m * p.ld_out + n0;
 #pragma unroll
             for (int g = 0; g < 8; ++g) {
               if (n0 + g * 4 < p.N) {
-                int4 v = make_int4((int32_t)r[4 * g] >> 8, (int32_t)r[4 * g + 1] >> 8,
-                                   (int32_t)r[4 * g + 2] >> 8, (int32_t)r[4 * g + 3] >> 8);
+                int4 v = make_int4((int32_t)rc[4 * g] >> 8, (int32_t)rc[4 * g + 1] >> 8,
+                                   (int32_t)rc[4 * g + 2] >> 8, (int32_t)rc[4 * g + 3] >> 8);
                 *reinterpret_cast<int4*>(dst + g * 4) = v;
               }
             }
@@ -354,8 +361,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 uint32_t h[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                  const float v0 = ((float)((int32_t)r[8 * g + 2 * e] >> 8) * sx) * swv[2 * e];
-                  const float v1 = ((float)((int32_t)r[8 * g + 2 * e + 1] >> 8) * sx) * swv[2 * e + 1];
+                  const float v0 = ((float)((int32_t)rc[8 * g + 2 * e] >> 8) * sx) * swv[2 * e];
+                  const float v1 = ((float)((int32_t)rc[8 * g + 2 * e + 1] >> 8) * sx) * swv[2 * e + 1];
                   __half2 hv = __floats2half2_rn(v0, v1);
                   h[e] = *reinterpret_cast<uint32_t*>(&hv);
                 }

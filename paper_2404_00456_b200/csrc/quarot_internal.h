@@ -30,5 +30,7 @@ cudaError_t launch_kv_quant(const void* k, int64_t ld_k, const void* v, int64_t 
 const int8_t* base_hadamard_host(int m);  // nullptr for unsupported m
 cudaError_t ensure_device_tables();
 const uint32_t* device_bfrag_table(int m);  // device pointer (valid after ensure_device_tables)
+// H_28 as mma.sync A fragments [mt][ks][lane][4] (rows b, cols b'), for hq_full28_kernel
+const uint32_t* device_afrag28();
 
 }  // namespace qr

@@ -73,6 +73,18 @@ def main():
         byts = 2 * T * 8 * (2 * d + d // 2 + 5) + T * 64 * d * 4
         res["kv"] = {"ms": ms, "gbs": byts / ms / 1e6, "frac_hbm": byts / ms / 1e6 / 6536}
         print("kv", json.dumps(res["kv"]), flush=True)
+    if "intmm" in a.what:
+        # library INT8 reference: cuBLASLt via torch._int_mm, 8192^3 (denominator context)
+        A = torch.randint(-7, 8, (8192, 8192), dtype=torch.int8, device=dev)
+        B = torch.randint(-7, 8, (8192, 8192), dtype=torch.int8, device=dev)
+        ms = timeit(lambda: torch._int_mm(A, B), a.iters)
+        res["cublaslt_int8_8192"] = {"ms": ms, "tops": 2 * 8192**3 / ms / 1e9}
+        print("intmm", json.dumps(res["cublaslt_int8_8192"]), flush=True)
+        Ab = A.to(torch.bfloat16)
+        Bb = B.to(torch.bfloat16)
+        ms = timeit(lambda: Ab @ Bb, a.iters)
+        res["cublas_bf16_8192"] = {"ms": ms, "tflops": 2 * 8192**3 / ms / 1e9}
+        print("bf16", json.dumps(res["cublas_bf16_8192"]), flush=True)
     print(json.dumps(res))
 
 
