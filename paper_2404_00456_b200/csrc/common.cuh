@@ -128,4 +128,42 @@ QR_DEVICE void sts_v4(uint32_t addr, uint4 v) {
                : "memory");
 }
 
+// ---------------------------------------------------------------- packed fp32x2 (sm_100)
+QR_DEVICE float2 f2add(float2 a, float2 b) {
+  float2 r;
+  asm("{\n\t.reg .b64 ra, rb, rc;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
+      "add.rn.f32x2 rc, ra, rb;\n\tmov.b64 {%0,%1}, rc;\n\t}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+QR_DEVICE float2 f2sub(float2 a, float2 b) {
+  float2 r;
+  asm("{\n\t.reg .b64 ra, rb, rc;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
+      "sub.rn.f32x2 rc, ra, rb;\n\tmov.b64 {%0,%1}, rc;\n\t}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+QR_DEVICE float2 f2fma(float2 a, float2 b, float2 cc) {
+  float2 r;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
+      "mov.b64 rc, {%6,%7};\n\tfma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0,%1}, rd;\n\t}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(cc.x), "f"(cc.y));
+  return r;
+}
+QR_DEVICE float2 f2mul(float2 a, float2 b) {
+  float2 r;
+  asm("{\n\t.reg .b64 ra, rb, rc;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
+      "mul.rn.f32x2 rc, ra, rb;\n\tmov.b64 {%0,%1}, rc;\n\t}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+// byte = nib(rne(clamp(v.x * inv))) | nib(rne(clamp(v.y * inv))) << 4; RNE via 1.5 * 2^23
+QR_DEVICE uint32_t quant_pair(float2 v, float inv) {
+  float2 m = f2mul(v, make_float2(inv, inv));
+  m.x = fminf(fmaxf(m.x, -7.f), 7.f);
+  m.y = fminf(fmaxf(m.y, -7.f), 7.f);
+  m = f2add(m, make_float2(12582912.f, 12582912.f));
+  return (__float_as_uint(m.x) & 0xFu) | ((__float_as_uint(m.y) & 0xFu) << 4);
+}
+
 }  // namespace qr

@@ -103,12 +103,14 @@ __global__ void __launch_bounds__(128) hq_none_kernel(const __half* __restrict__
 }
 
 // ------------------------------------------------------------------ ACROSS_HEADS
-// Thread (p, g): column pair j = 2p, 2p+1 of head_dim, heads h = g*HPT + r, r < HPT.
-// Lane = g + G * p_lo: the FWHT over r runs in registers, over g with warp shuffles.
+// Thread (p, g): column pair j = 2p, 2p+1 of head_dim (one float2), heads h = g*HPT + r.
+// Lane = g + G * p_lo: the FWHT over r runs in registers on fp32x2 pairs (FADD2), over g
+// with warp shuffles (G <= 2 for the Llama head counts: at most one shuffle stage).
 template <int HPT, int G>
-__global__ void hq_heads_kernel(const __half* __restrict__ x, int64_t K, int64_t ld_x, int head_dim, float clip,
-                                uint8_t* __restrict__ q, int64_t ld_q, float* __restrict__ scale) {
-  extern __shared__ uint8_t sh_bytes[];  // K/2 packed bytes + reduction scratch
+__global__ void __launch_bounds__(128) hq_heads_kernel(const __half* __restrict__ x, int64_t K, int64_t ld_x,
+                                                       int head_dim, float clip, uint8_t* __restrict__ q,
+                                                       int64_t ld_q, float* __restrict__ scale) {
+  extern __shared__ __align__(16) uint8_t sh_bytes[];  // K/2 packed bytes + reduction scratch
   float* red = reinterpret_cast<float*>(sh_bytes + (K >> 1));
   const int64_t row = blockIdx.x;
   const int lane = threadIdx.x & 31;
@@ -116,46 +118,38 @@ __global__ void hq_heads_kernel(const __half* __restrict__ x, int64_t K, int64_t
   const int p = (threadIdx.x / 32) * (32 / G) + lane / G;  // column pair index
   const int P2 = head_dim >> 1;
   const __half* xr = x + row * ld_x;
-  float v0[HPT], v1[HPT];
+  float2 v[HPT];
   const bool active = p < P2;
 #pragma unroll
   for (int r = 0; r < HPT; ++r) {
     const int h = g * HPT + r;
-    float2 f = make_float2(0.f, 0.f);
-    if (active) f = __half22float2(*reinterpret_cast<const __half2*>(xr + (int64_t)h * head_dim + 2 * p));
-    v0[r] = f.x;
-    v1[r] = f.y;
+    v[r] = active ? __half22float2(__ldg(reinterpret_cast<const __half2*>(xr + (int64_t)h * head_dim + 2 * p)))
+                  : make_float2(0.f, 0.f);
   }
-  // in-register butterflies over r (low bits of h)
 #pragma unroll
   for (int st = 1; st < HPT; st <<= 1) {
 #pragma unroll
     for (int r = 0; r < HPT; ++r) {
       if (!(r & st)) {
-        const float a0 = v0[r], b0 = v0[r + st], a1 = v1[r], b1 = v1[r + st];
-        v0[r] = a0 + b0;
-        v0[r + st] = a0 - b0;
-        v1[r] = a1 + b1;
-        v1[r + st] = a1 - b1;
+        const float2 a = v[r], b = v[r + st];
+        v[r] = f2add(a, b);
+        v[r + st] = f2sub(a, b);
       }
     }
   }
-  // shuffle butterflies over g (high bits of h)
 #pragma unroll
   for (int st = 1; st < G; st <<= 1) {
-    const bool upper = (g & st) != 0;
+    const float sg = (g & st) ? -1.f : 1.f;
 #pragma unroll
     for (int r = 0; r < HPT; ++r) {
-      const float o0 = __shfl_xor_sync(0xffffffffu, v0[r], st);
-      const float o1 = __shfl_xor_sync(0xffffffffu, v1[r], st);
-      v0[r] = upper ? (o0 - v0[r]) : (v0[r] + o0);
-      v1[r] = upper ? (o1 - v1[r]) : (v1[r] + o1);
+      const float o0 = __shfl_xor_sync(0xffffffffu, v[r].x, st);
+      const float o1 = __shfl_xor_sync(0xffffffffu, v[r].y, st);
+      v[r] = f2fma(make_float2(sg, sg), v[r], make_float2(o0, o1));  // lower: v + o, upper: o - v
     }
   }
   float amax = 0.f;
 #pragma unroll
-  for (int r = 0; r < HPT; ++r) amax = fmax_nan(amax, fmax_nan(fabsf(v0[r]), fabsf(v1[r])));
-  // block reduce (variable warp count)
+  for (int r = 0; r < HPT; ++r) amax = fmax_nan(amax, fmax_nan(fabsf(v[r].x), fabsf(v[r].y)));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) amax = fmax_nan(amax, __shfl_xor_sync(0xffffffffu, amax, o));
   const int nwarps = blockDim.x >> 5;
@@ -171,7 +165,7 @@ __global__ void hq_heads_kernel(const __half* __restrict__ x, int64_t K, int64_t
 #pragma unroll
     for (int r = 0; r < HPT; ++r) {
       const int h = g * HPT + r;
-      sh_bytes[h * P2 + p] = (uint8_t)(nib(code_of(v0[r], inv)) | (nib(code_of(v1[r], inv)) << 4));
+      sh_bytes[h * P2 + p] = inv != 0.f ? (uint8_t)quant_pair(v[r], inv) : (uint8_t)0;
     }
   }
   __syncthreads();
@@ -385,36 +379,6 @@ constexpr int OUT_BYTES = K / 2;     // 14336 (aliases Z after phase 2 has read 
 constexpr size_t SMEM = XS_BYTES + Z_BYTES + 256;
 }  // namespace f28
 
-QR_DEVICE float2 f2add(float2 a, float2 b) {
-  float2 r;
-  asm("{\n\t.reg .b64 ra, rb, rc;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
-      "add.rn.f32x2 rc, ra, rb;\n\tmov.b64 {%0,%1}, rc;\n\t}"
-      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
-  return r;
-}
-QR_DEVICE float2 f2sub(float2 a, float2 b) {
-  float2 r;
-  asm("{\n\t.reg .b64 ra, rb, rc;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
-      "sub.rn.f32x2 rc, ra, rb;\n\tmov.b64 {%0,%1}, rc;\n\t}"
-      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
-  return r;
-}
-QR_DEVICE float2 f2mul(float2 a, float2 b) {
-  float2 r;
-  asm("{\n\t.reg .b64 ra, rb, rc;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
-      "mul.rn.f32x2 rc, ra, rb;\n\tmov.b64 {%0,%1}, rc;\n\t}"
-      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
-  return r;
-}
-// byte = nib(rne(clamp(v.x * inv))) | nib(rne(clamp(v.y * inv))) << 4; RNE via 1.5 * 2^23
-QR_DEVICE uint32_t quant_pair(float2 v, float inv) {
-  float2 m = f2mul(v, make_float2(inv, inv));
-  m.x = fminf(fmaxf(m.x, -7.f), 7.f);
-  m.y = fminf(fmaxf(m.y, -7.f), 7.f);
-  m = f2add(m, make_float2(12582912.f, 12582912.f));
-  return (__float_as_uint(m.x) & 0xFu) | ((__float_as_uint(m.y) & 0xFu) << 4);
-}
-
 __global__ void __launch_bounds__(f28::NT, 1)
     hq_full28_kernel(const __half* __restrict__ x, int64_t M, int64_t ld_x, float clip, uint8_t* __restrict__ q,
                      int64_t ld_q, float* __restrict__ scale, const uint32_t* __restrict__ afrag) {
@@ -608,12 +572,13 @@ cudaError_t launch_hq_heads(const void* x, int64_t M, int64_t K, int64_t ld_x, i
   const int n_h = (int)(K / head_dim);
   const int P2 = head_dim / 2;
   const __half* xh = static_cast<const __half*>(x);
-  // G groups of heads per column pair; HPT = n_h / G heads per thread (<= 16 in registers)
-  int G = n_h > 16 ? n_h / 16 : 1;
-  if (G > 32) return cudaErrorInvalidValue;
+  // G groups of heads per column pair; HPT = n_h / G heads per thread (<= 32 in registers)
+  const int G = n_h > 32 ? n_h / 32 : 1;
+  if (G > 16) return cudaErrorInvalidValue;
   const int HPT = n_h / G;
   int threads = P2 * G;
   threads = ((threads + 31) / 32) * 32;
+  if (threads > 128) return cudaErrorInvalidValue;
   const size_t smem = (size_t)(K / 2) + 64 * sizeof(float);
   const dim3 grid((unsigned)M);
 #define QR_HEADS(H, GG) \
@@ -625,14 +590,14 @@ cudaError_t launch_hq_heads(const void* x, int64_t M, int64_t K, int64_t ld_x, i
         case 2: QR_HEADS(2, 1); break;
         case 4: QR_HEADS(4, 1); break;
         case 8: QR_HEADS(8, 1); break;
-        default: QR_HEADS(16, 1); break;
+        case 16: QR_HEADS(16, 1); break;
+        default: QR_HEADS(32, 1); break;
       }
       break;
-    case 2: QR_HEADS(16, 2); break;
-    case 4: QR_HEADS(16, 4); break;
-    case 8: QR_HEADS(16, 8); break;
-    case 16: QR_HEADS(16, 16); break;
-    default: QR_HEADS(16, 32); break;
+    case 2: QR_HEADS(32, 2); break;
+    case 4: QR_HEADS(32, 4); break;
+    case 8: QR_HEADS(32, 8); break;
+    default: QR_HEADS(32, 16); break;
   }
 #undef QR_HEADS
   return cudaPeekAtLastError();

@@ -15,168 +15,189 @@
 namespace qr {
 namespace kvq {
 
-QR_DEVICE float warp_min(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-QR_DEVICE float warp_max(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
+// Layout of the work: the (token, group) pairs of one launch are flattened,
+// f = t * G + g with G = 2 n_kv + n_q groups per token (K heads, V heads, Q heads); each group
+// of head_dim elements is held by LPG = head_dim / 32 consecutive lanes, 32 elements per lane
+// (four 16-byte loads), so a warp processes 32 / LPG groups at once.  The Walsh-Hadamard
+// butterflies run on bits 0-4 of the element index in registers (fp32x2 where the pairs line
+// up) and on the log2(LPG) lane bits with shuffles.
+constexpr int EPL = 32;  // elements per lane
 
-template <int E>
-QR_DEVICE void fwht_warp(float (&v)[E], int lane) {
+QR_DEVICE void fwht32_regs(float (&v)[EPL]) {
 #pragma unroll
-  for (int st = 1; st < E; st <<= 1) {
+  for (int j = 0; j < EPL; j += 2) {  // index bit 0
+    const float a = v[j], b = v[j + 1];
+    v[j] = a + b;
+    v[j + 1] = a - b;
+  }
 #pragma unroll
-    for (int j = 0; j < E; ++j) {
+  for (int st = 2; st < EPL; st <<= 1) {  // index bits 1..4, as fp32x2 pairs
+#pragma unroll
+    for (int j = 0; j < EPL; j += 2) {
       if (!(j & st)) {
-        const float a = v[j], b = v[j + st];
-        v[j] = a + b;
-        v[j + st] = a - b;
+        const float2 a = make_float2(v[j], v[j + 1]), b = make_float2(v[j + st], v[j + st + 1]);
+        const float2 s = f2add(a, b), d = f2sub(a, b);
+        v[j] = s.x;
+        v[j + 1] = s.y;
+        v[j + st] = d.x;
+        v[j + st + 1] = d.y;
       }
     }
   }
+}
+
+template <int LPG>
+QR_DEVICE void fwht_lanes(float (&v)[EPL], int sub) {
 #pragma unroll
-  for (int st = 1; st < 32; st <<= 1) {
-    const bool upper = (lane & st) != 0;
+  for (int st = 1; st < LPG; st <<= 1) {
+    const float sg = (sub & st) ? -1.f : 1.f;
 #pragma unroll
-    for (int j = 0; j < E; ++j) {
-      const float o = __shfl_xor_sync(0xffffffffu, v[j], st);
-      v[j] = upper ? (o - v[j]) : (v[j] + o);
+    for (int j = 0; j < EPL; j += 2) {
+      const float o0 = __shfl_xor_sync(0xffffffffu, v[j], st);
+      const float o1 = __shfl_xor_sync(0xffffffffu, v[j + 1], st);
+      const float2 r = f2fma(make_float2(sg, sg), make_float2(v[j], v[j + 1]), make_float2(o0, o1));
+      v[j] = r.x;
+      v[j + 1] = r.y;
     }
   }
 }
 
-template <int E>
-QR_DEVICE void load_half(const __half* p, float (&v)[E]) {
-  if constexpr (E == 8) {
-    const uint4 u = *reinterpret_cast<const uint4*>(p);
-    const __half2* h = reinterpret_cast<const __half2*>(&u);
+template <int LPG>
+QR_DEVICE float group_min(float x) {
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float2 f = __half22float2(h[e]);
-      v[2 * e] = f.x;
-      v[2 * e + 1] = f.y;
-    }
-  } else if constexpr (E == 4) {
-    const uint2 u = *reinterpret_cast<const uint2*>(p);
-    const __half2* h = reinterpret_cast<const __half2*>(&u);
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const float2 f = __half22float2(h[e]);
-      v[2 * e] = f.x;
-      v[2 * e + 1] = f.y;
-    }
-  } else {
-    const float2 f = __half22float2(*reinterpret_cast<const __half2*>(p));
-    v[0] = f.x;
-    v[1] = f.y;
-  }
+  for (int o = 1; o < LPG; o <<= 1) x = fminf(x, __shfl_xor_sync(0xffffffffu, x, o));
+  return x;
 }
-
-// Asymmetric 4-bit quantization of one group held by the warp (unnormalized values v,
-// true values = v * norm).  Writes E/2 packed bytes per lane, scale and zero by lane 0.
-template <int E>
-QR_DEVICE void quant_group(const float (&v)[E], double norm, float clip, int lane, uint8_t* codes,
-                           float* scale_out, uint8_t* zero_out) {
-  float mn = v[0], mx = v[0];
-  bool finite = true;
+template <int LPG>
+QR_DEVICE float group_max(float x) {
 #pragma unroll
-  for (int j = 0; j < E; ++j) {
-    mn = fminf(mn, v[j]);
-    mx = fmaxf(mx, v[j]);
-    finite = finite && isfinite(v[j]);
-  }
-  mn = warp_min(mn);
-  mx = warp_max(mx);
-  finite = __all_sync(0xffffffffu, finite);
-  const double lo = (double)clip * (double)fminf(mn, 0.f) * norm;
-  const double hi = (double)clip * (double)fmaxf(mx, 0.f) * norm;
-  float s;
-  int z;
-  float inv;
-  if (!finite) {
-    s = __int_as_float(0x7fc00000);
-    z = 0;
-    inv = 0.f;
-  } else if (hi == lo) {
-    s = 1.f;
-    z = 0;
-    inv = 0.f;
-  } else {
-    s = (float)((hi - lo) / 15.0);
-    const double zr = rint(-lo / (double)s);
-    z = (int)(zr < 0.0 ? 0.0 : (zr > 15.0 ? 15.0 : zr));
-    inv = (float)(norm / (double)s);
-  }
-  uint32_t packed = 0;
-#pragma unroll
-  for (int j = 0; j < E; ++j) {
-    int c = __float2int_rn(v[j] * inv) + z;
-    c = c < 0 ? 0 : (c > 15 ? 15 : c);
-    if (inv == 0.f) c = 0;
-    packed |= (uint32_t)c << (4 * j);
-  }
-  if constexpr (E == 8) {
-    *reinterpret_cast<uint32_t*>(codes + lane * 4) = packed;
-  } else if constexpr (E == 4) {
-    *reinterpret_cast<uint16_t*>(codes + lane * 2) = (uint16_t)packed;
-  } else {
-    codes[lane] = (uint8_t)packed;
-  }
-  if (lane == 0) {
-    *scale_out = s;
-    *zero_out = (uint8_t)z;
-  }
+  for (int o = 1; o < LPG; o <<= 1) x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, o));
+  return x;
 }
-
-template <int E>
-__global__ void kv_quant_kernel(const __half* __restrict__ k, int64_t ld_k, const __half* __restrict__ v,
-                                int64_t ld_v, __half* q, int64_t ld_q, int64_t T, int n_kv, int n_q, uint32_t flags, float clip, uint8_t* __restrict__ k_codes,
-                                float* __restrict__ k_scale, uint8_t* __restrict__ k_zero,
-                                uint8_t* __restrict__ v_codes, float* __restrict__ v_scale,
-                                uint8_t* __restrict__ v_zero) {
-  constexpr int HD = 32 * E;
+template <int LPG>
+QR_DEVICE bool group_all(bool b) {
+  const unsigned m = __ballot_sync(0xffffffffu, b);
   const int lane = threadIdx.x & 31;
-  const int64_t per_tok = 2 * (int64_t)n_kv + n_q;
-  const int64_t total = T * per_tok;
-  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const unsigned gm = ((1u << LPG) - 1u) << (lane & ~(LPG - 1));
+  return (m & gm) == gm;
+}
+
+template <int LPG>
+__global__ void __launch_bounds__(256) kv_quant_kernel(const __half* __restrict__ k, int64_t ld_k,
+                                                       const __half* __restrict__ v, int64_t ld_v, __half* q,
+                                                       int64_t ld_q, int64_t T, int n_kv, int n_q, uint32_t flags,
+                                                       float clip, uint8_t* __restrict__ k_codes,
+                                                       float* __restrict__ k_scale, uint8_t* __restrict__ k_zero,
+                                                       uint8_t* __restrict__ v_codes, float* __restrict__ v_scale,
+                                                       uint8_t* __restrict__ v_zero) {
+  constexpr int HD = 32 * LPG;
+  constexpr int GPW = 32 / LPG;  // groups per warp
+  const int lane = threadIdx.x & 31;
+  const int sub = lane % LPG;
+  const int G = 2 * n_kv + n_q;
+  const int64_t total = T * G;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const double rnorm = rsqrt((double)HD);
-  for (int64_t task = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); task < total; task += wstride) {
-    const int64_t t = task / per_tok;
-    const int which = (int)(task - t * per_tok);
-    float x[E];
-    if (which < 2 * n_kv) {
-      const bool is_k = which < n_kv;
-      const int h = is_k ? which : which - n_kv;
-      const int64_t g = t * n_kv + h;
-      load_half<E>(is_k ? (k + t * ld_k + h * HD + lane * E) : (v + t * ld_v + h * HD + lane * E), x);
-      const bool rot = is_k ? (flags & 1u) : (flags & 2u);
-      if (rot) fwht_warp<E>(x, lane);
-      if (is_k)
-        quant_group<E>(x, rot ? rnorm : 1.0, clip, lane, k_codes + g * (HD / 2), k_scale + g, k_zero + g);
-      else
-        quant_group<E>(x, rot ? rnorm : 1.0, clip, lane, v_codes + g * (HD / 2), v_scale + g, v_zero + g);
-    } else {
-      const int h = which - 2 * n_kv;
-      __half* qp = q + t * ld_q + h * HD + lane * E;
-      load_half<E>(qp, x);
-      fwht_warp<E>(x, lane);
-      const float rn = (float)rnorm;
-      __half2 out[E / 2];
+  for (int64_t f0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * GPW; f0 < total;
+       f0 += nwarps * GPW) {
+    const int64_t f = f0 + lane / LPG;
+    const bool ok = f < total;
+    const int64_t t = ok ? f / G : 0;
+    const int which = ok ? (int)(f - t * G) : 0;
+    const bool is_k = which < n_kv, is_v = !is_k && which < 2 * n_kv, is_q = which >= 2 * n_kv;
+    const __half* src = is_k ? k + t * ld_k + which * HD
+                             : (is_v ? v + t * ld_v + (which - n_kv) * HD : q + t * ld_q + (which - 2 * n_kv) * HD);
+    src += sub * EPL;
+    float x[EPL];
+    if (ok) {
 #pragma unroll
-      for (int e = 0; e < E / 2; ++e) {
-        // product in fp64 then one rounding to fp16 would need fp64; fp32 product
-        // (|err| <= 2^-24 relative) then RNE to fp16 matches the oracle's fp16(H^ q) except
-        // at rare fp16 ties.
-        out[e] = __floats2half2_rn(x[2 * e] * rn, x[2 * e + 1] * rn);
+      for (int c = 0; c < 4; ++c) {
+        const uint4 u = __ldg(reinterpret_cast<const uint4*>(src) + c);
+        const __half2* h = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 ff = __half22float2(h[e]);
+          x[8 * c + 2 * e] = ff.x;
+          x[8 * c + 2 * e + 1] = ff.y;
+        }
       }
-      if constexpr (E == 8) *reinterpret_cast<uint4*>(qp) = *reinterpret_cast<uint4*>(out);
-      else if constexpr (E == 4) *reinterpret_cast<uint2*>(qp) = *reinterpret_cast<uint2*>(out);
-      else *reinterpret_cast<__half2*>(qp) = out[0];
+    } else {
+#pragma unroll
+      for (int j = 0; j < EPL; ++j) x[j] = 0.f;
+    }
+    const bool rot = is_q || (is_k && (flags & 1u)) || (is_v && (flags & 2u));
+    // rotation is group-uniform; shuffles need the whole warp, so every lane runs the
+    // butterflies and non-rotated groups discard the result
+    float y[EPL];
+#pragma unroll
+    for (int j = 0; j < EPL; ++j) y[j] = x[j];
+    fwht32_regs(y);
+    fwht_lanes<LPG>(y, sub);
+    if (rot) {
+#pragma unroll
+      for (int j = 0; j < EPL; ++j) x[j] = y[j];
+    }
+    // ---- K / V: asymmetric 4-bit group quantization (Z14), scale / zero per group
+    float mn = x[0], mx = x[0];
+    bool finite = true;
+#pragma unroll
+    for (int j = 0; j < EPL; ++j) {
+      mn = fminf(mn, x[j]);
+      mx = fmaxf(mx, x[j]);
+      finite = finite && isfinite(x[j]);
+    }
+    mn = group_min<LPG>(mn);
+    mx = group_max<LPG>(mx);
+    finite = group_all<LPG>(finite);
+    if (!ok) continue;
+    if (!is_q) {
+      const double norm = rot ? rnorm : 1.0;
+      const double lo = (double)clip * (double)fminf(mn, 0.f) * norm;
+      const double hi = (double)clip * (double)fmaxf(mx, 0.f) * norm;
+      float s = 1.f, inv = 0.f;
+      int z = 0;
+      if (!finite) {
+        s = __int_as_float(0x7fc00000);
+      } else if (hi != lo) {
+        s = (float)((hi - lo) / 15.0);
+        const double zr = rint(-lo / (double)s);
+        z = (int)(zr < 0.0 ? 0.0 : (zr > 15.0 ? 15.0 : zr));
+        inv = (float)(norm / (double)s);
+      }
+      uint32_t w[4] = {0u, 0u, 0u, 0u};
+      if (inv != 0.f) {
+        const float zf = (float)z;
+#pragma unroll
+        for (int j = 0; j < EPL; j += 2) {
+          // rne(x * inv) + z == rne(x * inv + z) (z integral); clamp to [0, 15]; magic-add RNE
+          float2 m = f2fma(make_float2(x[j], x[j + 1]), make_float2(inv, inv), make_float2(zf, zf));
+          m.x = fminf(fmaxf(m.x, 0.f), 15.f);
+          m.y = fminf(fmaxf(m.y, 0.f), 15.f);
+          m = f2add(m, make_float2(12582912.f, 12582912.f));
+          const uint32_t byte = (__float_as_uint(m.x) & 0xFu) | ((__float_as_uint(m.y) & 0xFu) << 4);
+          w[j >> 3] |= byte << (8 * ((j >> 1) & 3));
+        }
+      }
+      const int h = is_k ? which : which - n_kv;
+      const int64_t gi = t * n_kv + h;
+      uint8_t* codes = (is_k ? k_codes : v_codes) + gi * (HD / 2) + sub * (EPL / 2);
+      *reinterpret_cast<uint4*>(codes) = make_uint4(w[0], w[1], w[2], w[3]);
+      if (sub == 0) {
+        (is_k ? k_scale : v_scale)[gi] = s;
+        (is_k ? k_zero : v_zero)[gi] = (uint8_t)z;
+      }
+    } else {
+      // ---- Q: rotated in place, rounded to fp16 (Eq. 13)
+      const float rn = (float)rnorm;
+      __half* dst = const_cast<__half*>(src);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint4 u;
+        __half2* h = reinterpret_cast<__half2*>(&u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) h[e] = __floats2half2_rn(x[8 * c + 2 * e] * rn, x[8 * c + 2 * e + 1] * rn);
+        reinterpret_cast<uint4*>(dst)[c] = u;
+      }
     }
   }
 }
@@ -184,21 +205,24 @@ __global__ void kv_quant_kernel(const __half* __restrict__ k, int64_t ld_k, cons
 }  // namespace kvq
 
 cudaError_t launch_kv_quant(const void* k, int64_t ld_k, const void* v, int64_t ld_v, int64_t T, int n_kv,
-                            int head_dim, void* q, int64_t ld_q, int n_q, uint32_t flags, float clip, uint8_t* k_codes, float* k_scale, uint8_t* k_zero,
-                            uint8_t* v_codes, float* v_scale, uint8_t* v_zero, cudaStream_t stream) {
-  const int64_t groups = T * (2 * (int64_t)n_kv + (q ? n_q : 0));
+                            int head_dim, void* q, int64_t ld_q, int n_q, uint32_t flags, float clip,
+                            uint8_t* k_codes, float* k_scale, uint8_t* k_zero, uint8_t* v_codes, float* v_scale,
+                            uint8_t* v_zero, cudaStream_t stream) {
+  const int nq = q ? n_q : 0;
+  const int64_t groups = T * (2 * (int64_t)n_kv + nq);
   if (groups == 0) return cudaSuccess;
   const int threads = 256;
-  int64_t blocks = (groups + 7) / 8;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  const int nq = q ? n_q : 0;
+  const int lpg = head_dim / 32;
+  const int64_t warps_needed = (groups + (32 / lpg) - 1) / (32 / lpg);
+  int64_t blocks = (warps_needed + 7) / 8;
+  if (blocks > 148 * 8) blocks = 148 * 8;
   const __half* kh = static_cast<const __half*>(k);
   const __half* vh = static_cast<const __half*>(v);
   __half* qh = static_cast<__half*>(q);
-#define QR_KV(E)                                                                                              \
-  kvq::kv_quant_kernel<E><<<(unsigned)blocks, threads, 0, stream>>>(kh, ld_k, vh, ld_v, qh, ld_q, T, n_kv, nq, flags, clip,  \
-                                                                     k_codes, k_scale, k_zero, v_codes,     \
-                                                                     v_scale, v_zero)
+#define QR_KV(L)                                                                                              \
+  kvq::kv_quant_kernel<L><<<(unsigned)blocks, threads, 0, stream>>>(kh, ld_k, vh, ld_v, qh, ld_q, T, n_kv, nq,  \
+                                                                     flags, clip, k_codes, k_scale, k_zero,     \
+                                                                     v_codes, v_scale, v_zero)
   if (head_dim == 64) QR_KV(2);
   else if (head_dim == 128) QR_KV(4);
   else QR_KV(8);
