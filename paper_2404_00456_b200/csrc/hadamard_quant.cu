@@ -359,61 +359,68 @@ __global__ void hq_full_kernel(const __half* __restrict__ x, int64_t ld_x, int P
 // ------------------------------------------------------------------ FULL, K = 1024 x 28
 // The bench / 70B down_proj width, K = 28672: i = a*28 + b, a = a_hi*32 + a_lo (reading Z2),
 // y = (H_32[a_hi] (x) H_32[a_lo] (x) H_28[b]) x   (Sylvester H_1024 = H_32 (x) H_32, Eq. 1).
-// Persistent CTAs (one per SM, 512 threads); per row:
-//  0) cp.async.bulk copies the fp16 row (57 KB) into smem; the copy of the NEXT row is in
-//     flight during phase 2 of this one;
-//  1) warp w takes slabs a_hi = w, w + 16 (32 x 28 contiguous elements): H_28 on tensor cores
-//     (mma.sync m16n8k16, A = H_28 padded to 32, B = slab^T: exact +-1 x fp16 products, fp32
-//     accumulation), then H_32 over a_lo on the fp32 fragments: 3 butterfly stages in
-//     registers (a_lo bits 0, 3, 4) + 2 with warp shuffles (bits 1, 2); results to smem Z
-//     in natural order (conflict-free: word stride 56 across t, 1 across g);
-//  2) thread t < 448 owns (a_lo = t / 14, b = 2(t % 14), +1) for all 32 a_hi: 32 LDS.64,
-//     H_32 over a_hi with packed fp32x2 butterflies (FADD2), row amax (block reduce), RNE
-//     codes via the magic-number add, one packed byte per a_hi at byte a_hi*448 + t — staged
-//     in smem and written out with 16-byte stores.
+// Persistent CTAs (one per SM) with two warp groups working on consecutive rows, so the
+// tensor-core phase of row i+1 overlaps the quantization phase of row i:
+//  * P1 (8 warps): waits for the cp.async.bulk copy of the fp16 row (57 KB) in smem; each
+//    warp takes 4 slabs a_hi (32 x 28 contiguous elements): H_28 on tensor cores
+//    (mma.sync m16n8k16, A = H_28 padded to 32, B = slab^T: exact +-1 x fp16 products, fp32
+//    accumulation), then H_32 over a_lo on the fp32 fragments (3 butterfly stages in
+//    registers with FADD2, 2 with warp shuffles + FFMA2); results to the fp32 buffer Z in
+//    natural order (conflict-free: word stride 56 across t, 1 across g).  Then it issues
+//    the next row's bulk copy.
+//  * P2 (14 warps): thread t owns (a_lo = t / 14, b = 2 (t % 14), +1) for all 32 a_hi:
+//    32 LDS.64, releases Z to P1, H_32 over a_hi with FADD2, row amax (NaN-propagating,
+//    reduced over P2), RNE codes via the magic-number add, one packed byte per a_hi at
+//    byte a_hi * 448 + t — staged in smem and written out with 16-byte stores.
 namespace f28 {
-constexpr int MB = 28, P = 1024, K = MB * P, NT = 512;  // (M is the row count)
-constexpr int XS_BYTES = K * 2;      // 57344
+constexpr int MB = 28, P = 1024, K = MB * P;  // (M is the row count)
+constexpr int P1_WARPS = 8, P2_WARPS = 14, NT = (P1_WARPS + P2_WARPS) * 32;  // 704 threads
+constexpr int P2_THREADS = P2_WARPS * 32;                                     // 448 = 32 * 14
+constexpr int XS_BYTES = K * 2;      // 57344 per row buffer, double-buffered
 constexpr int Z_BYTES = K * 4;       // 114688
-constexpr int OUT_BYTES = K / 2;     // 14336 (aliases Z after phase 2 has read it)
-constexpr size_t SMEM = XS_BYTES + Z_BYTES + 256;
+constexpr int OUT_BYTES = K / 2;     // 14336
+constexpr size_t SMEM = 2 * XS_BYTES + Z_BYTES + 256;  // 229632 of the 232448 available
 }  // namespace f28
+
+QR_DEVICE void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 __global__ void __launch_bounds__(f28::NT, 1)
     hq_full28_kernel(const __half* __restrict__ x, int64_t M, int64_t ld_x, float clip, uint8_t* __restrict__ q,
                      int64_t ld_q, float* __restrict__ scale, const uint32_t* __restrict__ afrag) {
   using namespace f28;
   extern __shared__ __align__(128) uint8_t smem[];
-  uint8_t* xs = smem;                                        // fp16 row
-  float* Z = reinterpret_cast<float*>(smem + XS_BYTES);     // fp32 after phase 1
-  uint8_t* out = smem + XS_BYTES;                            // packed bytes, aliases Z
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + XS_BYTES + Z_BYTES);
-  float* red = reinterpret_cast<float*>(smem + XS_BYTES + Z_BYTES + 64);
+  uint8_t* xs0 = smem;                                              // fp16 rows [2]
+  float* Z = reinterpret_cast<float*>(smem + 2 * XS_BYTES);         // fp32 after phase 1
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * XS_BYTES + Z_BYTES);
+  uint64_t* xs_full = bars;       // [2]
+  uint64_t* z_full = bars + 2;
+  uint64_t* z_empty = bars + 3;
+  float* red = reinterpret_cast<float*>(bars + 4);  // [2][16]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane >> 2, t = lane & 3;
 
   if (threadIdx.x == 0) {
-    mbar_init(bar, 1);
+    mbar_init(&xs_full[0], 1);
+    mbar_init(&xs_full[1], 1);
+    mbar_init(z_full, P1_WARPS * 32);
+    mbar_init(z_empty, P2_THREADS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  auto issue_row = [&](int64_t row) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(XS_BYTES)
+  auto issue_row = [&](int64_t row, int buf) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&xs_full[buf])),
+                 "r"(XS_BYTES)
                  : "memory");
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(xs)),
-        "l"(x + row * ld_x), "r"(XS_BYTES), "r"(smem_u32(bar))
+            smem_u32(xs0 + buf * XS_BYTES)),
+        "l"(x + row * ld_x), "r"(XS_BYTES), "r"(smem_u32(&xs_full[buf]))
         : "memory");
   };
-  int64_t row = blockIdx.x;
-  if (threadIdx.x == 0 && row < M) issue_row(row);
-  uint32_t phase = 0;
-  const uint32_t* xw = reinterpret_cast<const uint32_t*>(xs);
-  for (; row < M; row += gridDim.x, phase ^= 1) {
-    // H_28 A fragments (2 m-tiles x 2 k-steps x 4 regs; L1-resident, reloaded per row so they
-    // do not occupy registers during phase 2)
-    uint32_t ha[2][2][4];
+
+  if (warp < P1_WARPS) {
+    // ======================= P1: bulk copy + H_28 (tensor cores) + H_32 over a_lo
+    const int g = lane >> 2, t = lane & 3;
+    uint32_t ha[2][2][4];  // H_28 A fragments (2 m-tiles x 2 k-steps x 4 regs)
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -424,87 +431,95 @@ __global__ void __launch_bounds__(f28::NT, 1)
         ha[mt][ks][2] = v.z;
         ha[mt][ks][3] = v.w;
       }
-    mbar_wait(bar, phase);
-    // ---------------- phase 1: H_28 (tensor cores) + H_32 over a_lo, per slab
+    if (threadIdx.x == 0) {  // prefetch the first two rows
+      if ((int64_t)blockIdx.x < M) issue_row(blockIdx.x, 0);
+      if ((int64_t)blockIdx.x + gridDim.x < M) issue_row(blockIdx.x + gridDim.x, 1);
+    }
+    int it = 0;
+    for (int64_t row = blockIdx.x; row < M; row += gridDim.x, ++it) {
+      const int buf = it & 1;
+      const uint32_t* xw = reinterpret_cast<const uint32_t*>(xs0 + buf * XS_BYTES);
+      mbar_wait(&xs_full[buf], (it >> 1) & 1);
+      mbar_wait(z_empty, (it & 1) ^ 1);
 #pragma unroll 1
-    for (int si = 0; si < 2; ++si) {
-      const int a_hi = warp + 16 * si;
-      float d[2][4][4];
+      for (int si = 0; si < 4; ++si) {
+        const int a_hi = warp + P1_WARPS * si;
+        float2 d[2][4][2];  // [mt][nt][h]: D1[b = 16 mt + g + 8 h][a_lo = 8 nt + 2 t + {0,1}]
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) {
-        const int a = a_hi * 32 + nt * 8 + g;  // B column n = g -> a_lo = 8 nt + g
-        const int wbase = a * (MB / 2);        // 14 words per chunk
-        uint32_t b[2][2];
-        b[0][0] = xw[wbase + t];
-        b[0][1] = xw[wbase + 4 + t];
-        b[1][0] = xw[wbase + 8 + t];
-        b[1][1] = (t < 2) ? xw[wbase + 12 + t] : 0u;
+        for (int nt = 0; nt < 4; ++nt) {
+          const int wbase = (a_hi * 32 + nt * 8 + g) * (MB / 2);  // B column n = g -> a_lo = 8 nt + g
+          uint32_t b[2][2];
+          b[0][0] = xw[wbase + t];
+          b[0][1] = xw[wbase + 4 + t];
+          b[1][0] = xw[wbase + 8 + t];
+          b[1][1] = (t < 2) ? xw[wbase + 12 + t] : 0u;
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-          d[mt][nt][0] = d[mt][nt][1] = d[mt][nt][2] = d[mt][nt][3] = 0.f;
+          for (int mt = 0; mt < 2; ++mt) {
+            float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-          for (int ks = 0; ks < 2; ++ks) mma_16816(d[mt][nt], ha[mt][ks], b[ks][0], b[ks][1]);
-        }
-      }
-      // d[mt][nt][e + 2h] = D1[b = 16 mt + g + 8 h][a_lo = 8 nt + 2 t + e]
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt) {  // a_lo bit 0 (register pair)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const float u = d[mt][nt][2 * h], v = d[mt][nt][2 * h + 1];
-            d[mt][nt][2 * h] = u + v;
-            d[mt][nt][2 * h + 1] = u - v;
+            for (int ks = 0; ks < 2; ++ks) mma_16816(acc, ha[mt][ks], b[ks][0], b[ks][1]);
+            // a_lo bit 0 lives inside the register pair
+            d[mt][nt][0] = make_float2(acc[0] + acc[1], acc[0] - acc[1]);
+            d[mt][nt][1] = make_float2(acc[2] + acc[3], acc[2] - acc[3]);
           }
         }
 #pragma unroll
-        for (int st = 1; st < 4; st <<= 1) {  // a_lo bits 3, 4 (n-tile index)
+        for (int mt = 0; mt < 2; ++mt) {
 #pragma unroll
-          for (int nt = 0; nt < 4; ++nt) {
-            if (!(nt & st)) {
+          for (int st = 1; st < 4; st <<= 1) {  // a_lo bits 3, 4 (n-tile index)
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float u = d[mt][nt][e], v = d[mt][nt + st][e];
-                d[mt][nt][e] = u + v;
-                d[mt][nt + st][e] = u - v;
+            for (int nt = 0; nt < 4; ++nt) {
+              if (!(nt & st)) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                  const float2 u = d[mt][nt][h], v = d[mt][nt + st][h];
+                  d[mt][nt][h] = f2add(u, v);
+                  d[mt][nt + st][h] = f2sub(u, v);
+                }
               }
             }
           }
-        }
 #pragma unroll
-        for (int st = 1; st < 4; st <<= 1) {  // a_lo bits 1, 2 (lane bits of t)
-          const float sg = (t & st) ? -1.f : 1.f;
+          for (int st = 1; st < 4; st <<= 1) {  // a_lo bits 1, 2 (lane bits of t)
+            const float sg = (t & st) ? -1.f : 1.f;
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const float ox = __shfl_xor_sync(0xffffffffu, d[mt][nt][h].x, st);
+                const float oy = __shfl_xor_sync(0xffffffffu, d[mt][nt][h].y, st);
+                d[mt][nt][h] = f2fma(make_float2(sg, sg), d[mt][nt][h], make_float2(ox, oy));
+              }
+          }
 #pragma unroll
           for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float o = __shfl_xor_sync(0xffffffffu, d[mt][nt][e], st);
-              d[mt][nt][e] = fmaf(sg, d[mt][nt][e], o);  // lower: v + o, upper: o - v
+            for (int h = 0; h < 2; ++h) {
+              const int bb = 16 * mt + g + 8 * h;
+              const int a = a_hi * 32 + nt * 8 + 2 * t;
+              if (bb < MB) {
+                Z[a * MB + bb] = d[mt][nt][h].x;
+                Z[(a + 1) * MB + bb] = d[mt][nt][h].y;
+              }
             }
         }
-        // store D1 rows b < 28 to Z in natural order
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int bb = 16 * mt + g + 8 * (e >> 1);
-            const int a = a_hi * 32 + nt * 8 + 2 * t + (e & 1);
-            if (bb < MB) Z[a * MB + bb] = d[mt][nt][e];
-          }
       }
+      mbar_arrive(z_full);
+      named_bar(1, P1_WARPS * 32);  // every P1 thread is done reading xs[buf]
+      if (threadIdx.x == 0 && row + 2 * (int64_t)gridDim.x < M) issue_row(row + 2 * (int64_t)gridDim.x, buf);
     }
-    __syncthreads();
-    // xs is free: start the next row's copy while this one finishes
-    if (threadIdx.x == 0 && row + gridDim.x < M) issue_row(row + gridDim.x);
-    // ---------------- phase 2: H_32 over a_hi (packed fp32x2), amax, codes
-    const bool active = threadIdx.x < 448;
-    float2 v[32];
-    float amax = 0.f;
-    if (active) {
-      const float2* zp = reinterpret_cast<const float2*>(Z) + threadIdx.x;  // (a_lo*28 + 2j) / 2 == t
+  } else {
+    // ======================= P2: H_32 over a_hi, amax, codes, packed output
+    const int tp = threadIdx.x - P1_WARPS * 32;  // 0..447
+    const int w2 = warp - P1_WARPS;
+    int it = 0;
+    for (int64_t row = blockIdx.x; row < M; row += gridDim.x, ++it) {
+      mbar_wait(z_full, it & 1);
+      float2 v[32];
+      const float2* zp = reinterpret_cast<const float2*>(Z) + tp;  // (a_lo * 28 + 2 j) / 2 == tp
 #pragma unroll
       for (int ah = 0; ah < 32; ++ah) v[ah] = zp[ah * 448];
+      mbar_arrive(z_empty);
 #pragma unroll
       for (int st = 1; st < 32; st <<= 1) {
 #pragma unroll
@@ -516,33 +531,31 @@ __global__ void __launch_bounds__(f28::NT, 1)
           }
         }
       }
+      float am[4] = {0.f, 0.f, 0.f, 0.f};  // 4 independent max chains
 #pragma unroll
-      for (int ah = 0; ah < 32; ++ah) amax = fmax_nan(amax, fmax_nan(fabsf(v[ah].x), fabsf(v[ah].y)));
-    }
+      for (int ah = 0; ah < 32; ++ah) am[ah & 3] = fmax_nan(am[ah & 3], fmax_nan(fabsf(v[ah].x), fabsf(v[ah].y)));
+      float amax = fmax_nan(fmax_nan(am[0], am[1]), fmax_nan(am[2], am[3]));
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) amax = fmax_nan(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-    if (lane == 0) red[warp] = amax;
-    __syncthreads();  // also: every thread has read its Z values -> Z may be overwritten
-    amax = red[0];
+      for (int o = 16; o > 0; o >>= 1) amax = fmax_nan(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      if (lane == 0) red[(it & 1) * 16 + w2] = amax;  // double-buffered: no barrier needed after the read
+      named_bar(2, P2_THREADS);
+      amax = red[(it & 1) * 16];
 #pragma unroll
-    for (int w = 1; w < NT / 32; ++w) amax = fmax_nan(amax, red[w]);
-    float s, inv;
-    row_scale(amax, rsqrt((double)K), clip, s, inv);
-    if (threadIdx.x == 0) scale[row] = s;
-    if (active) {
+      for (int w = 1; w < P2_WARPS; ++w) amax = fmax_nan(amax, red[(it & 1) * 16 + w]);
+      float s, inv;
+      row_scale(amax, rsqrt((double)K), clip, s, inv);
+      if (tp == 0) scale[row] = s;
+      // packed byte of (a_hi, a_lo, b-pair) lands at a_hi * 448 + tp: a warp writes 32
+      // consecutive bytes per a_hi (one full sector)
+      uint8_t* qr = q + row * ld_q + tp;
       if (inv != 0.f) {
 #pragma unroll
-        for (int ah = 0; ah < 32; ++ah) out[ah * 448 + threadIdx.x] = (uint8_t)quant_pair(v[ah], inv);
+        for (int ah = 0; ah < 32; ++ah) qr[ah * 448] = (uint8_t)quant_pair(v[ah], inv);
       } else {
 #pragma unroll
-        for (int ah = 0; ah < 32; ++ah) out[ah * 448 + threadIdx.x] = 0;
+        for (int ah = 0; ah < 32; ++ah) qr[ah * 448] = 0;
       }
     }
-    __syncthreads();
-    uint8_t* qr = q + row * ld_q;
-    for (int i = threadIdx.x; i < OUT_BYTES / 16; i += NT)
-      *reinterpret_cast<uint4*>(qr + i * 16) = reinterpret_cast<const uint4*>(out)[i];
-    __syncthreads();  // out (= Z) is rewritten by the next row's phase 1
   }
 }
 
