@@ -38,6 +38,24 @@ QR_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(addr, parity)) {
   }
 }
+// try_wait with a suspend-time hint: the waiting warp sleeps (until the phase completes or the
+// hint elapses) instead of spinning, so idle roles do not steal issue slots from busy ones.
+QR_DEVICE bool mbar_try_wait_sleep(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity), "r"(1000000u)
+      : "memory");
+  return ok != 0;
+}
+QR_DEVICE void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  while (!mbar_try_wait_sleep(addr, parity)) {
+  }
+}
 
 // ---------------------------------------------------------------- proxy fences
 // generic-proxy st.shared -> async-proxy (tcgen05.mma operand) visibility
@@ -84,6 +102,13 @@ QR_DEVICE void mma_commit(uint64_t* bar) {
         "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),    \
         "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),    \
         "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                                             \
+      : "r"(taddr))
+#define QR_TMEM_LD16(taddr, r)                                                                        \
+  asm volatile(                                                                                       \
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),           \
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),       \
+        "=r"(r[14]), "=r"(r[15])                                                                       \
       : "r"(taddr))
 QR_DEVICE void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 

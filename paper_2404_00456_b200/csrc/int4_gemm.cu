@@ -46,18 +46,18 @@ constexpr int BN = 256;            // pair tile cols (128 B rows per CTA)
 constexpr int BNC = 128;
 constexpr int BK = 128;            // int8 elements per k-block
 constexpr int BKP = BK / 2;        // packed bytes per row per k-block
-constexpr int SSTAGES = 8;         // packed staging ring (TMA destination)
-constexpr int OSTAGES = 4;         // widened operand ring (TMEM A + smem B)
+constexpr int SSTAGES = 6;         // packed staging ring (TMA destination)
+constexpr int OSTAGES = 7;         // widened operand ring (TMEM A: 7 x 32 columns + smem B)
 constexpr int SA_BYTES = BMC * BKP;                 // 8 KB packed A
 constexpr int SB_BYTES = BNC * BKP;                 // 8 KB packed B
 constexpr int SSTAGE_BYTES = SA_BYTES + SB_BYTES;   // 16 KB
 constexpr int OB_BYTES = BNC * BK;                  // 16 KB widened B (SW128 K-major)
 constexpr int NUM_EPI_WARPS = 8;                    // warps 0..7: TMEM lane quarter w % 4, column half w / 4
 constexpr int A_WARP0 = 8;                          // warps 8..11
-constexpr int B_WARP0 = 12;                         // warps 12..15
-constexpr int TMA_WARP = 16;
-constexpr int MMA_WARP = 17;
-constexpr int NUM_THREADS = 18 * 32;
+constexpr int B_WARP0 = 12;                         // warps 12..19: two groups of 4, alternating k-blocks
+constexpr int TMA_WARP = 20;
+constexpr int MMA_WARP = 21;
+constexpr int NUM_THREADS = 22 * 32;
 constexpr int TMEM_COLS = 512;
 constexpr int ACC_COL = 0;                          // accumulator: columns [0, 256)
 constexpr int A_COL0 = 256;                         // A stages: 32 columns each
@@ -144,7 +144,7 @@ QR_DEVICE void mma_commit_pair(uint64_t* bar) {
       "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])                      \
       : "memory")
 
-template <bool kS32>
+template <bool kS32, int kDbg = 0>  // kDbg: 0 normal; roofline probes: 1 MMA only, 2 no widening, 3 no TMA
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     int4_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const Params p) {
@@ -197,7 +197,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   const int my_tiles = (p.num_tiles > pair) ? (p.num_tiles - 1 - pair) / num_pairs + 1 : 0;
   const int total = my_tiles * p.num_kb;
 
-  if (warp == TMA_WARP) {
+  constexpr bool kMmaOnly = kDbg == 1;
+  if (kMmaOnly && warp != MMA_WARP && warp >= NUM_EPI_WARPS) {
+    // roofline probe: no producers
+  } else if (warp == TMA_WARP) {
     // ===================== TMA producer: packed k-blocks -> staging ring =====================
     if (lane == 0) {
       for (int it = 0; it < total; ++it) {
@@ -206,11 +209,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         int mb, nb;
         tile_coords(p, pair + tl * num_pairs, mb, nb);
         const int s = it % SSTAGES;
-        mbar_wait(&st_empty[s], ((it / SSTAGES) & 1) ^ 1);
-        mbar_expect_tx(&st_full[s], SSTAGE_BYTES);
-        const uint32_t dst = smem_u32(stage_smem + s * SSTAGE_BYTES);
-        tma_load_2d(dst, &tmA, kb * BKP, mb * BM + (int)rank * BMC, &st_full[s]);
-        tma_load_2d(dst + SA_BYTES, &tmB, kb * BKP, nb * BN + (int)rank * BNC, &st_full[s]);
+        mbar_wait_sleep(&st_empty[s], ((it / SSTAGES) & 1) ^ 1);
+        if (kDbg == 3) {
+          mbar_arrive(&st_full[s]);
+        } else {
+          mbar_expect_tx(&st_full[s], SSTAGE_BYTES);
+          const uint32_t dst = smem_u32(stage_smem + s * SSTAGE_BYTES);
+          tma_load_2d(dst, &tmA, kb * BKP, mb * BM + (int)rank * BMC, &st_full[s]);
+          tma_load_2d(dst + SA_BYTES, &tmB, kb * BKP, nb * BN + (int)rank * BNC, &st_full[s]);
+        }
       }
     }
   } else if (warp >= A_WARP0 && warp < A_WARP0 + 4) {
@@ -222,7 +229,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     for (int it = 0; it < total; ++it) {
       const int s = it % SSTAGES;
       const int o = it % OSTAGES;
-      mbar_wait(&st_full[s], (it / SSTAGES) & 1);
+      mbar_wait_sleep(&st_full[s], (it / SSTAGES) & 1);
       const uint32_t src = smem_u32(stage_smem + s * SSTAGE_BYTES) + (uint32_t)row * BKP;
       uint4 w[4];
 #pragma unroll
@@ -241,22 +248,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&st_empty[s]);
-      mbar_wait(&op_empty[o], ((it / OSTAGES) & 1) ^ 1);
+      mbar_wait_sleep(&op_empty[o], ((it / OSTAGES) & 1) ^ 1);
       tc_fence_after();
-      QR_TMEM_ST32(tmem_base + tlane + (uint32_t)(A_COL0 + 32 * o), r);
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      if (kDbg != 2) {
+        QR_TMEM_ST32(tmem_base + tlane + (uint32_t)(A_COL0 + 32 * o), r);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(opfull_leader + (uint32_t)o * 8u);
     }
-  } else if (warp >= B_WARP0 && warp < B_WARP0 + 4) {
+  } else if (warp >= B_WARP0 && warp < B_WARP0 + 8) {
     // ===================== B widen: packed smem -> int8 SW128 smem =====================
-    const int t = threadIdx.x - B_WARP0 * 32;  // 0..127
+    // two groups of 4 warps take alternate k-blocks, so one group's proxy fence (a MEMBAR
+    // that drains its STS) overlaps the other group's loads and stores
+    const int grp = (warp - B_WARP0) >> 2;
+    const int t = threadIdx.x - (B_WARP0 + 4 * grp) * 32;  // 0..127
     const uint32_t opfull_leader = map_to_rank(&op_full[0], 0);
-    for (int it = 0; it < total; ++it) {
+    for (int it = grp; it < total; it += 2) {
       const int s = it % SSTAGES;
       const int o = it % OSTAGES;
-      mbar_wait(&st_full[s], (it / SSTAGES) & 1);
+      mbar_wait_sleep(&st_full[s], (it / SSTAGES) & 1);
       const uint32_t src = smem_u32(stage_smem + s * SSTAGE_BYTES) + SA_BYTES;
       uint4 w[4];
 #pragma unroll
@@ -267,10 +279,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&st_empty[s]);
-      mbar_wait(&op_empty[o], ((it / OSTAGES) & 1) ^ 1);
+      mbar_wait_sleep(&op_empty[o], ((it / OSTAGES) & 1) ^ 1);
       const uint32_t dbase = smem_u32(opb_smem + o * OB_BYTES);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < (kDbg == 2 ? 0 : 4); ++i) {
         const int c = t + 128 * i;
         const int rr = c >> 2, q = c & 3;
         const uint32_t rowb = dbase + (uint32_t)(rr >> 3) * 1024u + (uint32_t)(rr & 7) * 128u;
@@ -293,8 +305,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + ACC_COL;
         for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
-          const int o = it % OSTAGES;
-          mbar_wait(&op_full[o], (it / OSTAGES) & 1);
+          const int o = kMmaOnly ? 0 : it % OSTAGES;
+          if (!kMmaOnly) mbar_wait(&op_full[o], (it / OSTAGES) & 1);
           tc_fence_after();
           const uint64_t b_desc = umma_desc_sw128(smem_u32(opb_smem + o * OB_BYTES));
           const uint32_t a_tmem = tmem_base + (uint32_t)(A_COL0 + 32 * o);
@@ -302,7 +314,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           for (int k = 0; k < BK / 32; ++k)
             mma_i8_ts_2sm(d_tmem, a_tmem + (uint32_t)(8 * k), b_desc + (uint64_t)(2 * k), IDESC,
                           (kb | k) != 0 ? 1u : 0u);
-          mma_commit_pair(&op_empty[o]);
+          if (!kMmaOnly) mma_commit_pair(&op_empty[o]);
         }
         mma_commit_pair(t_full);
       }
@@ -318,32 +330,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     for (int tl = 0; tl < my_tiles; ++tl) {
       int mb, nb;
       tile_coords(p, pair + tl * num_pairs, mb, nb);
-      mbar_wait(t_full, tl & 1);
+      mbar_wait_sleep(t_full, tl & 1);
       tc_fence_after();
       const int64_t m = (int64_t)mb * BM + row_in_tile;
       const bool row_ok = m < p.M;
       float sx = 0.f;
       if (!kS32 && row_ok) sx = __ldg(p.x_scale + m);
       const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + ACC_COL + (uint32_t)(chalf * 128);
-      uint32_t r[2][32];
-      QR_TMEM_LD32(taddr, r[0]);
+      uint32_t r[2][16];
+      QR_TMEM_LD16(taddr, r[0]);
 #pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {
+      for (int cc = 0; cc < 8; ++cc) {
         tmem_ld_wait();
-        if (cc + 1 < 4) {
-          QR_TMEM_LD32(taddr + (uint32_t)((cc + 1) * 32), r[(cc + 1) & 1]);
+        if (cc + 1 < 8) {
+          QR_TMEM_LD16(taddr + (uint32_t)((cc + 1) * 16), r[(cc + 1) & 1]);
         } else {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(tempty_leader);
         }
         const uint32_t* rc = r[cc & 1];
-        const int64_t n0 = (int64_t)nb * BN + chalf * 128 + cc * 32;
+        const int64_t n0 = (int64_t)nb * BN + chalf * 128 + cc * 16;
         if (row_ok) {
           if constexpr (kS32) {
             int32_t* dst = reinterpret_cast<int32_t*>(p.out) + m * p.ld_out + n0;
 #pragma unroll
-            for (int g = 0; g < 8; ++g) {
+            for (int g = 0; g < 4; ++g) {
               if (n0 + g * 4 < p.N) {
                 int4 v = make_int4((int32_t)rc[4 * g] >> 8, (int32_t)rc[4 * g + 1] >> 8,
                                    (int32_t)rc[4 * g + 2] >> 8, (int32_t)rc[4 * g + 3] >> 8);
@@ -353,7 +365,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           } else {
             __half* dst = reinterpret_cast<__half*>(p.out) + m * p.ld_out + n0;
 #pragma unroll
-            for (int g = 0; g < 4; ++g) {
+            for (int g = 0; g < 2; ++g) {
               if (n0 + g * 8 < p.N) {
                 const float4 s0 = __ldg(reinterpret_cast<const float4*>(p.w_scale + n0 + g * 8));
                 const float4 s1 = __ldg(reinterpret_cast<const float4*>(p.w_scale + n0 + g * 8 + 4));
@@ -432,6 +444,8 @@ bool make_packed_map(CUtensorMap* map, const uint8_t* base, int64_t rows, int64_
 
 }  // namespace
 
+int g_gemm_debug_mode = 0;
+
 template <bool kS32>
 static cudaError_t launch_gemm_impl(const uint8_t* xq, const float* xs, int64_t M, int64_t K, int64_t ld_xq,
                                     const uint8_t* wq, const float* ws, int64_t N, int64_t ld_wq, void* out,
@@ -463,9 +477,20 @@ static cudaError_t launch_gemm_impl(const uint8_t* xq, const float* xs, int64_t 
   p.num_tiles = p.num_m * p.num_n;
   const int max_pairs = num_sms_current() / 2;
   const int pairs = p.num_tiles < max_pairs ? p.num_tiles : max_pairs;
-  int4_gemm_kernel<kS32><<<2 * pairs, NUM_THREADS, SMEM_BYTES, stream>>>(ma, mb, p);
+  if (g_gemm_debug_mode >= 1 && g_gemm_debug_mode <= 3) {
+    auto kern = g_gemm_debug_mode == 1 ? int4_gemm_kernel<kS32, 1>
+                                        : (g_gemm_debug_mode == 2 ? int4_gemm_kernel<kS32, 2> : int4_gemm_kernel<kS32, 3>);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    kern<<<2 * pairs, NUM_THREADS, SMEM_BYTES, stream>>>(ma, mb, p);
+  } else {
+    int4_gemm_kernel<kS32><<<2 * pairs, NUM_THREADS, SMEM_BYTES, stream>>>(ma, mb, p);
+  }
   return cudaPeekAtLastError();
 }
+
+// Debug / roofline probe (not in the public header): mode 1 = MMA issue only.
+extern "C" void quarot_debug_gemm_mode(int mode) { g_gemm_debug_mode = mode; }
 
 cudaError_t launch_int4_gemm(const uint8_t* xq, const float* xs, int64_t M, int64_t K, int64_t ld_xq,
                              const uint8_t* wq, const float* ws, int64_t N, int64_t ld_wq, void* y,

@@ -38,6 +38,22 @@ def main():
     M = a.tokens
     dev = "cuda"
     res = {}
+    if "gemm_mmaonly" in a.what:
+        # roofline probe: the same kernel with producers disabled (MMA issue rate only)
+        import ctypes
+        q.lib().quarot_debug_gemm_mode.argtypes = [ctypes.c_int]
+        xq = synth.packed_weight_codes(M, 8192, 1, dev)
+        N, K = 57344, 8192
+        wq = synth.packed_weight_codes(N, K, 2, dev)
+        xs = torch.rand(M, device=dev) + 0.5
+        ws = synth.weight_scales(N, 3, dev)
+        y = torch.empty(M, N, dtype=torch.float16, device=dev)
+        for mode, name in ((0, "normal"), (1, "mma_only"), (2, "no_widen_stores"), (3, "no_tma")):
+            q.lib().quarot_debug_gemm_mode(mode)
+            ms = timeit(lambda: q.int4_linear(xq, xs, wq, ws, y=y), a.iters)
+            res["gate_up_" + name] = {"ms": ms, "tops": 2 * M * N * K / ms / 1e9}
+            print(name, json.dumps(res["gate_up_" + name]), flush=True)
+        q.lib().quarot_debug_gemm_mode(0)
     if "gemm" in a.what:
         xq_big = synth.packed_weight_codes(M, 28672, 1, dev)
         for name, N, K in (("qkv", 10240, 8192), ("o", 8192, 8192), ("gate_up", 57344, 8192), ("down", 8192, 28672)):
