@@ -374,7 +374,7 @@ __global__ void hq_full_kernel(const __half* __restrict__ x, int64_t ld_x, int P
 //    byte a_hi * 448 + t — staged in smem and written out with 16-byte stores.
 namespace f28 {
 constexpr int MB = 28, P = 1024, K = MB * P;  // (M is the row count)
-constexpr int P1_WARPS = 8, P2_WARPS = 14, NT = (P1_WARPS + P2_WARPS) * 32;  // 704 threads
+constexpr int P1_WARPS = 16, P2_WARPS = 14, NT = (P1_WARPS + 16) * 32;  // 1024 threads: P2 = 4 warpgroups (2 idle warps)
 constexpr int P2_THREADS = P2_WARPS * 32;                                     // 448 = 32 * 14
 constexpr int XS_BYTES = K * 2;      // 57344 per row buffer, double-buffered
 constexpr int Z_BYTES = K * 4;       // 114688
@@ -419,18 +419,19 @@ __global__ void __launch_bounds__(f28::NT, 1)
 
   if (warp < P1_WARPS) {
     // ======================= P1: bulk copy + H_28 (tensor cores) + H_32 over a_lo
+    // warp w owns m-tile mt = w & 1 (b rows 16 mt .. 16 mt + 15) of slabs a_hi = w / 2 + 8 i
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 48;");
     const int g = lane >> 2, t = lane & 3;
-    uint32_t ha[2][2][4];  // H_28 A fragments (2 m-tiles x 2 k-steps x 4 regs)
+    const int mt = warp & 1;
+    uint32_t ha[2][4];  // H_28 A fragments of this m-tile (2 k-steps x 4 regs)
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-      for (int ks = 0; ks < 2; ++ks) {
-        const uint4 v = __ldg(reinterpret_cast<const uint4*>(afrag) + ((mt * 2 + ks) * 32 + lane));
-        ha[mt][ks][0] = v.x;
-        ha[mt][ks][1] = v.y;
-        ha[mt][ks][2] = v.z;
-        ha[mt][ks][3] = v.w;
-      }
+    for (int ks = 0; ks < 2; ++ks) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(afrag) + ((mt * 2 + ks) * 32 + lane));
+      ha[ks][0] = v.x;
+      ha[ks][1] = v.y;
+      ha[ks][2] = v.z;
+      ha[ks][3] = v.w;
+    }
     if (threadIdx.x == 0) {  // prefetch the first two rows
       if ((int64_t)blockIdx.x < M) issue_row(blockIdx.x, 0);
       if ((int64_t)blockIdx.x + gridDim.x < M) issue_row(blockIdx.x + gridDim.x, 1);
@@ -439,70 +440,61 @@ __global__ void __launch_bounds__(f28::NT, 1)
     for (int64_t row = blockIdx.x; row < M; row += gridDim.x, ++it) {
       const int buf = it & 1;
       const uint32_t* xw = reinterpret_cast<const uint32_t*>(xs0 + buf * XS_BYTES);
-      mbar_wait(&xs_full[buf], (it >> 1) & 1);
-      mbar_wait(z_empty, (it & 1) ^ 1);
+      mbar_wait_sleep(&xs_full[buf], (it >> 1) & 1);
+      mbar_wait_sleep(z_empty, (it & 1) ^ 1);
 #pragma unroll 1
       for (int si = 0; si < 4; ++si) {
-        const int a_hi = warp + P1_WARPS * si;
-        float2 d[2][4][2];  // [mt][nt][h]: D1[b = 16 mt + g + 8 h][a_lo = 8 nt + 2 t + {0,1}]
+        const int a_hi = (warp >> 1) + 8 * si;
+        float2 d[4][2];  // [nt][h]: D1[b = 16 mt + g + 8 h][a_lo = 8 nt + 2 t + {0,1}]
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt) {
           const int wbase = (a_hi * 32 + nt * 8 + g) * (MB / 2);  // B column n = g -> a_lo = 8 nt + g
-          uint32_t b[2][2];
-          b[0][0] = xw[wbase + t];
-          b[0][1] = xw[wbase + 4 + t];
-          b[1][0] = xw[wbase + 8 + t];
-          b[1][1] = (t < 2) ? xw[wbase + 12 + t] : 0u;
-#pragma unroll
-          for (int mt = 0; mt < 2; ++mt) {
-            float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-            for (int ks = 0; ks < 2; ++ks) mma_16816(acc, ha[mt][ks], b[ks][0], b[ks][1]);
-            // a_lo bit 0 lives inside the register pair
-            d[mt][nt][0] = make_float2(acc[0] + acc[1], acc[0] - acc[1]);
-            d[mt][nt][1] = make_float2(acc[2] + acc[3], acc[2] - acc[3]);
-          }
+          const uint32_t b00 = xw[wbase + t], b01 = xw[wbase + 4 + t], b10 = xw[wbase + 8 + t];
+          const uint32_t b11 = (t < 2) ? xw[wbase + 12 + t] : 0u;
+          float acc[4] = {0.f, 0.f, 0.f, 0.f};
+          mma_16816(acc, ha[0], b00, b01);
+          mma_16816(acc, ha[1], b10, b11);
+          // a_lo bit 0 lives inside the register pair
+          d[nt][0] = make_float2(acc[0] + acc[1], acc[0] - acc[1]);
+          d[nt][1] = make_float2(acc[2] + acc[3], acc[2] - acc[3]);
         }
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
+        for (int st = 1; st < 4; st <<= 1) {  // a_lo bits 3, 4 (n-tile index)
 #pragma unroll
-          for (int st = 1; st < 4; st <<= 1) {  // a_lo bits 3, 4 (n-tile index)
+          for (int nt = 0; nt < 4; ++nt) {
+            if (!(nt & st)) {
 #pragma unroll
-            for (int nt = 0; nt < 4; ++nt) {
-              if (!(nt & st)) {
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                  const float2 u = d[mt][nt][h], v = d[mt][nt + st][h];
-                  d[mt][nt][h] = f2add(u, v);
-                  d[mt][nt + st][h] = f2sub(u, v);
-                }
+              for (int h = 0; h < 2; ++h) {
+                const float2 u = d[nt][h], v = d[nt + st][h];
+                d[nt][h] = f2add(u, v);
+                d[nt + st][h] = f2sub(u, v);
               }
             }
           }
+        }
 #pragma unroll
-          for (int st = 1; st < 4; st <<= 1) {  // a_lo bits 1, 2 (lane bits of t)
-            const float sg = (t & st) ? -1.f : 1.f;
-#pragma unroll
-            for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                const float ox = __shfl_xor_sync(0xffffffffu, d[mt][nt][h].x, st);
-                const float oy = __shfl_xor_sync(0xffffffffu, d[mt][nt][h].y, st);
-                d[mt][nt][h] = f2fma(make_float2(sg, sg), d[mt][nt][h], make_float2(ox, oy));
-              }
-          }
+        for (int st = 1; st < 4; st <<= 1) {  // a_lo bits 1, 2 (lane bits of t)
+          const float sg = (t & st) ? -1.f : 1.f;
 #pragma unroll
           for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-              const int bb = 16 * mt + g + 8 * h;
-              const int a = a_hi * 32 + nt * 8 + 2 * t;
-              if (bb < MB) {
-                Z[a * MB + bb] = d[mt][nt][h].x;
-                Z[(a + 1) * MB + bb] = d[mt][nt][h].y;
-              }
+              const float ox = __shfl_xor_sync(0xffffffffu, d[nt][h].x, st);
+              const float oy = __shfl_xor_sync(0xffffffffu, d[nt][h].y, st);
+              d[nt][h] = f2fma(make_float2(sg, sg), d[nt][h], make_float2(ox, oy));
             }
         }
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int bb = 16 * mt + g + 8 * h;
+            const int a = a_hi * 32 + nt * 8 + 2 * t;
+            if (bb < MB) {
+              Z[a * MB + bb] = d[nt][h].x;
+              Z[(a + 1) * MB + bb] = d[nt][h].y;
+            }
+          }
       }
       mbar_arrive(z_full);
       named_bar(1, P1_WARPS * 32);  // every P1 thread is done reading xs[buf]
@@ -510,11 +502,13 @@ __global__ void __launch_bounds__(f28::NT, 1)
     }
   } else {
     // ======================= P2: H_32 over a_hi, amax, codes, packed output
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 80;");  // 512*48 + 512*80 = 65536 = the launch allocation
+    if (warp >= P1_WARPS + P2_WARPS) return;  // padding warps of the last warpgroup
     const int tp = threadIdx.x - P1_WARPS * 32;  // 0..447
     const int w2 = warp - P1_WARPS;
     int it = 0;
     for (int64_t row = blockIdx.x; row < M; row += gridDim.x, ++it) {
-      mbar_wait(z_full, it & 1);
+      mbar_wait_sleep(z_full, it & 1);
       float2 v[32];
       const float2* zp = reinterpret_cast<const float2*>(Z) + tp;  // (a_lo * 28 + 2 j) / 2 == tp
 #pragma unroll
