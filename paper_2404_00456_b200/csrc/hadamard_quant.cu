@@ -175,6 +175,110 @@ __global__ void __launch_bounds__(128) hq_heads_kernel(const __half* __restrict_
     *reinterpret_cast<uint4*>(qr + (int64_t)i * 16) = reinterpret_cast<const uint4*>(sh_bytes)[i];
 }
 
+// Persistent variant (the bench path): each CTA streams rows; the fp16 row (2K bytes) is
+// bulk-copied into a double-buffered smem slot two rows ahead, so loads are asynchronous
+// and overlap the butterflies / quantization of the current row.
+template <int HPT, int G>
+__global__ void __launch_bounds__(128, 4) hq_heads_persist_kernel(const __half* __restrict__ x, int64_t M, int64_t K,
+                                                               int64_t ld_x, int head_dim, float clip,
+                                                               uint8_t* __restrict__ q, int64_t ld_q,
+                                                               float* __restrict__ scale) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int row_bytes = (int)(2 * K);
+  uint8_t* bufs = smem;                                                // [2][row_bytes]
+  uint8_t* out = smem + 2 * row_bytes;                                 // K/2 packed bytes
+  uint64_t* bars = reinterpret_cast<uint64_t*>(out + (K >> 1));        // [2]
+  float* red = reinterpret_cast<float*>(bars + 2);                     // [2][4]
+  const int lane = threadIdx.x & 31;
+  const int g = lane % G;
+  const int p = (threadIdx.x / 32) * (32 / G) + lane / G;
+  const int P2 = head_dim >> 1;
+  const bool active = p < P2;
+  const int nwarps = blockDim.x >> 5;
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](int64_t row, int b) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bars[b])), "r"(row_bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(bufs + b * row_bytes)),
+        "l"(x + row * ld_x), "r"(row_bytes), "r"(smem_u32(&bars[b]))
+        : "memory");
+  };
+  if (threadIdx.x == 0) {
+    if ((int64_t)blockIdx.x < M) issue(blockIdx.x, 0);
+    if ((int64_t)blockIdx.x + gridDim.x < M) issue(blockIdx.x + gridDim.x, 1);
+  }
+  const int n_h = (int)(K / head_dim);
+  const double norm = rsqrt((double)n_h);
+  int it = 0;
+  for (int64_t row = blockIdx.x; row < M; row += gridDim.x, ++it) {
+    const int b = it & 1;
+    mbar_wait_sleep(&bars[b], (it >> 1) & 1);
+    const __half* xr = reinterpret_cast<const __half*>(bufs + b * row_bytes);
+    float2 v[HPT];
+#pragma unroll
+    for (int r = 0; r < HPT; ++r) {
+      const int h = g * HPT + r;
+      v[r] = active ? __half22float2(*reinterpret_cast<const __half2*>(xr + h * head_dim + 2 * p))
+                    : make_float2(0.f, 0.f);
+    }
+    __syncthreads();  // buffer b fully read: refill it two rows ahead
+    if (threadIdx.x == 0 && row + 2 * (int64_t)gridDim.x < M) issue(row + 2 * (int64_t)gridDim.x, b);
+#pragma unroll
+    for (int st = 1; st < HPT; st <<= 1) {
+#pragma unroll
+      for (int r = 0; r < HPT; ++r) {
+        if (!(r & st)) {
+          const float2 a = v[r], c = v[r + st];
+          v[r] = f2add(a, c);
+          v[r + st] = f2sub(a, c);
+        }
+      }
+    }
+#pragma unroll
+    for (int st = 1; st < G; st <<= 1) {
+      const float sg = (g & st) ? -1.f : 1.f;
+#pragma unroll
+      for (int r = 0; r < HPT; ++r) {
+        const float o0 = __shfl_xor_sync(0xffffffffu, v[r].x, st);
+        const float o1 = __shfl_xor_sync(0xffffffffu, v[r].y, st);
+        v[r] = f2fma(make_float2(sg, sg), v[r], make_float2(o0, o1));
+      }
+    }
+    float am[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int r = 0; r < HPT; ++r) am[r & 3] = fmax_nan(am[r & 3], fmax_nan(fabsf(v[r].x), fabsf(v[r].y)));
+    float amax = fmax_nan(fmax_nan(am[0], am[1]), fmax_nan(am[2], am[3]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) amax = fmax_nan(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    if (lane == 0) red[b * 4 + (threadIdx.x >> 5)] = amax;
+    __syncthreads();
+    amax = red[b * 4];
+    for (int w = 1; w < nwarps; ++w) amax = fmax_nan(amax, red[b * 4 + w]);
+    float sc, inv;
+    row_scale(amax, norm, clip, sc, inv);
+    if (threadIdx.x == 0) scale[row] = sc;
+    if (active) {
+#pragma unroll
+      for (int r = 0; r < HPT; ++r) {
+        const int h = g * HPT + r;
+        out[h * P2 + p] = inv != 0.f ? (uint8_t)quant_pair(v[r], inv) : (uint8_t)0;
+      }
+    }
+    __syncthreads();
+    uint8_t* qr = q + row * ld_q;
+    const int nvec = (int)(K >> 5);
+    for (int i = threadIdx.x; i < nvec; i += blockDim.x)
+      *reinterpret_cast<uint4*>(qr + (int64_t)i * 16) = reinterpret_cast<const uint4*>(out)[i];
+  }
+}
+
 // ------------------------------------------------------------------ FULL
 // One row per CTA, staged in shared memory: X (fp16, K) and Z (fp32, K).
 //  1) copy x -> X (m > 1) or -> Z (m == 1);
@@ -586,10 +690,20 @@ cudaError_t launch_hq_heads(const void* x, int64_t M, int64_t K, int64_t ld_x, i
   int threads = P2 * G;
   threads = ((threads + 31) / 32) * 32;
   if (threads > 128) return cudaErrorInvalidValue;
-  const size_t smem = (size_t)(K / 2) + 64 * sizeof(float);
-  const dim3 grid((unsigned)M);
-#define QR_HEADS(H, GG) \
-  hq::hq_heads_kernel<H, GG><<<grid, threads, smem, stream>>>(xh, K, ld_x, head_dim, clip, q, ld_q, scale)
+  const size_t smem = (size_t)(2 * 2 * K) + (size_t)(K / 2) + 64;
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want = (int64_t)nsm * 6;
+  const dim3 grid((unsigned)(M < want ? M : want));
+#define QR_HEADS(H, GG)                                                                                         \
+  do {                                                                                                          \
+    cudaError_t ee = cudaFuncSetAttribute(hq::hq_heads_persist_kernel<H, GG>,                                   \
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);              \
+    if (ee != cudaSuccess) return ee;                                                                           \
+    hq::hq_heads_persist_kernel<H, GG><<<grid, threads, smem, stream>>>(xh, M, K, ld_x, head_dim, clip, q, ld_q, \
+                                                                        scale);                                 \
+  } while (0)
   switch (G) {
     case 1:
       switch (HPT) {
