@@ -65,6 +65,12 @@ typedef enum {
   QUAROT_HAD_ACROSS_HEADS = 2
 } quarot_had_mode;
 
+/* Mode flag (OR-ed into `mode`, NONE only): RMS-normalize each row first, x <- x / sqrt(mean(x^2)
+ * + 1e-5), in FP32 — the scale-free RMSNorm feeding "quantize" (Fig. ffn_quarot; reading
+ * Z21).  A positive per-row scaling leaves the codes unchanged, so the kernel quantizes x and
+ * divides the scale by the row RMS: one pass over x (SURVEY §8 a8 fused, f1). */
+#define QUAROT_HAD_RMSNORM 0x100
+
 /* Rows a1|a2 + a3 of the hot path: online Hadamard + per-token symmetric INT4 RTN + pack.
  *
  *   x      fp16 [M][ld_x] row-major (K used); 16-B aligned; ld_x % 8 == 0.
@@ -98,6 +104,14 @@ quarot_status quarot_int4_linear(const uint8_t* xq, const float* x_scale, int64_
                                  int64_t ld_xq, const uint8_t* wq, const float* w_scale,
                                  int64_t N, int64_t ld_wq, void* y, int64_t ld_y, void* stream);
 
+/* quarot_int4_linear with the residual add of the decoder layer fused into the epilogue
+ * (SURVEY §8 a8): y = fp16_rn( (fp32)acc * x_scale[m] * w_scale[n] + (fp32)residual[m][n] ).
+ *   residual fp16 [M][ld_r] (ld_r % 8 == 0, 16-B aligned); it may alias y (in-place add). */
+quarot_status quarot_int4_linear_residual(const uint8_t* xq, const float* x_scale, int64_t M, int64_t K,
+                                          int64_t ld_xq, const uint8_t* wq, const float* w_scale,
+                                          int64_t N, int64_t ld_wq, const void* residual, int64_t ld_r,
+                                          void* y, int64_t ld_y, void* stream);
+
 /* Parity only: the same tcgen05 mainloop, raw accumulators acc int32 [M][ld_acc]
  * (ld_acc % 4 == 0).  Same requirements as quarot_int4_linear. */
 quarot_status quarot_int4_matmul_s32(const uint8_t* xq, int64_t M, int64_t K, int64_t ld_xq,
@@ -126,6 +140,19 @@ quarot_status quarot_kv_quant(const void* k, int64_t ld_k, const void* v, int64_
                               float clip_ratio, uint8_t* k_codes, float* k_scale,
                               uint8_t* k_zero, uint8_t* v_codes, float* v_scale,
                               uint8_t* v_zero, void* stream);
+
+/* Decoder-layer glue.
+ * quarot_rope: Llama-2 rotary position embedding ("Pos", Eqs. 10-12), in place on
+ *   x fp16 [T][ld_x] holding n_heads x head_dim per token: for pair (i, i + d/2),
+ *   angle = pos * theta^(-2i/d), pos = (pos0 + t) % seq_len; fp32 math, fp16 RNE result.
+ *   head_dim even and <= 256; ld_x % 8 == 0; x 16-B aligned.  Apply it to the Q|K block of a
+ *   fused QKV output (n_heads = n_q + n_kv) before quarot_kv_quant.
+ * quarot_swiglu: act[m][f] = fp16(silu(gu[m][f]) * gu[m][F + f]) — the gated FFN activation of
+ *   Fig. ffn_orig with [gate | up] column halves; F % 8 == 0, ld % 8 == 0, 16-B aligned. */
+quarot_status quarot_rope(void* x, int64_t T, int32_t n_heads, int32_t head_dim, int64_t ld_x,
+                          int64_t pos0, int32_t seq_len, float theta, void* stream);
+quarot_status quarot_swiglu(const void* gate_up, int64_t M, int64_t F, int64_t ld_gu, void* act,
+                            int64_t ld_act, void* stream);
 
 /* Host-side utilities (no GPU work). */
 const char* quarot_status_string(int32_t status);

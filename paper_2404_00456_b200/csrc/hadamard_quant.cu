@@ -58,16 +58,19 @@ QR_DEVICE float block_max(float v, float* red) {
 
 // ------------------------------------------------------------------ NONE
 // One row per 128-thread CTA; each thread owns CPT 8-element chunks held in registers.
-template <int CPT>
+// kRms: the row is RMS-normalized first (scale-free RMSNorm): the codes of x / rms
+// equal the codes of x, so only the scale changes (scale / rms).
+template <int CPT, bool kRms>
 __global__ void __launch_bounds__(128) hq_none_kernel(const __half* __restrict__ x, int64_t K, int64_t ld_x,
                                                       float clip, uint8_t* __restrict__ q, int64_t ld_q,
                                                       float* __restrict__ scale) {
   __shared__ float red[4];
+  __shared__ float red2[4];
   const int64_t row = blockIdx.x;
   const int nchunk = (int)(K >> 3);
   const __half* xr = x + row * ld_x;
   uint4 v[CPT];
-  float amax = 0.f;
+  float amax = 0.f, ssq = 0.f;
 #pragma unroll
   for (int i = 0; i < CPT; ++i) {
     const int c = threadIdx.x + i * 128;
@@ -78,12 +81,23 @@ __global__ void __launch_bounds__(128) hq_none_kernel(const __half* __restrict__
       for (int e = 0; e < 4; ++e) {
         const float2 f = __half22float2(h[e]);
         amax = fmax_nan(amax, fmax_nan(fabsf(f.x), fabsf(f.y)));
+        if (kRms) ssq = fmaf(f.x, f.x, fmaf(f.y, f.y, ssq));
       }
     }
   }
-  amax = block_max<4>(amax, red);
+  double norm = 1.0;
+  if (kRms) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ssq += __shfl_xor_sync(0xffffffffu, ssq, o);
+    if ((threadIdx.x & 31) == 0) red2[threadIdx.x >> 5] = ssq;
+  }
+  amax = block_max<4>(amax, red);  // (its __syncthreads also publishes red2)
+  if (kRms) {
+    const double tot = (double)red2[0] + (double)red2[1] + (double)red2[2] + (double)red2[3];
+    norm = 1.0 / sqrt(tot / (double)K + 1e-5);
+  }
   float s, inv;
-  row_scale(amax, 1.0, clip, s, inv);
+  row_scale(amax, norm, clip, s, inv);
   if (threadIdx.x == 0) scale[row] = s;
   uint8_t* qr = q + row * ld_q;
 #pragma unroll
@@ -662,12 +676,16 @@ __global__ void __launch_bounds__(f28::NT, 1)
 // ------------------------------------------------------------------ launchers
 
 cudaError_t launch_hq_none(const void* x, int64_t M, int64_t K, int64_t ld_x, float clip, uint8_t* q,
-                           int64_t ld_q, float* scale, cudaStream_t stream) {
+                           int64_t ld_q, float* scale, cudaStream_t stream, bool rmsnorm) {
   const int64_t nchunk = K / 8;
   const int cpt = (int)((nchunk + 127) / 128);
   const dim3 grid((unsigned)M);
   const __half* xh = static_cast<const __half*>(x);
-#define QR_NONE(C) hq::hq_none_kernel<C><<<grid, 128, 0, stream>>>(xh, K, ld_x, clip, q, ld_q, scale)
+#define QR_NONE(C)                                                                               \
+  do {                                                                                           \
+    if (rmsnorm) hq::hq_none_kernel<C, true><<<grid, 128, 0, stream>>>(xh, K, ld_x, clip, q, ld_q, scale);  \
+    else hq::hq_none_kernel<C, false><<<grid, 128, 0, stream>>>(xh, K, ld_x, clip, q, ld_q, scale);        \
+  } while (0)
   if (cpt <= 1) QR_NONE(1);
   else if (cpt <= 2) QR_NONE(2);
   else if (cpt <= 4) QR_NONE(4);

@@ -69,7 +69,8 @@ struct Params {
   const float* x_scale;
   const float* w_scale;
   void* out;  // fp16 y or int32 acc
-  int64_t M, N, K, ld_out;
+  const __half* residual;  // optional fp16 residual added in the epilogue (decoder layer, a8)
+  int64_t M, N, K, ld_out, ld_r;
   int num_m, num_n, num_kb, num_tiles;  // num_m in 256-row pair tiles
 };
 
@@ -371,10 +372,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 const float4 s1 = __ldg(reinterpret_cast<const float4*>(p.w_scale + n0 + g * 8 + 4));
                 const float swv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
                 uint32_t h[4];
+                uint4 rres = make_uint4(0, 0, 0, 0);
+                if (p.residual) rres = *reinterpret_cast<const uint4*>(p.residual + m * p.ld_r + n0 + g * 8);
+                const __half2* r2 = reinterpret_cast<const __half2*>(&rres);
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                  const float v0 = ((float)((int32_t)rc[8 * g + 2 * e] >> 8) * sx) * swv[2 * e];
-                  const float v1 = ((float)((int32_t)rc[8 * g + 2 * e + 1] >> 8) * sx) * swv[2 * e + 1];
+                  float v0 = ((float)((int32_t)rc[8 * g + 2 * e] >> 8) * sx) * swv[2 * e];
+                  float v1 = ((float)((int32_t)rc[8 * g + 2 * e + 1] >> 8) * sx) * swv[2 * e + 1];
+                  if (p.residual) {
+                    const float2 rf = __half22float2(r2[e]);
+                    v0 += rf.x;
+                    v1 += rf.y;
+                  }
                   __half2 hv = __floats2half2_rn(v0, v1);
                   h[e] = *reinterpret_cast<uint32_t*>(&hv);
                 }
@@ -449,7 +458,8 @@ int g_gemm_debug_mode = 0;
 template <bool kS32>
 static cudaError_t launch_gemm_impl(const uint8_t* xq, const float* xs, int64_t M, int64_t K, int64_t ld_xq,
                                     const uint8_t* wq, const float* ws, int64_t N, int64_t ld_wq, void* out,
-                                    int64_t ld_out, cudaStream_t stream) {
+                                    int64_t ld_out, cudaStream_t stream, const void* residual = nullptr,
+                                    int64_t ld_r = 0) {
   using namespace gemm;
   static bool attr_set[64] = {};
   int dev = 0;
@@ -467,6 +477,8 @@ static cudaError_t launch_gemm_impl(const uint8_t* xq, const float* xs, int64_t 
   p.x_scale = xs;
   p.w_scale = ws;
   p.out = out;
+  p.residual = static_cast<const __half*>(residual);
+  p.ld_r = ld_r;
   p.M = M;
   p.N = N;
   p.K = K;
@@ -494,8 +506,8 @@ extern "C" void quarot_debug_gemm_mode(int mode) { g_gemm_debug_mode = mode; }
 
 cudaError_t launch_int4_gemm(const uint8_t* xq, const float* xs, int64_t M, int64_t K, int64_t ld_xq,
                              const uint8_t* wq, const float* ws, int64_t N, int64_t ld_wq, void* y,
-                             int64_t ld_y, cudaStream_t stream) {
-  return launch_gemm_impl<false>(xq, xs, M, K, ld_xq, wq, ws, N, ld_wq, y, ld_y, stream);
+                             int64_t ld_y, cudaStream_t stream, const void* residual, int64_t ld_r) {
+  return launch_gemm_impl<false>(xq, xs, M, K, ld_xq, wq, ws, N, ld_wq, y, ld_y, stream, residual, ld_r);
 }
 
 cudaError_t launch_int4_gemm_s32(const uint8_t* xq, int64_t M, int64_t K, int64_t ld_xq, const uint8_t* wq,

@@ -62,7 +62,10 @@ quarot_status quarot_hadamard_quant(const void* x, int64_t M, int64_t K, int64_t
                                     int32_t head_dim, float clip_ratio, uint8_t* q, int64_t ld_q, float* scale,
                                     void* stream) {
   g_last_launches = 0;
+  const bool rms = (mode & QUAROT_HAD_RMSNORM) != 0;
+  mode &= ~QUAROT_HAD_RMSNORM;
   if (mode < QUAROT_HAD_NONE || mode > QUAROT_HAD_ACROSS_HEADS) return QUAROT_ERR_ARG;
+  if (rms && mode != QUAROT_HAD_NONE) return QUAROT_ERR_ARG;
   if (!clip_ok(clip_ratio)) return QUAROT_ERR_ARG;
   if (M < 0 || K <= 0 || (K & 1) || ld_x < K || ld_q < K / 2) return QUAROT_ERR_DIM;
   if (M > 0x7fffffffLL) return QUAROT_ERR_DIM;
@@ -75,7 +78,7 @@ quarot_status quarot_hadamard_quant(const void* x, int64_t M, int64_t K, int64_t
   if (mode == QUAROT_HAD_NONE) {
     if (K % 16) return QUAROT_ERR_ALIGN;
     if (K > 32768) return QUAROT_ERR_UNSUPPORTED_SIZE;
-    e = qr::launch_hq_none(x, M, K, ld_x, clip_ratio, q, ld_q, scale, st);
+    e = qr::launch_hq_none(x, M, K, ld_x, clip_ratio, q, ld_q, scale, st, rms);
   } else if (mode == QUAROT_HAD_ACROSS_HEADS) {
     if (head_dim <= 0 || K % head_dim) return QUAROT_ERR_DIM;
     if (!pow2(head_dim) || head_dim < 64 || !pow2(K / head_dim) || K / head_dim > 512)
@@ -121,6 +124,52 @@ quarot_status quarot_int4_linear(const uint8_t* xq, const float* x_scale, int64_
   if (!aligned16(w_scale)) return QUAROT_ERR_ALIGN;
   cudaError_t e = qr::launch_int4_gemm(xq, x_scale, M, K, ld_xq, wq, w_scale, N, ld_wq, y, ld_y,
                                        static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return QUAROT_ERR_CUDA;
+  g_last_launches = 1;
+  return QUAROT_OK;
+}
+
+quarot_status quarot_int4_linear_residual(const uint8_t* xq, const float* x_scale, int64_t M, int64_t K,
+                                          int64_t ld_xq, const uint8_t* wq, const float* w_scale, int64_t N,
+                                          int64_t ld_wq, const void* residual, int64_t ld_r, void* y, int64_t ld_y,
+                                          void* stream) {
+  g_last_launches = 0;
+  quarot_status s = check_gemm(xq, M, K, ld_xq, wq, N, ld_wq, y, ld_y, 8);
+  if (s != QUAROT_OK || M == 0) return s;
+  if (!x_scale || !w_scale || !residual) return QUAROT_ERR_NULL;
+  if (ld_r < N) return QUAROT_ERR_DIM;
+  if (!aligned16(w_scale) || !aligned16(residual) || (ld_r % 8)) return QUAROT_ERR_ALIGN;
+  cudaError_t e = qr::launch_int4_gemm(xq, x_scale, M, K, ld_xq, wq, w_scale, N, ld_wq, y, ld_y,
+                                       static_cast<cudaStream_t>(stream), residual, ld_r);
+  if (e != cudaSuccess) return QUAROT_ERR_CUDA;
+  g_last_launches = 1;
+  return QUAROT_OK;
+}
+
+quarot_status quarot_rope(void* x, int64_t T, int32_t n_heads, int32_t head_dim, int64_t ld_x, int64_t pos0,
+                          int32_t seq_len, float theta, void* stream) {
+  g_last_launches = 0;
+  if (T < 0 || n_heads <= 0 || head_dim <= 0 || seq_len <= 0 || pos0 < 0) return QUAROT_ERR_DIM;
+  if (head_dim % 16 || head_dim > 256) return QUAROT_ERR_UNSUPPORTED_SIZE;
+  if (ld_x < (int64_t)n_heads * head_dim) return QUAROT_ERR_DIM;
+  if (!(theta > 1.f)) return QUAROT_ERR_ARG;
+  if (T == 0) return QUAROT_OK;
+  if (!x) return QUAROT_ERR_NULL;
+  if (!aligned16(x) || (ld_x % 8)) return QUAROT_ERR_ALIGN;
+  cudaError_t e = qr::launch_rope(x, T, n_heads, head_dim, ld_x, pos0, seq_len, theta, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return QUAROT_ERR_CUDA;
+  g_last_launches = 1;
+  return QUAROT_OK;
+}
+
+quarot_status quarot_swiglu(const void* gate_up, int64_t M, int64_t F, int64_t ld_gu, void* act, int64_t ld_act,
+                            void* stream) {
+  g_last_launches = 0;
+  if (M < 0 || F <= 0 || ld_gu < 2 * F || ld_act < F) return QUAROT_ERR_DIM;
+  if (M == 0) return QUAROT_OK;
+  if (!gate_up || !act) return QUAROT_ERR_NULL;
+  if (F % 8 || ld_gu % 8 || ld_act % 8 || !aligned16(gate_up) || !aligned16(act)) return QUAROT_ERR_ALIGN;
+  cudaError_t e = qr::launch_swiglu(gate_up, M, F, ld_gu, act, ld_act, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return QUAROT_ERR_CUDA;
   g_last_launches = 1;
   return QUAROT_OK;

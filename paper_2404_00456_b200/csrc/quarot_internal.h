@@ -8,13 +8,14 @@ namespace qr {
 // int4_gemm.cu
 cudaError_t launch_int4_gemm(const uint8_t* xq, const float* xs, int64_t M, int64_t K, int64_t ld_xq,
                              const uint8_t* wq, const float* ws, int64_t N, int64_t ld_wq, void* y,
-                             int64_t ld_y, cudaStream_t stream);
+                             int64_t ld_y, cudaStream_t stream, const void* residual = nullptr,
+                             int64_t ld_r = 0);
 cudaError_t launch_int4_gemm_s32(const uint8_t* xq, int64_t M, int64_t K, int64_t ld_xq, const uint8_t* wq,
                                  int64_t N, int64_t ld_wq, int32_t* acc, int64_t ld_acc, cudaStream_t stream);
 
 // hadamard_quant.cu
 cudaError_t launch_hq_none(const void* x, int64_t M, int64_t K, int64_t ld_x, float clip, uint8_t* q,
-                           int64_t ld_q, float* scale, cudaStream_t stream);
+                           int64_t ld_q, float* scale, cudaStream_t stream, bool rmsnorm = false);
 cudaError_t launch_hq_heads(const void* x, int64_t M, int64_t K, int64_t ld_x, int head_dim, float clip,
                             uint8_t* q, int64_t ld_q, float* scale, cudaStream_t stream);
 cudaError_t launch_hq_full(const void* x, int64_t M, int64_t K, int64_t ld_x, int pow2, int m, float clip,
@@ -24,6 +25,12 @@ cudaError_t launch_hq_full(const void* x, int64_t M, int64_t K, int64_t ld_x, in
 cudaError_t launch_kv_quant(const void* k, int64_t ld_k, const void* v, int64_t ld_v, int64_t T, int n_kv,
                             int head_dim, void* q, int64_t ld_q, int n_q, uint32_t flags, float clip, uint8_t* k_codes, float* k_scale, uint8_t* k_zero,
                             uint8_t* v_codes, float* v_scale, uint8_t* v_zero, cudaStream_t stream);
+
+// glue.cu
+cudaError_t launch_rope(void* x, int64_t T, int n_heads, int head_dim, int64_t ld_x, int64_t pos0, int seq_len,
+                        float theta, cudaStream_t stream);
+cudaError_t launch_swiglu(const void* gu, int64_t M, int64_t F, int64_t ld_gu, void* act, int64_t ld_act,
+                          cudaStream_t stream);
 
 // hadamard_tables.cu — host construction of the stored H_m (m = 28, 172), verified H H^T = m I,
 // and their device-side mma.sync B-fragment tables (built once per device).

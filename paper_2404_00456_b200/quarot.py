@@ -16,6 +16,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libquarot.so")
 
 NONE, FULL, ACROSS_HEADS = 0, 1, 2
+RMSNORM = 0x100  # mode flag: scale-free RMSNorm fused into the NONE quantizer
 MODES = {"none": NONE, "full": FULL, "across_heads": ACROSS_HEADS}
 KV_ROTATE_K, KV_ROTATE_V = 1, 2
 
@@ -25,6 +26,10 @@ _SIGS = {
     "quarot_hadamard_quant": [_vp, _c_i64, _c_i64, _c_i64, _c_i32, _c_i32, _c_f32, _vp, _c_i64, _vp, _vp],
     "quarot_int4_linear": [_vp, _vp, _c_i64, _c_i64, _c_i64, _vp, _vp, _c_i64, _c_i64, _vp, _c_i64, _vp],
     "quarot_int4_matmul_s32": [_vp, _c_i64, _c_i64, _c_i64, _vp, _c_i64, _c_i64, _vp, _c_i64, _vp],
+    "quarot_int4_linear_residual": [_vp, _vp, _c_i64, _c_i64, _c_i64, _vp, _vp, _c_i64, _c_i64, _vp, _c_i64, _vp,
+                                    _c_i64, _vp],
+    "quarot_rope": [_vp, _c_i64, _c_i32, _c_i32, _c_i64, _c_i64, _c_i32, _c_f32, _vp],
+    "quarot_swiglu": [_vp, _c_i64, _c_i64, _c_i64, _vp, _c_i64, _vp],
     "quarot_kv_quant": [_vp, _c_i64, _vp, _c_i64, _c_i64, _c_i32, _c_i32, _vp, _c_i64, _c_i32, _c_u32,
                         _c_f32, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "quarot_status_string": [_c_i32],
@@ -96,9 +101,13 @@ def base_hadamard(m: int) -> torch.Tensor:
 
 
 def hadamard_quant(x: torch.Tensor, mode="none", head_dim: int = 128, clip_ratio: float = 0.9,
-                   q: torch.Tensor | None = None, scale: torch.Tensor | None = None, stream=None):
-    """quarot_hadamard_quant: fp16 x [M, K] -> (packed uint8 q [M, K/2], fp32 scale [M])."""
+                   q: torch.Tensor | None = None, scale: torch.Tensor | None = None, stream=None,
+                   rmsnorm: bool = False):
+    """quarot_hadamard_quant: fp16 x [M, K] -> (packed uint8 q [M, K/2], fp32 scale [M]).
+    rmsnorm=True (NONE only): RMS-normalize each row first (scale-free RMSNorm, fused)."""
     mode_i = MODES[mode] if isinstance(mode, str) else int(mode)
+    if rmsnorm:
+        mode_i |= RMSNORM
     M, K = x.shape
     if q is None:
         q = torch.empty(M, K // 2, dtype=torch.uint8, device=x.device)
@@ -112,17 +121,49 @@ def hadamard_quant(x: torch.Tensor, mode="none", head_dim: int = 128, clip_ratio
 
 
 def int4_linear(xq: torch.Tensor, x_scale: torch.Tensor, wq: torch.Tensor, w_scale: torch.Tensor,
-                y: torch.Tensor | None = None, stream=None) -> torch.Tensor:
-    """quarot_int4_linear: y fp16 [M, N] = fp16(acc * s_x * s_w)."""
+                y: torch.Tensor | None = None, stream=None, residual: torch.Tensor | None = None) -> torch.Tensor:
+    """quarot_int4_linear: y fp16 [M, N] = fp16(acc * s_x * s_w) (+ residual, fused:
+    quarot_int4_linear_residual)."""
     M, Kh = xq.shape
     N = wq.shape[0]
     if y is None:
         y = torch.empty(M, N, dtype=torch.float16, device=xq.device)
-    st = lib().quarot_int4_linear(_dev(xq, "xq", torch.uint8), _dev(x_scale, "x_scale", torch.float32), M, 2 * Kh,
-                                  xq.stride(0), _dev(wq, "wq", torch.uint8), _dev(w_scale, "w_scale", torch.float32),
-                                  N, wq.stride(0), _dev(y, "y", torch.float16), y.stride(0), _stream(stream))
-    _check("quarot_int4_linear", st)
+    if residual is None:
+        st = lib().quarot_int4_linear(_dev(xq, "xq", torch.uint8), _dev(x_scale, "x_scale", torch.float32), M,
+                                      2 * Kh, xq.stride(0), _dev(wq, "wq", torch.uint8),
+                                      _dev(w_scale, "w_scale", torch.float32), N, wq.stride(0),
+                                      _dev(y, "y", torch.float16), y.stride(0), _stream(stream))
+        _check("quarot_int4_linear", st)
+    else:
+        st = lib().quarot_int4_linear_residual(
+            _dev(xq, "xq", torch.uint8), _dev(x_scale, "x_scale", torch.float32), M, 2 * Kh, xq.stride(0),
+            _dev(wq, "wq", torch.uint8), _dev(w_scale, "w_scale", torch.float32), N, wq.stride(0),
+            _dev(residual, "residual", torch.float16), residual.stride(0), _dev(y, "y", torch.float16), y.stride(0),
+            _stream(stream))
+        _check("quarot_int4_linear_residual", st)
     return y
+
+
+def rope(x: torch.Tensor, pos0: int = 0, seq_len: int = 2048, theta: float = 10000.0, stream=None) -> torch.Tensor:
+    """quarot_rope, in place on x fp16 [T, n_heads, head_dim] (token stride arbitrary, heads
+    contiguous): Llama-2 rotary embedding at positions (pos0 + t) % seq_len."""
+    T, n, d = x.shape
+    if x.stride(2) != 1 or x.stride(1) != d:
+        raise ValueError("x: heads of a token must be contiguous [n, d]")
+    _check("quarot_rope", lib().quarot_rope(_dev(x, "x", torch.float16), T, n, d, x.stride(0), pos0, seq_len, theta,
+                                            _stream(stream)))
+    return x
+
+
+def swiglu(gate_up: torch.Tensor, act: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """quarot_swiglu: act [M, F] = silu(gate_up[:, :F]) * gate_up[:, F:]."""
+    M, F2 = gate_up.shape
+    F = F2 // 2
+    if act is None:
+        act = torch.empty(M, F, dtype=torch.float16, device=gate_up.device)
+    _check("quarot_swiglu", lib().quarot_swiglu(_dev(gate_up, "gate_up", torch.float16), M, F, gate_up.stride(0),
+                                                _dev(act, "act", torch.float16), act.stride(0), _stream(stream)))
+    return act
 
 
 def int4_matmul_s32(xq: torch.Tensor, wq: torch.Tensor, acc: torch.Tensor | None = None,

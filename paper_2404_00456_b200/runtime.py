@@ -175,3 +175,94 @@ class HostPipeline:
                     self.host_out[k][r0:r1].copy_(self.step.kv[k][r0:r1], non_blocking=True)
         cur = torch.cuda.current_stream()
         cur.wait_stream(self.s_d2h)
+
+
+class DecoderLayerStep:
+    """The QuaRot decoder-layer prefill chain (BASELINE config 5) with the
+    attention core excluded — the out_proj input is a supplied activation:
+
+      1. RMSNorm + quantize(x)            (fused)         -> QKV GEMM          -> qkv
+      2. RoPE on the Q|K block of qkv     (in place)
+      3. KV-cache Init: per-head H on K (and Q in place), asym INT4 K/V
+      4. Hadamard-heads + quantize(attn_out)              -> O GEMM + x        -> o
+      5. RMSNorm + quantize(o)            (fused)         -> gate/up GEMM      -> gu
+      6. SwiGLU(gu)                                                            -> act
+      7. Hadamard (FULL) + quantize(act)                  -> down GEMM + o     -> out
+    = 11 kernel launches."""
+
+    LAUNCHES = 11
+
+    def __init__(self, layer: QuaRotLayer, tokens: int, device="cuda", seq_len: int = 2048, theta: float = 10000.0):
+        self.layer, self.tokens, self.device = layer, tokens, torch.device(device)
+        self.seq_len, self.theta = seq_len, theta
+        L = layer
+        max_k = max(s.k for s in L.specs)
+        self.xq = torch.empty(tokens, max_k // 2, dtype=torch.uint8, device=device)
+        self.xs = torch.empty(tokens, dtype=torch.float32, device=device)
+        self.qkv = torch.empty(tokens, L.qkv_out, dtype=torch.float16, device=device)
+        self.o = torch.empty(tokens, L.hidden, dtype=torch.float16, device=device)
+        self.gu = torch.empty(tokens, 2 * L.ffn, dtype=torch.float16, device=device)
+        self.act = torch.empty(tokens, L.ffn, dtype=torch.float16, device=device)
+        self.out = torch.empty(tokens, L.hidden, dtype=torch.float16, device=device)
+        d = L.head_dim
+        self.kv = {
+            "k_codes": torch.empty(tokens, L.n_kv, d // 2, dtype=torch.uint8, device=device),
+            "k_scale": torch.empty(tokens, L.n_kv, dtype=torch.float32, device=device),
+            "k_zero": torch.empty(tokens, L.n_kv, dtype=torch.uint8, device=device),
+            "v_codes": torch.empty(tokens, L.n_kv, d // 2, dtype=torch.uint8, device=device),
+            "v_scale": torch.empty(tokens, L.n_kv, dtype=torch.float32, device=device),
+            "v_zero": torch.empty(tokens, L.n_kv, dtype=torch.uint8, device=device),
+        }
+
+    def bytes_glue(self) -> int:
+        """Algorithmic HBM bytes of the glue kernels (RoPE read+write of Q|K, SwiGLU)."""
+        L, T = self.layer, self.tokens
+        rope = T * (L.n_heads + L.n_kv) * L.head_dim * 2 * 2
+        swi = T * L.ffn * 2 * 3
+        return rope + swi
+
+    def run_rows(self, x: torch.Tensor, attn_out: torch.Tensor, r0: int, r1: int, stream=None, events=None):
+        """x: residual stream [T, hidden] fp16; attn_out: [T, hidden] fp16 stand-in for the
+        attention core's output.  Rows [r0, r1); positions (r0 + t) % seq_len."""
+        L = self.layer
+        stream = torch.cuda.current_stream() if stream is None else stream
+        d = L.head_dim
+        T = r1 - r0
+
+        def mark(name):
+            if events is not None:
+                events.append((name, torch.cuda.Event(enable_timing=True)))
+                events[-1][1].record(stream)
+
+        def linear(spec, xin, rms, out, residual=None):
+            xq = self.xq[r0:r1, : spec.k // 2]
+            xs = self.xs[r0:r1]
+            q.hadamard_quant(xin, spec.mode, d, L.clip_act, q=xq, scale=xs, stream=stream, rmsnorm=rms)
+            mark(f"hq_{spec.name}")
+            wq, ws = L.weights[spec.name]
+            q.int4_linear(xq, xs, wq, ws, y=out, stream=stream, residual=residual)
+            mark(f"gemm_{spec.name}")
+
+        qkv_s, o_s, gu_s, down_s = L.specs
+        xr = x[r0:r1]
+        qkv = self.qkv[r0:r1]
+        linear(qkv_s, xr, True, qkv)
+        nq, nkv = L.n_heads * d, L.n_kv * d
+        q.rope(qkv[:, : nq + nkv].view(T, L.n_heads + L.n_kv, d), pos0=r0, seq_len=self.seq_len,
+               theta=self.theta, stream=stream)
+        mark("rope")
+        q.kv_quant(qkv[:, nq:nq + nkv].view(T, L.n_kv, d), qkv[:, nq + nkv:].view(T, L.n_kv, d),
+                   qkv[:, :nq].view(T, L.n_heads, d), flags=q.KV_ROTATE_K, clip_ratio=L.clip_kv,
+                   out={k: t[r0:r1] for k, t in self.kv.items()}, stream=stream)
+        mark("kv_quant")
+        o = self.o[r0:r1]
+        linear(o_s, attn_out[r0:r1], False, o, residual=xr)
+        gu = self.gu[r0:r1]
+        linear(gu_s, o, True, gu)
+        act = self.act[r0:r1]
+        q.swiglu(gu, act=act, stream=stream)
+        mark("swiglu")
+        linear(down_s, act, False, self.out[r0:r1], residual=o)
+
+    def run_device(self, x, attn_out, stream=None, events=None):
+        self.run_rows(x, attn_out, 0, self.tokens, stream, events)

@@ -1,0 +1,172 @@
+"""GPU parity of the decoder-layer glue and of the whole decoder-layer chain
+(BASELINE config 5 minus the attention core) against oracle/glue.py."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import glue as oglue
+from oracle import layer as olayer
+from tests import _parity as P
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+@pytest.fixture(scope="module")
+def q():
+    import paper_2404_00456_b200 as q
+    q.lib()
+    return q
+
+
+@pytest.mark.parametrize("K", [256, 4096, 8192])
+def test_rmsnorm_quant(q, K):
+    x = synth.activations(37, K, "outlier", seed=K, device=DEV) * 0.01
+    x[3] = 0
+    xq, xs = q.hadamard_quant(x, "none", rmsnorm=True)
+    rc, _, rs = oglue.rmsnorm_quant(x.float().cpu().numpy().astype(np.float64))
+    P.assert_codes(P.unpack_signed(xq.cpu().numpy()), rc, "rmsnorm codes")
+    P.assert_scales(xs.cpu().numpy(), rs, "rmsnorm scales")
+    with pytest.raises(q.QuarotError):
+        q.hadamard_quant(x, "full", rmsnorm=True)  # only NONE takes the flag
+
+
+def test_linear_residual(q):
+    M, N, K = 300, 512, 4096
+    xq = synth.packed_weight_codes(M, K, 1, DEV)
+    wq = synth.packed_weight_codes(N, K, 2, DEV)
+    xs = torch.rand(M, device=DEV) * 0.01 + 0.001
+    ws = synth.weight_scales(N, 3, DEV)
+    r = synth.activations(M, N, "normal", 4, DEV)
+    y = q.int4_linear(xq, xs, wq, ws, residual=r)
+    acc = q.int4_matmul_s32(xq, wq).cpu().numpy().astype(np.float64)
+    ref = (acc * xs.cpu().numpy().astype(np.float64)[:, None] * ws.cpu().numpy().astype(np.float64)[None, :]
+           + r.cpu().numpy().astype(np.float64)).astype(np.float16)
+    assert P.max_fp16_ulp(y.cpu().numpy(), ref) <= 2
+    y2 = r.clone()
+    q.int4_linear(xq, xs, wq, ws, y=y2, residual=y2)  # in-place residual
+    assert torch.equal(y, y2)
+
+
+@pytest.mark.parametrize("T,n,d,pos0", [(37, 9, 128, 0), (5, 3, 64, 2040), (4100, 2, 128, 0)])
+def test_rope(q, T, n, d, pos0):
+    x = synth.activations(T, n * d + 64, "normal", seed=T, device=DEV)
+    view = x[:, : n * d].view(T, n, d)
+    ref = oglue.rope(view.float().cpu().numpy().astype(np.float64), (pos0 + np.arange(T)) % 2048)
+    tail = x[:, n * d:].clone()
+    q.rope(view, pos0=pos0, seq_len=2048)
+    assert P.max_fp16_ulp(view.cpu().numpy(), ref.astype(np.float16)) <= 1
+    assert torch.equal(x[:, n * d:], tail)  # the rest of the row untouched
+
+
+def test_swiglu(q):
+    gu = synth.activations(77, 2 * 448, "normal", seed=5, device=DEV) * 3
+    act = q.swiglu(gu)
+    g = gu.float().cpu().numpy().astype(np.float64)
+    ref = oglue.swiglu(g[:, :448], g[:, 448:]).astype(np.float16)
+    assert P.max_fp16_ulp(act.cpu().numpy(), ref) <= 2
+
+
+def _layer_weights(S, device, seed=2000):
+    from paper_2404_00456_b200.runtime import QuaRotLayer
+    dims = {"qkv": (S["qkv"], S["hidden"]), "o": (S["hidden"], S["hidden"]), "gate_up": (2 * S["ffn"], S["hidden"]),
+            "down": (S["hidden"], S["ffn"])}
+    w = {name: (synth.packed_weight_codes(n, k, seed + i, device), synth.weight_scales(n, seed + 10 + i, device))
+         for i, (name, (n, k)) in enumerate(dims.items())}
+    return QuaRotLayer(S["hidden"], S["ffn"], S["n_heads"], S["n_kv"], 128, w), w
+
+
+def _chain_check(q, S, T, rows, end_to_end: bool):
+    """Stage-by-stage parity of the decoder chain: every stage is checked against the oracle
+    applied to the GPU's own input to that stage (quantization is discontinuous, so a 1-ulp
+    difference upstream can legitimately flip a code downstream).  GEMM stages are checked on
+    sampled (row, column) blocks so the full-size configs stay cheap."""
+    from oracle import gemm as ogemm
+    from oracle import kv as okv
+    from oracle import quant as oquant
+    from paper_2404_00456_b200.runtime import DecoderLayerStep
+    layer, w = _layer_weights(S, DEV)
+    x = synth.activations(T, S["hidden"], "outlier", 100, DEV) * 0.05
+    z = synth.activations(T, S["hidden"], "normal", 101, DEV)
+    step = DecoderLayerStep(layer, T, DEV)
+    step.run_device(x, z)
+    torch.cuda.synchronize()
+    rows = np.asarray(rows)
+    rt = torch.as_tensor(rows, device=DEV)
+    R = len(rows)
+    d, nh, nkv, F = 128, S["n_heads"], S["n_kv"], S["ffn"]
+    nq, nk = nh * d, nkv * d
+    rng = np.random.default_rng(7)
+
+    def lin_ref(codes, sx, name, cols, residual=None):
+        wq, ws = w[name]
+        ct = torch.as_tensor(cols, device=DEV)
+        cw = oquant.unpack_int4_signed(wq[ct].cpu().numpy())
+        acc = ogemm.int_matmul_exact_f64(codes, cw)
+        y = acc * sx.astype(np.float64)[:, None] * ws[ct].cpu().numpy().astype(np.float64)[None, :]
+        if residual is not None:
+            y = y + residual
+        return y.astype(np.float16)
+
+    xh = x[rt].float().cpu().numpy().astype(np.float64)
+    # --- stage A: RMSNorm+quant -> QKV GEMM; V columns direct, Q/K heads through RoPE (+H on Q)
+    cx, _, sx = oglue.rmsnorm_quant(xh)
+    vcols = nq + nk + np.sort(rng.choice(nk, size=min(128, nk), replace=False))
+    g_qkv = step.qkv[rt].cpu().numpy()
+    assert P.frob_rel(g_qkv[:, vcols], lin_ref(cx, sx, "qkv", vcols)) <= P.FROB_REL
+    for h in sorted({0, nh - 1}):
+        qh = lin_ref(cx, sx, "qkv", np.arange(h * d, (h + 1) * d)).astype(np.float64).reshape(R, 1, d)
+        qr = oglue.rope(qh, rows % 2048).astype(np.float16).astype(np.float64)
+        qrot = okv.kv_init(qr, qr, qr)["q_rot"].reshape(R, d)
+        assert P.frob_rel(g_qkv[:, h * d:(h + 1) * d], qrot) <= P.FROB_REL
+    kh = lin_ref(cx, sx, "qkv", np.arange(nq, nq + d)).astype(np.float64).reshape(R, 1, d)
+    assert P.frob_rel(g_qkv[:, nq:nq + d], oglue.rope(kh, rows % 2048).reshape(R, d).astype(np.float16)) <= P.FROB_REL
+    # --- stage B: KV cache of the GPU's own post-RoPE K and V
+    kg = g_qkv[:, nq:nq + nk].astype(np.float64).reshape(R, nkv, d)
+    vg = g_qkv[:, nq + nk:].astype(np.float64).reshape(R, nkv, d)
+    cache = okv.kv_init(kg, vg)
+    for t in ("k", "v"):
+        P.assert_codes(P.unpack_unsigned(step.kv[f"{t}_codes"][rt].cpu().numpy()),
+                       P.unpack_unsigned(cache[f"{t}_codes"]), f"{t} codes")
+        P.assert_scales(step.kv[f"{t}_scale"][rt].cpu().numpy(), cache[f"{t}_scale"], f"{t} scales")
+    # --- stage C: heads-H + quant -> O GEMM + residual x
+    cz, _, sz = olayer.hadamard_quant(z[rt].float().cpu().numpy().astype(np.float64), "across_heads", d)
+    ocols = np.sort(rng.choice(S["hidden"], size=min(256, S["hidden"]), replace=False))
+    g_o = step.o[rt].cpu().numpy()
+    assert P.frob_rel(g_o[:, ocols], lin_ref(cz, sz, "o", ocols, xh[:, ocols])) <= P.FROB_REL
+    # --- stage D: RMSNorm+quant(o) -> gate/up GEMM
+    co, _, so = oglue.rmsnorm_quant(g_o.astype(np.float64))
+    fcols = np.sort(rng.choice(F, size=min(128, F), replace=False))
+    gucols = np.concatenate([fcols, F + fcols])
+    g_gu = step.gu[rt].cpu().numpy()
+    assert P.frob_rel(g_gu[:, gucols], lin_ref(co, so, "gate_up", gucols)) <= P.FROB_REL
+    # --- stage E: SwiGLU
+    g_act = step.act[rt].cpu().numpy()
+    ref_act = oglue.swiglu(g_gu[:, :F].astype(np.float64), g_gu[:, F:].astype(np.float64)).astype(np.float16)
+    assert P.max_fp16_ulp(g_act, ref_act) <= 2
+    # --- stage F: FULL Hadamard + quant -> down GEMM + residual o
+    ca, _, sa = olayer.hadamard_quant(g_act.astype(np.float64), "full", d)
+    dcols = np.sort(rng.choice(S["hidden"], size=min(256, S["hidden"]), replace=False))
+    g_out = step.out[rt].cpu().numpy()
+    assert P.frob_rel(g_out[:, dcols], lin_ref(ca, sa, "down", dcols, g_o[:, dcols].astype(np.float64))) <= P.FROB_REL
+    if end_to_end:
+        # whole chain from the oracle's own intermediates: bounded by code flips cascading
+        wo = {n: (P.unpack_signed(wq.cpu().numpy()), ws.cpu().numpy()) for n, (wq, ws) in w.items()}
+        ref = oglue.decoder_layer(x[rt].cpu().numpy(), z[rt].cpu().numpy(), wo, rows % 2048,
+                                  {"n_heads": nh, "n_kv": nkv, "head_dim": d, "ffn": F})
+        assert P.frob_rel(g_out, ref["out"]) <= 5e-2
+
+
+def test_decoder_chain_small(q):
+    S = {"hidden": 512, "ffn": 28 * 32, "n_heads": 4, "n_kv": 1}
+    S["qkv"] = (S["n_heads"] + 2 * S["n_kv"]) * 128
+    _chain_check(q, S, 300, np.arange(300), end_to_end=True)
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_decoder_chain_full_size_sampled(q, cfg):
+    spec = synth.CONFIGS[cfg]
+    Sh, T = spec["shapes"], spec["tokens"]
+    S = {"hidden": Sh.hidden, "ffn": Sh.ffn, "n_heads": Sh.n_heads, "n_kv": Sh.n_kv_heads, "qkv": Sh.qkv_out}
+    _chain_check(q, S, T, olayer.token_sample(T, 8), end_to_end=False)
