@@ -1,11 +1,13 @@
 #!/usr/bin/env python
 """QuaRot hot-path benchmark (driver contract).
 
-A step = one pass of every SURVEY §8(a) row over one batch: for a Llama-2-70B decoder
-layer (hidden 8192, FFN 28672 = 1024 x H_28, 64 Q / 8 KV heads x 128) and 64 x 2048 =
-131072 tokens per GPU: quantize -> INT4 QKV GEMM, KV-cache Init on the QKV output,
-Hadamard-heads + quantize -> INT4 O GEMM, quantize -> INT4 gate/up GEMM, Hadamard
-(1024 x H_28) + quantize -> INT4 down GEMM (9 kernel launches, all ours).
+A step = one pass of every SURVEY §8(a) row over one batch: one Llama-2-70B decoder layer
+(hidden 8192, FFN 28672 = 1024 x H_28, 64 Q / 8 KV heads x 128) prefilling 64 x 2048 = 131072
+tokens per GPU, as the chain of runtime.DecoderLayerStep (attention core excluded):
+RMSNorm+quantize -> INT4 QKV GEMM -> RoPE -> KV-cache Init (+Q rotation) ; Hadamard-heads +
+quantize -> INT4 O GEMM + residual ; RMSNorm+quantize -> INT4 gate/up GEMM -> SwiGLU ;
+Hadamard (1024 x H_28) + quantize -> INT4 down GEMM + residual (11 kernel launches, all ours).
+`--step linears` times rows a1-a7 alone on independent inputs (9 launches).
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
@@ -117,9 +119,12 @@ def make_layer(device, seed_base=1000):
     return QuaRotLayer(S.hidden, S.ffn, S.n_heads, S.n_kv_heads, S.head_dim, weights)
 
 
-def make_inputs(tokens, device, rank):
+def make_inputs(tokens, device, rank, step="chain"):
     S = synth.inputs.LLAMA2_70B
     base = 100 + 10 * rank
+    if step == "chain":
+        return {"x": synth.activations(tokens, S.hidden, "outlier", base + 0, device),
+                "attn_out": synth.activations(tokens, S.hidden, "normal", base + 1, device)}
     return {"attn_in": synth.activations(tokens, S.hidden, "outlier", base + 0, device),
             "attn_out": synth.activations(tokens, S.hidden, "normal", base + 1, device),
             "ffn_in": synth.activations(tokens, S.hidden, "outlier", base + 2, device),
@@ -161,6 +166,44 @@ def oracle_step(host_in: dict, host_w: dict, layer_dims: dict) -> None:
     return outs
 
 
+def _block_linear(cx, sx, wq, ws, residual=None):
+    """Oracle int4 linear with the packed weights unpacked in row blocks (memory bound)."""
+    from oracle import layer as olayer
+    from oracle import quant as oquant
+    ys = []
+    for r0 in range(0, wq.shape[0], 2048):
+        cw = oquant.unpack_int4_signed(wq[r0:r0 + 2048])
+        acc = olayer.int4_linear(cx, sx, cw, ws[r0:r0 + 2048])[0]
+        ys.append(acc * sx.astype(np.float64)[:, None] * ws[r0:r0 + 2048].astype(np.float64)[None, :])
+    y = np.concatenate(ys, axis=1)
+    if residual is not None:
+        y = y + residual.astype(np.float64)
+    return y.astype(np.float16)
+
+
+def oracle_chain_step(host_in: dict, host_w: dict, dims: dict, positions) -> dict:
+    """The CPU oracle on host rows for the decoder-layer chain (oracle/glue.py pieces)."""
+    from oracle import glue as oglue
+    from oracle import kv as okv
+    from oracle import layer as olayer
+    d, nh, nkv, F = dims["head_dim"], dims["n_heads"], dims["n_kv"], dims["ffn"]
+    x = host_in["x"]
+    T = x.shape[0]
+    cx, _, sx = oglue.rmsnorm_quant(x.astype(np.float64))
+    qkv = _block_linear(cx, sx, *host_w["qkv"]).astype(np.float64)
+    nq, nk = nh * d, nkv * d
+    qr = oglue.rope(qkv[:, :nq].reshape(T, nh, d), positions).astype(np.float16).astype(np.float64)
+    kr = oglue.rope(qkv[:, nq:nq + nk].reshape(T, nkv, d), positions).astype(np.float16).astype(np.float64)
+    cache = okv.kv_init(kr, qkv[:, nq + nk:].reshape(T, nkv, d), qr)
+    cz, _, sz = olayer.hadamard_quant(host_in["attn_out"].astype(np.float64), "across_heads", d)
+    o = _block_linear(cz, sz, *host_w["o"], residual=x)
+    co, _, so = oglue.rmsnorm_quant(o.astype(np.float64))
+    gu = _block_linear(co, so, *host_w["gate_up"]).astype(np.float64)
+    act = oglue.swiglu(gu[:, :F], gu[:, F:]).astype(np.float16)
+    ca, _, sa = olayer.hadamard_quant(act.astype(np.float64), "full", d)
+    return {"out": _block_linear(ca, sa, *host_w["down"], residual=o), "cache": cache}
+
+
 def cpu_threads():
     try:
         from threadpoolctl import threadpool_info
@@ -174,11 +217,17 @@ def host_sample(inputs: dict, layer, sample: int):
     rows = torch.linspace(0, next(iter(inputs.values())).shape[0] - 1, sample).round().long()
     host_in = {k: v[rows.to(v.device)].cpu().numpy() for k, v in inputs.items()}
     host_w = {k: (w.cpu().numpy(), s.cpu().numpy()) for k, (w, s) in layer.weights.items()}
-    return host_in, host_w
+    return host_in, host_w, rows.numpy()
 
 
 def layer_dims(layer):
-    return {"head_dim": layer.head_dim, "n_heads": layer.n_heads, "n_kv": layer.n_kv}
+    return {"head_dim": layer.head_dim, "n_heads": layer.n_heads, "n_kv": layer.n_kv, "ffn": layer.ffn}
+
+
+def run_oracle(args, host_in, host_w, layer, rows):
+    if args.step == "chain":
+        return oracle_chain_step(host_in, host_w, layer_dims(layer), rows % 2048)
+    return oracle_step(host_in, host_w, layer_dims(layer))
 
 
 def run_reference(args):
@@ -189,21 +238,22 @@ def run_reference(args):
     device = "cuda" if torch.cuda.is_available() else "cpu"
     layer = make_layer(device)
     sample = args.ref_tokens
-    inputs = make_inputs(sample * 16, device, 0)
-    host_in, host_w = host_sample(inputs, layer, sample)
+    inputs = make_inputs(sample * 16, device, 0, args.step)
+    host_in, host_w, rows = host_sample(inputs, layer, sample)
     for _ in range(args.warmup):
-        oracle_step(host_in, host_w, layer_dims(layer))
+        run_oracle(args, host_in, host_w, layer, rows)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        oracle_step(host_in, host_w, layer_dims(layer))
+        run_oracle(args, host_in, host_w, layer, rows)
     dt = (time.perf_counter() - t0) / args.steps
     cores, blas = cpu_threads()
     value = sample / dt
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "tokens_per_step": sample, "sample": f"{sample} tokens of the "
-                       "64x2048 batch through all 9 steps (full-width layer, dense fp64 Hadamard, int64 GEMM)"},
+            "config": {"workload": WORKLOAD, "step": args.step, "tokens_per_step": sample,
+                       "sample": f"{sample} tokens of the 64x2048 batch through the whole {args.step} step "
+                                 "(full-width layer, dense fp64 Hadamard, int64 GEMM)"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "blas_threads": blas,
                              "kind": "oracle", "sample": f"{sample} tokens per step"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -226,6 +276,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--profile-steps", type=int, default=0, help="run N untimed steps and exit (ncu)")
+    ap.add_argument("--step", default="chain", choices=["chain", "linears"],
+                    help="chain: the decoder-layer chain (a1-a8, 11 launches); linears: a1-a7 on independent inputs")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -241,12 +293,12 @@ def main():
 
     import paper_2404_00456_b200 as q
     from paper_2404_00456_b200 import dist as qd
-    from paper_2404_00456_b200.runtime import HostPipeline, PrefillStep
+    from paper_2404_00456_b200.runtime import DecoderLayerStep, HostPipeline, PrefillStep
     q.lib()
     layer = make_layer(dev)
     T = args.tokens
-    inputs = make_inputs(T, dev, rank)
-    step = PrefillStep(layer, T, dev)
+    inputs = make_inputs(T, dev, rank, args.step)
+    step = DecoderLayerStep(layer, T, dev) if args.step == "chain" else PrefillStep(layer, T, dev)
     stream = torch.cuda.current_stream()
     if args.profile_steps:
         for _ in range(args.profile_steps):
@@ -295,6 +347,7 @@ def main():
     gemm_tops = layer.gemm_ops(T) / (gemm_ms * 1e-3) / 1e12
     hq_gbs = layer.hq_bytes(T) / (hq_ms * 1e-3) / 1e9
     kv_gbs = layer.kv_bytes(T) / (kern_ms["kv_quant"] * 1e-3) / 1e9
+    glue_bytes = {"rope": T * (layer.n_heads + layer.n_kv) * layer.head_dim * 4, "swiglu": T * layer.ffn * 6}
     traffic = load_traffic()
     kernels = {}
     for s in layer.specs:
@@ -304,6 +357,10 @@ def main():
         kernels[f"hq_{s.name}"]["frac_hbm"] = kernels[f"hq_{s.name}"]["gbs"] / peaks["hbm_gbs"]
         kernels[f"gemm_{s.name}"]["frac_int8"] = kernels[f"gemm_{s.name}"]["tops"] / int8_peak
     kernels["kv_quant"] = {"ms": kern_ms["kv_quant"], "gbs": kv_gbs, "frac_hbm": kv_gbs / peaks["hbm_gbs"]}
+    for gname, gb in glue_bytes.items():
+        if gname in kern_ms:
+            g_gbs = gb / (kern_ms[gname] * 1e-3) / 1e9
+            kernels[gname] = {"ms": kern_ms[gname], "gbs": g_gbs, "frac_hbm": g_gbs / peaks["hbm_gbs"]}
 
     tokens_total = T * world
     line = {
@@ -311,10 +368,12 @@ def main():
         "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int4xint4->int32 (fp16 io, fp32 transform)",
         "data": "synthetic (seeded; random INT4 weight codes, Llama-2-70B shapes)",
-        "config": {"workload": WORKLOAD, "tokens_per_gpu": T, "global_batch": 64 * world, "seq_len": 2048,
+        "config": {"workload": WORKLOAD, "step": args.step, "tokens_per_gpu": T, "global_batch": 64 * world,
+                   "seq_len": 2048,
                    "hidden": layer.hidden, "ffn": layer.ffn, "heads": [layer.n_heads, layer.n_kv, layer.head_dim],
                    "parallelism": f"token-shard x{world} (no data-path collective)",
-                   "l2": "inputs larger than L2 (activations 13.9 GB/step)"},
+                   "l2": "inputs larger than L2 (GB-scale activations per step)",
+                   "attention_core": "excluded (SURVEY §8 a8): the out_proj input is a synthetic activation"},
         "roofline": {"bound": "tensor", "kernel": "int4_gemm (tcgen05 kind::i8, 4 launches/step)",
                      "achieved": gemm_tops, "peak": int8_peak, "unit": "TFLOP/s",
                      "frac": gemm_tops / int8_peak,
@@ -327,7 +386,7 @@ def main():
                          "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": hq_gbs / peaks["hbm_gbs"],
                          "traffic": traffic.get("hadamard_quant")},
         "kernels": kernels,
-        "gpu_launches": PrefillStep.LAUNCHES * args.steps,
+        "gpu_launches": step.LAUNCHES * args.steps,
         "clocks": clocks,
     }
 
@@ -359,15 +418,15 @@ def main():
     # ---- CPU oracle baseline (rank 0, N == 1 only)
     if not args.no_cpu_baseline and world == 1 and rank == 0:
         sample = args.ref_tokens
-        host_in, host_w = host_sample(inputs, layer, sample)
+        host_in, host_w, rows = host_sample(inputs, layer, sample)
         t0 = time.perf_counter()
-        oracle_step(host_in, host_w, layer_dims(layer))
+        run_oracle(args, host_in, host_w, layer, rows)
         dt = time.perf_counter() - t0
         cores, blas = cpu_threads()
         line["cpu_baseline"] = {"value": sample / dt, "unit": UNIT, "cores": cores, "blas_threads": blas,
                                 "kind": "oracle",
-                                "sample": f"{sample} tokens (evenly spaced rows of the batch) through all 9 steps, "
-                                          f"{dt:.1f} s"}
+                                "sample": f"{sample} tokens (evenly spaced rows of the batch) through the whole "
+                                          f"{args.step} step, {dt:.1f} s"}
     if world > 1:
         import torch.distributed as dist
         dist.barrier()

@@ -92,9 +92,9 @@ __global__ void __launch_bounds__(128) hq_none_kernel(const __half* __restrict__
     if ((threadIdx.x & 31) == 0) red2[threadIdx.x >> 5] = ssq;
   }
   amax = block_max<4>(amax, red);  // (its __syncthreads also publishes red2)
-  if (kRms) {
-    const double tot = (double)red2[0] + (double)red2[1] + (double)red2[2] + (double)red2[3];
-    norm = 1.0 / sqrt(tot / (double)K + 1e-5);
+  if (kRms) {  // fp32 ("RMSNorm ... in FP32"); 1/rms carries ~1 ulp
+    const float tot = (red2[0] + red2[1]) + (red2[2] + red2[3]);
+    norm = (double)rsqrtf(tot / (float)K + 1e-5f);
   }
   float s, inv;
   row_scale(amax, norm, clip, s, inv);

@@ -9,9 +9,9 @@ prefill uses them (Fig. ffn_quarot, Fig. attn_quarot, App. P
   4. quantize(x_ffn)                       NONE   -> INT4 gate/up GEMM -> gate_up fp16
   5. Hadamard + quantize(ffn_act)          FULL   -> INT4 down GEMM -> down fp16
 
-= 9 kernel launches through the C ABI.  The glue between them (RMSNorm, RoPE, SwiGLU,
-attention core) is out of scope for this round, so the four linear
-inputs are independent synthetic activations.
+= 9 kernel launches through the C ABI (`PrefillStep`, rows a1-a7 with independent synthetic
+inputs per linear).  `DecoderLayerStep` adds the a8 glue and chains the linears into a real
+decoder layer (attention core excluded): 11 launches, the bench default.
 
 `run_device` enqueues a step on one stream with inputs resident in HBM.  `run_host` is
 the end-to-end path for callers whose activations live in (pinned) host memory: the
@@ -130,22 +130,23 @@ class PrefillStep:
     def run_device(self, inputs: dict, stream=None, events=None):
         self.run_rows(inputs, 0, self.tokens, stream, events)
 
+    INPUTS = ("attn_in", "attn_out", "ffn_in", "ffn_act")
+
+    def result_tensors(self) -> dict:
+        return {"down": self.out["down"], **self.kv}
+
 
 class HostPipeline:
     """End-to-end step from pinned host inputs to pinned host results, chunked over tokens
     so H2D (stream 1), the kernels (stream 2) and D2H (stream 3) overlap.  Results copied
-    back per step: the layer output (down_proj) and the quantized KV cache."""
+    back per step: the step's `result_tensors()` (layer output and quantized KV cache)."""
 
-    RESULT_KEYS = ("k_codes", "k_scale", "k_zero", "v_codes", "v_scale", "v_zero")
-
-    def __init__(self, step: PrefillStep, host_inputs: dict, chunks: int = 8):
+    def __init__(self, step, host_inputs: dict, chunks: int = 8):
         self.step, self.host_in, self.chunks = step, host_inputs, chunks
         dev = step.device
         self.dev_in = {k: torch.empty(v.shape, dtype=v.dtype, device=dev) for k, v in host_inputs.items()}
-        self.host_out = {"down": torch.empty(step.out["down"].shape, dtype=torch.float16, pin_memory=True)}
-        for k in self.RESULT_KEYS:
-            t = step.kv[k]
-            self.host_out[k] = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        self.results = step.result_tensors()
+        self.host_out = {k: torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for k, t in self.results.items()}
         self.s_h2d, self.s_cmp, self.s_d2h = (torch.cuda.Stream(dev) for _ in range(3))
 
     def h2d_bytes(self) -> int:
@@ -170,9 +171,8 @@ class HostPipeline:
             e_cmp.record(self.s_cmp)
             self.s_d2h.wait_event(e_cmp)
             with torch.cuda.stream(self.s_d2h):
-                self.host_out["down"][r0:r1].copy_(self.step.out["down"][r0:r1], non_blocking=True)
-                for k in self.RESULT_KEYS:
-                    self.host_out[k][r0:r1].copy_(self.step.kv[k][r0:r1], non_blocking=True)
+                for k, t in self.results.items():
+                    self.host_out[k][r0:r1].copy_(t[r0:r1], non_blocking=True)
         cur = torch.cuda.current_stream()
         cur.wait_stream(self.s_d2h)
 
@@ -221,9 +221,16 @@ class DecoderLayerStep:
         swi = T * L.ffn * 2 * 3
         return rope + swi
 
-    def run_rows(self, x: torch.Tensor, attn_out: torch.Tensor, r0: int, r1: int, stream=None, events=None):
-        """x: residual stream [T, hidden] fp16; attn_out: [T, hidden] fp16 stand-in for the
-        attention core's output.  Rows [r0, r1); positions (r0 + t) % seq_len."""
+    INPUTS = ("x", "attn_out")
+
+    def result_tensors(self) -> dict:
+        """Per-step results a host caller keeps: the layer output and the quantized KV cache."""
+        return {"out": self.out, **self.kv}
+
+    def run_rows(self, inputs: dict, r0: int, r1: int, stream=None, events=None):
+        """inputs: 'x' residual stream [T, hidden] fp16, 'attn_out' [T, hidden] fp16 stand-in for
+        the attention core's output.  Rows [r0, r1); positions (r0 + t) % seq_len."""
+        x, attn_out = inputs["x"], inputs["attn_out"]
         L = self.layer
         stream = torch.cuda.current_stream() if stream is None else stream
         d = L.head_dim
@@ -264,5 +271,5 @@ class DecoderLayerStep:
         mark("swiglu")
         linear(down_s, act, False, self.out[r0:r1], residual=o)
 
-    def run_device(self, x, attn_out, stream=None, events=None):
-        self.run_rows(x, attn_out, 0, self.tokens, stream, events)
+    def run_device(self, inputs: dict, stream=None, events=None):
+        self.run_rows(inputs, 0, self.tokens, stream, events)

@@ -90,7 +90,7 @@ def _chain_check(q, S, T, rows, end_to_end: bool):
     x = synth.activations(T, S["hidden"], "outlier", 100, DEV) * 0.05
     z = synth.activations(T, S["hidden"], "normal", 101, DEV)
     step = DecoderLayerStep(layer, T, DEV)
-    step.run_device(x, z)
+    step.run_device({"x": x, "attn_out": z})
     torch.cuda.synchronize()
     rows = np.asarray(rows)
     rt = torch.as_tensor(rows, device=DEV)
