@@ -198,8 +198,14 @@ def oracle_chain_step(host_in: dict, host_w: dict, dims: dict, positions) -> dic
     cz, _, sz = olayer.hadamard_quant(host_in["attn_out"].astype(np.float64), "across_heads", d)
     o = _block_linear(cz, sz, *host_w["o"], residual=x)
     co, _, so = oglue.rmsnorm_quant(o.astype(np.float64))
-    gu = _block_linear(co, so, *host_w["gate_up"]).astype(np.float64)
-    act = oglue.swiglu(gu[:, :F], gu[:, F:]).astype(np.float16)
+    wq_gu, ws_gu = host_w["gate_up"]
+    acts = []
+    for f0 in range(0, F, 1024):  # gate/up rows in blocks (memory bound), SwiGLU on fp64 values
+        from oracle import quant as oquant
+        f1 = min(F, f0 + 1024)
+        rows_blk = np.concatenate([np.arange(f0, f1), F + np.arange(f0, f1)])
+        acts.append(oglue.linear_swiglu(co, so, oquant.unpack_int4_signed(wq_gu[rows_blk]), ws_gu[rows_blk], f1 - f0))
+    act = np.concatenate(acts, axis=1)
     ca, _, sa = olayer.hadamard_quant(act.astype(np.float64), "full", d)
     return {"out": _block_linear(ca, sa, *host_w["down"], residual=o), "cache": cache}
 
@@ -348,6 +354,8 @@ def main():
     hq_gbs = layer.hq_bytes(T) / (hq_ms * 1e-3) / 1e9
     kv_gbs = layer.kv_bytes(T) / (kern_ms["kv_quant"] * 1e-3) / 1e9
     glue_bytes = {"rope": T * (layer.n_heads + layer.n_kv) * layer.head_dim * 4, "swiglu": T * layer.ffn * 6}
+    if args.step == "chain" and step.fuse_swiglu:  # the gate/up GEMM writes act (F wide), not gate|up
+        kernels_note = "gate/up GEMM epilogue computes SwiGLU (writes act)"
     traffic = load_traffic()
     kernels = {}
     for s in layer.specs:

@@ -112,6 +112,17 @@ quarot_status quarot_int4_linear_residual(const uint8_t* xq, const float* x_scal
                                           int64_t N, int64_t ld_wq, const void* residual, int64_t ld_r,
                                           void* y, int64_t ld_y, void* stream);
 
+/* Gate/up projection with the SwiGLU activation fused into the epilogue (SURVEY §8 a8 + f1):
+ * the N2 = 2F rows of wq / w_scale are the gate and up rows interleaved in blocks of 8 —
+ * row 16j + i is gate feature 8j + i and row 16j + 8 + i is up feature 8j + i (i < 8), an
+ * offline layout choice (quarot.interleave_gate_up) — and the output is
+ *   act[m][f] = fp16_rn( silu(g) * u ),  g = acc_gate * x_scale[m] * w_scale[gate row],
+ *   u = acc_up * x_scale[m] * w_scale[up row]  (fp32; the gate/up products are never rounded
+ *   to fp16).  act fp16 [M][ld_act], ld_act >= N2/2, % 8 == 0.  N2 % 16 == 0. */
+quarot_status quarot_int4_linear_swiglu(const uint8_t* xq, const float* x_scale, int64_t M, int64_t K,
+                                        int64_t ld_xq, const uint8_t* wq, const float* w_scale, int64_t N2,
+                                        int64_t ld_wq, void* act, int64_t ld_act, void* stream);
+
 /* Parity only: the same tcgen05 mainloop, raw accumulators acc int32 [M][ld_acc]
  * (ld_acc % 4 == 0).  Same requirements as quarot_int4_linear. */
 quarot_status quarot_int4_matmul_s32(const uint8_t* xq, int64_t M, int64_t K, int64_t ld_xq,

@@ -44,6 +44,15 @@ def swiglu(gate: np.ndarray, up: np.ndarray) -> np.ndarray:
     return g / (1.0 + np.exp(-g)) * np.asarray(up, dtype=np.float64)
 
 
+def linear_swiglu(cx, sx, cw_gate_up, sw_gate_up, ffn: int):
+    """Gate/up INT4 linear with SwiGLU applied to the fp64 epilogue values (no fp16 rounding
+    of gate/up in between): act = fp16(silu(g) * u).  W rows [gate (ffn) ; up (ffn)]."""
+    from .gemm import int_matmul_exact_f64
+    acc = int_matmul_exact_f64(cx, cw_gate_up).astype(np.float64)
+    y = acc * np.asarray(sx, np.float64)[:, None] * np.asarray(sw_gate_up, np.float64)[None, :]
+    return swiglu(y[:, :ffn], y[:, ffn:]).astype(np.float16)
+
+
 def rmsnorm_quant(x: np.ndarray, clip_ratio: float = 0.9, eps: float = RMS_EPS):
     """RMSNorm (fp64, no fp16 round trip) then per-token INT4 quantization (NONE mode):
     Fig. ffn_quarot's norm -> quantize."""
@@ -77,7 +86,7 @@ def decoder_layer(x, attn_out, w, positions, shapes: dict, clip=0.9, clip_kv=0.9
          + np.asarray(x, dtype=np.float64)).astype(np.float16)
     cn, _, sn = rmsnorm_quant(o, clip)
     gu = olayer.int4_linear(cn, sn, *w["gate_up"], exact_f64=True)[1]
-    act = swiglu(gu[:, :ffn], gu[:, ffn:]).astype(np.float16)
+    act = linear_swiglu(cn, sn, *w["gate_up"], ffn)  # SwiGLU fused into the gate/up epilogue
     cd, _, sd = olayer.hadamard_quant(act, "full", d, clip)
     acc_d = olayer.int4_linear(cd, sd, *w["down"], exact_f64=True)[0]
     out = (acc_d * sd.astype(np.float64)[:, None] * w["down"][1].astype(np.float64)[None, :]

@@ -70,6 +70,7 @@ struct Params {
   const float* w_scale;
   void* out;  // fp16 y or int32 acc
   const __half* residual;  // optional fp16 residual added in the epilogue (decoder layer, a8)
+  int swiglu;              // 1: rows of W interleaved [8 gate | 8 up]; out = silu(gate) * up, N/2 wide
   int64_t M, N, K, ld_out, ld_r;
   int num_m, num_n, num_kb, num_tiles;  // num_m in 256-row pair tiles
 };
@@ -363,6 +364,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 *reinterpret_cast<int4*>(dst + g * 4) = v;
               }
             }
+          } else if (p.swiglu) {
+            // chunk = [8 gate | 8 up] columns of features n0/2 .. n0/2 + 7 (interleaved W rows)
+            if (n0 < p.N) {
+              const float4 g0 = __ldg(reinterpret_cast<const float4*>(p.w_scale + n0));
+              const float4 g1 = __ldg(reinterpret_cast<const float4*>(p.w_scale + n0 + 4));
+              const float4 u0 = __ldg(reinterpret_cast<const float4*>(p.w_scale + n0 + 8));
+              const float4 u1 = __ldg(reinterpret_cast<const float4*>(p.w_scale + n0 + 12));
+              const float sg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+              const float su[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+              uint32_t h[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                float a[2];
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                  const int c = 2 * e + j;
+                  const float gv = ((float)((int32_t)rc[c] >> 8) * sx) * sg[c];
+                  const float uv = ((float)((int32_t)rc[8 + c] >> 8) * sx) * su[c];
+                  a[j] = gv / (1.f + __expf(-gv)) * uv;
+                }
+                __half2 hv = __floats2half2_rn(a[0], a[1]);
+                h[e] = *reinterpret_cast<uint32_t*>(&hv);
+              }
+              *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(p.out) + m * p.ld_out + (n0 >> 1)) =
+                  make_uint4(h[0], h[1], h[2], h[3]);
+            }
           } else {
             __half* dst = reinterpret_cast<__half*>(p.out) + m * p.ld_out + n0;
 #pragma unroll
@@ -459,7 +486,7 @@ template <bool kS32>
 static cudaError_t launch_gemm_impl(const uint8_t* xq, const float* xs, int64_t M, int64_t K, int64_t ld_xq,
                                     const uint8_t* wq, const float* ws, int64_t N, int64_t ld_wq, void* out,
                                     int64_t ld_out, cudaStream_t stream, const void* residual = nullptr,
-                                    int64_t ld_r = 0) {
+                                    int64_t ld_r = 0, int swiglu = 0) {
   using namespace gemm;
   static bool attr_set[64] = {};
   int dev = 0;
@@ -479,6 +506,7 @@ static cudaError_t launch_gemm_impl(const uint8_t* xq, const float* xs, int64_t 
   p.out = out;
   p.residual = static_cast<const __half*>(residual);
   p.ld_r = ld_r;
+  p.swiglu = swiglu;
   p.M = M;
   p.N = N;
   p.K = K;
@@ -508,6 +536,12 @@ cudaError_t launch_int4_gemm(const uint8_t* xq, const float* xs, int64_t M, int6
                              const uint8_t* wq, const float* ws, int64_t N, int64_t ld_wq, void* y,
                              int64_t ld_y, cudaStream_t stream, const void* residual, int64_t ld_r) {
   return launch_gemm_impl<false>(xq, xs, M, K, ld_xq, wq, ws, N, ld_wq, y, ld_y, stream, residual, ld_r);
+}
+
+cudaError_t launch_int4_gemm_swiglu(const uint8_t* xq, const float* xs, int64_t M, int64_t K, int64_t ld_xq,
+                                    const uint8_t* wq, const float* ws, int64_t N2, int64_t ld_wq, void* act,
+                                    int64_t ld_act, cudaStream_t stream) {
+  return launch_gemm_impl<false>(xq, xs, M, K, ld_xq, wq, ws, N2, ld_wq, act, ld_act, stream, nullptr, 0, 1);
 }
 
 cudaError_t launch_int4_gemm_s32(const uint8_t* xq, int64_t M, int64_t K, int64_t ld_xq, const uint8_t* wq,

@@ -146,6 +146,23 @@ quarot_status quarot_int4_linear_residual(const uint8_t* xq, const float* x_scal
   return QUAROT_OK;
 }
 
+quarot_status quarot_int4_linear_swiglu(const uint8_t* xq, const float* x_scale, int64_t M, int64_t K,
+                                        int64_t ld_xq, const uint8_t* wq, const float* w_scale, int64_t N2,
+                                        int64_t ld_wq, void* act, int64_t ld_act, void* stream) {
+  g_last_launches = 0;
+  if (N2 <= 0 || N2 % 16) return N2 <= 0 ? QUAROT_ERR_DIM : QUAROT_ERR_ALIGN;
+  if (ld_act < N2 / 2) return QUAROT_ERR_DIM;
+  quarot_status s = check_gemm(xq, M, K, ld_xq, wq, N2, ld_wq, act, N2, 8);
+  if (s != QUAROT_OK || M == 0) return s;
+  if (!x_scale || !w_scale) return QUAROT_ERR_NULL;
+  if (!aligned16(w_scale) || (ld_act % 8)) return QUAROT_ERR_ALIGN;
+  cudaError_t e = qr::launch_int4_gemm_swiglu(xq, x_scale, M, K, ld_xq, wq, w_scale, N2, ld_wq, act, ld_act,
+                                              static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return QUAROT_ERR_CUDA;
+  g_last_launches = 1;
+  return QUAROT_OK;
+}
+
 quarot_status quarot_rope(void* x, int64_t T, int32_t n_heads, int32_t head_dim, int64_t ld_x, int64_t pos0,
                           int32_t seq_len, float theta, void* stream) {
   g_last_launches = 0;

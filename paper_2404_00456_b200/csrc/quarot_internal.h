@@ -10,6 +10,9 @@ cudaError_t launch_int4_gemm(const uint8_t* xq, const float* xs, int64_t M, int6
                              const uint8_t* wq, const float* ws, int64_t N, int64_t ld_wq, void* y,
                              int64_t ld_y, cudaStream_t stream, const void* residual = nullptr,
                              int64_t ld_r = 0);
+cudaError_t launch_int4_gemm_swiglu(const uint8_t* xq, const float* xs, int64_t M, int64_t K, int64_t ld_xq,
+                                    const uint8_t* wq, const float* ws, int64_t N2, int64_t ld_wq, void* act,
+                                    int64_t ld_act, cudaStream_t stream);
 cudaError_t launch_int4_gemm_s32(const uint8_t* xq, int64_t M, int64_t K, int64_t ld_xq, const uint8_t* wq,
                                  int64_t N, int64_t ld_wq, int32_t* acc, int64_t ld_acc, cudaStream_t stream);
 

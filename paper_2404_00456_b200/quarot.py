@@ -28,6 +28,7 @@ _SIGS = {
     "quarot_int4_matmul_s32": [_vp, _c_i64, _c_i64, _c_i64, _vp, _c_i64, _c_i64, _vp, _c_i64, _vp],
     "quarot_int4_linear_residual": [_vp, _vp, _c_i64, _c_i64, _c_i64, _vp, _vp, _c_i64, _c_i64, _vp, _c_i64, _vp,
                                     _c_i64, _vp],
+    "quarot_int4_linear_swiglu": [_vp, _vp, _c_i64, _c_i64, _c_i64, _vp, _vp, _c_i64, _c_i64, _vp, _c_i64, _vp],
     "quarot_rope": [_vp, _c_i64, _c_i32, _c_i32, _c_i64, _c_i64, _c_i32, _c_f32, _vp],
     "quarot_swiglu": [_vp, _c_i64, _c_i64, _c_i64, _vp, _c_i64, _vp],
     "quarot_kv_quant": [_vp, _c_i64, _vp, _c_i64, _c_i64, _c_i32, _c_i32, _vp, _c_i64, _c_i32, _c_u32,
@@ -142,6 +143,31 @@ def int4_linear(xq: torch.Tensor, x_scale: torch.Tensor, wq: torch.Tensor, w_sca
             _stream(stream))
         _check("quarot_int4_linear_residual", st)
     return y
+
+
+def interleave_gate_up(wq: torch.Tensor, w_scale: torch.Tensor):
+    """Offline weight layout for quarot_int4_linear_swiglu: [gate (F rows) ; up (F rows)] ->
+    rows interleaved in blocks of 8 ([8 gate | 8 up] per 16).  Pure row permutation."""
+    F = wq.shape[0] // 2
+    if wq.shape[0] != 2 * F or F % 8:
+        raise ValueError("gate/up weight needs 2F rows with F % 8 == 0")
+    idx = torch.arange(2 * F, device=wq.device).view(2, F // 8, 8).transpose(0, 1).reshape(-1)
+    return wq[idx].contiguous(), w_scale[idx].contiguous()
+
+
+def int4_linear_swiglu(xq: torch.Tensor, x_scale: torch.Tensor, wq_il: torch.Tensor, w_scale_il: torch.Tensor,
+                       act: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """quarot_int4_linear_swiglu: act [M, F] = silu(gate) * up from interleaved gate/up weights."""
+    M, Kh = xq.shape
+    N2 = wq_il.shape[0]
+    if act is None:
+        act = torch.empty(M, N2 // 2, dtype=torch.float16, device=xq.device)
+    st = lib().quarot_int4_linear_swiglu(_dev(xq, "xq", torch.uint8), _dev(x_scale, "x_scale", torch.float32), M,
+                                         2 * Kh, xq.stride(0), _dev(wq_il, "wq", torch.uint8),
+                                         _dev(w_scale_il, "w_scale", torch.float32), N2, wq_il.stride(0),
+                                         _dev(act, "act", torch.float16), act.stride(0), _stream(stream))
+    _check("quarot_int4_linear_swiglu", st)
+    return act
 
 
 def rope(x: torch.Tensor, pos0: int = 0, seq_len: int = 2048, theta: float = 10000.0, stream=None) -> torch.Tensor:

@@ -185,23 +185,26 @@ class DecoderLayerStep:
       2. RoPE on the Q|K block of qkv     (in place)
       3. KV-cache Init: per-head H on K (and Q in place), asym INT4 K/V
       4. Hadamard-heads + quantize(attn_out)              -> O GEMM + x        -> o
-      5. RMSNorm + quantize(o)            (fused)         -> gate/up GEMM      -> gu
-      6. SwiGLU(gu)                                                            -> act
-      7. Hadamard (FULL) + quantize(act)                  -> down GEMM + o     -> out
-    = 11 kernel launches."""
+      5. RMSNorm + quantize(o)            (fused)         -> gate/up GEMM with SwiGLU fused
+                                                             in its epilogue   -> act
+      6. Hadamard (FULL) + quantize(act)                  -> down GEMM + o     -> out
+    = 10 kernel launches (11 with fuse_swiglu=False: gate/up GEMM -> gu, then SwiGLU)."""
 
-    LAUNCHES = 11
-
-    def __init__(self, layer: QuaRotLayer, tokens: int, device="cuda", seq_len: int = 2048, theta: float = 10000.0):
+    def __init__(self, layer: QuaRotLayer, tokens: int, device="cuda", seq_len: int = 2048, theta: float = 10000.0,
+                 fuse_swiglu: bool = True):
         self.layer, self.tokens, self.device = layer, tokens, torch.device(device)
         self.seq_len, self.theta = seq_len, theta
+        self.fuse_swiglu = fuse_swiglu
+        self.LAUNCHES = 10 if fuse_swiglu else 11
+        if fuse_swiglu:  # offline: gate/up rows interleaved in blocks of 8 for the fused epilogue
+            self.gate_up_il = q.interleave_gate_up(*layer.weights["gate_up"])
         L = layer
         max_k = max(s.k for s in L.specs)
         self.xq = torch.empty(tokens, max_k // 2, dtype=torch.uint8, device=device)
         self.xs = torch.empty(tokens, dtype=torch.float32, device=device)
         self.qkv = torch.empty(tokens, L.qkv_out, dtype=torch.float16, device=device)
         self.o = torch.empty(tokens, L.hidden, dtype=torch.float16, device=device)
-        self.gu = torch.empty(tokens, 2 * L.ffn, dtype=torch.float16, device=device)
+        self.gu = None if fuse_swiglu else torch.empty(tokens, 2 * L.ffn, dtype=torch.float16, device=device)
         self.act = torch.empty(tokens, L.ffn, dtype=torch.float16, device=device)
         self.out = torch.empty(tokens, L.hidden, dtype=torch.float16, device=device)
         d = L.head_dim
@@ -213,13 +216,6 @@ class DecoderLayerStep:
             "v_scale": torch.empty(tokens, L.n_kv, dtype=torch.float32, device=device),
             "v_zero": torch.empty(tokens, L.n_kv, dtype=torch.uint8, device=device),
         }
-
-    def bytes_glue(self) -> int:
-        """Algorithmic HBM bytes of the glue kernels (RoPE read+write of Q|K, SwiGLU)."""
-        L, T = self.layer, self.tokens
-        rope = T * (L.n_heads + L.n_kv) * L.head_dim * 2 * 2
-        swi = T * L.ffn * 2 * 3
-        return rope + swi
 
     INPUTS = ("x", "attn_out")
 
@@ -264,11 +260,19 @@ class DecoderLayerStep:
         mark("kv_quant")
         o = self.o[r0:r1]
         linear(o_s, attn_out[r0:r1], False, o, residual=xr)
-        gu = self.gu[r0:r1]
-        linear(gu_s, o, True, gu)
         act = self.act[r0:r1]
-        q.swiglu(gu, act=act, stream=stream)
-        mark("swiglu")
+        if self.fuse_swiglu:
+            xq = self.xq[r0:r1, : gu_s.k // 2]
+            xs = self.xs[r0:r1]
+            q.hadamard_quant(o, "none", d, L.clip_act, q=xq, scale=xs, stream=stream, rmsnorm=True)
+            mark("hq_gate_up")
+            q.int4_linear_swiglu(xq, xs, *self.gate_up_il, act=act, stream=stream)
+            mark("gemm_gate_up")
+        else:
+            gu = self.gu[r0:r1]
+            linear(gu_s, o, True, gu)
+            q.swiglu(gu, act=act, stream=stream)
+            mark("swiglu")
         linear(down_s, act, False, self.out[r0:r1], residual=o)
 
     def run_device(self, inputs: dict, stream=None, events=None):

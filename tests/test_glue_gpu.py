@@ -68,6 +68,21 @@ def test_swiglu(q):
     assert P.max_fp16_ulp(act.cpu().numpy(), ref) <= 2
 
 
+def test_linear_swiglu_fused(q):
+    M, F, K = 300, 448, 4096
+    xq = synth.packed_weight_codes(M, K, 1, DEV)
+    wq = synth.packed_weight_codes(2 * F, K, 2, DEV)
+    xs = torch.rand(M, device=DEV) * 0.02 + 0.001
+    ws = synth.weight_scales(2 * F, 3, DEV)
+    act = q.int4_linear_swiglu(xq, xs, *q.interleave_gate_up(wq, ws))
+    ref = oglue.linear_swiglu(P.unpack_signed(xq.cpu().numpy()), xs.cpu().numpy(), P.unpack_signed(wq.cpu().numpy()),
+                              ws.cpu().numpy(), F)
+    assert P.max_fp16_ulp(act.cpu().numpy(), ref) <= 2
+    # unfused path (GEMM -> fp16 gate/up -> SwiGLU kernel) agrees within fp16 rounding
+    act2 = q.swiglu(q.int4_linear(xq, xs, wq, ws))
+    assert P.frob_rel(act2.cpu().numpy(), act.cpu().numpy()) < 2e-3
+
+
 def _layer_weights(S, device, seed=2000):
     from paper_2404_00456_b200.runtime import QuaRotLayer
     dims = {"qkv": (S["qkv"], S["hidden"]), "o": (S["hidden"], S["hidden"]), "gate_up": (2 * S["ffn"], S["hidden"]),
@@ -135,16 +150,18 @@ def _chain_check(q, S, T, rows, end_to_end: bool):
     ocols = np.sort(rng.choice(S["hidden"], size=min(256, S["hidden"]), replace=False))
     g_o = step.o[rt].cpu().numpy()
     assert P.frob_rel(g_o[:, ocols], lin_ref(cz, sz, "o", ocols, xh[:, ocols])) <= P.FROB_REL
-    # --- stage D: RMSNorm+quant(o) -> gate/up GEMM
+    # --- stage D+E: RMSNorm+quant(o) -> gate/up GEMM with SwiGLU fused in the epilogue
     co, _, so = oglue.rmsnorm_quant(g_o.astype(np.float64))
     fcols = np.sort(rng.choice(F, size=min(128, F), replace=False))
     gucols = np.concatenate([fcols, F + fcols])
-    g_gu = step.gu[rt].cpu().numpy()
-    assert P.frob_rel(g_gu[:, gucols], lin_ref(co, so, "gate_up", gucols)) <= P.FROB_REL
-    # --- stage E: SwiGLU
+    wq_gu, ws_gu = w["gate_up"]
+    gct = torch.as_tensor(gucols, device=DEV)
+    ref_act = oglue.linear_swiglu(co, so, oquant.unpack_int4_signed(wq_gu[gct].cpu().numpy()),
+                                  ws_gu[gct].cpu().numpy(), len(fcols))
     g_act = step.act[rt].cpu().numpy()
-    ref_act = oglue.swiglu(g_gu[:, :F].astype(np.float64), g_gu[:, F:].astype(np.float64)).astype(np.float16)
-    assert P.max_fp16_ulp(g_act, ref_act) <= 2
+    # (the oracle re-quantizes the GPU's o, so an allowed +-1 code flip can move a near-zero
+    # output by many ulps: the per-linear bar, relative Frobenius, applies)
+    assert P.frob_rel(g_act[:, fcols], ref_act) <= P.FROB_REL
     # --- stage F: FULL Hadamard + quant -> down GEMM + residual o
     ca, _, sa = olayer.hadamard_quant(g_act.astype(np.float64), "full", d)
     dcols = np.sort(rng.choice(S["hidden"], size=min(256, S["hidden"]), replace=False))
