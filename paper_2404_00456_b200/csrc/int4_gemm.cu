@@ -44,14 +44,18 @@ constexpr int BM = 256;            // pair tile rows (128 per CTA)
 constexpr int BMC = 128;
 constexpr int BN = 256;            // pair tile cols (128 B rows per CTA)
 constexpr int BNC = 128;
-constexpr int BK = 128;            // int8 elements per k-block
-constexpr int BKP = BK / 2;        // packed bytes per row per k-block
-constexpr int SSTAGES = 6;         // packed staging ring (TMA destination)
-constexpr int OSTAGES = 7;         // widened operand ring (TMEM A: 7 x 32 columns + smem B)
-constexpr int SA_BYTES = BMC * BKP;                 // 8 KB packed A
-constexpr int SB_BYTES = BNC * BKP;                 // 8 KB packed B
-constexpr int SSTAGE_BYTES = SA_BYTES + SB_BYTES;   // 16 KB
-constexpr int OB_BYTES = BNC * BK;                  // 16 KB widened B (SW128 K-major)
+constexpr int BK = 256;            // int8 elements per k-block (8 MMAs of K = 32)
+constexpr int BKP = BK / 2;        // packed bytes per row per k-block (128 B: one TMA SWIZZLE_128B row)
+constexpr int CPR = BKP / 16;      // 16-byte packed chunks per row per k-block
+constexpr int KATOMS = BK / 128;   // 128-byte K-major swizzle atoms per widened row
+constexpr int SSTAGES = 4;         // packed staging ring (TMA destination)
+constexpr int OSTAGES = 3;         // widened operand ring (TMEM A: 3 x 64 columns + smem B)
+constexpr int A_COLS = BK / 4;                      // TMEM columns per A stage (4 int8 per column)
+constexpr int SA_BYTES = BMC * BKP;                 // 16 KB packed A
+constexpr int SB_BYTES = BNC * BKP;                 // 16 KB packed B
+constexpr int SSTAGE_BYTES = SA_BYTES + SB_BYTES;   // 32 KB
+constexpr int OB_BYTES = BNC * BK;                  // 32 KB widened B: KATOMS x [128 rows][128 B] SW128
+static_assert(256 + OSTAGES * A_COLS <= 512, "TMEM budget");
 constexpr int NUM_EPI_WARPS = 8;                    // warps 0..7: TMEM lane quarter w % 4, column half w / 4
 constexpr int A_WARP0 = 8;                          // warps 8..11
 constexpr int B_WARP0 = 12;                         // warps 12..19: two groups of 4, alternating k-blocks
@@ -60,7 +64,7 @@ constexpr int MMA_WARP = 21;
 constexpr int NUM_THREADS = 22 * 32;
 constexpr int TMEM_COLS = 512;
 constexpr int ACC_COL = 0;                          // accumulator: columns [0, 256)
-constexpr int A_COL0 = 256;                         // A stages: 32 columns each
+constexpr int A_COL0 = 256;                         // A stages: A_COLS columns each
 constexpr int GROUP_M = 8;                          // pair-rows per raster group
 constexpr uint32_t IDESC = idesc_i8(BM, BN);
 constexpr size_t SMEM_BYTES = SSTAGES * SSTAGE_BYTES + OSTAGES * OB_BYTES + 1024 + 512;
@@ -225,7 +229,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   } else if (warp >= A_WARP0 && warp < A_WARP0 + 4) {
     // ===================== A widen: thread = row, packed smem -> int8 TMEM =====================
     const int row = (warp - A_WARP0) * 32 + lane;            // == TMEM lane (warp % 4 quarter)
-    const uint32_t sw = (uint32_t)((row >> 1) & 3);           // TMA SWIZZLE_64B chunk xor
+    const uint32_t sw = (uint32_t)(row & 7);                  // TMA SWIZZLE_128B chunk xor
     const uint32_t opfull_leader = map_to_rank(&op_full[0], 0);
     const uint32_t tlane = (uint32_t)((warp - A_WARP0) * 32) << 16;
     for (int it = 0; it < total; ++it) {
@@ -233,29 +237,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       const int o = it % OSTAGES;
       mbar_wait_sleep(&st_full[s], (it / SSTAGES) & 1);
       const uint32_t src = smem_u32(stage_smem + s * SSTAGE_BYTES) + (uint32_t)row * BKP;
-      uint4 w[4];
+      uint4 w[CPR];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) w[c] = lds_v4(src + (((uint32_t)c ^ sw) << 4));
-      uint32_t r[32];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {  // packed chunk c -> MMA k-step c: [16 lo | 16 hi] int8
-        r[8 * c + 0] = lo_nib16(w[c].x);
-        r[8 * c + 1] = lo_nib16(w[c].y);
-        r[8 * c + 2] = lo_nib16(w[c].z);
-        r[8 * c + 3] = lo_nib16(w[c].w);
-        r[8 * c + 4] = hi_nib16(w[c].x);
-        r[8 * c + 5] = hi_nib16(w[c].y);
-        r[8 * c + 6] = hi_nib16(w[c].z);
-        r[8 * c + 7] = hi_nib16(w[c].w);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&st_empty[s]);
+      for (int c = 0; c < CPR; ++c) w[c] = lds_v4(src + (((uint32_t)c ^ sw) << 4));
       mbar_wait_sleep(&op_empty[o], ((it / OSTAGES) & 1) ^ 1);
       tc_fence_after();
-      if (kDbg != 2) {
-        QR_TMEM_ST32(tmem_base + tlane + (uint32_t)(A_COL0 + 32 * o), r);
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int half = 0; half < CPR / 4; ++half) {
+        uint32_t r[32];
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {  // packed chunk c -> MMA k-step c: [16 lo | 16 hi] int8
+          const uint4 v = w[4 * half + cc];
+          r[8 * cc + 0] = lo_nib16(v.x);
+          r[8 * cc + 1] = lo_nib16(v.y);
+          r[8 * cc + 2] = lo_nib16(v.z);
+          r[8 * cc + 3] = lo_nib16(v.w);
+          r[8 * cc + 4] = hi_nib16(v.x);
+          r[8 * cc + 5] = hi_nib16(v.y);
+          r[8 * cc + 6] = hi_nib16(v.z);
+          r[8 * cc + 7] = hi_nib16(v.w);
+        }
+        if (kDbg != 2) QR_TMEM_ST32(tmem_base + tlane + (uint32_t)(A_COL0 + A_COLS * o + 32 * half), r);
       }
+      // the staging slot is released only once every lane has consumed its loads (the stores
+      // above read the registers): an arrive does not wait for in-flight LDS, so releasing
+      // right after issuing them lets the next TMA write overtake the reads
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&st_empty[s]);
+      if (kDbg != 2) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(opfull_leader + (uint32_t)o * 8u);
@@ -272,31 +281,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       const int o = it % OSTAGES;
       mbar_wait_sleep(&st_full[s], (it / SSTAGES) & 1);
       const uint32_t src = smem_u32(stage_smem + s * SSTAGE_BYTES) + SA_BYTES;
-      uint4 w[4];
+      constexpr int CPT_B = BNC * CPR / 128;  // packed chunks per thread
+      uint4 w[CPT_B];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < CPT_B; ++i) {
         const int c = t + 128 * i;
-        const int rr = c >> 2, q = c & 3;
-        w[i] = lds_v4(src + (uint32_t)rr * BKP + ((((uint32_t)q) ^ (uint32_t)((rr >> 1) & 3)) << 4));
+        const int rr = c / CPR, q = c % CPR;
+        w[i] = lds_v4(src + (uint32_t)rr * BKP + ((((uint32_t)q) ^ (uint32_t)(rr & 7)) << 4));
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&st_empty[s]);
       mbar_wait_sleep(&op_empty[o], ((it / OSTAGES) & 1) ^ 1);
       const uint32_t dbase = smem_u32(opb_smem + o * OB_BYTES);
 #pragma unroll
-      for (int i = 0; i < (kDbg == 2 ? 0 : 4); ++i) {
+      for (int i = 0; i < (kDbg == 2 ? 0 : CPT_B); ++i) {
         const int c = t + 128 * i;
-        const int rr = c >> 2, q = c & 3;
-        const uint32_t rowb = dbase + (uint32_t)(rr >> 3) * 1024u + (uint32_t)(rr & 7) * 128u;
+        const int rr = c / CPR, q = c % CPR;
+        const int atom = q >> 2, qa = q & 3;  // K atom of 128 int8, chunk pair within the atom
+        const uint32_t rowb = dbase + (uint32_t)atom * (BNC * 128u) + (uint32_t)(rr >> 3) * 1024u +
+                              (uint32_t)(rr & 7) * 128u;
         const uint32_t swz = (uint32_t)(rr & 7);
-        sts_v4(rowb + ((((uint32_t)(2 * q)) ^ swz) << 4),
+        sts_v4(rowb + ((((uint32_t)(2 * qa)) ^ swz) << 4),
                make_uint4(lo_nib16(w[i].x), lo_nib16(w[i].y), lo_nib16(w[i].z), lo_nib16(w[i].w)));
-        sts_v4(rowb + ((((uint32_t)(2 * q + 1)) ^ swz) << 4),
+        sts_v4(rowb + ((((uint32_t)(2 * qa + 1)) ^ swz) << 4),
                make_uint4(hi_nib16(w[i].x), hi_nib16(w[i].y), hi_nib16(w[i].z), hi_nib16(w[i].w)));
       }
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(opfull_leader + (uint32_t)o * 8u);
+      if (lane == 0) {
+        mbar_arrive(&st_empty[s]);  // after the STS consumed the loaded registers (see A widen)
+        mbar_arrive_cluster(opfull_leader + (uint32_t)o * 8u);
+      }
     }
   } else if (warp == MMA_WARP) {
     // ===================== MMA issuer (leader CTA, one thread) =====================
@@ -311,10 +324,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           if (!kMmaOnly) mbar_wait(&op_full[o], (it / OSTAGES) & 1);
           tc_fence_after();
           const uint64_t b_desc = umma_desc_sw128(smem_u32(opb_smem + o * OB_BYTES));
-          const uint32_t a_tmem = tmem_base + (uint32_t)(A_COL0 + 32 * o);
+          const uint32_t a_tmem = tmem_base + (uint32_t)(A_COL0 + A_COLS * o);
 #pragma unroll
-          for (int k = 0; k < BK / 32; ++k)
-            mma_i8_ts_2sm(d_tmem, a_tmem + (uint32_t)(8 * k), b_desc + (uint64_t)(2 * k), IDESC,
+          for (int k = 0; k < BK / 32; ++k)  // atom k/4 at +16 KB, 32 bytes along K within it
+            mma_i8_ts_2sm(d_tmem, a_tmem + (uint32_t)(8 * k),
+                          b_desc + (uint64_t)((k >> 2) * (BNC * 128 / 16) + 2 * (k & 3)), IDESC,
                           (kb | k) != 0 ? 1u : 0u);
           if (!kMmaOnly) mma_commit_pair(&op_empty[o]);
         }
@@ -462,9 +476,9 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// 2-D map over packed INT4 rows: [rows][K/2 bytes] with row pitch ld bytes; box 64 B x 128
-// rows, SWIZZLE_64B (16-byte chunk c of row r lands at chunk c ^ ((r >> 1) & 3)); rows past
-// the end are zero-filled.
+// 2-D map over packed INT4 rows: [rows][K/2 bytes] with row pitch ld bytes; box 128 B x 128
+// rows, SWIZZLE_128B (16-byte chunk c of row r lands at chunk c ^ (r & 7)); rows past the end
+// are zero-filled.
 bool make_packed_map(CUtensorMap* map, const uint8_t* base, int64_t rows, int64_t kbytes, int64_t ld) {
   auto fn = encode_fn();
   if (!fn) return false;
@@ -473,7 +487,7 @@ bool make_packed_map(CUtensorMap* map, const uint8_t* base, int64_t rows, int64_
   cuuint32_t box[2] = {(cuuint32_t)gemm::BKP, 128u};
   cuuint32_t estr[2] = {1u, 1u};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -513,7 +527,7 @@ static cudaError_t launch_gemm_impl(const uint8_t* xq, const float* xs, int64_t 
   p.ld_out = ld_out;
   p.num_m = (int)((M + BM - 1) / BM);
   p.num_n = (int)((N + BN - 1) / BN);
-  p.num_kb = (int)(K / BK);
+  p.num_kb = (int)((K + BK - 1) / BK);  // a K % 256 == 128 tail is zero-filled by the TMA
   p.num_tiles = p.num_m * p.num_n;
   const int max_pairs = num_sms_current() / 2;
   const int pairs = p.num_tiles < max_pairs ? p.num_tiles : max_pairs;

@@ -112,6 +112,24 @@ def test_int4_gemm_s32_bit_exact(q, M, N, K):
     assert np.array_equal(acc.cpu().numpy().astype(np.int64), ref)
 
 
+@pytest.mark.parametrize("M,N,K", [(2085, 4120, 4096), (1100, 8200, 2176)])
+def test_int4_gemm_multi_tile_full_matrix(q, M, N, K):
+    # more 256x256 tiles than CTA pairs (>= 2 tiles per persistent pair), so the staging and
+    # operand rings run across tile boundaries; ragged M and N, and a K % 256 == 128 tail.
+    # Every element is checked: a ring race corrupts ~1 % of entries by one k-step.
+    xq = _rand_codes_packed(M, K, seed=M)
+    wq = _rand_codes_packed(N, K, seed=N + 1)
+    xs = torch.rand(M, device=DEV) * 0.1 + 0.01
+    ws = synth.weight_scales(N, seed=9, device=DEV)
+    acc = q.int4_matmul_s32(xq, wq)
+    y = q.int4_linear(xq, xs, wq, ws)
+    torch.cuda.synchronize()
+    ref = ogemm.int_matmul_exact_f64(P.unpack_signed(xq.cpu().numpy()), P.unpack_signed(wq.cpu().numpy()))
+    assert np.array_equal(acc.cpu().numpy().astype(np.int64), ref)
+    yref = ogemm.dequant_epilogue(ref, xs.cpu().numpy(), ws.cpu().numpy())
+    assert P.max_fp16_ulp(y.cpu().numpy(), yref) <= 2
+
+
 def test_int4_gemm_extreme_codes_bit_exact(q):
     # all +-7: the largest accumulators (|acc| = 49 K); checks the x256 scaling path
     M, N, K = 130, 264, 28672
