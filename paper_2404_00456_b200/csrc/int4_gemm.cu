@@ -48,8 +48,20 @@ constexpr int BK = 256;            // int8 elements per k-block (8 MMAs of K = 3
 constexpr int BKP = BK / 2;        // packed bytes per row per k-block (128 B: one TMA SWIZZLE_128B row)
 constexpr int CPR = BKP / 16;      // 16-byte packed chunks per row per k-block
 constexpr int KATOMS = BK / 128;   // 128-byte K-major swizzle atoms per widened row
-constexpr int SSTAGES = 4;         // packed staging ring (TMA destination)
-constexpr int OSTAGES = 3;         // widened operand ring (TMEM A: 3 x 64 columns + smem B)
+#ifndef QR_GEMM_SSTAGES
+#define QR_GEMM_SSTAGES 4
+#endif
+#ifndef QR_GEMM_OSTAGES
+#define QR_GEMM_OSTAGES 3
+#endif
+#ifndef QR_OPWAIT
+#define QR_OPWAIT mbar_wait_sleep
+#endif
+constexpr int SSTAGES = QR_GEMM_SSTAGES;  // packed staging ring (TMA destination)
+// the two B-widen groups take alternate k-blocks: with an even ring each staging slot is always
+// read by the same group, so no waiter can run two phases ahead of a slot (parity aliasing)
+static_assert(QR_GEMM_SSTAGES % 2 == 0, "staging ring must be even");
+constexpr int OSTAGES = QR_GEMM_OSTAGES;  // widened operand ring (TMEM A: 64 columns + smem B each)
 constexpr int A_COLS = BK / 4;                      // TMEM columns per A stage (4 int8 per column)
 constexpr int SA_BYTES = BMC * BKP;                 // 16 KB packed A
 constexpr int SB_BYTES = BNC * BKP;                 // 16 KB packed B
@@ -67,7 +79,8 @@ constexpr int ACC_COL = 0;                          // accumulator: columns [0, 
 constexpr int A_COL0 = 256;                         // A stages: A_COLS columns each
 constexpr int GROUP_M = 8;                          // pair-rows per raster group
 constexpr uint32_t IDESC = idesc_i8(BM, BN);
-constexpr size_t SMEM_BYTES = SSTAGES * SSTAGE_BYTES + OSTAGES * OB_BYTES + 1024 + 512;
+constexpr size_t SMEM_BYTES = SSTAGES * SSTAGE_BYTES + OSTAGES * OB_BYTES + 1024 + 512 + BN * 4;
+static_assert(SMEM_BYTES <= 232448, "227 KB dynamic smem");
 
 struct Params {
   const float* x_scale;
@@ -92,6 +105,8 @@ QR_DEVICE void tile_coords(const Params& p, int t, int& mb, int& nb) {
 QR_DEVICE uint32_t lo_nib16(uint32_t w) { return (w << 4) & 0xF0F0F0F0u; }
 QR_DEVICE uint32_t hi_nib16(uint32_t w) { return w & 0xF0F0F0F0u; }
 
+// named barrier over the 8 epilogue warps (id 1; id 0 is __syncthreads)
+QR_DEVICE void epi_bar_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 QR_DEVICE uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -150,7 +165,7 @@ QR_DEVICE void mma_commit_pair(uint64_t* bar) {
       "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])                      \
       : "memory")
 
-template <bool kS32, int kDbg = 0>  // kDbg: 0 normal; roofline probes: 1 MMA only, 2 no widening, 3 no TMA
+template <bool kS32, int kDbg = 0>  // kDbg: 0 normal; roofline probes: 1 MMA only, 2 no widening, 3 no TMA, 4 no fp16 stores
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     int4_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const Params p) {
@@ -166,6 +181,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   uint64_t* t_full = op_empty + OSTAGES;             // MMA commit -> epilogue
   uint64_t* t_empty = t_full + 1;                    // epilogues of both CTAs -> leader MMA
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(t_empty + 1);
+  float* ws_smem = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 512);  // [BN] tile's w_scale
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -240,7 +256,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       uint4 w[CPR];
 #pragma unroll
       for (int c = 0; c < CPR; ++c) w[c] = lds_v4(src + (((uint32_t)c ^ sw) << 4));
-      mbar_wait_sleep(&op_empty[o], ((it / OSTAGES) & 1) ^ 1);
+      QR_OPWAIT(&op_empty[o], ((it / OSTAGES) & 1) ^ 1);
       tc_fence_after();
 #pragma unroll
       for (int half = 0; half < CPR / 4; ++half) {
@@ -275,34 +291,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     // that drains its STS) overlaps the other group's loads and stores
     const int grp = (warp - B_WARP0) >> 2;
     const int t = threadIdx.x - (B_WARP0 + 4 * grp) * 32;  // 0..127
+    // thread t owns packed chunk q = t % 8 of rows t / 8 + 16 i (i < CPT_B): the swizzle phase
+    // (row & 7) and the chunk are the same for all i, so every address is a base + immediate.
+    // Widened: chunk q -> K atom q / 4, int8 chunks 2 (q % 4) (lo nibbles) and +1 (hi nibbles)
+    // of a [8-row x 128 B] SW128 group; row r at (r / 8) * 1024 + (r % 8) * 128.
+    constexpr int CPT_B = BNC * CPR / 128;  // packed chunks per thread
+    static_assert(CPR == 8 && BNC % 16 == 0, "B widen mapping assumes 8 chunks per row");
+    const uint32_t rr0 = (uint32_t)t >> 3, q = (uint32_t)t & 7u, swz = rr0 & 7u;
+    const uint32_t src_off = rr0 * BKP + ((q ^ swz) << 4);
+    const uint32_t atom = q >> 2, qa = q & 3u, odd = atom & 1u;
+    const uint32_t dst_row = atom * (BNC * 128u) + (rr0 >> 3) * 1024u + swz * 128u;
+    // lanes 8j..8j+7 share a row and form one 128-byte store phase: atom-0 lanes store their lo
+    // chunk first and atom-1 lanes their hi chunk, so each phase covers all 8 chunk slots of
+    // the bank window (the same order for both atoms is a 2-way bank conflict)
+    const uint32_t d0 = ((2u * qa + odd) ^ swz) << 4, d1 = ((2u * qa + (odd ^ 1u)) ^ swz) << 4;
+    const uint32_t sh0 = odd ? 0u : 4u, sh1 = odd ? 4u : 0u;  // lo = (w << 4) & F0.., hi = w & F0..
     const uint32_t opfull_leader = map_to_rank(&op_full[0], 0);
     for (int it = grp; it < total; it += 2) {
       const int s = it % SSTAGES;
       const int o = it % OSTAGES;
       mbar_wait_sleep(&st_full[s], (it / SSTAGES) & 1);
-      const uint32_t src = smem_u32(stage_smem + s * SSTAGE_BYTES) + SA_BYTES;
-      constexpr int CPT_B = BNC * CPR / 128;  // packed chunks per thread
+      const uint32_t src = smem_u32(stage_smem + s * SSTAGE_BYTES) + SA_BYTES + src_off;
       uint4 w[CPT_B];
 #pragma unroll
-      for (int i = 0; i < CPT_B; ++i) {
-        const int c = t + 128 * i;
-        const int rr = c / CPR, q = c % CPR;
-        w[i] = lds_v4(src + (uint32_t)rr * BKP + ((((uint32_t)q) ^ (uint32_t)(rr & 7)) << 4));
-      }
-      mbar_wait_sleep(&op_empty[o], ((it / OSTAGES) & 1) ^ 1);
-      const uint32_t dbase = smem_u32(opb_smem + o * OB_BYTES);
+      for (int i = 0; i < CPT_B; ++i) w[i] = lds_v4(src + (uint32_t)i * (16u * BKP));
+      QR_OPWAIT(&op_empty[o], ((it / OSTAGES) & 1) ^ 1);
+      const uint32_t dst = smem_u32(opb_smem + o * OB_BYTES) + dst_row;
 #pragma unroll
       for (int i = 0; i < (kDbg == 2 ? 0 : CPT_B); ++i) {
-        const int c = t + 128 * i;
-        const int rr = c / CPR, q = c % CPR;
-        const int atom = q >> 2, qa = q & 3;  // K atom of 128 int8, chunk pair within the atom
-        const uint32_t rowb = dbase + (uint32_t)atom * (BNC * 128u) + (uint32_t)(rr >> 3) * 1024u +
-                              (uint32_t)(rr & 7) * 128u;
-        const uint32_t swz = (uint32_t)(rr & 7);
-        sts_v4(rowb + ((((uint32_t)(2 * qa)) ^ swz) << 4),
-               make_uint4(lo_nib16(w[i].x), lo_nib16(w[i].y), lo_nib16(w[i].z), lo_nib16(w[i].w)));
-        sts_v4(rowb + ((((uint32_t)(2 * qa + 1)) ^ swz) << 4),
-               make_uint4(hi_nib16(w[i].x), hi_nib16(w[i].y), hi_nib16(w[i].z), hi_nib16(w[i].w)));
+        const uint4 v = w[i];
+        sts_v4(dst + (uint32_t)i * 2048u + d0,
+               make_uint4((v.x << sh0) & 0xF0F0F0F0u, (v.y << sh0) & 0xF0F0F0F0u, (v.z << sh0) & 0xF0F0F0F0u,
+                          (v.w << sh0) & 0xF0F0F0F0u));
+        sts_v4(dst + (uint32_t)i * 2048u + d1,
+               make_uint4((v.x << sh1) & 0xF0F0F0F0u, (v.y << sh1) & 0xF0F0F0F0u, (v.z << sh1) & 0xF0F0F0F0u,
+                          (v.w << sh1) & 0xF0F0F0F0u));
       }
       fence_proxy_async_smem();
       __syncwarp();
@@ -343,15 +366,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     const uint32_t tempty_leader = map_to_rank(t_empty, 0);
     const int quarter = warp & 3, chalf = warp >> 2;
     const int row_in_tile = (int)rank * BMC + quarter * 32 + lane;
+    const int et = threadIdx.x;  // 0..255: epilogue warps are warps 0..7
     for (int tl = 0; tl < my_tiles; ++tl) {
       int mb, nb;
       tile_coords(p, pair + tl * num_pairs, mb, nb);
-      mbar_wait_sleep(t_full, tl & 1);
-      tc_fence_after();
       const int64_t m = (int64_t)mb * BM + row_in_tile;
       const bool row_ok = m < p.M;
+      // scales are fetched while the accumulator is still being computed, so the TMEM drain
+      // (which gates the next tile's MMAs) never waits on a global load
       float sx = 0.f;
-      if (!kS32 && row_ok) sx = __ldg(p.x_scale + m);
+      if (!kS32) {
+        if (row_ok) sx = __ldg(p.x_scale + m);
+        const int64_t n = (int64_t)nb * BN + et;
+        ws_smem[et] = n < p.N ? __ldg(p.w_scale + n) : 0.f;
+        epi_bar_sync();
+      }
+      mbar_wait_sleep(t_full, tl & 1);
+      tc_fence_after();
       const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + ACC_COL + (uint32_t)(chalf * 128);
       uint32_t r[2][16];
       QR_TMEM_LD16(taddr, r[0]);
@@ -365,6 +396,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(tempty_leader);
         }
+        const float* wsc = ws_smem + chalf * 128 + cc * 16;  // this chunk's 16 column scales
         const uint32_t* rc = r[cc & 1];
         const int64_t n0 = (int64_t)nb * BN + chalf * 128 + cc * 16;
         if (row_ok) {
@@ -381,10 +413,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           } else if (p.swiglu) {
             // chunk = [8 gate | 8 up] columns of features n0/2 .. n0/2 + 7 (interleaved W rows)
             if (n0 < p.N) {
-              const float4 g0 = __ldg(reinterpret_cast<const float4*>(p.w_scale + n0));
-              const float4 g1 = __ldg(reinterpret_cast<const float4*>(p.w_scale + n0 + 4));
-              const float4 u0 = __ldg(reinterpret_cast<const float4*>(p.w_scale + n0 + 8));
-              const float4 u1 = __ldg(reinterpret_cast<const float4*>(p.w_scale + n0 + 12));
+              const float4 g0 = *reinterpret_cast<const float4*>(wsc);
+              const float4 g1 = *reinterpret_cast<const float4*>(wsc + 4);
+              const float4 u0 = *reinterpret_cast<const float4*>(wsc + 8);
+              const float4 u1 = *reinterpret_cast<const float4*>(wsc + 12);
               const float sg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
               const float su[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
               uint32_t h[4];
@@ -409,8 +441,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
             for (int g = 0; g < 2; ++g) {
               if (n0 + g * 8 < p.N) {
-                const float4 s0 = __ldg(reinterpret_cast<const float4*>(p.w_scale + n0 + g * 8));
-                const float4 s1 = __ldg(reinterpret_cast<const float4*>(p.w_scale + n0 + g * 8 + 4));
+                const float4 s0 = *reinterpret_cast<const float4*>(wsc + g * 8);
+                const float4 s1 = *reinterpret_cast<const float4*>(wsc + g * 8 + 4);
                 const float swv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
                 uint32_t h[4];
                 uint4 rres = make_uint4(0, 0, 0, 0);
@@ -428,12 +460,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                   __half2 hv = __floats2half2_rn(v0, v1);
                   h[e] = *reinterpret_cast<uint32_t*>(&hv);
                 }
-                *reinterpret_cast<uint4*>(dst + g * 8) = make_uint4(h[0], h[1], h[2], h[3]);
+                if (kDbg != 4 || (h[0] == 0x7c017c01u && h[1] == 0x7c017c01u))  // probe 4: no stores
+                  *reinterpret_cast<uint4*>(dst + g * 8) = make_uint4(h[0], h[1], h[2], h[3]);
               }
             }
           }
         }
       }
+      if (!kS32) epi_bar_sync();  // every warp is done with ws_smem before the next tile's fill
     }
   }
 
@@ -531,9 +565,11 @@ static cudaError_t launch_gemm_impl(const uint8_t* xq, const float* xs, int64_t 
   p.num_tiles = p.num_m * p.num_n;
   const int max_pairs = num_sms_current() / 2;
   const int pairs = p.num_tiles < max_pairs ? p.num_tiles : max_pairs;
-  if (g_gemm_debug_mode >= 1 && g_gemm_debug_mode <= 3) {
-    auto kern = g_gemm_debug_mode == 1 ? int4_gemm_kernel<kS32, 1>
-                                        : (g_gemm_debug_mode == 2 ? int4_gemm_kernel<kS32, 2> : int4_gemm_kernel<kS32, 3>);
+  if (g_gemm_debug_mode >= 1 && g_gemm_debug_mode <= 4) {
+    auto kern = g_gemm_debug_mode == 1   ? int4_gemm_kernel<kS32, 1>
+                : g_gemm_debug_mode == 2 ? int4_gemm_kernel<kS32, 2>
+                : g_gemm_debug_mode == 3 ? int4_gemm_kernel<kS32, 3>
+                                         : int4_gemm_kernel<kS32, 4>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
     if (e != cudaSuccess) return e;
     kern<<<2 * pairs, NUM_THREADS, SMEM_BYTES, stream>>>(ma, mb, p);

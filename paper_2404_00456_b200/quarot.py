@@ -13,7 +13,8 @@ import os
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libquarot.so")
+# QUAROT_LIB: an alternative build of the same library (kernel-variant experiments)
+LIB_PATH = os.environ.get("QUAROT_LIB") or os.path.join(_PKG, "libquarot.so")
 
 NONE, FULL, ACROSS_HEADS = 0, 1, 2
 RMSNORM = 0x100  # mode flag: scale-free RMSNorm fused into the NONE quantizer

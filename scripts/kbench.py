@@ -54,6 +54,26 @@ def main():
             res["gate_up_" + name] = {"ms": ms, "tops": 2 * M * N * K / ms / 1e9}
             print(name, json.dumps(res["gate_up_" + name]), flush=True)
         q.lib().quarot_debug_gemm_mode(0)
+    if "ksweep" in a.what:
+        # per-tile fixed cost: time(K) = tiles/pairs * (t_tile0 + t_kb * K / 256)
+        import ctypes
+        q.lib().quarot_debug_gemm_mode.argtypes = [ctypes.c_int]
+        Ms, N = 65536, 8192
+        xq_big = synth.packed_weight_codes(Ms, 32768, 1, dev)
+        wq_big = synth.packed_weight_codes(N, 32768, 2, dev)
+        xs = torch.rand(Ms, device=dev) + 0.5
+        ws = synth.weight_scales(N, 3, dev)
+        y = torch.empty(Ms, N, dtype=torch.float16, device=dev)
+        for mode in [int(m) for m in os.environ.get("KSWEEP_MODES", "0,1").split(",")]:
+            q.lib().quarot_debug_gemm_mode(mode)
+            for K in (8192, 16384, 32768):
+                xq, wq = xq_big[:, : K // 2], wq_big[:, : K // 2]
+                ms = timeit(lambda: q.int4_linear(xq, xs, wq, ws, y=y), a.iters)
+                tiles_per_pair = (Ms // 256) * (N // 256) / 74
+                print(json.dumps({"mode": mode, "K": K, "ms": ms, "tops": 2 * Ms * N * K / ms / 1e9,
+                                  "us_per_tile": ms * 1e3 / tiles_per_pair}), flush=True)
+        q.lib().quarot_debug_gemm_mode(0)
+        del xq_big, wq_big, y
     if "gemm" in a.what:
         xq_big = synth.packed_weight_codes(M, 28672, 1, dev)
         for name, N, K in (("qkv", 10240, 8192), ("o", 8192, 8192), ("gate_up", 57344, 8192), ("down", 8192, 28672)):
