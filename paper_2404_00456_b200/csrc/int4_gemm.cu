@@ -73,7 +73,13 @@ constexpr int A_WARP0 = 8;                          // warps 8..11
 constexpr int B_WARP0 = 12;                         // warps 12..19: two groups of 4, alternating k-blocks
 constexpr int TMA_WARP = 20;
 constexpr int MMA_WARP = 21;
-constexpr int NUM_THREADS = 22 * 32;
+constexpr int NUM_THREADS = 24 * 32;                // warps 22, 23 only pad warpgroup 5
+// per-role register budgets (setmaxnreg; the launch gives every warp 80): warpgroup 5 (TMA,
+// MMA, 2 idle) and the B-widen warpgroups give registers to the epilogue, which holds three
+// 32-column accumulator chunks at once.  6144 + 6144 freed = 12288 = 256 x (128 - 80).
+constexpr int EPI_REGS = 128;
+constexpr int BW_REGS = 56;
+constexpr int CTL_REGS = 32;
 constexpr int TMEM_COLS = 512;
 constexpr int ACC_COL = 0;                          // accumulator: columns [0, 256)
 constexpr int A_COL0 = 256;                         // A stages: A_COLS columns each
@@ -105,8 +111,16 @@ QR_DEVICE void tile_coords(const Params& p, int t, int& mb, int& nb) {
 QR_DEVICE uint32_t lo_nib16(uint32_t w) { return (w << 4) & 0xF0F0F0F0u; }
 QR_DEVICE uint32_t hi_nib16(uint32_t w) { return w & 0xF0F0F0F0u; }
 
+// fp16_rn(lo) | fp16_rn(hi) << 16 in a register
+QR_DEVICE uint32_t pack_half2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
 // named barrier over the 8 epilogue warps (id 1; id 0 is __syncthreads)
 QR_DEVICE void epi_bar_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+#define QR_SETMAXNREG_INC(n) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(n))
+#define QR_SETMAXNREG_DEC(n) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(n))
 QR_DEVICE uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -165,6 +179,80 @@ QR_DEVICE void mma_commit_pair(uint64_t* bar) {
       "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])                      \
       : "memory")
 
+// Converts and stores one 32-column accumulator chunk of one row (columns n0 .. n0 + 31;
+// wsc = their 32 weight scales in smem).  fp16: y = fp16_rn(fp32(acc) * s_x * s_w [+ r]);
+// s32: raw accumulators; SwiGLU: the chunk is [8 gate | 8 up] x 2 (interleaved weight rows)
+// and 16 act = silu(g) * u values go to column n0 / 2.
+template <bool kS32, int kDbg>
+QR_DEVICE void epi_chunk(const Params& p, const uint32_t (&rc)[32], int64_t m, bool row_ok, int64_t n0, float sx,
+                         const float* wsc) {
+  if (!row_ok) return;
+  if constexpr (kS32) {
+    int32_t* dst = reinterpret_cast<int32_t*>(p.out) + m * p.ld_out + n0;
+#pragma unroll
+    for (int g = 0; g < 8; ++g)
+      if (n0 + g * 4 < p.N)
+        *reinterpret_cast<int4*>(dst + g * 4) = make_int4((int32_t)rc[4 * g] >> 8, (int32_t)rc[4 * g + 1] >> 8,
+                                                          (int32_t)rc[4 * g + 2] >> 8, (int32_t)rc[4 * g + 3] >> 8);
+  } else if (p.swiglu) {
+#pragma unroll
+    for (int hgrp = 0; hgrp < 2; ++hgrp) {
+      const int64_t nn = n0 + 16 * hgrp;
+      if (nn < p.N) {
+        const float* sg = wsc + 16 * hgrp;
+        uint32_t h[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float a[2];
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int c = 2 * e + j;
+            const float gv = ((float)((int32_t)rc[16 * hgrp + c] >> 8) * sx) * sg[c];
+            const float uv = ((float)((int32_t)rc[16 * hgrp + 8 + c] >> 8) * sx) * sg[8 + c];
+            a[j] = gv / (1.f + __expf(-gv)) * uv;
+          }
+          h[e] = pack_half2(a[0], a[1]);
+        }
+        *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(p.out) + m * p.ld_out + (nn >> 1)) =
+            make_uint4(h[0], h[1], h[2], h[3]);
+      }
+    }
+  } else {
+    __half* dst = reinterpret_cast<__half*>(p.out) + m * p.ld_out + n0;
+    uint4 rres0 = make_uint4(0, 0, 0, 0), rres1 = rres0, rres2 = rres0, rres3 = rres0;
+    if (p.residual) {  // all four loads in flight at once
+      const __half* rrow = p.residual + m * p.ld_r + n0;
+      if (n0 < p.N) rres0 = *reinterpret_cast<const uint4*>(rrow);
+      if (n0 + 8 < p.N) rres1 = *reinterpret_cast<const uint4*>(rrow + 8);
+      if (n0 + 16 < p.N) rres2 = *reinterpret_cast<const uint4*>(rrow + 16);
+      if (n0 + 24 < p.N) rres3 = *reinterpret_cast<const uint4*>(rrow + 24);
+    }
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      if (n0 + g * 8 < p.N) {
+        const float4 s0 = *reinterpret_cast<const float4*>(wsc + g * 8);
+        const float4 s1 = *reinterpret_cast<const float4*>(wsc + g * 8 + 4);
+        const float swv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+        const uint4 rr = g == 0 ? rres0 : g == 1 ? rres1 : g == 2 ? rres2 : rres3;
+        const uint32_t rw[4] = {rr.x, rr.y, rr.z, rr.w};
+        uint32_t h[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float v0 = ((float)((int32_t)rc[8 * g + 2 * e] >> 8) * sx) * swv[2 * e];
+          float v1 = ((float)((int32_t)rc[8 * g + 2 * e + 1] >> 8) * sx) * swv[2 * e + 1];
+          if (p.residual) {
+            v0 += __half2float(__ushort_as_half((unsigned short)(rw[e] & 0xFFFFu)));
+            v1 += __half2float(__ushort_as_half((unsigned short)(rw[e] >> 16)));
+          }
+          h[e] = pack_half2(v0, v1);
+        }
+        if (kDbg != 4 || (h[0] == 0x7c017c01u && h[1] == 0x7c017c01u))  // probe 4: no stores
+          *reinterpret_cast<uint4*>(dst + g * 8) = make_uint4(h[0], h[1], h[2], h[3]);
+      }
+    }
+  }
+}
+
 template <bool kS32, int kDbg = 0>  // kDbg: 0 normal; roofline probes: 1 MMA only, 2 no widening, 3 no TMA, 4 no fp16 stores
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     int4_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -220,149 +308,160 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   const int total = my_tiles * p.num_kb;
 
   constexpr bool kMmaOnly = kDbg == 1;
-  if (kMmaOnly && warp != MMA_WARP && warp >= NUM_EPI_WARPS) {
-    // roofline probe: no producers
-  } else if (warp == TMA_WARP) {
-    // ===================== TMA producer: packed k-blocks -> staging ring =====================
-    if (lane == 0) {
-      for (int it = 0; it < total; ++it) {
-        const int tl = it / p.num_kb;
-        const int kb = it - tl * p.num_kb;
-        int mb, nb;
-        tile_coords(p, pair + tl * num_pairs, mb, nb);
-        const int s = it % SSTAGES;
-        mbar_wait_sleep(&st_empty[s], ((it / SSTAGES) & 1) ^ 1);
-        if (kDbg == 3) {
-          mbar_arrive(&st_full[s]);
-        } else {
-          mbar_expect_tx(&st_full[s], SSTAGE_BYTES);
-          const uint32_t dst = smem_u32(stage_smem + s * SSTAGE_BYTES);
-          tma_load_2d(dst, &tmA, kb * BKP, mb * BM + (int)rank * BMC, &st_full[s]);
-          tma_load_2d(dst + SA_BYTES, &tmB, kb * BKP, nb * BN + (int)rank * BNC, &st_full[s]);
-        }
-      }
-    }
-  } else if (warp >= A_WARP0 && warp < A_WARP0 + 4) {
-    // ===================== A widen: thread = row, packed smem -> int8 TMEM =====================
-    const int row = (warp - A_WARP0) * 32 + lane;            // == TMEM lane (warp % 4 quarter)
-    const uint32_t sw = (uint32_t)(row & 7);                  // TMA SWIZZLE_128B chunk xor
-    const uint32_t opfull_leader = map_to_rank(&op_full[0], 0);
-    const uint32_t tlane = (uint32_t)((warp - A_WARP0) * 32) << 16;
-    for (int it = 0; it < total; ++it) {
-      const int s = it % SSTAGES;
-      const int o = it % OSTAGES;
-      mbar_wait_sleep(&st_full[s], (it / SSTAGES) & 1);
-      const uint32_t src = smem_u32(stage_smem + s * SSTAGE_BYTES) + (uint32_t)row * BKP;
-      uint4 w[CPR];
-#pragma unroll
-      for (int c = 0; c < CPR; ++c) w[c] = lds_v4(src + (((uint32_t)c ^ sw) << 4));
-      QR_OPWAIT(&op_empty[o], ((it / OSTAGES) & 1) ^ 1);
-      tc_fence_after();
-#pragma unroll
-      for (int half = 0; half < CPR / 4; ++half) {
-        uint32_t r[32];
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {  // packed chunk c -> MMA k-step c: [16 lo | 16 hi] int8
-          const uint4 v = w[4 * half + cc];
-          r[8 * cc + 0] = lo_nib16(v.x);
-          r[8 * cc + 1] = lo_nib16(v.y);
-          r[8 * cc + 2] = lo_nib16(v.z);
-          r[8 * cc + 3] = lo_nib16(v.w);
-          r[8 * cc + 4] = hi_nib16(v.x);
-          r[8 * cc + 5] = hi_nib16(v.y);
-          r[8 * cc + 6] = hi_nib16(v.z);
-          r[8 * cc + 7] = hi_nib16(v.w);
-        }
-        if (kDbg != 2) QR_TMEM_ST32(tmem_base + tlane + (uint32_t)(A_COL0 + A_COLS * o + 32 * half), r);
-      }
-      // the staging slot is released only once every lane has consumed its loads (the stores
-      // above read the registers): an arrive does not wait for in-flight LDS, so releasing
-      // right after issuing them lets the next TMA write overtake the reads
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&st_empty[s]);
-      if (kDbg != 2) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(opfull_leader + (uint32_t)o * 8u);
-    }
-  } else if (warp >= B_WARP0 && warp < B_WARP0 + 8) {
-    // ===================== B widen: packed smem -> int8 SW128 smem =====================
-    // two groups of 4 warps take alternate k-blocks, so one group's proxy fence (a MEMBAR
-    // that drains its STS) overlaps the other group's loads and stores
-    const int grp = (warp - B_WARP0) >> 2;
-    const int t = threadIdx.x - (B_WARP0 + 4 * grp) * 32;  // 0..127
-    // thread t owns packed chunk q = t % 8 of rows t / 8 + 16 i (i < CPT_B): the swizzle phase
-    // (row & 7) and the chunk are the same for all i, so every address is a base + immediate.
-    // Widened: chunk q -> K atom q / 4, int8 chunks 2 (q % 4) (lo nibbles) and +1 (hi nibbles)
-    // of a [8-row x 128 B] SW128 group; row r at (r / 8) * 1024 + (r % 8) * 128.
-    constexpr int CPT_B = BNC * CPR / 128;  // packed chunks per thread
-    static_assert(CPR == 8 && BNC % 16 == 0, "B widen mapping assumes 8 chunks per row");
-    const uint32_t rr0 = (uint32_t)t >> 3, q = (uint32_t)t & 7u, swz = rr0 & 7u;
-    const uint32_t src_off = rr0 * BKP + ((q ^ swz) << 4);
-    const uint32_t atom = q >> 2, qa = q & 3u, odd = atom & 1u;
-    const uint32_t dst_row = atom * (BNC * 128u) + (rr0 >> 3) * 1024u + swz * 128u;
-    // lanes 8j..8j+7 share a row and form one 128-byte store phase: atom-0 lanes store their lo
-    // chunk first and atom-1 lanes their hi chunk, so each phase covers all 8 chunk slots of
-    // the bank window (the same order for both atoms is a 2-way bank conflict)
-    const uint32_t d0 = ((2u * qa + odd) ^ swz) << 4, d1 = ((2u * qa + (odd ^ 1u)) ^ swz) << 4;
-    const uint32_t sh0 = odd ? 0u : 4u, sh1 = odd ? 4u : 0u;  // lo = (w << 4) & F0.., hi = w & F0..
-    const uint32_t opfull_leader = map_to_rank(&op_full[0], 0);
-    for (int it = grp; it < total; it += 2) {
-      const int s = it % SSTAGES;
-      const int o = it % OSTAGES;
-      mbar_wait_sleep(&st_full[s], (it / SSTAGES) & 1);
-      const uint32_t src = smem_u32(stage_smem + s * SSTAGE_BYTES) + SA_BYTES + src_off;
-      uint4 w[CPT_B];
-#pragma unroll
-      for (int i = 0; i < CPT_B; ++i) w[i] = lds_v4(src + (uint32_t)i * (16u * BKP));
-      QR_OPWAIT(&op_empty[o], ((it / OSTAGES) & 1) ^ 1);
-      const uint32_t dst = smem_u32(opb_smem + o * OB_BYTES) + dst_row;
-#pragma unroll
-      for (int i = 0; i < (kDbg == 2 ? 0 : CPT_B); ++i) {
-        const uint4 v = w[i];
-        sts_v4(dst + (uint32_t)i * 2048u + d0,
-               make_uint4((v.x << sh0) & 0xF0F0F0F0u, (v.y << sh0) & 0xF0F0F0F0u, (v.z << sh0) & 0xF0F0F0F0u,
-                          (v.w << sh0) & 0xF0F0F0F0u));
-        sts_v4(dst + (uint32_t)i * 2048u + d1,
-               make_uint4((v.x << sh1) & 0xF0F0F0F0u, (v.y << sh1) & 0xF0F0F0F0u, (v.z << sh1) & 0xF0F0F0F0u,
-                          (v.w << sh1) & 0xF0F0F0F0u));
-      }
-      fence_proxy_async_smem();
-      __syncwarp();
+  // roles by warpgroup (setmaxnreg is warpgroup-wide); kMmaOnly (probe 1) idles the producers
+  if (warp >= TMA_WARP) {
+    QR_SETMAXNREG_DEC(CTL_REGS);
+    if (warp == TMA_WARP && !kMmaOnly) {
+      // ===================== TMA producer: packed k-blocks -> staging ring =====================
       if (lane == 0) {
-        mbar_arrive(&st_empty[s]);  // after the STS consumed the loaded registers (see A widen)
-        mbar_arrive_cluster(opfull_leader + (uint32_t)o * 8u);
-      }
-    }
-  } else if (warp == MMA_WARP) {
-    // ===================== MMA issuer (leader CTA, one thread) =====================
-    if (rank == 0 && lane == 0) {
-      int it = 0;
-      for (int tl = 0; tl < my_tiles; ++tl) {
-        mbar_wait(t_empty, (tl & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t d_tmem = tmem_base + ACC_COL;
-        for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
-          const int o = kMmaOnly ? 0 : it % OSTAGES;
-          if (!kMmaOnly) mbar_wait(&op_full[o], (it / OSTAGES) & 1);
-          tc_fence_after();
-          const uint64_t b_desc = umma_desc_sw128(smem_u32(opb_smem + o * OB_BYTES));
-          const uint32_t a_tmem = tmem_base + (uint32_t)(A_COL0 + A_COLS * o);
-#pragma unroll
-          for (int k = 0; k < BK / 32; ++k)  // atom k/4 at +16 KB, 32 bytes along K within it
-            mma_i8_ts_2sm(d_tmem, a_tmem + (uint32_t)(8 * k),
-                          b_desc + (uint64_t)((k >> 2) * (BNC * 128 / 16) + 2 * (k & 3)), IDESC,
-                          (kb | k) != 0 ? 1u : 0u);
-          if (!kMmaOnly) mma_commit_pair(&op_empty[o]);
+        for (int it = 0; it < total; ++it) {
+          const int tl = it / p.num_kb;
+          const int kb = it - tl * p.num_kb;
+          int mb, nb;
+          tile_coords(p, pair + tl * num_pairs, mb, nb);
+          const int s = it % SSTAGES;
+          mbar_wait_sleep(&st_empty[s], ((it / SSTAGES) & 1) ^ 1);
+          if (kDbg == 3) {
+            mbar_arrive(&st_full[s]);
+          } else {
+            mbar_expect_tx(&st_full[s], SSTAGE_BYTES);
+            const uint32_t dst = smem_u32(stage_smem + s * SSTAGE_BYTES);
+            tma_load_2d(dst, &tmA, kb * BKP, mb * BM + (int)rank * BMC, &st_full[s]);
+            tma_load_2d(dst + SA_BYTES, &tmB, kb * BKP, nb * BN + (int)rank * BNC, &st_full[s]);
+          }
         }
-        mma_commit_pair(t_full);
+      }
+    } else if (warp == MMA_WARP) {
+      // ===================== MMA issuer (leader CTA, one thread) =====================
+      if (rank == 0 && lane == 0) {
+        int it = 0;
+        for (int tl = 0; tl < my_tiles; ++tl) {
+          mbar_wait(t_empty, (tl & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem_base + ACC_COL;
+          for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
+            const int o = kMmaOnly ? 0 : it % OSTAGES;
+            if (!kMmaOnly) mbar_wait(&op_full[o], (it / OSTAGES) & 1);
+            tc_fence_after();
+            const uint64_t b_desc = umma_desc_sw128(smem_u32(opb_smem + o * OB_BYTES));
+            const uint32_t a_tmem = tmem_base + (uint32_t)(A_COL0 + A_COLS * o);
+  #pragma unroll
+            for (int k = 0; k < BK / 32; ++k)  // atom k/4 at +16 KB, 32 bytes along K within it
+              mma_i8_ts_2sm(d_tmem, a_tmem + (uint32_t)(8 * k),
+                            b_desc + (uint64_t)((k >> 2) * (BNC * 128 / 16) + 2 * (k & 3)), IDESC,
+                            (kb | k) != 0 ? 1u : 0u);
+            if (!kMmaOnly) mma_commit_pair(&op_empty[o]);
+          }
+          mma_commit_pair(t_full);
+        }
+      }
+      __syncwarp();
+    }
+  } else if (warp >= B_WARP0) {
+    QR_SETMAXNREG_DEC(BW_REGS);
+    if (!kMmaOnly) {
+      // ===================== B widen: packed smem -> int8 SW128 smem =====================
+      // two groups of 4 warps take alternate k-blocks, so one group's proxy fence (a MEMBAR
+      // that drains its STS) overlaps the other group's loads and stores
+      const int grp = (warp - B_WARP0) >> 2;
+      const int t = threadIdx.x - (B_WARP0 + 4 * grp) * 32;  // 0..127
+      // thread t owns packed chunk q = t % 8 of rows t / 8 + 16 i (i < CPT_B): the swizzle phase
+      // (row & 7) and the chunk are the same for all i, so every address is a base + immediate.
+      // Widened: chunk q -> K atom q / 4, int8 chunks 2 (q % 4) (lo nibbles) and +1 (hi nibbles)
+      // of a [8-row x 128 B] SW128 group; row r at (r / 8) * 1024 + (r % 8) * 128.
+      constexpr int CPT_B = BNC * CPR / 128;  // packed chunks per thread
+      static_assert(CPR == 8 && BNC % 16 == 0, "B widen mapping assumes 8 chunks per row");
+      const uint32_t rr0 = (uint32_t)t >> 3, q = (uint32_t)t & 7u, swz = rr0 & 7u;
+      const uint32_t src_off = rr0 * BKP + ((q ^ swz) << 4);
+      const uint32_t atom = q >> 2, qa = q & 3u, odd = atom & 1u;
+      const uint32_t dst_row = atom * (BNC * 128u) + (rr0 >> 3) * 1024u + swz * 128u;
+      // lanes 8j..8j+7 share a row and form one 128-byte store phase: atom-0 lanes store their lo
+      // chunk first and atom-1 lanes their hi chunk, so each phase covers all 8 chunk slots of
+      // the bank window (the same order for both atoms is a 2-way bank conflict)
+      const uint32_t d0 = ((2u * qa + odd) ^ swz) << 4, d1 = ((2u * qa + (odd ^ 1u)) ^ swz) << 4;
+      const uint32_t sh0 = odd ? 0u : 4u, sh1 = odd ? 4u : 0u;  // lo = (w << 4) & F0.., hi = w & F0..
+      const uint32_t opfull_leader = map_to_rank(&op_full[0], 0);
+      for (int it = grp; it < total; it += 2) {
+        const int s = it % SSTAGES;
+        const int o = it % OSTAGES;
+        mbar_wait_sleep(&st_full[s], (it / SSTAGES) & 1);
+        const uint32_t src = smem_u32(stage_smem + s * SSTAGE_BYTES) + SA_BYTES + src_off;
+        uint4 w[CPT_B];
+  #pragma unroll
+        for (int i = 0; i < CPT_B; ++i) w[i] = lds_v4(src + (uint32_t)i * (16u * BKP));
+        QR_OPWAIT(&op_empty[o], ((it / OSTAGES) & 1) ^ 1);
+        const uint32_t dst = smem_u32(opb_smem + o * OB_BYTES) + dst_row;
+  #pragma unroll
+        for (int i = 0; i < (kDbg == 2 ? 0 : CPT_B); ++i) {
+          const uint4 v = w[i];
+          sts_v4(dst + (uint32_t)i * 2048u + d0,
+                 make_uint4((v.x << sh0) & 0xF0F0F0F0u, (v.y << sh0) & 0xF0F0F0F0u, (v.z << sh0) & 0xF0F0F0F0u,
+                            (v.w << sh0) & 0xF0F0F0F0u));
+          sts_v4(dst + (uint32_t)i * 2048u + d1,
+                 make_uint4((v.x << sh1) & 0xF0F0F0F0u, (v.y << sh1) & 0xF0F0F0F0u, (v.z << sh1) & 0xF0F0F0F0u,
+                            (v.w << sh1) & 0xF0F0F0F0u));
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&st_empty[s]);  // after the STS consumed the loaded registers (see A widen)
+          mbar_arrive_cluster(opfull_leader + (uint32_t)o * 8u);
+        }
       }
     }
-    __syncwarp();
+  } else if (warp >= A_WARP0) {
+    if (!kMmaOnly) {
+      // ===================== A widen: thread = row, packed smem -> int8 TMEM =====================
+      const int row = (warp - A_WARP0) * 32 + lane;            // == TMEM lane (warp % 4 quarter)
+      const uint32_t sw = (uint32_t)(row & 7);                  // TMA SWIZZLE_128B chunk xor
+      const uint32_t opfull_leader = map_to_rank(&op_full[0], 0);
+      const uint32_t tlane = (uint32_t)((warp - A_WARP0) * 32) << 16;
+      for (int it = 0; it < total; ++it) {
+        const int s = it % SSTAGES;
+        const int o = it % OSTAGES;
+        mbar_wait_sleep(&st_full[s], (it / SSTAGES) & 1);
+        const uint32_t src = smem_u32(stage_smem + s * SSTAGE_BYTES) + (uint32_t)row * BKP;
+        uint4 w[CPR];
+  #pragma unroll
+        for (int c = 0; c < CPR; ++c) w[c] = lds_v4(src + (((uint32_t)c ^ sw) << 4));
+        QR_OPWAIT(&op_empty[o], ((it / OSTAGES) & 1) ^ 1);
+        tc_fence_after();
+  #pragma unroll
+        for (int half = 0; half < CPR / 4; ++half) {
+          uint32_t r[32];
+  #pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {  // packed chunk c -> MMA k-step c: [16 lo | 16 hi] int8
+            const uint4 v = w[4 * half + cc];
+            r[8 * cc + 0] = lo_nib16(v.x);
+            r[8 * cc + 1] = lo_nib16(v.y);
+            r[8 * cc + 2] = lo_nib16(v.z);
+            r[8 * cc + 3] = lo_nib16(v.w);
+            r[8 * cc + 4] = hi_nib16(v.x);
+            r[8 * cc + 5] = hi_nib16(v.y);
+            r[8 * cc + 6] = hi_nib16(v.z);
+            r[8 * cc + 7] = hi_nib16(v.w);
+          }
+          if (kDbg != 2) QR_TMEM_ST32(tmem_base + tlane + (uint32_t)(A_COL0 + A_COLS * o + 32 * half), r);
+        }
+        // the staging slot is released only once every lane has consumed its loads (the stores
+        // above read the registers): an arrive does not wait for in-flight LDS, so releasing
+        // right after issuing them lets the next TMA write overtake the reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&st_empty[s]);
+        if (kDbg != 2) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(opfull_leader + (uint32_t)o * 8u);
+      }
+    }
   } else {
     // ===================== epilogue warps 0..7 (each CTA: its 128 rows) =====================
-    // warp w reads TMEM lanes 32 (w % 4) .. +31 (its rows) and columns 128 (w / 4) .. +127;
-    // the next 32-column chunk is loaded while the current one is converted and stored.
+    // warp w owns TMEM lanes 32 (w % 4) .. +31 (its rows) and columns 128 (w / 4) .. +127, in
+    // four 32-column chunks.  The accumulator gates the next tile's MMAs, so it is drained
+    // first: chunks 0-2 are loaded together, chunk 0 is converted and stored, chunk 3 is
+    // loaded into its registers and the accumulator is released; the remaining three chunks
+    // are converted and stored while the next tile's MMAs already run.
+    QR_SETMAXNREG_INC(EPI_REGS);
     const uint32_t tempty_leader = map_to_rank(t_empty, 0);
     const int quarter = warp & 3, chalf = warp >> 2;
     const int row_in_tile = (int)rank * BMC + quarter * 32 + lane;
@@ -372,101 +471,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       tile_coords(p, pair + tl * num_pairs, mb, nb);
       const int64_t m = (int64_t)mb * BM + row_in_tile;
       const bool row_ok = m < p.M;
-      // scales are fetched while the accumulator is still being computed, so the TMEM drain
-      // (which gates the next tile's MMAs) never waits on a global load
+      const int64_t ncol0 = (int64_t)nb * BN + chalf * 128;  // this warp's first column
+      // scales (and the residual row segment, into L2) are fetched while the accumulator is
+      // still being computed, so the drain never waits on DRAM
       float sx = 0.f;
       if (!kS32) {
         if (row_ok) sx = __ldg(p.x_scale + m);
         const int64_t n = (int64_t)nb * BN + et;
         ws_smem[et] = n < p.N ? __ldg(p.w_scale + n) : 0.f;
+        if (p.residual && row_ok) {
+          const __half* rrow = p.residual + m * p.ld_r + ncol0;
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(rrow));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(rrow + 64));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(rrow + 127));
+        }
         epi_bar_sync();
       }
       mbar_wait_sleep(t_full, tl & 1);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + ACC_COL + (uint32_t)(chalf * 128);
-      uint32_t r[2][16];
-      QR_TMEM_LD16(taddr, r[0]);
-#pragma unroll
-      for (int cc = 0; cc < 8; ++cc) {
-        tmem_ld_wait();
-        if (cc + 1 < 8) {
-          QR_TMEM_LD16(taddr + (uint32_t)((cc + 1) * 16), r[(cc + 1) & 1]);
-        } else {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_cluster(tempty_leader);
-        }
-        const float* wsc = ws_smem + chalf * 128 + cc * 16;  // this chunk's 16 column scales
-        const uint32_t* rc = r[cc & 1];
-        const int64_t n0 = (int64_t)nb * BN + chalf * 128 + cc * 16;
-        if (row_ok) {
-          if constexpr (kS32) {
-            int32_t* dst = reinterpret_cast<int32_t*>(p.out) + m * p.ld_out + n0;
-#pragma unroll
-            for (int g = 0; g < 4; ++g) {
-              if (n0 + g * 4 < p.N) {
-                int4 v = make_int4((int32_t)rc[4 * g] >> 8, (int32_t)rc[4 * g + 1] >> 8,
-                                   (int32_t)rc[4 * g + 2] >> 8, (int32_t)rc[4 * g + 3] >> 8);
-                *reinterpret_cast<int4*>(dst + g * 4) = v;
-              }
-            }
-          } else if (p.swiglu) {
-            // chunk = [8 gate | 8 up] columns of features n0/2 .. n0/2 + 7 (interleaved W rows)
-            if (n0 < p.N) {
-              const float4 g0 = *reinterpret_cast<const float4*>(wsc);
-              const float4 g1 = *reinterpret_cast<const float4*>(wsc + 4);
-              const float4 u0 = *reinterpret_cast<const float4*>(wsc + 8);
-              const float4 u1 = *reinterpret_cast<const float4*>(wsc + 12);
-              const float sg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-              const float su[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
-              uint32_t h[4];
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                float a[2];
-#pragma unroll
-                for (int j = 0; j < 2; ++j) {
-                  const int c = 2 * e + j;
-                  const float gv = ((float)((int32_t)rc[c] >> 8) * sx) * sg[c];
-                  const float uv = ((float)((int32_t)rc[8 + c] >> 8) * sx) * su[c];
-                  a[j] = gv / (1.f + __expf(-gv)) * uv;
-                }
-                __half2 hv = __floats2half2_rn(a[0], a[1]);
-                h[e] = *reinterpret_cast<uint32_t*>(&hv);
-              }
-              *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(p.out) + m * p.ld_out + (n0 >> 1)) =
-                  make_uint4(h[0], h[1], h[2], h[3]);
-            }
-          } else {
-            __half* dst = reinterpret_cast<__half*>(p.out) + m * p.ld_out + n0;
-#pragma unroll
-            for (int g = 0; g < 2; ++g) {
-              if (n0 + g * 8 < p.N) {
-                const float4 s0 = *reinterpret_cast<const float4*>(wsc + g * 8);
-                const float4 s1 = *reinterpret_cast<const float4*>(wsc + g * 8 + 4);
-                const float swv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-                uint32_t h[4];
-                uint4 rres = make_uint4(0, 0, 0, 0);
-                if (p.residual) rres = *reinterpret_cast<const uint4*>(p.residual + m * p.ld_r + n0 + g * 8);
-                const __half2* r2 = reinterpret_cast<const __half2*>(&rres);
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  float v0 = ((float)((int32_t)rc[8 * g + 2 * e] >> 8) * sx) * swv[2 * e];
-                  float v1 = ((float)((int32_t)rc[8 * g + 2 * e + 1] >> 8) * sx) * swv[2 * e + 1];
-                  if (p.residual) {
-                    const float2 rf = __half22float2(r2[e]);
-                    v0 += rf.x;
-                    v1 += rf.y;
-                  }
-                  __half2 hv = __floats2half2_rn(v0, v1);
-                  h[e] = *reinterpret_cast<uint32_t*>(&hv);
-                }
-                if (kDbg != 4 || (h[0] == 0x7c017c01u && h[1] == 0x7c017c01u))  // probe 4: no stores
-                  *reinterpret_cast<uint4*>(dst + g * 8) = make_uint4(h[0], h[1], h[2], h[3]);
-              }
-            }
-          }
-        }
-      }
+      uint32_t ra[32], rb[32], rc[32];
+      QR_TMEM_LD32(taddr, ra);
+      QR_TMEM_LD32(taddr + 32u, rb);
+      QR_TMEM_LD32(taddr + 64u, rc);
+      tmem_ld_wait();
+      epi_chunk<kS32, kDbg>(p, ra, m, row_ok, ncol0, sx, ws_smem + chalf * 128);
+      QR_TMEM_LD32(taddr + 96u, ra);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_leader);
+      epi_chunk<kS32, kDbg>(p, rb, m, row_ok, ncol0 + 32, sx, ws_smem + chalf * 128 + 32);
+      epi_chunk<kS32, kDbg>(p, rc, m, row_ok, ncol0 + 64, sx, ws_smem + chalf * 128 + 64);
+      epi_chunk<kS32, kDbg>(p, ra, m, row_ok, ncol0 + 96, sx, ws_smem + chalf * 128 + 96);
       if (!kS32) epi_bar_sync();  // every warp is done with ws_smem before the next tile's fill
     }
   }
