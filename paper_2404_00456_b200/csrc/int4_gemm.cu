@@ -83,7 +83,6 @@ constexpr int CTL_REGS = 32;
 constexpr int TMEM_COLS = 512;
 constexpr int ACC_COL = 0;                          // accumulator: columns [0, 256)
 constexpr int A_COL0 = 256;                         // A stages: A_COLS columns each
-constexpr int GROUP_M = 8;                          // pair-rows per raster group
 constexpr uint32_t IDESC = idesc_i8(BM, BN);
 constexpr size_t SMEM_BYTES = SSTAGES * SSTAGE_BYTES + OSTAGES * OB_BYTES + 1024 + 512 + BN * 4;
 static_assert(SMEM_BYTES <= 232448, "227 KB dynamic smem");
@@ -96,13 +95,14 @@ struct Params {
   int swiglu;              // 1: rows of W interleaved [8 gate | 8 up]; out = silu(gate) * up, N/2 wide
   int64_t M, N, K, ld_out, ld_r;
   int num_m, num_n, num_kb, num_tiles;  // num_m in 256-row pair tiles
+  int group_m;  // raster: pair-rows per group (tiles walk m fastest inside a group, then n)
 };
 
 QR_DEVICE void tile_coords(const Params& p, int t, int& mb, int& nb) {
-  const int per_group = GROUP_M * p.num_n;
+  const int per_group = p.group_m * p.num_n;
   const int group = t / per_group;
-  const int first_m = group * GROUP_M;
-  const int gm = min(p.num_m - first_m, GROUP_M);
+  const int first_m = group * p.group_m;
+  const int gm = min(p.num_m - first_m, p.group_m);
   const int within = t - group * per_group;
   mb = first_m + within % gm;
   nb = within / gm;
@@ -566,6 +566,7 @@ bool make_packed_map(CUtensorMap* map, const uint8_t* base, int64_t rows, int64_
 }  // namespace
 
 int g_gemm_debug_mode = 0;
+int g_gemm_group_m = 0;  // debug override of the raster group (0 = automatic)
 
 template <bool kS32>
 static cudaError_t launch_gemm_impl(const uint8_t* xq, const float* xs, int64_t M, int64_t K, int64_t ld_xq,
@@ -600,6 +601,17 @@ static cudaError_t launch_gemm_impl(const uint8_t* xq, const float* xs, int64_t 
   p.num_n = (int)((N + BN - 1) / BN);
   p.num_kb = (int)((K + BK - 1) / BK);  // a K % 256 == 128 tail is zero-filled by the TMA
   p.num_tiles = p.num_m * p.num_n;
+  // Raster group: the ~74 concurrently running tiles share the A rows of group_m pair-rows,
+  // which stay in L2 while the group walks across N, so B is re-read from DRAM num_m / group_m
+  // times.  ~64 MB of A per group, 8..32 pair-rows (measured best on the Llama-2-70B linears:
+  // 32 at K = 8192, 16 at K = 28672; within 3% across 8..64).
+  {
+    const int64_t a_tile_bytes = (int64_t)BM * (K / 2);
+    int g = (int)((64ll << 20) / (a_tile_bytes > 0 ? a_tile_bytes : 1));
+    g = g < 8 ? 8 : (g > 32 ? 32 : g);
+    if (g_gemm_group_m > 0) g = g_gemm_group_m;
+    p.group_m = g < 1 ? 1 : (g > p.num_m ? p.num_m : g);
+  }
   const int max_pairs = num_sms_current() / 2;
   const int pairs = p.num_tiles < max_pairs ? p.num_tiles : max_pairs;
   if (g_gemm_debug_mode >= 1 && g_gemm_debug_mode <= 4) {
@@ -618,6 +630,7 @@ static cudaError_t launch_gemm_impl(const uint8_t* xq, const float* xs, int64_t 
 
 // Debug / roofline probe (not in the public header): mode 1 = MMA issue only.
 extern "C" void quarot_debug_gemm_mode(int mode) { g_gemm_debug_mode = mode; }
+extern "C" void quarot_debug_gemm_group_m(int g) { g_gemm_group_m = g; }
 
 cudaError_t launch_int4_gemm(const uint8_t* xq, const float* xs, int64_t M, int64_t K, int64_t ld_xq,
                              const uint8_t* wq, const float* ws, int64_t N, int64_t ld_wq, void* y,
