@@ -14,6 +14,7 @@
  *   quarot_kv_quant         KV-cache "Init": per-head Hadamard on K (and optionally Q, in
  *                           place) + asymmetric INT4 group quantization
  *                           (P:210-225 Stage 1d, P:236-237 Stage 2c)
+ *   quarot_kv_quant_rope    the same with RoPE fused in front
  *
  * Conventions (all entry points)
  *  - Tensor pointers are CUDA DEVICE pointers owned by the caller.  The library never
@@ -25,7 +26,7 @@
  *  - Arguments are validated before any launch; a failing call launches nothing and
  *    leaves outputs untouched.  Launch failures map to QUAROT_ERR_CUDA; asynchronous
  *    faults surface at the caller's next synchronization.  Nothing throws.
- *  - Outputs must not alias inputs (except q in quarot_kv_quant, rotated in place).
+ *  - Outputs must not alias inputs (except q in quarot_kv_quant[_rope], rotated in place).
  *  - Results are bitwise deterministic for identical inputs and independent of how
  *    rows are split across calls or GPUs (no atomics in any reduction).
  *  - INT4 signed codes are stored two per byte, two's complement nibbles, LOW nibble =
@@ -151,6 +152,20 @@ quarot_status quarot_kv_quant(const void* k, int64_t ld_k, const void* v, int64_
                               float clip_ratio, uint8_t* k_codes, float* k_scale,
                               uint8_t* k_zero, uint8_t* v_codes, float* v_scale,
                               uint8_t* v_zero, void* stream);
+
+/* quarot_kv_quant with RoPE fused in front ("RoPE + per-head H + KV quant"
+ * in one pass).  Same arguments and outputs as quarot_kv_quant, plus the quarot_rope
+ * parameters (pos0, seq_len, theta).  K and Q are read PRE-RoPE; each K / Q head gets
+ *   r = fp16_rn(rope(x))  (exactly quarot_rope's arithmetic: fp64 angle table rounded to fp32,
+ *   fp32 rotate-half, fp16 RNE), then the rotation / quantization of quarot_kv_quant.
+ * K stays untouched in memory (only its codes are written); Q is overwritten with
+ * fp16(H^ fp16(rope(q))).  V gets no RoPE.  Requirements: quarot_kv_quant's, seq_len >= 1,
+ * theta > 0, pos0 >= 0. */
+quarot_status quarot_kv_quant_rope(const void* k, int64_t ld_k, const void* v, int64_t ld_v, int64_t T,
+                                   int32_t n_kv, int32_t head_dim, void* q, int64_t ld_q, int32_t n_q,
+                                   uint32_t flags, float clip_ratio, int64_t pos0, int32_t seq_len,
+                                   float theta, uint8_t* k_codes, float* k_scale, uint8_t* k_zero,
+                                   uint8_t* v_codes, float* v_scale, uint8_t* v_zero, void* stream);
 
 /* Decoder-layer glue.
  * quarot_rope: Llama-2 rotary position embedding ("Pos", Eqs. 10-12), in place on

@@ -57,6 +57,11 @@ QR_DEVICE void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// RoPE rotate-half of one pair with explicitly rounded fp32 products (no FMA
+// contraction), so the standalone RoPE kernel and the RoPE fused into the KV pass agree bitwise.
+QR_DEVICE float rope_first(float x1, float x2, float c, float s) { return __fsub_rn(__fmul_rn(x1, c), __fmul_rn(x2, s)); }
+QR_DEVICE float rope_second(float x1, float x2, float c, float s) { return __fadd_rn(__fmul_rn(x2, c), __fmul_rn(x1, s)); }
+
 // ---------------------------------------------------------------- proxy fences
 // generic-proxy st.shared -> async-proxy (tcgen05.mma operand) visibility
 QR_DEVICE void fence_proxy_async_smem() {

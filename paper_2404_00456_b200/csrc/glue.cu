@@ -42,8 +42,8 @@ __global__ void __launch_bounds__(256) rope_kernel(__half* __restrict__ x, int64
       for (int e = 0; e < 4; ++e) {
         const float2 x1 = __half22float2(a1[e]), x2 = __half22float2(a2[e]);
         const float2 c0 = cs[v * 8 + 2 * e], c1 = cs[v * 8 + 2 * e + 1];
-        a1[e] = __floats2half2_rn(x1.x * c0.x - x2.x * c0.y, x1.y * c1.x - x2.y * c1.y);
-        a2[e] = __floats2half2_rn(x2.x * c0.x + x1.x * c0.y, x2.y * c1.x + x1.y * c1.y);
+        a1[e] = __floats2half2_rn(rope_first(x1.x, x2.x, c0.x, c0.y), rope_first(x1.y, x2.y, c1.x, c1.y));
+        a2[e] = __floats2half2_rn(rope_second(x1.x, x2.x, c0.x, c0.y), rope_second(x1.y, x2.y, c1.x, c1.y));
       }
       *reinterpret_cast<uint4*>(p1) = u1;
       *reinterpret_cast<uint4*>(p2) = u2;

@@ -82,14 +82,24 @@ QR_DEVICE bool group_all(bool b) {
   return (m & gm) == gm;
 }
 
-template <int LPG>
+// RoPE parameters of the fused variant (kRope): position = (pos0 + t) % seq_len; the cos/sin
+// table of a batch of `tpb` tokens is built in smem (fp64 -> fp32, as quarot_rope does)
+struct RopeArgs {
+  int64_t pos0;
+  int seq_len;
+  float theta;
+  int tpb;
+};
+
+template <int LPG, bool kRope>
 __global__ void __launch_bounds__(256) kv_quant_kernel(const __half* __restrict__ k, int64_t ld_k,
                                                        const __half* __restrict__ v, int64_t ld_v, __half* q,
                                                        int64_t ld_q, int64_t T, int n_kv, int n_q, uint32_t flags,
                                                        float clip, uint8_t* __restrict__ k_codes,
                                                        float* __restrict__ k_scale, uint8_t* __restrict__ k_zero,
                                                        uint8_t* __restrict__ v_codes, float* __restrict__ v_scale,
-                                                       uint8_t* __restrict__ v_zero) {
+                                                       uint8_t* __restrict__ v_zero, RopeArgs ra) {
+  extern __shared__ float2 rope_cs[];  // kRope: [tpb][HD / 2] (cos, sin)
   constexpr int HD = 32 * LPG;
   constexpr int GPW = 32 / LPG;  // groups per warp
   const int lane = threadIdx.x & 31;
@@ -98,32 +108,54 @@ __global__ void __launch_bounds__(256) kv_quant_kernel(const __half* __restrict_
   const int64_t total = T * G;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const double rnorm = rsqrt((double)HD);
-  for (int64_t f0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * GPW; f0 < total;
-       f0 += nwarps * GPW) {
-    const int64_t f = f0 + lane / LPG;
-    const bool ok = f < total;
-    const int64_t t = ok ? f / G : 0;
-    const int which = ok ? (int)(f - t * G) : 0;
+  // one (token, group) item per LPG lanes; warp-uniform control flow around the shuffles
+  auto item = [&](const int64_t t, const int which, const bool ok, const int tt) {
     const bool is_k = which < n_kv, is_v = !is_k && which < 2 * n_kv, is_q = which >= 2 * n_kv;
     const __half* src = is_k ? k + t * ld_k + which * HD
                              : (is_v ? v + t * ld_v + (which - n_kv) * HD : q + t * ld_q + (which - 2 * n_kv) * HD);
     src += sub * EPL;
     float x[EPL];
+    uint32_t raw[EPL / 2];  // the lane's 32 fp16 inputs as 16 packed words
     if (ok) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const uint4 u = __ldg(reinterpret_cast<const uint4*>(src) + c);
-        const __half2* h = reinterpret_cast<const __half2*>(&u);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 ff = __half22float2(h[e]);
-          x[8 * c + 2 * e] = ff.x;
-          x[8 * c + 2 * e + 1] = ff.y;
-        }
+        raw[4 * c] = u.x;
+        raw[4 * c + 1] = u.y;
+        raw[4 * c + 2] = u.z;
+        raw[4 * c + 3] = u.w;
       }
     } else {
 #pragma unroll
-      for (int j = 0; j < EPL; ++j) x[j] = 0.f;
+      for (int j = 0; j < EPL / 2; ++j) raw[j] = 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < EPL / 2; ++j) {
+      const float2 ff = __half22float2(*reinterpret_cast<const __half2*>(&raw[j]));
+      x[2 * j] = ff.x;
+      x[2 * j + 1] = ff.y;
+    }
+    if constexpr (kRope) {
+      // RoPE on K and Q (rotate-half pairs (i, i + HD/2)): the partner half lives
+      // LPG/2 lanes away (exchanged as packed fp16 words); the result is rounded to fp16 as
+      // the unfused path stores it (Z22)
+      constexpr int HALF = HD / 2;
+      const bool first = sub < LPG / 2;
+      const float2* cs = rope_cs + tt * HALF + (sub % (LPG / 2)) * EPL;
+      const bool do_rope = is_k || is_q;
+#pragma unroll
+      for (int j = 0; j < EPL / 2; ++j) {
+        const uint32_t ow = __shfl_xor_sync(0xffffffffu, raw[j], LPG / 2);
+        const float2 o = __half22float2(*reinterpret_cast<const __half2*>(&ow));
+        const float4 c2 = *reinterpret_cast<const float4*>(cs + 2 * j);  // (cos, sin) of 2 pairs
+        const float r0 = first ? rope_first(x[2 * j], o.x, c2.x, c2.y) : rope_second(o.x, x[2 * j], c2.x, c2.y);
+        const float r1 =
+            first ? rope_first(x[2 * j + 1], o.y, c2.z, c2.w) : rope_second(o.y, x[2 * j + 1], c2.z, c2.w);
+        if (do_rope) {
+          x[2 * j] = __half2float(__float2half_rn(r0));
+          x[2 * j + 1] = __half2float(__float2half_rn(r1));
+        }
+      }
     }
     const bool rot = is_q || (is_k && (flags & 1u)) || (is_v && (flags & 2u));
     // rotation is group-uniform; shuffles need the whole warp, so every lane runs the
@@ -149,7 +181,7 @@ __global__ void __launch_bounds__(256) kv_quant_kernel(const __half* __restrict_
     mn = group_min<LPG>(mn);
     mx = group_max<LPG>(mx);
     finite = group_all<LPG>(finite);
-    if (!ok) continue;
+    if (!ok) return;
     if (!is_q) {
       const double norm = rot ? rnorm : 1.0;
       const double lo = (double)clip * (double)fminf(mn, 0.f) * norm;
@@ -199,6 +231,43 @@ __global__ void __launch_bounds__(256) kv_quant_kernel(const __half* __restrict_
         reinterpret_cast<uint4*>(dst)[c] = u;
       }
     }
+  };
+  if constexpr (!kRope) {
+    for (int64_t f0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * GPW; f0 < total;
+         f0 += nwarps * GPW) {
+      const int64_t f = f0 + lane / LPG;
+      const bool ok = f < total;
+      const int64_t t = ok ? f / G : 0;
+      item(t, ok ? (int)(f - t * G) : 0, ok, 0);
+    }
+  } else {
+    // a block takes tpb tokens at a time: their cos/sin tables, then tpb * G items over its warps
+    constexpr int HALF = HD / 2;
+    const int units = ra.tpb * G;
+    const int bw = (int)(blockDim.x >> 5), w = (int)(threadIdx.x >> 5);
+    double* inv_freq = reinterpret_cast<double*>(rope_cs + 2 * ra.tpb * HALF);  // [HALF], after 2 tables
+    for (int i = threadIdx.x; i < HALF; i += blockDim.x)
+      inv_freq[i] = pow((double)ra.theta, -2.0 * (double)i / (double)HD);
+    __syncthreads();
+    int buf = 0;
+    for (int64_t t0 = (int64_t)blockIdx.x * ra.tpb; t0 < T; t0 += (int64_t)gridDim.x * ra.tpb, buf ^= 1) {
+      // double-buffered table: the batch before last is no longer read once this sync passes
+      float2* tab = rope_cs + buf * ra.tpb * HALF;
+      for (int i = threadIdx.x; i < ra.tpb * HALF; i += blockDim.x) {
+        const int tt = i / HALF, ii = i - tt * HALF;
+        const int64_t pos = (ra.pos0 + t0 + tt) % ra.seq_len;
+        double sn, cn;
+        sincos((double)pos * inv_freq[ii], &sn, &cn);  // == pos * theta^(-2 ii / d), as quarot_rope
+        tab[i] = make_float2((float)cn, (float)sn);
+      }
+      __syncthreads();
+      for (int u0 = w * GPW; u0 < units; u0 += bw * GPW) {
+        const int u = u0 + lane / LPG;
+        const int tt = u < units ? u / G : 0;
+        const bool ok = u < units && t0 + tt < T;
+        item(t0 + tt, ok ? u - tt * G : 0, ok, tt + buf * ra.tpb);
+      }
+    }
   }
 }
 
@@ -219,14 +288,49 @@ cudaError_t launch_kv_quant(const void* k, int64_t ld_k, const void* v, int64_t 
   const __half* kh = static_cast<const __half*>(k);
   const __half* vh = static_cast<const __half*>(v);
   __half* qh = static_cast<__half*>(q);
-#define QR_KV(L)                                                                                              \
-  kvq::kv_quant_kernel<L><<<(unsigned)blocks, threads, 0, stream>>>(kh, ld_k, vh, ld_v, qh, ld_q, T, n_kv, nq,  \
-                                                                     flags, clip, k_codes, k_scale, k_zero,     \
-                                                                     v_codes, v_scale, v_zero)
+#define QR_KV(L)                                                                                                \
+  kvq::kv_quant_kernel<L, false><<<(unsigned)blocks, threads, 0, stream>>>(kh, ld_k, vh, ld_v, qh, ld_q, T, n_kv,  \
+                                                                          nq, flags, clip, k_codes, k_scale,      \
+                                                                          k_zero, v_codes, v_scale, v_zero,       \
+                                                                          kvq::RopeArgs{0, 1, 0.f, 0})
   if (head_dim == 64) QR_KV(2);
   else if (head_dim == 128) QR_KV(4);
   else QR_KV(8);
 #undef QR_KV
+  return cudaPeekAtLastError();
+}
+
+cudaError_t launch_kv_quant_rope(const void* k, int64_t ld_k, const void* v, int64_t ld_v, int64_t T, int n_kv,
+                                 int head_dim, void* q, int64_t ld_q, int n_q, uint32_t flags, float clip,
+                                 int64_t pos0, int seq_len, float theta, uint8_t* k_codes, float* k_scale,
+                                 uint8_t* k_zero, uint8_t* v_codes, float* v_scale, uint8_t* v_zero,
+                                 cudaStream_t stream) {
+  const int nq = q ? n_q : 0;
+  const int G = 2 * n_kv + nq;
+  if (T == 0 || G == 0) return cudaSuccess;
+  const int threads = 256;
+  const int lpg = head_dim / 32;
+  const int gpb = (threads / 32) * (32 / lpg);  // items one pass of the block covers
+  // tokens per block batch: a whole number of passes when possible (G = 80, 64 items -> 4)
+  int tpb = 1;
+  while (tpb < 16 && (tpb * G) % gpb) tpb *= 2;
+  if (tpb < 8 && T >= 8 * 148) tpb = 8;  // fewer table builds / barriers per item
+  int64_t blocks = (T + tpb - 1) / tpb;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  const size_t smem = (size_t)2 * tpb * (head_dim / 2) * sizeof(float2) + (head_dim / 2) * sizeof(double);
+  const kvq::RopeArgs ra{pos0, seq_len, theta, tpb};
+  const __half* kh = static_cast<const __half*>(k);
+  const __half* vh = static_cast<const __half*>(v);
+  __half* qh = static_cast<__half*>(q);
+#define QR_KVR(L)                                                                                              \
+  kvq::kv_quant_kernel<L, true><<<(unsigned)blocks, threads, smem, stream>>>(kh, ld_k, vh, ld_v, qh, ld_q, T,    \
+                                                                            n_kv, nq, flags, clip, k_codes,    \
+                                                                            k_scale, k_zero, v_codes, v_scale, \
+                                                                            v_zero, ra)
+  if (head_dim == 64) QR_KVR(2);
+  else if (head_dim == 128) QR_KVR(4);
+  else QR_KVR(8);
+#undef QR_KVR
   return cudaPeekAtLastError();
 }
 

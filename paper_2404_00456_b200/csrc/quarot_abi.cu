@@ -230,4 +230,32 @@ quarot_status quarot_kv_quant(const void* k, int64_t ld_k, const void* v, int64_
   return QUAROT_OK;
 }
 
+quarot_status quarot_kv_quant_rope(const void* k, int64_t ld_k, const void* v, int64_t ld_v, int64_t T,
+                                   int32_t n_kv, int32_t head_dim, void* q, int64_t ld_q, int32_t n_q,
+                                   uint32_t flags, float clip_ratio, int64_t pos0, int32_t seq_len, float theta,
+                                   uint8_t* k_codes, float* k_scale, uint8_t* k_zero, uint8_t* v_codes,
+                                   float* v_scale, uint8_t* v_zero, void* stream) {
+  g_last_launches = 0;
+  if (flags & ~3u) return QUAROT_ERR_ARG;
+  if (!clip_ok(clip_ratio)) return QUAROT_ERR_ARG;
+  if (seq_len < 1 || pos0 < 0 || !(theta > 0.f)) return QUAROT_ERR_ARG;
+  if (T < 0 || n_kv <= 0 || n_q < 0 || head_dim <= 0) return QUAROT_ERR_DIM;
+  if (!(head_dim == 64 || head_dim == 128 || head_dim == 256)) return QUAROT_ERR_UNSUPPORTED_SIZE;
+  const bool has_q = q != nullptr && n_q > 0;
+  if (ld_k < (int64_t)n_kv * head_dim || ld_v < (int64_t)n_kv * head_dim ||
+      (has_q && ld_q < (int64_t)n_q * head_dim))
+    return QUAROT_ERR_DIM;
+  if (T == 0) return QUAROT_OK;
+  if (!k || !v || !k_codes || !k_scale || !k_zero || !v_codes || !v_scale || !v_zero) return QUAROT_ERR_NULL;
+  if (!aligned16(k) || !aligned16(v) || (has_q && !aligned16(q)) || !aligned16(k_codes) || !aligned16(v_codes))
+    return QUAROT_ERR_ALIGN;
+  if ((ld_k % 8) || (ld_v % 8) || (has_q && (ld_q % 8))) return QUAROT_ERR_ALIGN;
+  cudaError_t e = qr::launch_kv_quant_rope(k, ld_k, v, ld_v, T, n_kv, head_dim, has_q ? q : nullptr, ld_q,
+                                           has_q ? n_q : 0, flags, clip_ratio, pos0, seq_len, theta, k_codes,
+                                           k_scale, k_zero, v_codes, v_scale, v_zero, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return QUAROT_ERR_CUDA;
+  g_last_launches = 1;
+  return QUAROT_OK;
+}
+
 }  // extern "C"

@@ -28,6 +28,11 @@ cudaError_t launch_hq_full(const void* x, int64_t M, int64_t K, int64_t ld_x, in
 cudaError_t launch_kv_quant(const void* k, int64_t ld_k, const void* v, int64_t ld_v, int64_t T, int n_kv,
                             int head_dim, void* q, int64_t ld_q, int n_q, uint32_t flags, float clip, uint8_t* k_codes, float* k_scale, uint8_t* k_zero,
                             uint8_t* v_codes, float* v_scale, uint8_t* v_zero, cudaStream_t stream);
+cudaError_t launch_kv_quant_rope(const void* k, int64_t ld_k, const void* v, int64_t ld_v, int64_t T, int n_kv,
+                                 int head_dim, void* q, int64_t ld_q, int n_q, uint32_t flags, float clip,
+                                 int64_t pos0, int seq_len, float theta, uint8_t* k_codes, float* k_scale,
+                                 uint8_t* k_zero, uint8_t* v_codes, float* v_scale, uint8_t* v_zero,
+                                 cudaStream_t stream);
 
 // glue.cu
 cudaError_t launch_rope(void* x, int64_t T, int n_heads, int head_dim, int64_t ld_x, int64_t pos0, int seq_len,

@@ -34,6 +34,8 @@ _SIGS = {
     "quarot_swiglu": [_vp, _c_i64, _c_i64, _c_i64, _vp, _c_i64, _vp],
     "quarot_kv_quant": [_vp, _c_i64, _vp, _c_i64, _c_i64, _c_i32, _c_i32, _vp, _c_i64, _c_i32, _c_u32,
                         _c_f32, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "quarot_kv_quant_rope": [_vp, _c_i64, _vp, _c_i64, _c_i64, _c_i32, _c_i32, _vp, _c_i64, _c_i32, _c_u32,
+                             _c_f32, _c_i64, _c_i32, _c_f32, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "quarot_status_string": [_c_i32],
     "quarot_abi_version": [],
     "quarot_base_hadamard": [_c_i32, _vp],
@@ -208,10 +210,12 @@ def int4_matmul_s32(xq: torch.Tensor, wq: torch.Tensor, acc: torch.Tensor | None
 
 
 def kv_quant(k: torch.Tensor, v: torch.Tensor, q: torch.Tensor | None = None, flags: int = KV_ROTATE_K,
-             clip_ratio: float = 0.95, out: dict | None = None, stream=None) -> dict:
+             clip_ratio: float = 0.95, out: dict | None = None, stream=None, rope: tuple | None = None) -> dict:
     """quarot_kv_quant (KV-cache Init): k, v fp16 [T, n_kv, d] (heads contiguous per token,
     any token stride — e.g. views into a fused QKV output); q optional fp16 [T, n_q, d]
-    rotated in place.  Returns dict of codes / scales / zeros for K and V."""
+    rotated in place.  rope = (pos0, seq_len, theta) calls quarot_kv_quant_rope instead: K and Q
+    are read pre-RoPE and RoPE is applied in the same pass.  Returns dict of codes / scales /
+    zeros for K and V."""
     T, n_kv, d = k.shape
     if v.shape != k.shape:
         raise ValueError("k and v shapes differ")
@@ -229,13 +233,16 @@ def kv_quant(k: torch.Tensor, v: torch.Tensor, q: torch.Tensor | None = None, fl
             "v_zero": torch.empty(T, n_kv, dtype=torch.uint8, device=dev),
         }
     n_q = 0 if q is None else q.shape[1]
-    st = lib().quarot_kv_quant(_dev(k, "k", torch.float16), k.stride(0), _dev(v, "v", torch.float16), v.stride(0),
-                               T, n_kv, d, None if q is None else _dev(q, "q", torch.float16),
-                               0 if q is None else q.stride(0), n_q, flags, clip_ratio,
-                               out["k_codes"].data_ptr(), out["k_scale"].data_ptr(), out["k_zero"].data_ptr(),
-                               out["v_codes"].data_ptr(), out["v_scale"].data_ptr(), out["v_zero"].data_ptr(),
-                               _stream(stream))
-    _check("quarot_kv_quant", st)
+    head = (_dev(k, "k", torch.float16), k.stride(0), _dev(v, "v", torch.float16), v.stride(0), T, n_kv, d,
+            None if q is None else _dev(q, "q", torch.float16), 0 if q is None else q.stride(0), n_q, flags,
+            clip_ratio)
+    outs = (out["k_codes"].data_ptr(), out["k_scale"].data_ptr(), out["k_zero"].data_ptr(),
+            out["v_codes"].data_ptr(), out["v_scale"].data_ptr(), out["v_zero"].data_ptr(), _stream(stream))
+    if rope is None:
+        _check("quarot_kv_quant", lib().quarot_kv_quant(*head, *outs))
+    else:
+        pos0, seq_len, theta = rope
+        _check("quarot_kv_quant_rope", lib().quarot_kv_quant_rope(*head, int(pos0), int(seq_len), float(theta), *outs))
     return out
 
 

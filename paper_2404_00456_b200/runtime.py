@@ -182,20 +182,21 @@ class DecoderLayerStep:
     attention core excluded — the out_proj input is a supplied activation:
 
       1. RMSNorm + quantize(x)            (fused)         -> QKV GEMM          -> qkv
-      2. RoPE on the Q|K block of qkv     (in place)
-      3. KV-cache Init: per-head H on K (and Q in place), asym INT4 K/V
+      2+3. RoPE on K and Q, per-head H on K (and Q, in place), asym INT4 K/V — one pass
+         (quarot_kv_quant_rope; fuse_rope=False: quarot_rope in place, then quarot_kv_quant)
       4. Hadamard-heads + quantize(attn_out)              -> O GEMM + x        -> o
       5. RMSNorm + quantize(o)            (fused)         -> gate/up GEMM with SwiGLU fused
                                                              in its epilogue   -> act
       6. Hadamard (FULL) + quantize(act)                  -> down GEMM + o     -> out
-    = 10 kernel launches (11 with fuse_swiglu=False: gate/up GEMM -> gu, then SwiGLU)."""
+    = 9 kernel launches (+1 with fuse_rope=False, +1 with fuse_swiglu=False: gate/up GEMM ->
+    gu, then SwiGLU)."""
 
     def __init__(self, layer: QuaRotLayer, tokens: int, device="cuda", seq_len: int = 2048, theta: float = 10000.0,
-                 fuse_swiglu: bool = True):
+                 fuse_swiglu: bool = True, fuse_rope: bool = True):
         self.layer, self.tokens, self.device = layer, tokens, torch.device(device)
         self.seq_len, self.theta = seq_len, theta
-        self.fuse_swiglu = fuse_swiglu
-        self.LAUNCHES = 10 if fuse_swiglu else 11
+        self.fuse_swiglu, self.fuse_rope = fuse_swiglu, fuse_rope
+        self.LAUNCHES = 9 + (not fuse_swiglu) + (not fuse_rope)
         if fuse_swiglu:  # offline: gate/up rows interleaved in blocks of 8 for the fused epilogue
             self.gate_up_il = q.interleave_gate_up(*layer.weights["gate_up"])
         L = layer
@@ -251,12 +252,14 @@ class DecoderLayerStep:
         qkv = self.qkv[r0:r1]
         linear(qkv_s, xr, True, qkv)
         nq, nkv = L.n_heads * d, L.n_kv * d
-        q.rope(qkv[:, : nq + nkv].view(T, L.n_heads + L.n_kv, d), pos0=r0, seq_len=self.seq_len,
-               theta=self.theta, stream=stream)
-        mark("rope")
+        if not self.fuse_rope:
+            q.rope(qkv[:, : nq + nkv].view(T, L.n_heads + L.n_kv, d), pos0=r0, seq_len=self.seq_len,
+                   theta=self.theta, stream=stream)
+            mark("rope")
         q.kv_quant(qkv[:, nq:nq + nkv].view(T, L.n_kv, d), qkv[:, nq + nkv:].view(T, L.n_kv, d),
                    qkv[:, :nq].view(T, L.n_heads, d), flags=q.KV_ROTATE_K, clip_ratio=L.clip_kv,
-                   out={k: t[r0:r1] for k, t in self.kv.items()}, stream=stream)
+                   out={k: t[r0:r1] for k, t in self.kv.items()}, stream=stream,
+                   rope=(r0, self.seq_len, self.theta) if self.fuse_rope else None)
         mark("kv_quant")
         o = self.o[r0:r1]
         linear(o_s, attn_out[r0:r1], False, o, residual=xr)

@@ -109,6 +109,11 @@ def main():
         byts = 2 * T * 8 * (2 * d + d // 2 + 5) + T * 64 * d * 4
         res["kv"] = {"ms": ms, "gbs": byts / ms / 1e6, "frac_hbm": byts / ms / 1e6 / 6536}
         print("kv", json.dumps(res["kv"]), flush=True)
+        ms = timeit(lambda: q.kv_quant(kv_, vv, qv, out=out, rope=(0, 2048, 10000.0)), a.iters)
+        res["kv_rope"] = {"ms": ms, "gbs": byts / ms / 1e6, "frac_hbm": byts / ms / 1e6 / 6536}
+        print("kv_rope", json.dumps(res["kv_rope"]), flush=True)
+        ms = timeit(lambda: q.rope(fused[:, :9216].view(T, 72, d)), a.iters)
+        print("rope", json.dumps({"ms": ms}), flush=True)
     if "intmm" in a.what:
         # library INT8 reference: cuBLASLt via torch._int_mm, 8192^3 (denominator context)
         A = torch.randint(-7, 8, (8192, 8192), dtype=torch.int8, device=dev)

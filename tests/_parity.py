@@ -43,13 +43,19 @@ def assert_codes(gpu_codes, ref_codes, what=""):
     return st
 
 
-def assert_scales(gpu_scale, ref_scale, what=""):
+# When an fp16 intermediate the oracle cannot observe (RoPE inside the fused KV pass, Z22) is
+# rounded on both sides from different-precision arithmetic, a group's extreme element may land
+# on the adjacent fp16 value: its scale then moves by up to one fp16 ulp, relative 2^-10.
+FP16_ULP_REL = 2.0 ** -10
+
+
+def assert_scales(gpu_scale, ref_scale, what="", rel_tol=SCALE_REL):
     g = np.asarray(gpu_scale, np.float64)
     r = np.asarray(ref_scale, np.float64)
     assert np.array_equal(np.isnan(g), np.isnan(r)), f"{what}: NaN pattern differs"
     ok = ~np.isnan(r)
     rel = np.abs(g[ok] - r[ok]) / np.maximum(np.abs(r[ok]), 1e-300)
-    assert rel.size == 0 or rel.max() <= SCALE_REL, f"{what}: scale rel diff {rel.max():.3g}"
+    assert rel.size == 0 or rel.max() <= rel_tol, f"{what}: scale rel diff {rel.max():.3g}"
     return float(rel.max()) if rel.size else 0.0
 
 

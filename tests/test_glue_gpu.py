@@ -92,7 +92,7 @@ def _layer_weights(S, device, seed=2000):
     return QuaRotLayer(S["hidden"], S["ffn"], S["n_heads"], S["n_kv"], 128, w), w
 
 
-def _chain_check(q, S, T, rows, end_to_end: bool):
+def _chain_check(q, S, T, rows, end_to_end: bool, fuse_rope: bool = True):
     """Stage-by-stage parity of the decoder chain: every stage is checked against the oracle
     applied to the GPU's own input to that stage (quantization is discontinuous, so a 1-ulp
     difference upstream can legitimately flip a code downstream).  GEMM stages are checked on
@@ -104,7 +104,7 @@ def _chain_check(q, S, T, rows, end_to_end: bool):
     layer, w = _layer_weights(S, DEV)
     x = synth.activations(T, S["hidden"], "outlier", 100, DEV) * 0.05
     z = synth.activations(T, S["hidden"], "normal", 101, DEV)
-    step = DecoderLayerStep(layer, T, DEV)
+    step = DecoderLayerStep(layer, T, DEV, fuse_rope=fuse_rope)
     step.run_device({"x": x, "attn_out": z})
     torch.cuda.synchronize()
     rows = np.asarray(rows)
@@ -136,15 +136,22 @@ def _chain_check(q, S, T, rows, end_to_end: bool):
         qrot = okv.kv_init(qr, qr, qr)["q_rot"].reshape(R, d)
         assert P.frob_rel(g_qkv[:, h * d:(h + 1) * d], qrot) <= P.FROB_REL
     kh = lin_ref(cx, sx, "qkv", np.arange(nq, nq + d)).astype(np.float64).reshape(R, 1, d)
-    assert P.frob_rel(g_qkv[:, nq:nq + d], oglue.rope(kh, rows % 2048).reshape(R, d).astype(np.float16)) <= P.FROB_REL
-    # --- stage B: KV cache of the GPU's own post-RoPE K and V
+    if step.fuse_rope:  # K stays pre-RoPE in memory; RoPE happens inside the KV pass
+        assert P.frob_rel(g_qkv[:, nq:nq + d], kh.reshape(R, d).astype(np.float16)) <= P.FROB_REL
+    else:
+        assert P.frob_rel(g_qkv[:, nq:nq + d],
+                          oglue.rope(kh, rows % 2048).reshape(R, d).astype(np.float16)) <= P.FROB_REL
+    # --- stage B: KV cache of the GPU's own post-RoPE K (fp16, Z22) and V
     kg = g_qkv[:, nq:nq + nk].astype(np.float64).reshape(R, nkv, d)
+    if step.fuse_rope:
+        kg = oglue.rope(kg, rows % 2048).astype(np.float16).astype(np.float64)
     vg = g_qkv[:, nq + nk:].astype(np.float64).reshape(R, nkv, d)
     cache = okv.kv_init(kg, vg)
     for t in ("k", "v"):
         P.assert_codes(P.unpack_unsigned(step.kv[f"{t}_codes"][rt].cpu().numpy()),
                        P.unpack_unsigned(cache[f"{t}_codes"]), f"{t} codes")
-        P.assert_scales(step.kv[f"{t}_scale"][rt].cpu().numpy(), cache[f"{t}_scale"], f"{t} scales")
+        P.assert_scales(step.kv[f"{t}_scale"][rt].cpu().numpy(), cache[f"{t}_scale"], f"{t} scales",
+                        rel_tol=P.FP16_ULP_REL if (t == "k" and step.fuse_rope) else P.SCALE_REL)
     # --- stage C: heads-H + quant -> O GEMM + residual x
     cz, _, sz = olayer.hadamard_quant(z[rt].float().cpu().numpy().astype(np.float64), "across_heads", d)
     ocols = np.sort(rng.choice(S["hidden"], size=min(256, S["hidden"]), replace=False))
@@ -175,10 +182,11 @@ def _chain_check(q, S, T, rows, end_to_end: bool):
         assert P.frob_rel(g_out, ref["out"]) <= 5e-2
 
 
-def test_decoder_chain_small(q):
+@pytest.mark.parametrize("fuse_rope", [True, False])
+def test_decoder_chain_small(q, fuse_rope):
     S = {"hidden": 512, "ffn": 28 * 32, "n_heads": 4, "n_kv": 1}
     S["qkv"] = (S["n_heads"] + 2 * S["n_kv"]) * 128
-    _chain_check(q, S, 300, np.arange(300), end_to_end=True)
+    _chain_check(q, S, 300, np.arange(300), end_to_end=True, fuse_rope=fuse_rope)
 
 
 @pytest.mark.parametrize("cfg", [1, 2])
@@ -187,3 +195,45 @@ def test_decoder_chain_full_size_sampled(q, cfg):
     Sh, T = spec["shapes"], spec["tokens"]
     S = {"hidden": Sh.hidden, "ffn": Sh.ffn, "n_heads": Sh.n_heads, "n_kv": Sh.n_kv_heads, "qkv": Sh.qkv_out}
     _chain_check(q, S, T, olayer.token_sample(T, 8), end_to_end=False)
+
+
+@pytest.mark.parametrize("T,n_kv,n_q,hd,pos0", [(37, 8, 64, 128, 0), (4100, 2, 6, 128, 1000), (9, 4, 4, 64, 5),
+                                                (3, 2, 2, 256, 2040), (5, 3, 0, 128, 7)])
+def test_kv_quant_rope_fused(q, T, n_kv, n_q, hd, pos0):
+    """RoPE + per-head H + KV quant in one pass, against the oracle
+    (fp64 RoPE rounded to fp16 (Z22), then kv_init) and against the unfused GPU path."""
+    from oracle import kv as okv
+    k, v, qq = synth.kv_inputs(T, n_kv, n_q, hd, seed=T + 1, device=DEV)
+    k[0, 0] = 0  # degenerate group survives RoPE as zeros
+    pos = (pos0 + np.arange(T)) % 2048
+    q_f = None if qq is None else qq.clone()
+    k_orig = k.clone()
+    out = q.kv_quant(k, v, q_f, rope=(pos0, 2048, 10000.0))
+    torch.cuda.synchronize()
+    kr = oglue.rope(k.cpu().numpy().astype(np.float64), pos).astype(np.float16)
+    qr = None if qq is None else oglue.rope(qq.cpu().numpy().astype(np.float64), pos).astype(np.float16)
+    ref = okv.kv_init(kr, v.cpu().numpy(), qr)
+    for t in ("k", "v"):
+        P.assert_codes(P.unpack_unsigned(out[f"{t}_codes"].cpu().numpy()), P.unpack_unsigned(ref[f"{t}_codes"]),
+                       f"{t} codes")
+        P.assert_scales(out[f"{t}_scale"].cpu().numpy(), ref[f"{t}_scale"], f"{t} scale",
+                        rel_tol=P.FP16_ULP_REL if t == "k" else P.SCALE_REL)
+    assert out["k_scale"][0, 0].item() == 1.0 and out["k_zero"][0, 0].item() == 0
+    if qq is not None:
+        # a 1-ulp difference in one fp16 RoPE output spreads over the head through H, so the
+        # rotated Q is compared in relative Frobenius norm (near-zero outputs make ulp counts
+        # meaningless once the inputs differ)
+        assert P.frob_rel(q_f.cpu().numpy(), ref["q_rot"]) <= 1e-3
+    # unfused: quarot_rope on copies, then quarot_kv_quant
+    k2 = k.clone()
+    q2 = None if qq is None else qq.clone()
+    q.rope(k2, pos0=pos0, seq_len=2048)
+    if q2 is not None:
+        q.rope(q2, pos0=pos0, seq_len=2048)
+    out2 = q.kv_quant(k2, v, q2)
+    torch.cuda.synchronize()
+    for key in ("k_codes", "k_scale", "k_zero", "v_codes", "v_scale", "v_zero"):  # same arithmetic: bitwise
+        assert torch.equal(out[key], out2[key]), key
+    if q2 is not None:
+        assert torch.equal(q_f, q2)
+    assert torch.equal(k, k_orig)  # K is read-only in the fused path
