@@ -189,6 +189,9 @@ int32_t quarot_abi_version(void);
 quarot_status quarot_base_hadamard(int32_t m, int8_t* out);
 /* Number of kernels the last successful entry point on this host thread enqueued. */
 int32_t quarot_last_launch_count(void);
+/* "cudaErrorName: description" of the last call on this host thread that returned
+ * QUAROT_ERR_CUDA ("" if none); the buffer is owned by the library. */
+const char* quarot_last_cuda_error(void);
 
 #ifdef __cplusplus
 }

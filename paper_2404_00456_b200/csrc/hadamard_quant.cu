@@ -475,34 +475,41 @@ __global__ void hq_full_kernel(const __half* __restrict__ x, int64_t ld_x, int P
 
 
 // ------------------------------------------------------------------ FULL, K = 1024 x 28
-// The bench / 70B down_proj width, K = 28672: i = a*28 + b, a = a_hi*32 + a_lo (reading Z2),
-// y = (H_32[a_hi] (x) H_32[a_lo] (x) H_28[b]) x   (Sylvester H_1024 = H_32 (x) H_32, Eq. 1).
+// The bench / 70B down_proj width, K = 28672: i = a*28 + b (reading Z2); Sylvester H_1024 is
+// the tensor product of H_2 over the 10 bits of a (Eq. 1), so its stages can run in any order.
 // Persistent CTAs (one per SM) with two warp groups working on consecutive rows, so the
-// tensor-core phase of row i+1 overlaps the quantization phase of row i:
-//  * P1 (8 warps): waits for the cp.async.bulk copy of the fp16 row (57 KB) in smem; each
-//    warp takes 4 slabs a_hi (32 x 28 contiguous elements): H_28 on tensor cores
-//    (mma.sync m16n8k16, A = H_28 padded to 32, B = slab^T: exact +-1 x fp16 products, fp32
-//    accumulation), then H_32 over a_lo on the fp32 fragments (3 butterfly stages in
-//    registers with FADD2, 2 with warp shuffles + FFMA2); results to the fp32 buffer Z in
-//    natural order (conflict-free: word stride 56 across t, 1 across g).  Then it issues
-//    the next row's bulk copy.
-//  * P2 (14 warps): thread t owns (a_lo = t / 14, b = 2 (t % 14), +1) for all 32 a_hi:
-//    32 LDS.64, releases Z to P1, H_32 over a_hi with FADD2, row amax (NaN-propagating,
-//    reduced over P2), RNE codes via the magic-number add, one packed byte per a_hi at
-//    byte a_hi * 448 + t — staged in smem and written out with 16-byte stores.
+// tensor-core phase of row i+1 overlaps the quantization phase of row i.  Element i = a*28 + b
+// (a < 1024, b < 28); y = (H_1024 (x) H_28) x.  The 10 bits of a are split so that no
+// transform stage needs a warp shuffle:
+//  * P1 (4 warps, 4 units per row each; unit = a-group ag of 128 a's x m-tile mt of 16 output
+//    b's): H_28 on tensor cores (mma.sync m16n8k16: A = H_28 padded to 32, B = x^T, exact
+//    +-1 x fp16 products, fp32 accumulation) over 16 n-tiles, then H over the 5 a-bits the
+//    accumulator fragment keeps in registers (column bit j = a1, n-tile bits = a0, a4, a5, a6)
+//    with FADD/FADD2.  B column n = g <-> a bits 1-3 (a stride of 2 rows = 28 words keeps the
+//    fragment loads bank-conflict-free).  Results go to Z as fp32.
+//  * P2 (14 warps): thread tp = c * 14 + bp owns P1-bit combination c and b-pair bp for the 32
+//    combinations p2 of the remaining bits (lane bits t = a2, a3 and ag = a7..a9): 32 LDS.64,
+//    releases Z, H_32 over p2 with FADD2, row amax (NaN-propagating), RNE codes with the magic
+//    add, one packed byte per p2.
+// Z layout: [p2 (32)][c (32) x b (28) + 8 pad] fp32 — P2 reads are contiguous per p2, and the
+// 8-word pad spreads P1's four t-lanes over distinct banks.
+#ifndef QR_F28_P1W
+#define QR_F28_P1W 4
+#endif
 namespace f28 {
 constexpr int MB = 28, P = 1024, K = MB * P;  // (M is the row count)
-constexpr int P1_WARPS = 16, P2_WARPS = 14, NT = (P1_WARPS + 16) * 32;  // 1024 threads: P2 = 4 warpgroups (2 idle warps)
-constexpr int P2_THREADS = P2_WARPS * 32;                                     // 448 = 32 * 14
-constexpr int XS_BYTES = K * 2;      // 57344 per row buffer, double-buffered
-constexpr int Z_BYTES = K * 4;       // 114688
-constexpr int OUT_BYTES = K / 2;     // 14336
-constexpr size_t SMEM = 2 * XS_BYTES + Z_BYTES + 256;  // 229632 of the 232448 available
+constexpr int P1_WARPS = QR_F28_P1W, P2_WARPS = 14, NT = (P1_WARPS + P2_WARPS) * 32;
+constexpr int UNITS = 16 / P1_WARPS;  // P1 units per warp per row
+constexpr int P2_THREADS = P2_WARPS * 32;                                      // 448 = 32 * 14
+constexpr int XS_BYTES = K * 2;         // 57344 per row buffer, double-buffered
+constexpr int ZP = 32 * MB + 8;         // floats per p2 slice (904)
+constexpr int Z_BYTES = 32 * ZP * 4;    // 115712
+constexpr size_t SMEM = 2 * XS_BYTES + Z_BYTES + 256;  // 230656 of the 232448 available
 }  // namespace f28
 
 QR_DEVICE void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-__global__ void __launch_bounds__(f28::NT, 1)
+__global__ void __launch_bounds__(f28::NT, 1)  // 18 warps: at most 5 per SM sub-partition -> 96 registers
     hq_full28_kernel(const __half* __restrict__ x, int64_t M, int64_t ld_x, float clip, uint8_t* __restrict__ q,
                      int64_t ld_q, float* __restrict__ scale, const uint32_t* __restrict__ afrag) {
   using namespace f28;
@@ -536,20 +543,8 @@ __global__ void __launch_bounds__(f28::NT, 1)
   };
 
   if (warp < P1_WARPS) {
-    // ======================= P1: bulk copy + H_28 (tensor cores) + H_32 over a_lo
-    // warp w owns m-tile mt = w & 1 (b rows 16 mt .. 16 mt + 15) of slabs a_hi = w / 2 + 8 i
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 48;");
+    // ======================= P1: bulk copy + H_28 (tensor cores) + H over 5 a-bits in registers
     const int g = lane >> 2, t = lane & 3;
-    const int mt = warp & 1;
-    uint32_t ha[2][4];  // H_28 A fragments of this m-tile (2 k-steps x 4 regs)
-#pragma unroll
-    for (int ks = 0; ks < 2; ++ks) {
-      const uint4 v = __ldg(reinterpret_cast<const uint4*>(afrag) + ((mt * 2 + ks) * 32 + lane));
-      ha[ks][0] = v.x;
-      ha[ks][1] = v.y;
-      ha[ks][2] = v.z;
-      ha[ks][3] = v.w;
-    }
     if (threadIdx.x == 0) {  // prefetch the first two rows
       if ((int64_t)blockIdx.x < M) issue_row(blockIdx.x, 0);
       if ((int64_t)blockIdx.x + gridDim.x < M) issue_row(blockIdx.x + gridDim.x, 1);
@@ -561,56 +556,57 @@ __global__ void __launch_bounds__(f28::NT, 1)
       mbar_wait_sleep(&xs_full[buf], (it >> 1) & 1);
       mbar_wait_sleep(z_empty, (it & 1) ^ 1);
 #pragma unroll 1
-      for (int si = 0; si < 4; ++si) {
-        const int a_hi = (warp >> 1) + 8 * si;
-        float2 d[4][2];  // [nt][h]: D1[b = 16 mt + g + 8 h][a_lo = 8 nt + 2 t + {0,1}]
+      for (int u = 0; u < UNITS; ++u) {
+        const int unit = warp * UNITS + u;  // 0..15
+        const int ag = unit >> 1, mt = unit & 1;
+        uint32_t ha[2][4];  // H_28 A fragments of this m-tile (2 k-steps x 4 regs)
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt) {
-          const int wbase = (a_hi * 32 + nt * 8 + g) * (MB / 2);  // B column n = g -> a_lo = 8 nt + g
-          const uint32_t b00 = xw[wbase + t], b01 = xw[wbase + 4 + t], b10 = xw[wbase + 8 + t];
-          const uint32_t b11 = (t < 2) ? xw[wbase + 12 + t] : 0u;
+        for (int ks = 0; ks < 2; ++ks) {
+          const uint4 v = __ldg(reinterpret_cast<const uint4*>(afrag) + ((mt * 2 + ks) * 32 + lane));
+          ha[ks][0] = v.x;
+          ha[ks][1] = v.y;
+          ha[ks][2] = v.z;
+          ha[ks][3] = v.w;
+        }
+        float2 d[16][2];  // [nt][h]: output b = 16 mt + g + 8 h; (j = 0, 1) in .x / .y
+#pragma unroll
+        for (int nt = 0; nt < 16; ++nt) {
+          // B column n = g: a = ag * 128 + (nt & 1) + 2 g + 16 (nt >> 1); k = input b
+          const int a = ag * 128 + (nt & 1) + 2 * g + 16 * (nt >> 1);
+          const uint32_t* xa = xw + a * (MB / 2) + t;
+          const uint32_t b00 = xa[0], b01 = xa[4], b10 = xa[8];
+          const uint32_t b11 = (t < 2) ? xa[12] : 0u;
           float acc[4] = {0.f, 0.f, 0.f, 0.f};
           mma_16816(acc, ha[0], b00, b01);
           mma_16816(acc, ha[1], b10, b11);
-          // a_lo bit 0 lives inside the register pair
+          // D column n = 2 t + j <-> a bits 1-3: j = a1 lives inside the register pair
           d[nt][0] = make_float2(acc[0] + acc[1], acc[0] - acc[1]);
           d[nt][1] = make_float2(acc[2] + acc[3], acc[2] - acc[3]);
         }
 #pragma unroll
-        for (int st = 1; st < 4; st <<= 1) {  // a_lo bits 3, 4 (n-tile index)
+        for (int st = 1; st < 16; st <<= 1) {  // n-tile bits = a0, a4, a5, a6
 #pragma unroll
-          for (int nt = 0; nt < 4; ++nt) {
+          for (int nt = 0; nt < 16; ++nt) {
             if (!(nt & st)) {
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
-                const float2 u = d[nt][h], v = d[nt + st][h];
-                d[nt][h] = f2add(u, v);
-                d[nt + st][h] = f2sub(u, v);
+                const float2 uu = d[nt][h], vv = d[nt + st][h];
+                d[nt][h] = f2add(uu, vv);
+                d[nt + st][h] = f2sub(uu, vv);
               }
             }
           }
         }
+        // Z[p2][c][b]: p2 = t | ag << 2 (a2, a3, a7..a9); c = a0 | j << 1 | (nt >> 1) << 2
+        float* zt = Z + (t | (ag << 2)) * ZP + 16 * mt + g;
 #pragma unroll
-        for (int st = 1; st < 4; st <<= 1) {  // a_lo bits 1, 2 (lane bits of t)
-          const float sg = (t & st) ? -1.f : 1.f;
-#pragma unroll
-          for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const float ox = __shfl_xor_sync(0xffffffffu, d[nt][h].x, st);
-              const float oy = __shfl_xor_sync(0xffffffffu, d[nt][h].y, st);
-              d[nt][h] = f2fma(make_float2(sg, sg), d[nt][h], make_float2(ox, oy));
-            }
-        }
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt)
+        for (int nt = 0; nt < 16; ++nt)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const int bb = 16 * mt + g + 8 * h;
-            const int a = a_hi * 32 + nt * 8 + 2 * t;
-            if (bb < MB) {
-              Z[a * MB + bb] = d[nt][h].x;
-              Z[(a + 1) * MB + bb] = d[nt][h].y;
+            const int c0 = (nt & 1) | ((nt >> 1) << 2);
+            if (16 * mt + 8 * h + g < MB) {
+              zt[c0 * MB + 8 * h] = d[nt][h].x;
+              zt[(c0 | 2) * MB + 8 * h] = d[nt][h].y;
             }
           }
       }
@@ -619,33 +615,35 @@ __global__ void __launch_bounds__(f28::NT, 1)
       if (threadIdx.x == 0 && row + 2 * (int64_t)gridDim.x < M) issue_row(row + 2 * (int64_t)gridDim.x, buf);
     }
   } else {
-    // ======================= P2: H_32 over a_hi, amax, codes, packed output
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 80;");  // 512*48 + 512*80 = 65536 = the launch allocation
-    if (warp >= P1_WARPS + P2_WARPS) return;  // padding warps of the last warpgroup
-    const int tp = threadIdx.x - P1_WARPS * 32;  // 0..447
+    // ======================= P2: H_32 over p2, amax, codes, packed output
+    const int tp = threadIdx.x - P1_WARPS * 32;  // 0..447 = c * 14 + bp
     const int w2 = warp - P1_WARPS;
+    const int c = tp / 14, bp = tp - 14 * (tp / 14);
+    // element a of (c, p2): a0 = c0, a1 = c1, a2..a3 = p2 & 3, a4..a6 = c >> 2, a7..a9 = p2 >> 2
+    const int a_c = (c & 3) | ((c >> 2) << 4);
     int it = 0;
     for (int64_t row = blockIdx.x; row < M; row += gridDim.x, ++it) {
       mbar_wait_sleep(z_full, it & 1);
       float2 v[32];
-      const float2* zp = reinterpret_cast<const float2*>(Z) + tp;  // (a_lo * 28 + 2 j) / 2 == tp
+      const float2* zp = reinterpret_cast<const float2*>(Z) + tp;  // (c * 28 + 2 bp) / 2 == tp
 #pragma unroll
-      for (int ah = 0; ah < 32; ++ah) v[ah] = zp[ah * 448];
+      for (int p2 = 0; p2 < 32; ++p2) v[p2] = zp[p2 * (ZP / 2)];
       mbar_arrive(z_empty);
 #pragma unroll
       for (int st = 1; st < 32; st <<= 1) {
 #pragma unroll
-        for (int ah = 0; ah < 32; ++ah) {
-          if (!(ah & st)) {
-            const float2 u = v[ah], w = v[ah + st];
-            v[ah] = f2add(u, w);
-            v[ah + st] = f2sub(u, w);
+        for (int p2 = 0; p2 < 32; ++p2) {
+          if (!(p2 & st)) {
+            const float2 uu = v[p2], ww = v[p2 + st];
+            v[p2] = f2add(uu, ww);
+            v[p2 + st] = f2sub(uu, ww);
           }
         }
       }
       float am[4] = {0.f, 0.f, 0.f, 0.f};  // 4 independent max chains
 #pragma unroll
-      for (int ah = 0; ah < 32; ++ah) am[ah & 3] = fmax_nan(am[ah & 3], fmax_nan(fabsf(v[ah].x), fabsf(v[ah].y)));
+      for (int p2 = 0; p2 < 32; ++p2)
+        am[p2 & 3] = fmax_nan(am[p2 & 3], fmax_nan(fabsf(v[p2].x), fabsf(v[p2].y)));
       float amax = fmax_nan(fmax_nan(am[0], am[1]), fmax_nan(am[2], am[3]));
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) amax = fmax_nan(amax, __shfl_xor_sync(0xffffffffu, amax, o));
@@ -657,15 +655,15 @@ __global__ void __launch_bounds__(f28::NT, 1)
       float s, inv;
       row_scale(amax, rsqrt((double)K), clip, s, inv);
       if (tp == 0) scale[row] = s;
-      // packed byte of (a_hi, a_lo, b-pair) lands at a_hi * 448 + tp: a warp writes 32
-      // consecutive bytes per a_hi (one full sector)
-      uint8_t* qr = q + row * ld_q + tp;
+      // byte of (a, b-pair) at a * 14 + bp
+      uint8_t* qr = q + row * ld_q + a_c * (MB / 2) + bp;
       if (inv != 0.f) {
 #pragma unroll
-        for (int ah = 0; ah < 32; ++ah) qr[ah * 448] = (uint8_t)quant_pair(v[ah], inv);
+        for (int p2 = 0; p2 < 32; ++p2)
+          qr[((p2 & 3) << 2 | (p2 >> 2) << 7) * (MB / 2)] = (uint8_t)quant_pair(v[p2], inv);
       } else {
 #pragma unroll
-        for (int ah = 0; ah < 32; ++ah) qr[ah * 448] = 0;
+        for (int p2 = 0; p2 < 32; ++p2) qr[((p2 & 3) << 2 | (p2 >> 2) << 7) * (MB / 2)] = 0;
       }
     }
   }

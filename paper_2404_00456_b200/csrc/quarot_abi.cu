@@ -1,11 +1,18 @@
 // quarot_abi.cu — the extern "C" boundary (include/quarot.h): argument validation and
 // dispatch to the sm_100a kernels.  No torch types, no allocation, no host synchronization.
+#include <cstdio>
 #include <cstring>
 
 #include "../../include/quarot.h"
 #include "quarot_internal.h"
 
 namespace {
+// the last launch failure, for quarot_last_cuda_error() (diagnostics only)
+thread_local char g_last_cuda_error[160] = "";
+quarot_status cuda_fail(cudaError_t e) {
+  std::snprintf(g_last_cuda_error, sizeof g_last_cuda_error, "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
+  return QUAROT_ERR_CUDA;
+}
 
 thread_local int32_t g_last_launches = 0;
 
@@ -47,6 +54,7 @@ const char* quarot_status_string(int32_t s) {
 }
 
 int32_t quarot_abi_version(void) { return QUAROT_ABI_VERSION; }
+const char* quarot_last_cuda_error(void) { return g_last_cuda_error; }
 
 int32_t quarot_last_launch_count(void) { return g_last_launches; }
 
@@ -93,11 +101,11 @@ quarot_status quarot_hadamard_quant(const void* x, int64_t M, int64_t K, int64_t
     if (m > 1) {
       if (!qr::base_hadamard_host(m)) return QUAROT_ERR_UNSUPPORTED_SIZE;
       e = qr::ensure_device_tables();
-      if (e != cudaSuccess) return QUAROT_ERR_CUDA;
+      if (e != cudaSuccess) return cuda_fail(e);
     }
     e = qr::launch_hq_full(x, M, K, ld_x, (int)p, m, clip_ratio, q, ld_q, scale, st);
   }
-  if (e != cudaSuccess) return QUAROT_ERR_CUDA;
+  if (e != cudaSuccess) return cuda_fail(e);
   g_last_launches = 1;
   return QUAROT_OK;
 }
@@ -124,7 +132,7 @@ quarot_status quarot_int4_linear(const uint8_t* xq, const float* x_scale, int64_
   if (!aligned16(w_scale)) return QUAROT_ERR_ALIGN;
   cudaError_t e = qr::launch_int4_gemm(xq, x_scale, M, K, ld_xq, wq, w_scale, N, ld_wq, y, ld_y,
                                        static_cast<cudaStream_t>(stream));
-  if (e != cudaSuccess) return QUAROT_ERR_CUDA;
+  if (e != cudaSuccess) return cuda_fail(e);
   g_last_launches = 1;
   return QUAROT_OK;
 }
@@ -141,7 +149,7 @@ quarot_status quarot_int4_linear_residual(const uint8_t* xq, const float* x_scal
   if (!aligned16(w_scale) || !aligned16(residual) || (ld_r % 8)) return QUAROT_ERR_ALIGN;
   cudaError_t e = qr::launch_int4_gemm(xq, x_scale, M, K, ld_xq, wq, w_scale, N, ld_wq, y, ld_y,
                                        static_cast<cudaStream_t>(stream), residual, ld_r);
-  if (e != cudaSuccess) return QUAROT_ERR_CUDA;
+  if (e != cudaSuccess) return cuda_fail(e);
   g_last_launches = 1;
   return QUAROT_OK;
 }
@@ -158,7 +166,7 @@ quarot_status quarot_int4_linear_swiglu(const uint8_t* xq, const float* x_scale,
   if (!aligned16(w_scale) || (ld_act % 8)) return QUAROT_ERR_ALIGN;
   cudaError_t e = qr::launch_int4_gemm_swiglu(xq, x_scale, M, K, ld_xq, wq, w_scale, N2, ld_wq, act, ld_act,
                                               static_cast<cudaStream_t>(stream));
-  if (e != cudaSuccess) return QUAROT_ERR_CUDA;
+  if (e != cudaSuccess) return cuda_fail(e);
   g_last_launches = 1;
   return QUAROT_OK;
 }
@@ -174,7 +182,7 @@ quarot_status quarot_rope(void* x, int64_t T, int32_t n_heads, int32_t head_dim,
   if (!x) return QUAROT_ERR_NULL;
   if (!aligned16(x) || (ld_x % 8)) return QUAROT_ERR_ALIGN;
   cudaError_t e = qr::launch_rope(x, T, n_heads, head_dim, ld_x, pos0, seq_len, theta, static_cast<cudaStream_t>(stream));
-  if (e != cudaSuccess) return QUAROT_ERR_CUDA;
+  if (e != cudaSuccess) return cuda_fail(e);
   g_last_launches = 1;
   return QUAROT_OK;
 }
@@ -187,7 +195,7 @@ quarot_status quarot_swiglu(const void* gate_up, int64_t M, int64_t F, int64_t l
   if (!gate_up || !act) return QUAROT_ERR_NULL;
   if (F % 8 || ld_gu % 8 || ld_act % 8 || !aligned16(gate_up) || !aligned16(act)) return QUAROT_ERR_ALIGN;
   cudaError_t e = qr::launch_swiglu(gate_up, M, F, ld_gu, act, ld_act, static_cast<cudaStream_t>(stream));
-  if (e != cudaSuccess) return QUAROT_ERR_CUDA;
+  if (e != cudaSuccess) return cuda_fail(e);
   g_last_launches = 1;
   return QUAROT_OK;
 }
@@ -199,7 +207,7 @@ quarot_status quarot_int4_matmul_s32(const uint8_t* xq, int64_t M, int64_t K, in
   if (s != QUAROT_OK || M == 0) return s;
   cudaError_t e =
       qr::launch_int4_gemm_s32(xq, M, K, ld_xq, wq, N, ld_wq, acc, ld_acc, static_cast<cudaStream_t>(stream));
-  if (e != cudaSuccess) return QUAROT_ERR_CUDA;
+  if (e != cudaSuccess) return cuda_fail(e);
   g_last_launches = 1;
   return QUAROT_OK;
 }
@@ -225,7 +233,7 @@ quarot_status quarot_kv_quant(const void* k, int64_t ld_k, const void* v, int64_
   cudaError_t e = qr::launch_kv_quant(k, ld_k, v, ld_v, T, n_kv, head_dim, has_q ? q : nullptr, ld_q,
                                       has_q ? n_q : 0, flags, clip_ratio, k_codes, k_scale, k_zero, v_codes,
                                       v_scale, v_zero, static_cast<cudaStream_t>(stream));
-  if (e != cudaSuccess) return QUAROT_ERR_CUDA;
+  if (e != cudaSuccess) return cuda_fail(e);
   g_last_launches = 1;
   return QUAROT_OK;
 }
@@ -253,7 +261,7 @@ quarot_status quarot_kv_quant_rope(const void* k, int64_t ld_k, const void* v, i
   cudaError_t e = qr::launch_kv_quant_rope(k, ld_k, v, ld_v, T, n_kv, head_dim, has_q ? q : nullptr, ld_q,
                                            has_q ? n_q : 0, flags, clip_ratio, pos0, seq_len, theta, k_codes,
                                            k_scale, k_zero, v_codes, v_scale, v_zero, static_cast<cudaStream_t>(stream));
-  if (e != cudaSuccess) return QUAROT_ERR_CUDA;
+  if (e != cudaSuccess) return cuda_fail(e);
   g_last_launches = 1;
   return QUAROT_OK;
 }

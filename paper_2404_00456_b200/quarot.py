@@ -40,6 +40,7 @@ _SIGS = {
     "quarot_abi_version": [],
     "quarot_base_hadamard": [_c_i32, _vp],
     "quarot_last_launch_count": [],
+    "quarot_last_cuda_error": [],
 }
 EXPORTS = tuple(_SIGS)
 
@@ -63,14 +64,17 @@ def lib() -> ctypes.CDLL:
         for name, args in _SIGS.items():
             f = getattr(h, name)
             f.argtypes = args
-            f.restype = ctypes.c_char_p if name == "quarot_status_string" else ctypes.c_int32
+            f.restype = ctypes.c_char_p if name in ("quarot_status_string", "quarot_last_cuda_error") else ctypes.c_int32
         _lib = h
     return _lib
 
 
 def _check(fn: str, status: int):
     if status != 0:
-        raise QuarotError(fn, status, lib().quarot_status_string(status).decode())
+        msg = lib().quarot_status_string(status).decode()
+        if status == 6:  # QUAROT_ERR_CUDA
+            msg += f" ({lib().quarot_last_cuda_error().decode()})"
+        raise QuarotError(fn, status, msg)
 
 
 def _stream(stream) -> int:
