@@ -21,4 +21,4 @@ Parity pins live in ``tests/test_oracle_*.py``.  Functions without an external
 pin say "parity unpinned" in their docstring; DESIGN.md lists them.
 """
 
-from . import hadamard, quant, gemm, kv, layer, glue  # noqa: F401
+from . import hadamard, quant, gemm, kv, layer, glue, attention  # noqa: F401
