@@ -15,6 +15,8 @@
  *                           place) + asymmetric INT4 group quantization
  *                           (P:210-225 Stage 1d, P:236-237 Stage 2c)
  *   quarot_kv_quant_rope    the same with RoPE fused in front
+ *   quarot_kv_append        routine "Append": one new token per sequence into the cache
+ *   quarot_kv_decode        routine "Decode": attention over the INT4 cache
  *
  * Conventions (all entry points)
  *  - Tensor pointers are CUDA DEVICE pointers owned by the caller.  The library never
@@ -166,6 +168,40 @@ quarot_status quarot_kv_quant_rope(const void* k, int64_t ld_k, const void* v, i
                                    uint32_t flags, float clip_ratio, int64_t pos0, int32_t seq_len,
                                    float theta, uint8_t* k_codes, float* k_scale, uint8_t* k_zero,
                                    uint8_t* v_codes, float* v_scale, uint8_t* v_zero, void* stream);
+
+/* the decoding routines of the paper's quantized attention.
+ * Cache layout (one cache per sequence, s_max rows each): *_codes uint8
+ * [B][s_max][n_kv][head_dim/2], *_scale fp32 [B][s_max][n_kv], *_zero uint8 [B][s_max][n_kv]
+ * — i.e. quarot_kv_quant's output layout with T = B * s_max tokens (Init fills rows 0..T-1 of
+ * a sequence by calling it on that sequence's slice).
+ *
+ * quarot_kv_append — routine 2 "Append": one new token per sequence.  k, v, q fp16
+ *   [B][ld_*] (heads [n][head_dim] contiguous; PRE-RoPE k and q).  positions int32 [B]
+ *   (DEVICE): the new token's row in its sequence's cache, also its RoPE position.  Applies
+ *   RoPE (theta) to K and Q, then exactly quarot_kv_quant's rotation / quantization; writes the
+ *   K/V groups at cache row positions[b] of sequence b and overwrites q with the rotated query
+ *   fp16(H^ fp16(rope(q))) that quarot_kv_decode consumes.  positions[b] < s_max (unchecked:
+ *   device data).  flags / clip_ratio as quarot_kv_quant. */
+quarot_status quarot_kv_append(const void* k, int64_t ld_k, const void* v, int64_t ld_v, int64_t B,
+                               int32_t n_kv, int32_t head_dim, void* q, int64_t ld_q, int32_t n_q,
+                               uint32_t flags, float clip_ratio, const int32_t* positions, float theta,
+                               int64_t s_max, uint8_t* k_codes, float* k_scale, uint8_t* k_zero,
+                               uint8_t* v_codes, float* v_scale, uint8_t* v_zero, void* stream);
+
+/* quarot_kv_decode — routine 3 "Decode": attention of one (rotated) query per sequence
+ * against the INT4 cache, rows 0 .. seq_lens[b]-1 (seq_lens int32 [B], DEVICE, 1 <= seq_lens[b]
+ * <= s_max, unchecked):  o = softmax(<q, k^_j> * sm_scale) . v^,  x^ = (c - z) * s,  GQA head
+ * h -> KV head h / (n_q / n_kv).  q fp16 [B][n_q][head_dim] contiguous; out fp16
+ * [B][n_q][head_dim] contiguous (o is in V's space: V is not rotated online).
+ * workspace fp32, quarot_kv_decode_workspace_bytes(B, n_q, head_dim, s_max) bytes, caller-owned.
+ * Requirements: head_dim == 128; n_q / n_kv in {1, 2, 4, 8}; sm_scale finite (the standard
+ * 1/sqrt(head_dim) is reading Z24); 16-B aligned pointers.  Two kernel launches. */
+quarot_status quarot_kv_decode(const void* q, const uint8_t* k_codes, const float* k_scale,
+                               const uint8_t* k_zero, const uint8_t* v_codes, const float* v_scale,
+                               const uint8_t* v_zero, const int32_t* seq_lens, int64_t B, int32_t n_q,
+                               int32_t n_kv, int32_t head_dim, int64_t s_max, float sm_scale, void* out,
+                               float* workspace, int64_t workspace_bytes, void* stream);
+int64_t quarot_kv_decode_workspace_bytes(int64_t B, int32_t n_q, int32_t head_dim, int64_t s_max);
 
 /* Decoder-layer glue.
  * quarot_rope: Llama-2 rotary position embedding ("Pos", Eqs. 10-12), in place on

@@ -89,6 +89,10 @@ struct RopeArgs {
   int seq_len;
   float theta;
   int tpb;
+  // Append (P:858 routine 2): token t is sequence t's new token at row positions[t] of its
+  // cache (s_max rows per sequence); its RoPE position is positions[t].  nullptr: Init.
+  const int32_t* positions;
+  int64_t s_max;
 };
 
 template <int LPG, bool kRope>
@@ -211,7 +215,8 @@ __global__ void __launch_bounds__(256) kv_quant_kernel(const __half* __restrict_
         }
       }
       const int h = is_k ? which : which - n_kv;
-      const int64_t gi = t * n_kv + h;
+      const int64_t row = (kRope && ra.positions) ? t * ra.s_max + __ldg(ra.positions + t) : t;
+      const int64_t gi = row * n_kv + h;
       uint8_t* codes = (is_k ? k_codes : v_codes) + gi * (HD / 2) + sub * (EPL / 2);
       *reinterpret_cast<uint4*>(codes) = make_uint4(w[0], w[1], w[2], w[3]);
       if (sub == 0) {
@@ -255,7 +260,8 @@ __global__ void __launch_bounds__(256) kv_quant_kernel(const __half* __restrict_
       float2* tab = rope_cs + buf * ra.tpb * HALF;
       for (int i = threadIdx.x; i < ra.tpb * HALF; i += blockDim.x) {
         const int tt = i / HALF, ii = i - tt * HALF;
-        const int64_t pos = (ra.pos0 + t0 + tt) % ra.seq_len;
+        const int64_t pos = ra.positions ? (t0 + tt < T ? (int64_t)__ldg(ra.positions + t0 + tt) : 0)
+                                         : (ra.pos0 + t0 + tt) % ra.seq_len;
         double sn, cn;
         sincos((double)pos * inv_freq[ii], &sn, &cn);  // == pos * theta^(-2 ii / d), as quarot_rope
         tab[i] = make_float2((float)cn, (float)sn);
@@ -292,7 +298,7 @@ cudaError_t launch_kv_quant(const void* k, int64_t ld_k, const void* v, int64_t 
   kvq::kv_quant_kernel<L, false><<<(unsigned)blocks, threads, 0, stream>>>(kh, ld_k, vh, ld_v, qh, ld_q, T, n_kv,  \
                                                                           nq, flags, clip, k_codes, k_scale,      \
                                                                           k_zero, v_codes, v_scale, v_zero,       \
-                                                                          kvq::RopeArgs{0, 1, 0.f, 0})
+                                                                          kvq::RopeArgs{0, 1, 0.f, 0, nullptr, 0})
   if (head_dim == 64) QR_KV(2);
   else if (head_dim == 128) QR_KV(4);
   else QR_KV(8);
@@ -304,7 +310,7 @@ cudaError_t launch_kv_quant_rope(const void* k, int64_t ld_k, const void* v, int
                                  int head_dim, void* q, int64_t ld_q, int n_q, uint32_t flags, float clip,
                                  int64_t pos0, int seq_len, float theta, uint8_t* k_codes, float* k_scale,
                                  uint8_t* k_zero, uint8_t* v_codes, float* v_scale, uint8_t* v_zero,
-                                 cudaStream_t stream) {
+                                 cudaStream_t stream, const int32_t* positions, int64_t s_max) {
   const int nq = q ? n_q : 0;
   const int G = 2 * n_kv + nq;
   if (T == 0 || G == 0) return cudaSuccess;
@@ -318,7 +324,7 @@ cudaError_t launch_kv_quant_rope(const void* k, int64_t ld_k, const void* v, int
   int64_t blocks = (T + tpb - 1) / tpb;
   if (blocks > 148 * 8) blocks = 148 * 8;
   const size_t smem = (size_t)2 * tpb * (head_dim / 2) * sizeof(float2) + (head_dim / 2) * sizeof(double);
-  const kvq::RopeArgs ra{pos0, seq_len, theta, tpb};
+  const kvq::RopeArgs ra{pos0, seq_len, theta, tpb, positions, s_max};
   const __half* kh = static_cast<const __half*>(k);
   const __half* vh = static_cast<const __half*>(v);
   __half* qh = static_cast<__half*>(q);

@@ -1,5 +1,6 @@
 // quarot_abi.cu — the extern "C" boundary (include/quarot.h): argument validation and
 // dispatch to the sm_100a kernels.  No torch types, no allocation, no host synchronization.
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 
@@ -263,6 +264,65 @@ quarot_status quarot_kv_quant_rope(const void* k, int64_t ld_k, const void* v, i
                                            k_scale, k_zero, v_codes, v_scale, v_zero, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e);
   g_last_launches = 1;
+  return QUAROT_OK;
+}
+
+quarot_status quarot_kv_append(const void* k, int64_t ld_k, const void* v, int64_t ld_v, int64_t B,
+                               int32_t n_kv, int32_t head_dim, void* q, int64_t ld_q, int32_t n_q,
+                               uint32_t flags, float clip_ratio, const int32_t* positions, float theta,
+                               int64_t s_max, uint8_t* k_codes, float* k_scale, uint8_t* k_zero,
+                               uint8_t* v_codes, float* v_scale, uint8_t* v_zero, void* stream) {
+  g_last_launches = 0;
+  if (flags & ~3u) return QUAROT_ERR_ARG;
+  if (!clip_ok(clip_ratio) || !(theta > 0.f)) return QUAROT_ERR_ARG;
+  if (B < 0 || n_kv <= 0 || n_q < 0 || head_dim <= 0 || s_max <= 0) return QUAROT_ERR_DIM;
+  if (!(head_dim == 64 || head_dim == 128 || head_dim == 256)) return QUAROT_ERR_UNSUPPORTED_SIZE;
+  const bool has_q = q != nullptr && n_q > 0;
+  if (ld_k < (int64_t)n_kv * head_dim || ld_v < (int64_t)n_kv * head_dim ||
+      (has_q && ld_q < (int64_t)n_q * head_dim))
+    return QUAROT_ERR_DIM;
+  if (B == 0) return QUAROT_OK;
+  if (!k || !v || !positions || !k_codes || !k_scale || !k_zero || !v_codes || !v_scale || !v_zero)
+    return QUAROT_ERR_NULL;
+  if (!aligned16(k) || !aligned16(v) || (has_q && !aligned16(q)) || !aligned16(k_codes) || !aligned16(v_codes))
+    return QUAROT_ERR_ALIGN;
+  if ((ld_k % 8) || (ld_v % 8) || (has_q && (ld_q % 8))) return QUAROT_ERR_ALIGN;
+  cudaError_t e = qr::launch_kv_quant_rope(k, ld_k, v, ld_v, B, n_kv, head_dim, has_q ? q : nullptr, ld_q,
+                                           has_q ? n_q : 0, flags, clip_ratio, 0, 1, theta, k_codes, k_scale,
+                                           k_zero, v_codes, v_scale, v_zero, static_cast<cudaStream_t>(stream),
+                                           positions, s_max);
+  if (e != cudaSuccess) return cuda_fail(e);
+  g_last_launches = 1;
+  return QUAROT_OK;
+}
+
+int64_t quarot_kv_decode_workspace_bytes(int64_t B, int32_t n_q, int32_t head_dim, int64_t s_max) {
+  if (B <= 0 || n_q <= 0 || head_dim <= 0 || s_max <= 0) return 0;
+  return (int64_t)qr::kv_decode_workspace_bytes((int)B, n_q, head_dim, (int)s_max);
+}
+
+quarot_status quarot_kv_decode(const void* q, const uint8_t* k_codes, const float* k_scale,
+                               const uint8_t* k_zero, const uint8_t* v_codes, const float* v_scale,
+                               const uint8_t* v_zero, const int32_t* seq_lens, int64_t B, int32_t n_q,
+                               int32_t n_kv, int32_t head_dim, int64_t s_max, float sm_scale, void* out,
+                               float* workspace, int64_t workspace_bytes, void* stream) {
+  g_last_launches = 0;
+  if (B < 0 || n_q <= 0 || n_kv <= 0 || head_dim <= 0 || s_max <= 0 || s_max > (1 << 30)) return QUAROT_ERR_DIM;
+  if (n_q % n_kv) return QUAROT_ERR_DIM;
+  const int G = n_q / n_kv;
+  if (head_dim != 128 || !(G == 1 || G == 2 || G == 4 || G == 8)) return QUAROT_ERR_UNSUPPORTED_SIZE;
+  if (!(sm_scale == sm_scale) || sm_scale == INFINITY || sm_scale == -INFINITY) return QUAROT_ERR_ARG;
+  if (B == 0) return QUAROT_OK;
+  if (!q || !k_codes || !k_scale || !k_zero || !v_codes || !v_scale || !v_zero || !seq_lens || !out || !workspace)
+    return QUAROT_ERR_NULL;
+  if (workspace_bytes < quarot_kv_decode_workspace_bytes(B, n_q, head_dim, s_max)) return QUAROT_ERR_ARG;
+  if (!aligned16(q) || !aligned16(k_codes) || !aligned16(v_codes) || !aligned16(out) || !aligned16(workspace))
+    return QUAROT_ERR_ALIGN;
+  cudaError_t e = qr::launch_kv_decode(q, k_codes, k_scale, k_zero, v_codes, v_scale, v_zero, seq_lens, (int)B, n_q,
+                                       n_kv, head_dim, (int)s_max, sm_scale, out, workspace,
+                                       static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e);
+  g_last_launches = 2;
   return QUAROT_OK;
 }
 

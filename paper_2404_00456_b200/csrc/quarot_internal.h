@@ -32,7 +32,13 @@ cudaError_t launch_kv_quant_rope(const void* k, int64_t ld_k, const void* v, int
                                  int head_dim, void* q, int64_t ld_q, int n_q, uint32_t flags, float clip,
                                  int64_t pos0, int seq_len, float theta, uint8_t* k_codes, float* k_scale,
                                  uint8_t* k_zero, uint8_t* v_codes, float* v_scale, uint8_t* v_zero,
-                                 cudaStream_t stream);
+                                 cudaStream_t stream, const int32_t* positions = nullptr, int64_t s_max = 0);
+// KV Decode: split-sequence flash decoding over the INT4 cache + the combine pass.
+size_t kv_decode_workspace_bytes(int B, int n_q, int head_dim, int s_max);
+cudaError_t launch_kv_decode(const void* q, const uint8_t* k_codes, const float* k_scale, const uint8_t* k_zero,
+                             const uint8_t* v_codes, const float* v_scale, const uint8_t* v_zero,
+                             const int32_t* seq_lens, int B, int n_q, int n_kv, int head_dim, int s_max,
+                             float sm_scale, void* out, float* workspace, cudaStream_t stream);
 
 // glue.cu
 cudaError_t launch_rope(void* x, int64_t T, int n_heads, int head_dim, int64_t ld_x, int64_t pos0, int seq_len,

@@ -36,6 +36,11 @@ _SIGS = {
                         _c_f32, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "quarot_kv_quant_rope": [_vp, _c_i64, _vp, _c_i64, _c_i64, _c_i32, _c_i32, _vp, _c_i64, _c_i32, _c_u32,
                              _c_f32, _c_i64, _c_i32, _c_f32, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "quarot_kv_append": [_vp, _c_i64, _vp, _c_i64, _c_i64, _c_i32, _c_i32, _vp, _c_i64, _c_i32, _c_u32, _c_f32,
+                         _vp, _c_f32, _c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "quarot_kv_decode": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_i64, _c_i32, _c_i32, _c_i32, _c_i64, _c_f32,
+                         _vp, _vp, _c_i64, _vp],
+    "quarot_kv_decode_workspace_bytes": [_c_i64, _c_i32, _c_i32, _c_i64],
     "quarot_status_string": [_c_i32],
     "quarot_abi_version": [],
     "quarot_base_hadamard": [_c_i32, _vp],
@@ -64,7 +69,8 @@ def lib() -> ctypes.CDLL:
         for name, args in _SIGS.items():
             f = getattr(h, name)
             f.argtypes = args
-            f.restype = ctypes.c_char_p if name in ("quarot_status_string", "quarot_last_cuda_error") else ctypes.c_int32
+            f.restype = (ctypes.c_char_p if name in ("quarot_status_string", "quarot_last_cuda_error")
+                         else ctypes.c_int64 if name == "quarot_kv_decode_workspace_bytes" else ctypes.c_int32)
         _lib = h
     return _lib
 
@@ -247,6 +253,64 @@ def kv_quant(k: torch.Tensor, v: torch.Tensor, q: torch.Tensor | None = None, fl
     else:
         pos0, seq_len, theta = rope
         _check("quarot_kv_quant_rope", lib().quarot_kv_quant_rope(*head, int(pos0), int(seq_len), float(theta), *outs))
+    return out
+
+
+def kv_cache_empty(B: int, s_max: int, n_kv: int, head_dim: int = 128, device="cuda") -> dict:
+    """Allocate a per-sequence INT4 KV cache (layout of quarot_kv_append / quarot_kv_decode)."""
+    return {"k_codes": torch.zeros(B, s_max, n_kv, head_dim // 2, dtype=torch.uint8, device=device),
+            "k_scale": torch.ones(B, s_max, n_kv, dtype=torch.float32, device=device),
+            "k_zero": torch.zeros(B, s_max, n_kv, dtype=torch.uint8, device=device),
+            "v_codes": torch.zeros(B, s_max, n_kv, head_dim // 2, dtype=torch.uint8, device=device),
+            "v_scale": torch.ones(B, s_max, n_kv, dtype=torch.float32, device=device),
+            "v_zero": torch.zeros(B, s_max, n_kv, dtype=torch.uint8, device=device)}
+
+
+def kv_append(k: torch.Tensor, v: torch.Tensor, q: torch.Tensor | None, positions: torch.Tensor, cache: dict,
+              flags: int = KV_ROTATE_K, clip_ratio: float = 0.95, theta: float = 10000.0, stream=None) -> dict:
+    """quarot_kv_append (routine Append): k, v [B, n_kv, d], q [B, n_q, d] pre-RoPE fp16
+    (q rotated in place); positions int32 [B] on the device; cache from kv_cache_empty."""
+    B, n_kv, d = k.shape
+    s_max = cache["k_codes"].shape[1]
+    for name, t in (("k", k), ("v", v), ("q", q)):
+        if t is not None and (t.stride(2) != 1 or t.stride(1) != d):
+            raise ValueError(f"{name}: heads of a token must be contiguous [n, d]")
+    if positions.dtype != torch.int32 or positions.device != k.device:
+        raise ValueError("positions: int32 on the device")
+    st = lib().quarot_kv_append(_dev(k, "k", torch.float16), k.stride(0), _dev(v, "v", torch.float16), v.stride(0),
+                                B, n_kv, d, None if q is None else _dev(q, "q", torch.float16),
+                                0 if q is None else q.stride(0), 0 if q is None else q.shape[1], flags, clip_ratio,
+                                positions.data_ptr(), theta, s_max,
+                                *(cache[n].data_ptr() for n in ("k_codes", "k_scale", "k_zero", "v_codes", "v_scale",
+                                                               "v_zero")), _stream(stream))
+    _check("quarot_kv_append", st)
+    return cache
+
+
+def kv_decode(q: torch.Tensor, cache: dict, seq_lens: torch.Tensor, n_kv: int | None = None,
+              sm_scale: float | None = None, out: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
+              stream=None) -> torch.Tensor:
+    """quarot_kv_decode (routine Decode): q fp16 [B, n_q, d] (rotated), seq_lens int32 [B]
+    on the device.  Returns fp16 [B, n_q, d]."""
+    B, n_q, d = q.shape
+    s_max, n_kv_c = cache["k_codes"].shape[1], cache["k_codes"].shape[2]
+    n_kv = n_kv_c if n_kv is None else n_kv
+    if not q.is_contiguous():
+        raise ValueError("q must be contiguous [B, n_q, d]")
+    if seq_lens.dtype != torch.int32 or seq_lens.device != q.device:
+        raise ValueError("seq_lens: int32 on the device")
+    if out is None:
+        out = torch.empty_like(q)
+    wsb = lib().quarot_kv_decode_workspace_bytes(B, n_q, d, s_max)
+    if workspace is None or workspace.numel() * workspace.element_size() < wsb:
+        workspace = torch.empty(max(1, wsb // 4), dtype=torch.float32, device=q.device)
+    st = lib().quarot_kv_decode(_dev(q, "q", torch.float16),
+                                *(cache[n].data_ptr() for n in ("k_codes", "k_scale", "k_zero", "v_codes", "v_scale",
+                                                               "v_zero")),
+                                seq_lens.data_ptr(), B, n_q, n_kv, d, s_max,
+                                float(d ** -0.5 if sm_scale is None else sm_scale), out.data_ptr(),
+                                workspace.data_ptr(), workspace.numel() * workspace.element_size(), _stream(stream))
+    _check("quarot_kv_decode", st)
     return out
 
 

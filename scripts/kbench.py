@@ -114,6 +114,32 @@ def main():
         print("kv_rope", json.dumps(res["kv_rope"]), flush=True)
         ms = timeit(lambda: q.rope(fused[:, :9216].view(T, 72, d)), a.iters)
         print("rope", json.dumps({"ms": ms}), flush=True)
+    if "decode" in a.what:
+        # SURVEY §8 f2 / tab:QAttention_bench: append + decode of one token per sequence on a
+        # cache of 2047 rows (seq_len 2048); bytes = the INT4 cache rows read (codes + scales)
+        for n_q, n_kv in ((32, 32), (40, 40), (64, 64), (64, 8)):
+            for B in (1, 8, 16, 32, 64):
+                L, d = 2048, 128
+                cache = q.kv_cache_empty(B, L, n_kv, d)
+                kn, vn, qn = synth.kv_inputs(B, n_kv, n_q, d, seed=1, device=dev)
+                pos = torch.full((B,), L - 1, dtype=torch.int32, device=dev)
+                lens = torch.full((B,), L, dtype=torch.int32, device=dev)
+                out = torch.empty(B, n_q, d, dtype=torch.float16, device=dev)
+                ws = torch.empty(q.lib().quarot_kv_decode_workspace_bytes(B, n_q, d, L) // 4, device=dev)
+                qb = qn.clone()
+
+                def step():
+                    qb.copy_(qn)
+                    q.kv_append(kn, vn, qb, pos, cache)
+                    q.kv_decode(qb, cache, lens, out=out, workspace=ws)
+                ms = timeit(step, max(a.iters, 20))
+                ms_dec = timeit(lambda: q.kv_decode(qb, cache, lens, out=out, workspace=ws), max(a.iters, 20))
+                byts = B * n_kv * L * (2 * d // 2 + 10)
+                key = f"decode_{n_q}x{n_kv}_b{B}"
+                res[key] = {"ms_append_decode": ms, "ms_decode": ms_dec, "gbs_decode": byts / ms_dec / 1e6,
+                            "frac_hbm": byts / ms_dec / 1e6 / 6536}
+                print(key, json.dumps(res[key]), flush=True)
+                del cache
     if "intmm" in a.what:
         # library INT8 reference: cuBLASLt via torch._int_mm, 8192^3 (denominator context)
         A = torch.randint(-7, 8, (8192, 8192), dtype=torch.int8, device=dev)
