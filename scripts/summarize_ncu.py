@@ -11,9 +11,9 @@ import subprocess
 import sys
 from collections import defaultdict
 
-# launch order of runtime.DecoderLayerStep (fused SwiGLU): the library's kernels only
-CHAIN = ["hq_qkv", "gemm_qkv", "rope", "kv_quant", "hq_o", "gemm_o", "hq_gate_up", "gemm_gate_up", "hq_down",
-         "gemm_down"]
+# launch order of runtime.DecoderLayerStep (fused SwiGLU, RoPE fused into the KV pass): the
+# library's kernels only
+CHAIN = ["hq_qkv", "gemm_qkv", "kv_quant", "hq_o", "gemm_o", "hq_gate_up", "gemm_gate_up", "hq_down", "gemm_down"]
 OURS = ("int4_gemm", "hq_", "kv_quant", "rope_kernel", "swiglu_kernel")
 
 
