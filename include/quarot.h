@@ -17,6 +17,7 @@
  *   quarot_kv_quant_rope    the same with RoPE fused in front
  *   quarot_kv_append        routine "Append": one new token per sequence into the cache
  *   quarot_kv_decode        routine "Decode": attention over the INT4 cache
+ *   quarot_hadamard_quant8, quarot_int8_linear   A8W8 (8-bit RTN configuration)
  *
  * Conventions (all entry points)
  *  - Tensor pointers are CUDA DEVICE pointers owned by the caller.  The library never
@@ -168,6 +169,25 @@ quarot_status quarot_kv_quant_rope(const void* k, int64_t ld_k, const void* v, i
                                    uint32_t flags, float clip_ratio, int64_t pos0, int32_t seq_len,
                                    float theta, uint8_t* k_codes, float* k_scale, uint8_t* k_zero,
                                    uint8_t* v_codes, float* v_scale, uint8_t* v_zero, void* stream);
+
+/* A8W8 QuaRot ("lossless" 8-bit RTN, P:6, tab:rtn_results): the native
+ * kind::i8 tensor path with no unpacking, the comparison point for the INT4 unpack cost.
+ * quarot_hadamard_quant8: as quarot_hadamard_quant but codes are int8 in [-127, 127], one byte
+ *   per element (q int8 [M][ld_q], ld_q >= K, % 8), scale = fp32(clip * amax / 127).  Only
+ *   mode QUAROT_HAD_NONE (optionally | QUAROT_HAD_RMSNORM) is built; FULL / ACROSS_HEADS return
+ *   QUAROT_ERR_UNSUPPORTED_SIZE.
+ * quarot_int8_linear: y[m,n] = fp16_rn(fp32(acc) * x_scale[m] * w_scale[n]),
+ *   acc = sum_k xq[m,k] * wq[n,k] (int8 x int8 -> exact int32).  xq int8 [M][ld_xq], wq int8
+ *   [N][ld_wq] (nn.Linear layout), ld % 16 == 0, K % 128 == 0, K <= 131072, N % 8 == 0.
+ * quarot_int8_matmul_s32: raw accumulators (parity only). */
+quarot_status quarot_hadamard_quant8(const void* x, int64_t M, int64_t K, int64_t ld_x, int32_t mode,
+                                     int32_t head_dim, float clip_ratio, int8_t* q, int64_t ld_q, float* scale,
+                                     void* stream);
+quarot_status quarot_int8_linear(const int8_t* xq, const float* x_scale, int64_t M, int64_t K, int64_t ld_xq,
+                                 const int8_t* wq, const float* w_scale, int64_t N, int64_t ld_wq, void* y,
+                                 int64_t ld_y, void* stream);
+quarot_status quarot_int8_matmul_s32(const int8_t* xq, int64_t M, int64_t K, int64_t ld_xq, const int8_t* wq,
+                                     int64_t N, int64_t ld_wq, int32_t* acc, int64_t ld_acc, void* stream);
 
 /* the decoding routines of the paper's quantized attention.
  * Cache layout (one cache per sequence, s_max rows each): *_codes uint8

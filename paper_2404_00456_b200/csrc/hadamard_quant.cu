@@ -17,11 +17,13 @@
 namespace qr {
 namespace hq {
 
-// RNE code in [-7, 7] of v * inv (inv = 1 / scale, or 0 for a zero / non-finite row)
+// RNE code in [-QMAX, QMAX] of v * inv (inv = 1 / scale, or 0 for a zero / non-finite row);
+// QMAX = 7 for INT4, 127 for the 8-bit configuration (§8 f4)
+template <int QMAX = 7>
 QR_DEVICE int code_of(float v, float inv) {
   int c = __float2int_rn(v * inv);
-  c = c > 7 ? 7 : c;
-  c = c < -7 ? -7 : c;
+  c = c > QMAX ? QMAX : c;
+  c = c < -QMAX ? -QMAX : c;
   return c;
 }
 QR_DEVICE uint32_t nib(int c) { return (uint32_t)c & 0xFu; }
@@ -29,7 +31,7 @@ QR_DEVICE uint32_t nib(int c) { return (uint32_t)c & 0xFu; }
 // Per-row scale from the unnormalized amax: scale = fp32(clip * amax * norm / 7);
 // returns inv = norm / scale so that code = rne(y_unnorm * inv).  Zero row -> scale 1,
 // inv 0 (all codes 0); non-finite -> scale NaN, inv 0.
-QR_DEVICE void row_scale(float amax_u, double norm, float clip, float& scale, float& inv) {
+QR_DEVICE void row_scale(float amax_u, double norm, float clip, float& scale, float& inv, double qmax = 7.0) {
   if (amax_u == 0.f) {
     scale = 1.f;
     inv = 0.f;
@@ -37,7 +39,7 @@ QR_DEVICE void row_scale(float amax_u, double norm, float clip, float& scale, fl
     scale = __int_as_float(0x7fc00000);
     inv = 0.f;
   } else {
-    const double s = (double)clip * (double)amax_u * norm / 7.0;
+    const double s = (double)clip * (double)amax_u * norm / qmax;
     scale = (float)s;
     inv = (float)(norm / (double)scale);
   }
@@ -60,7 +62,7 @@ QR_DEVICE float block_max(float v, float* red) {
 // One row per 128-thread CTA; each thread owns CPT 8-element chunks held in registers.
 // kRms: the row is RMS-normalized first (scale-free RMSNorm): the codes of x / rms
 // equal the codes of x, so only the scale changes (scale / rms).
-template <int CPT, bool kRms>
+template <int CPT, bool kRms, bool kQ8 = false>  // kQ8: int8 codes, one byte per element (A8, §8 f4)
 __global__ void __launch_bounds__(128) hq_none_kernel(const __half* __restrict__ x, int64_t K, int64_t ld_x,
                                                       float clip, uint8_t* __restrict__ q, int64_t ld_q,
                                                       float* __restrict__ scale) {
@@ -97,7 +99,7 @@ __global__ void __launch_bounds__(128) hq_none_kernel(const __half* __restrict__
     norm = (double)rsqrtf(tot / (float)K + 1e-5f);
   }
   float s, inv;
-  row_scale(amax, norm, clip, s, inv);
+  row_scale(amax, norm, clip, s, inv, kQ8 ? 127.0 : 7.0);
   if (threadIdx.x == 0) scale[row] = s;
   uint8_t* qr = q + row * ld_q;
 #pragma unroll
@@ -105,13 +107,24 @@ __global__ void __launch_bounds__(128) hq_none_kernel(const __half* __restrict__
     const int c = threadIdx.x + i * 128;
     if (c < nchunk) {
       const __half2* h = reinterpret_cast<const __half2*>(&v[i]);
-      uint32_t packed = 0;
+      if constexpr (kQ8) {
+        uint32_t w[2] = {0u, 0u};
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 f = __half22float2(h[e]);
-        packed |= (nib(code_of(f.x, inv)) | (nib(code_of(f.y, inv)) << 4)) << (8 * e);
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __half22float2(h[e]);
+          w[e >> 1] |= (((uint32_t)code_of<127>(f.x, inv) & 0xFFu) | (((uint32_t)code_of<127>(f.y, inv) & 0xFFu) << 8))
+                       << (16 * (e & 1));
+        }
+        *reinterpret_cast<uint2*>(qr + (int64_t)c * 8) = make_uint2(w[0], w[1]);
+      } else {
+        uint32_t packed = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __half22float2(h[e]);
+          packed |= (nib(code_of(f.x, inv)) | (nib(code_of(f.y, inv)) << 4)) << (8 * e);
+        }
+        *reinterpret_cast<uint32_t*>(qr + (int64_t)c * 4) = packed;
       }
-      *reinterpret_cast<uint32_t*>(qr + (int64_t)c * 4) = packed;
     }
   }
 }
@@ -496,6 +509,9 @@ __global__ void hq_full_kernel(const __half* __restrict__ x, int64_t ld_x, int P
 #ifndef QR_F28_P1W
 #define QR_F28_P1W 4
 #endif
+#ifdef QR_F28_PROF
+__device__ unsigned long long g_f28_prof[148 * 8];  // per CTA: p1_wait_x, p1_wait_z, p1_total, p2_wait, p2_total
+#endif
 namespace f28 {
 constexpr int MB = 28, P = 1024, K = MB * P;  // (M is the row count)
 constexpr int P1_WARPS = QR_F28_P1W, P2_WARPS = 14, NT = (P1_WARPS + P2_WARPS) * 32;
@@ -542,6 +558,9 @@ __global__ void __launch_bounds__(f28::NT, 1)  // 18 warps: at most 5 per SM sub
         : "memory");
   };
 
+#ifdef QR_F28_PROF
+  const long long t_start = clock64();
+#endif
   if (warp < P1_WARPS) {
     // ======================= P1: bulk copy + H_28 (tensor cores) + H over 5 a-bits in registers
     const int g = lane >> 2, t = lane & 3;
@@ -553,8 +572,20 @@ __global__ void __launch_bounds__(f28::NT, 1)  // 18 warps: at most 5 per SM sub
     for (int64_t row = blockIdx.x; row < M; row += gridDim.x, ++it) {
       const int buf = it & 1;
       const uint32_t* xw = reinterpret_cast<const uint32_t*>(xs0 + buf * XS_BYTES);
+#ifdef QR_F28_PROF
+      const long long t0 = clock64();
+#endif
       mbar_wait_sleep(&xs_full[buf], (it >> 1) & 1);
+#ifdef QR_F28_PROF
+      const long long t1 = clock64();
+#endif
       mbar_wait_sleep(z_empty, (it & 1) ^ 1);
+#ifdef QR_F28_PROF
+      if (threadIdx.x == 0) {
+        atomicAdd(&g_f28_prof[blockIdx.x * 8 + 0], (unsigned long long)(t1 - t0));
+        atomicAdd(&g_f28_prof[blockIdx.x * 8 + 1], (unsigned long long)(clock64() - t1));
+      }
+#endif
 #pragma unroll 1
       for (int u = 0; u < UNITS; ++u) {
         const int unit = warp * UNITS + u;  // 0..15
@@ -614,6 +645,9 @@ __global__ void __launch_bounds__(f28::NT, 1)  // 18 warps: at most 5 per SM sub
       named_bar(1, P1_WARPS * 32);  // every P1 thread is done reading xs[buf]
       if (threadIdx.x == 0 && row + 2 * (int64_t)gridDim.x < M) issue_row(row + 2 * (int64_t)gridDim.x, buf);
     }
+#ifdef QR_F28_PROF
+    if (threadIdx.x == 0) atomicAdd(&g_f28_prof[blockIdx.x * 8 + 2], (unsigned long long)(clock64() - t_start));
+#endif
   } else {
     // ======================= P2: H_32 over p2, amax, codes, packed output
     const int tp = threadIdx.x - P1_WARPS * 32;  // 0..447 = c * 14 + bp
@@ -623,7 +657,13 @@ __global__ void __launch_bounds__(f28::NT, 1)  // 18 warps: at most 5 per SM sub
     const int a_c = (c & 3) | ((c >> 2) << 4);
     int it = 0;
     for (int64_t row = blockIdx.x; row < M; row += gridDim.x, ++it) {
+#ifdef QR_F28_PROF
+      const long long t2 = clock64();
+#endif
       mbar_wait_sleep(z_full, it & 1);
+#ifdef QR_F28_PROF
+      if (threadIdx.x == P1_WARPS * 32) atomicAdd(&g_f28_prof[blockIdx.x * 8 + 3], (unsigned long long)(clock64() - t2));
+#endif
       float2 v[32];
       const float2* zp = reinterpret_cast<const float2*>(Z) + tp;  // (c * 28 + 2 bp) / 2 == tp
 #pragma unroll
@@ -666,6 +706,9 @@ __global__ void __launch_bounds__(f28::NT, 1)  // 18 warps: at most 5 per SM sub
         for (int p2 = 0; p2 < 32; ++p2) qr[((p2 & 3) << 2 | (p2 >> 2) << 7) * (MB / 2)] = 0;
       }
     }
+#ifdef QR_F28_PROF
+    if (threadIdx.x == P1_WARPS * 32) atomicAdd(&g_f28_prof[blockIdx.x * 8 + 4], (unsigned long long)(clock64() - t_start));
+#endif
   }
 }
 
@@ -691,6 +734,28 @@ cudaError_t launch_hq_none(const void* x, int64_t M, int64_t K, int64_t ld_x, fl
   else if (cpt <= 16) QR_NONE(16);
   else QR_NONE(32);
 #undef QR_NONE
+  return cudaPeekAtLastError();
+}
+
+cudaError_t launch_hq_none_q8(const void* x, int64_t M, int64_t K, int64_t ld_x, float clip, int8_t* q, int64_t ld_q,
+                              float* scale, cudaStream_t stream, bool rmsnorm) {
+  const int64_t nchunk = K / 8;
+  const int cpt = (int)((nchunk + 127) / 128);
+  const dim3 grid((unsigned)M);
+  const __half* xh = static_cast<const __half*>(x);
+  uint8_t* qb = reinterpret_cast<uint8_t*>(q);
+#define QR_NONE8(C)                                                                                            \
+  do {                                                                                                         \
+    if (rmsnorm) hq::hq_none_kernel<C, true, true><<<grid, 128, 0, stream>>>(xh, K, ld_x, clip, qb, ld_q, scale);  \
+    else hq::hq_none_kernel<C, false, true><<<grid, 128, 0, stream>>>(xh, K, ld_x, clip, qb, ld_q, scale);        \
+  } while (0)
+  if (cpt <= 1) QR_NONE8(1);
+  else if (cpt <= 2) QR_NONE8(2);
+  else if (cpt <= 4) QR_NONE8(4);
+  else if (cpt <= 8) QR_NONE8(8);
+  else if (cpt <= 16) QR_NONE8(16);
+  else QR_NONE8(32);
+#undef QR_NONE8
   return cudaPeekAtLastError();
 }
 
@@ -781,3 +846,12 @@ cudaError_t launch_hq_full(const void* x, int64_t M, int64_t K, int64_t ld_x, in
 }
 
 }  // namespace qr
+
+#ifdef QR_F28_PROF
+extern "C" void quarot_debug_f28_prof(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, qr::hq::g_f28_prof, sizeof(unsigned long long) * 148 * 8);
+  cudaMemset(nullptr, 0, 0);
+  static unsigned long long zero[148 * 8] = {};
+  cudaMemcpyToSymbol(qr::hq::g_f28_prof, zero, sizeof(zero));
+}
+#endif

@@ -183,7 +183,7 @@ QR_DEVICE void mma_commit_pair(uint64_t* bar) {
 // wsc = their 32 weight scales in smem).  fp16: y = fp16_rn(fp32(acc) * s_x * s_w [+ r]);
 // s32: raw accumulators; SwiGLU: the chunk is [8 gate | 8 up] x 2 (interleaved weight rows)
 // and 16 act = silu(g) * u values go to column n0 / 2.
-template <bool kS32, int kDbg>
+template <bool kS32, int kDbg, int kShift = 8>  // kShift: the x16 nibble scaling of both operands (A4W4)
 QR_DEVICE void epi_chunk(const Params& p, const uint32_t (&rc)[32], int64_t m, bool row_ok, int64_t n0, float sx,
                          const float* wsc) {
   if (!row_ok) return;
@@ -192,8 +192,9 @@ QR_DEVICE void epi_chunk(const Params& p, const uint32_t (&rc)[32], int64_t m, b
 #pragma unroll
     for (int g = 0; g < 8; ++g)
       if (n0 + g * 4 < p.N)
-        *reinterpret_cast<int4*>(dst + g * 4) = make_int4((int32_t)rc[4 * g] >> 8, (int32_t)rc[4 * g + 1] >> 8,
-                                                          (int32_t)rc[4 * g + 2] >> 8, (int32_t)rc[4 * g + 3] >> 8);
+        *reinterpret_cast<int4*>(dst + g * 4) =
+            make_int4((int32_t)rc[4 * g] >> kShift, (int32_t)rc[4 * g + 1] >> kShift,
+                      (int32_t)rc[4 * g + 2] >> kShift, (int32_t)rc[4 * g + 3] >> kShift);
   } else if (p.swiglu) {
 #pragma unroll
     for (int hgrp = 0; hgrp < 2; ++hgrp) {
@@ -207,8 +208,8 @@ QR_DEVICE void epi_chunk(const Params& p, const uint32_t (&rc)[32], int64_t m, b
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
             const int c = 2 * e + j;
-            const float gv = ((float)((int32_t)rc[16 * hgrp + c] >> 8) * sx) * sg[c];
-            const float uv = ((float)((int32_t)rc[16 * hgrp + 8 + c] >> 8) * sx) * sg[8 + c];
+            const float gv = ((float)((int32_t)rc[16 * hgrp + c] >> kShift) * sx) * sg[c];
+            const float uv = ((float)((int32_t)rc[16 * hgrp + 8 + c] >> kShift) * sx) * sg[8 + c];
             a[j] = gv / (1.f + __expf(-gv)) * uv;
           }
           h[e] = pack_half2(a[0], a[1]);
@@ -238,8 +239,8 @@ QR_DEVICE void epi_chunk(const Params& p, const uint32_t (&rc)[32], int64_t m, b
         uint32_t h[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          float v0 = ((float)((int32_t)rc[8 * g + 2 * e] >> 8) * sx) * swv[2 * e];
-          float v1 = ((float)((int32_t)rc[8 * g + 2 * e + 1] >> 8) * sx) * swv[2 * e + 1];
+          float v0 = ((float)((int32_t)rc[8 * g + 2 * e] >> kShift) * sx) * swv[2 * e];
+          float v1 = ((float)((int32_t)rc[8 * g + 2 * e + 1] >> kShift) * sx) * swv[2 * e + 1];
           if (p.residual) {
             v0 += __half2float(__ushort_as_half((unsigned short)(rw[e] & 0xFFFFu)));
             v1 += __half2float(__ushort_as_half((unsigned short)(rw[e] >> 16)));
@@ -516,6 +517,185 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
+// ============================================================================ A8W8 (§8 f4)
+// INT8 x INT8 -> INT32 (QuaRot's 8-bit RTN configuration, P:6, tab:rtn_results): the native
+// kind::i8 tensor path with no unpacking — the comparison point for the INT4 unpack cost.
+// Both operands are TMA'd straight into the UMMA SW128 K-major layout (two 128-byte swizzle
+// atoms per 256-wide k-block), the MMA reads both from smem (SS form), and with no A stages in
+// TMEM the accumulator is double-buffered (2 x 256 columns): the epilogue of tile t overlaps
+// the mainloop of tile t + 1.  Warps per CTA: 0-7 epilogue, 8 TMA, 9 relay (its CTA's stage
+// landed -> the leader's "ready" barrier), 10 MMA issuer (leader CTA).
+namespace i8 {
+constexpr int STAGES = 3;
+constexpr int A_BYTES = BMC * BK;              // 32 KB: 128 rows x 256 int8
+constexpr int B_BYTES = BNC * BK;              // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // 64 KB
+constexpr int TMA_WARP = 8, RELAY_WARP = 9, MMA_WARP = 10;
+constexpr int NUM_THREADS = 12 * 32;
+constexpr size_t SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 512 + BN * 4;
+static_assert(SMEM_BYTES <= 232448, "227 KB dynamic smem");
+}  // namespace i8
+
+QR_DEVICE void mma_i8_ss_2sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}"
+      ::"r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(acc));
+}
+
+template <bool kS32>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(i8::NUM_THREADS, 1)
+    int8_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + i8::STAGES * i8::STAGE_BYTES);
+  uint64_t* full = bars;                 // [i8::STAGES] local TMA complete
+  uint64_t* ready = full + i8::STAGES;       // [i8::STAGES] leader: both CTAs' stage landed (2 arrivals)
+  uint64_t* empty = ready + i8::STAGES;      // [i8::STAGES] MMA commit (multicast) -> TMA
+  uint64_t* t_full = empty + i8::STAGES;     // [2] MMA commit (multicast) -> epilogue
+  uint64_t* t_empty = t_full + 2;        // [2] leader: epilogues of both CTAs
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(t_empty + 2);
+  float* ws_smem = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 512);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int pair = (int)blockIdx.x >> 1;
+  const int num_pairs = (int)gridDim.x >> 1;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < i8::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&ready[s], 2);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&t_full[b], 1);
+      mbar_init(&t_empty[b], 2 * NUM_EPI_WARPS);
+    }
+    fence_barrier_init();
+  }
+  if (warp == i8::MMA_WARP) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  if (warp == i8::TMA_WARP && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  const int my_tiles = (p.num_tiles > pair) ? (p.num_tiles - 1 - pair) / num_pairs + 1 : 0;
+  const int total = my_tiles * p.num_kb;
+
+  if (warp == i8::TMA_WARP) {
+    if (lane == 0) {
+      for (int it = 0; it < total; ++it) {
+        const int tl = it / p.num_kb, kb = it - tl * p.num_kb;
+        int mb, nb;
+        tile_coords(p, pair + tl * num_pairs, mb, nb);
+        const int s = it % i8::STAGES;
+        mbar_wait_sleep(&empty[s], ((it / i8::STAGES) & 1) ^ 1);
+        mbar_expect_tx(&full[s], i8::STAGE_BYTES);
+        const uint32_t dst = smem_u32(smem + s * i8::STAGE_BYTES);
+        const int ya = mb * BM + (int)rank * BMC, yb = nb * BN + (int)rank * BNC;
+        tma_load_2d(dst, &tmA, kb * BK, ya, &full[s]);
+        tma_load_2d(dst + BMC * 128, &tmA, kb * BK + 128, ya, &full[s]);
+        tma_load_2d(dst + i8::A_BYTES, &tmB, kb * BK, yb, &full[s]);
+        tma_load_2d(dst + i8::A_BYTES + BNC * 128, &tmB, kb * BK + 128, yb, &full[s]);
+      }
+    }
+  } else if (warp == i8::RELAY_WARP) {
+    if (lane == 0) {
+      const uint32_t ready_leader = map_to_rank(&ready[0], 0);
+      for (int it = 0; it < total; ++it) {
+        const int s = it % i8::STAGES;
+        mbar_wait(&full[s], (it / i8::STAGES) & 1);
+        mbar_arrive_cluster(ready_leader + (uint32_t)s * 8u);
+      }
+    }
+  } else if (warp == i8::MMA_WARP) {
+    if (rank == 0 && lane == 0) {
+      int it = 0;
+      for (int tl = 0; tl < my_tiles; ++tl) {
+        const int ab = tl & 1;
+        mbar_wait(&t_empty[ab], ((tl >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)(ab * BN);
+        for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
+          const int s = it % i8::STAGES;
+          mbar_wait(&ready[s], (it / i8::STAGES) & 1);
+          tc_fence_after();
+          const uint32_t base = smem_u32(smem + s * i8::STAGE_BYTES);
+          const uint64_t a_desc = umma_desc_sw128(base), b_desc = umma_desc_sw128(base + i8::A_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 32; ++k) {  // atom k/4 at +16 KB, 32 bytes along K within it
+            const uint64_t off = (uint64_t)((k >> 2) * (BMC * 128 / 16) + 2 * (k & 3));
+            mma_i8_ss_2sm(d_tmem, a_desc + off, b_desc + off, IDESC, (kb | k) != 0 ? 1u : 0u);
+          }
+          mma_commit_pair(&empty[s]);
+        }
+        mma_commit_pair(&t_full[ab]);
+      }
+    }
+    __syncwarp();
+  } else if (warp < NUM_EPI_WARPS) {
+    const uint32_t tempty_leader = map_to_rank(&t_empty[0], 0);
+    const int quarter = warp & 3, chalf = warp >> 2;
+    const int row_in_tile = (int)rank * BMC + quarter * 32 + lane;
+    const int et = threadIdx.x;
+    for (int tl = 0; tl < my_tiles; ++tl) {
+      const int ab = tl & 1;
+      int mb, nb;
+      tile_coords(p, pair + tl * num_pairs, mb, nb);
+      const int64_t m = (int64_t)mb * BM + row_in_tile;
+      const bool row_ok = m < p.M;
+      const int64_t ncol0 = (int64_t)nb * BN + chalf * 128;
+      float sx = 0.f;
+      if (!kS32) {
+        if (row_ok) sx = __ldg(p.x_scale + m);
+        const int64_t n = (int64_t)nb * BN + et;
+        ws_smem[et] = n < p.N ? __ldg(p.w_scale + n) : 0.f;
+        if (p.residual && row_ok) {
+          const __half* rrow = p.residual + m * p.ld_r + ncol0;
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(rrow));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(rrow + 64));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(rrow + 127));
+        }
+        epi_bar_sync();
+      }
+      mbar_wait_sleep(&t_full[ab], (tl >> 1) & 1);
+      tc_fence_after();
+      const uint32_t taddr =
+          tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(ab * BN) + (uint32_t)(chalf * 128);
+      uint32_t ra[32], rb[32], rc[32];
+      QR_TMEM_LD32(taddr, ra);
+      QR_TMEM_LD32(taddr + 32u, rb);
+      QR_TMEM_LD32(taddr + 64u, rc);
+      tmem_ld_wait();
+      epi_chunk<kS32, 0, 0>(p, ra, m, row_ok, ncol0, sx, ws_smem + chalf * 128);
+      QR_TMEM_LD32(taddr + 96u, ra);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_leader + (uint32_t)ab * 8u);
+      epi_chunk<kS32, 0, 0>(p, rb, m, row_ok, ncol0 + 32, sx, ws_smem + chalf * 128 + 32);
+      epi_chunk<kS32, 0, 0>(p, rc, m, row_ok, ncol0 + 64, sx, ws_smem + chalf * 128 + 64);
+      epi_chunk<kS32, 0, 0>(p, ra, m, row_ok, ncol0 + 96, sx, ws_smem + chalf * 128 + 96);
+      if (!kS32) epi_bar_sync();
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == i8::MMA_WARP) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+  }
+}
+
 }  // namespace gemm
 
 namespace {
@@ -626,6 +806,76 @@ static cudaError_t launch_gemm_impl(const uint8_t* xq, const float* xs, int64_t 
     int4_gemm_kernel<kS32><<<2 * pairs, NUM_THREADS, SMEM_BYTES, stream>>>(ma, mb, p);
   }
   return cudaPeekAtLastError();
+}
+
+// A8W8: int8 rows [rows][K] (ld bytes), box 128 B x 128 rows, SWIZZLE_128B (one UMMA atom)
+static bool make_i8_map(CUtensorMap* map, const uint8_t* base, int64_t rows, int64_t K, int64_t ld) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld};
+  cuuint32_t box[2] = {128u, 128u};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <bool kS32>
+static cudaError_t launch_i8_impl(const int8_t* xq, const float* xs, int64_t M, int64_t K, int64_t ld_xq,
+                                  const int8_t* wq, const float* ws, int64_t N, int64_t ld_wq, void* out,
+                                  int64_t ld_out, cudaStream_t stream, const void* residual, int64_t ld_r) {
+  using namespace gemm;
+  static bool attr_set[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!attr_set[dev & 63]) {
+    cudaError_t e = cudaFuncSetAttribute(int8_gemm_kernel<kS32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)i8::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set[dev & 63] = true;
+  }
+  CUtensorMap ma, mb;
+  if (!make_i8_map(&ma, reinterpret_cast<const uint8_t*>(xq), M, K, ld_xq) ||
+      !make_i8_map(&mb, reinterpret_cast<const uint8_t*>(wq), N, K, ld_wq))
+    return cudaErrorInvalidValue;
+  Params p;
+  p.x_scale = xs;
+  p.w_scale = ws;
+  p.out = out;
+  p.residual = static_cast<const __half*>(residual);
+  p.ld_r = ld_r;
+  p.swiglu = 0;
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.ld_out = ld_out;
+  p.num_m = (int)((M + BM - 1) / BM);
+  p.num_n = (int)((N + BN - 1) / BN);
+  p.num_kb = (int)((K + BK - 1) / BK);
+  p.num_tiles = p.num_m * p.num_n;
+  {
+    const int64_t a_tile_bytes = (int64_t)BM * K;
+    int g = (int)((64ll << 20) / (a_tile_bytes > 0 ? a_tile_bytes : 1));
+    g = g < 8 ? 8 : (g > 32 ? 32 : g);
+    p.group_m = g > p.num_m ? p.num_m : g;
+  }
+  const int max_pairs = num_sms_current() / 2;
+  const int pairs = p.num_tiles < max_pairs ? p.num_tiles : max_pairs;
+  int8_gemm_kernel<kS32><<<2 * pairs, i8::NUM_THREADS, i8::SMEM_BYTES, stream>>>(ma, mb, p);
+  return cudaPeekAtLastError();
+}
+
+cudaError_t launch_int8_gemm(const int8_t* xq, const float* xs, int64_t M, int64_t K, int64_t ld_xq,
+                             const int8_t* wq, const float* ws, int64_t N, int64_t ld_wq, void* y, int64_t ld_y,
+                             cudaStream_t stream, const void* residual, int64_t ld_r) {
+  return launch_i8_impl<false>(xq, xs, M, K, ld_xq, wq, ws, N, ld_wq, y, ld_y, stream, residual, ld_r);
+}
+
+cudaError_t launch_int8_gemm_s32(const int8_t* xq, int64_t M, int64_t K, int64_t ld_xq, const int8_t* wq, int64_t N,
+                                 int64_t ld_wq, int32_t* acc, int64_t ld_acc, cudaStream_t stream) {
+  return launch_i8_impl<true>(xq, nullptr, M, K, ld_xq, wq, nullptr, N, ld_wq, acc, ld_acc, stream, nullptr, 0);
 }
 
 // Debug / roofline probe (not in the public header): mode 1 = MMA issue only.

@@ -213,6 +213,69 @@ quarot_status quarot_int4_matmul_s32(const uint8_t* xq, int64_t M, int64_t K, in
   return QUAROT_OK;
 }
 
+// ---- A8W8
+quarot_status quarot_hadamard_quant8(const void* x, int64_t M, int64_t K, int64_t ld_x, int32_t mode,
+                                     int32_t head_dim, float clip_ratio, int8_t* q, int64_t ld_q, float* scale,
+                                     void* stream) {
+  (void)head_dim;
+  g_last_launches = 0;
+  const bool rms = (mode & QUAROT_HAD_RMSNORM) != 0;
+  mode &= ~QUAROT_HAD_RMSNORM;
+  if (mode < QUAROT_HAD_NONE || mode > QUAROT_HAD_ACROSS_HEADS) return QUAROT_ERR_ARG;
+  if (mode != QUAROT_HAD_NONE) return QUAROT_ERR_UNSUPPORTED_SIZE;  // 8-bit FULL / ACROSS_HEADS: not built
+  if (!clip_ok(clip_ratio)) return QUAROT_ERR_ARG;
+  if (M < 0 || K <= 0 || ld_x < K || ld_q < K) return QUAROT_ERR_DIM;
+  if (M > 0x7fffffffLL) return QUAROT_ERR_DIM;
+  if (M == 0) return QUAROT_OK;
+  if (!x || !q || !scale) return QUAROT_ERR_NULL;
+  if (!aligned16(x) || !aligned16(q) || (ld_x % 8) || (ld_q % 8) || (K % 16)) return QUAROT_ERR_ALIGN;
+  if (K > 32768) return QUAROT_ERR_UNSUPPORTED_SIZE;
+  cudaError_t e = qr::launch_hq_none_q8(x, M, K, ld_x, clip_ratio, q, ld_q, scale, static_cast<cudaStream_t>(stream),
+                                        rms);
+  if (e != cudaSuccess) return cuda_fail(e);
+  g_last_launches = 1;
+  return QUAROT_OK;
+}
+
+static quarot_status check_gemm8(const int8_t* xq, int64_t M, int64_t K, int64_t ld_xq, const int8_t* wq, int64_t N,
+                                 int64_t ld_wq, const void* out, int64_t ld_out, int64_t out_elems_align) {
+  if (M < 0 || N <= 0 || K <= 0 || ld_xq < K || ld_wq < K || ld_out < N) return QUAROT_ERR_DIM;
+  if (M > 0x7fffffffLL || N > 0x7fffffffLL) return QUAROT_ERR_DIM;
+  if (M == 0) return QUAROT_OK;
+  if (!xq || !wq || !out) return QUAROT_ERR_NULL;
+  if (K % 128 || N % 8 || ld_xq % 16 || ld_wq % 16 || ld_out % out_elems_align) return QUAROT_ERR_ALIGN;
+  if (!aligned16(xq) || !aligned16(wq) || !aligned16(out)) return QUAROT_ERR_ALIGN;
+  if (K > 131072) return QUAROT_ERR_UNSUPPORTED_SIZE;  // 127 * 127 * K must fit int32
+  return QUAROT_OK;
+}
+
+quarot_status quarot_int8_linear(const int8_t* xq, const float* x_scale, int64_t M, int64_t K, int64_t ld_xq,
+                                 const int8_t* wq, const float* w_scale, int64_t N, int64_t ld_wq, void* y,
+                                 int64_t ld_y, void* stream) {
+  g_last_launches = 0;
+  quarot_status s = check_gemm8(xq, M, K, ld_xq, wq, N, ld_wq, y, ld_y, 8);
+  if (s != QUAROT_OK || M == 0) return s;
+  if (!x_scale || !w_scale) return QUAROT_ERR_NULL;
+  if (!aligned16(w_scale)) return QUAROT_ERR_ALIGN;
+  cudaError_t e = qr::launch_int8_gemm(xq, x_scale, M, K, ld_xq, wq, w_scale, N, ld_wq, y, ld_y,
+                                       static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e);
+  g_last_launches = 1;
+  return QUAROT_OK;
+}
+
+quarot_status quarot_int8_matmul_s32(const int8_t* xq, int64_t M, int64_t K, int64_t ld_xq, const int8_t* wq,
+                                     int64_t N, int64_t ld_wq, int32_t* acc, int64_t ld_acc, void* stream) {
+  g_last_launches = 0;
+  quarot_status s = check_gemm8(xq, M, K, ld_xq, wq, N, ld_wq, acc, ld_acc, 4);
+  if (s != QUAROT_OK || M == 0) return s;
+  cudaError_t e =
+      qr::launch_int8_gemm_s32(xq, M, K, ld_xq, wq, N, ld_wq, acc, ld_acc, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e);
+  g_last_launches = 1;
+  return QUAROT_OK;
+}
+
 quarot_status quarot_kv_quant(const void* k, int64_t ld_k, const void* v, int64_t ld_v, int64_t T, int32_t n_kv,
                               int32_t head_dim, void* q, int64_t ld_q, int32_t n_q, uint32_t flags, float clip_ratio,
                               uint8_t* k_codes, float* k_scale, uint8_t* k_zero, uint8_t* v_codes, float* v_scale,

@@ -33,6 +33,15 @@ cudaError_t launch_kv_quant_rope(const void* k, int64_t ld_k, const void* v, int
                                  int64_t pos0, int seq_len, float theta, uint8_t* k_codes, float* k_scale,
                                  uint8_t* k_zero, uint8_t* v_codes, float* v_scale, uint8_t* v_zero,
                                  cudaStream_t stream, const int32_t* positions = nullptr, int64_t s_max = 0);
+// A8W8: int8 per-token quantizer (mode NONE, optional RMSNorm) and the
+// int8 x int8 GEMM with the same epilogues
+cudaError_t launch_hq_none_q8(const void* x, int64_t M, int64_t K, int64_t ld_x, float clip, int8_t* q, int64_t ld_q,
+                              float* scale, cudaStream_t stream, bool rmsnorm);
+cudaError_t launch_int8_gemm(const int8_t* xq, const float* xs, int64_t M, int64_t K, int64_t ld_xq,
+                             const int8_t* wq, const float* ws, int64_t N, int64_t ld_wq, void* y, int64_t ld_y,
+                             cudaStream_t stream, const void* residual = nullptr, int64_t ld_r = 0);
+cudaError_t launch_int8_gemm_s32(const int8_t* xq, int64_t M, int64_t K, int64_t ld_xq, const int8_t* wq, int64_t N,
+                                 int64_t ld_wq, int32_t* acc, int64_t ld_acc, cudaStream_t stream);
 // KV Decode: split-sequence flash decoding over the INT4 cache + the combine pass.
 size_t kv_decode_workspace_bytes(int B, int n_q, int head_dim, int s_max);
 cudaError_t launch_kv_decode(const void* q, const uint8_t* k_codes, const float* k_scale, const uint8_t* k_zero,

@@ -41,6 +41,9 @@ _SIGS = {
     "quarot_kv_decode": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_i64, _c_i32, _c_i32, _c_i32, _c_i64, _c_f32,
                          _vp, _vp, _c_i64, _vp],
     "quarot_kv_decode_workspace_bytes": [_c_i64, _c_i32, _c_i32, _c_i64],
+    "quarot_hadamard_quant8": [_vp, _c_i64, _c_i64, _c_i64, _c_i32, _c_i32, _c_f32, _vp, _c_i64, _vp, _vp],
+    "quarot_int8_linear": [_vp, _vp, _c_i64, _c_i64, _c_i64, _vp, _vp, _c_i64, _c_i64, _vp, _c_i64, _vp],
+    "quarot_int8_matmul_s32": [_vp, _c_i64, _c_i64, _c_i64, _vp, _c_i64, _c_i64, _vp, _c_i64, _vp],
     "quarot_status_string": [_c_i32],
     "quarot_abi_version": [],
     "quarot_base_hadamard": [_c_i32, _vp],
@@ -254,6 +257,43 @@ def kv_quant(k: torch.Tensor, v: torch.Tensor, q: torch.Tensor | None = None, fl
         pos0, seq_len, theta = rope
         _check("quarot_kv_quant_rope", lib().quarot_kv_quant_rope(*head, int(pos0), int(seq_len), float(theta), *outs))
     return out
+
+
+def hadamard_quant8(x: torch.Tensor, clip_ratio: float = 0.9, rmsnorm: bool = False, q: torch.Tensor | None = None,
+                    scale: torch.Tensor | None = None, stream=None):
+    """quarot_hadamard_quant8 (A8W8, §8 f4; mode NONE): int8 codes [M, K] and fp32 scales [M]."""
+    M, K = x.shape
+    if x.stride(1) != 1:
+        raise ValueError("x rows must be contiguous")
+    q = torch.empty(M, K, dtype=torch.int8, device=x.device) if q is None else q
+    scale = torch.empty(M, dtype=torch.float32, device=x.device) if scale is None else scale
+    st = lib().quarot_hadamard_quant8(_dev(x, "x", torch.float16), M, K, x.stride(0), NONE | (RMSNORM if rmsnorm else 0),
+                                      128, clip_ratio, q.data_ptr(), q.stride(0), scale.data_ptr(), _stream(stream))
+    _check("quarot_hadamard_quant8", st)
+    return q, scale
+
+
+def int8_linear(xq: torch.Tensor, x_scale: torch.Tensor, wq: torch.Tensor, w_scale: torch.Tensor,
+                y: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """quarot_int8_linear (A8W8, §8 f4): int8 [M, K] x int8 [N, K] -> fp16 [M, N]."""
+    M, K = xq.shape
+    N = wq.shape[0]
+    y = torch.empty(M, N, dtype=torch.float16, device=xq.device) if y is None else y
+    st = lib().quarot_int8_linear(_dev(xq, "xq", torch.int8), _dev(x_scale, "x_scale", torch.float32), M, K,
+                                  xq.stride(0), _dev(wq, "wq", torch.int8), _dev(w_scale, "w_scale", torch.float32), N,
+                                  wq.stride(0), y.data_ptr(), y.stride(0), _stream(stream))
+    _check("quarot_int8_linear", st)
+    return y
+
+
+def int8_matmul_s32(xq: torch.Tensor, wq: torch.Tensor, stream=None) -> torch.Tensor:
+    M, K = xq.shape
+    N = wq.shape[0]
+    acc = torch.empty(M, N, dtype=torch.int32, device=xq.device)
+    st = lib().quarot_int8_matmul_s32(_dev(xq, "xq", torch.int8), M, K, xq.stride(0), _dev(wq, "wq", torch.int8), N,
+                                      wq.stride(0), acc.data_ptr(), acc.stride(0), _stream(stream))
+    _check("quarot_int8_matmul_s32", st)
+    return acc
 
 
 def kv_cache_empty(B: int, s_max: int, n_kv: int, head_dim: int = 128, device="cuda") -> dict:

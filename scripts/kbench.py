@@ -140,6 +140,22 @@ def main():
                             "frac_hbm": byts / ms_dec / 1e6 / 6536}
                 print(key, json.dumps(res[key]), flush=True)
                 del cache
+    if "gemm8" in a.what:
+        # A8W8: the native kind::i8 path, same shapes as the W4A4 bench; the
+        # difference to "gemm" is the cost of unpacking INT4 on B200
+        xq_big = torch.randint(-127, 128, (M, 28672), dtype=torch.int8, device=dev)
+        for name, N, K in (("qkv", 10240, 8192), ("o", 8192, 8192), ("gate_up", 57344, 8192), ("down", 8192, 28672)):
+            xq = xq_big[:, :K]
+            wq = torch.randint(-127, 128, (N, K), dtype=torch.int8, device=dev)
+            xs = torch.rand(M, device=dev) + 0.5
+            ws = synth.weight_scales(N, 3, dev)
+            y = torch.empty(M, N, dtype=torch.float16, device=dev)
+            ms = timeit(lambda: q.int8_linear(xq, xs, wq, ws, y=y), a.iters)
+            tops = 2 * M * N * K / ms / 1e9
+            res[f"gemm8_{name}"] = {"ms": ms, "tops": tops, "frac_int8_2x_bf16_sustained": tops / 2765.6}
+            print("a8w8", name, json.dumps(res[f"gemm8_{name}"]), flush=True)
+            del wq, y
+        del xq_big
     if "intmm" in a.what:
         # library INT8 reference: cuBLASLt via torch._int_mm, 8192^3 (denominator context)
         A = torch.randint(-7, 8, (8192, 8192), dtype=torch.int8, device=dev)

@@ -222,3 +222,27 @@ def test_quarot_linear_close_to_fp():
     y = layer.quarot_linear(x, cw, sw, "full").astype(np.float64)
     ref = x.astype(np.float64) @ w.T
     assert np.linalg.norm(y - ref) / np.linalg.norm(ref) < 0.25
+
+
+# ---- 8-bit (A8W8): the same RTN definition with qmax = 127 (P:6, tab:rtn_results)
+def test_sym8_brute_force_and_ties():
+    rng = np.random.default_rng(5)
+    for _ in range(30):
+        y = rng.standard_normal((1, 11)) * rng.uniform(0.1, 10)
+        codes, scale = quant.quantize_sym_rows(y, 0.9, qmax=127)
+        s = float(scale[0])
+        assert np.isclose(s, 0.9 * np.max(np.abs(y)) / 127, rtol=1e-6)
+        for v, c in zip(y[0], codes[0]):
+            assert c == _brute_code(v, s, qmax=127)
+    # clip 1, amax 127 -> s = 1: exact ties round half to even, the top clamps at 127
+    codes, scale = quant.quantize_sym_rows(np.array([[127.0, 2.5, -0.5, 126.5, -3.5]]), 1.0, qmax=127)
+    assert scale[0] == 1.0 and codes[0].tolist() == [127, 2, 0, 126, -4]
+
+
+def test_int8_matmul_exactness_bound():
+    # 127 * 127 * K < 2^31 up to K = 131072 (the A8W8 ABI limit), and the fp64 path stays exact
+    assert 127 * 127 * 131072 < 2 ** 31
+    rng = np.random.default_rng(6)
+    a = rng.integers(-127, 128, (5, 3000))
+    b = rng.integers(-127, 128, (4, 3000))
+    assert np.array_equal(gemm.int_matmul_exact_f64(a, b), a @ b.T)
