@@ -206,7 +206,10 @@ __global__ void __launch_bounds__(128) hq_heads_kernel(const __half* __restrict_
 // bulk-copied into a double-buffered smem slot two rows ahead, so loads are asynchronous
 // and overlap the butterflies / quantization of the current row.
 template <int HPT, int G>
-__global__ void __launch_bounds__(128, 4) hq_heads_persist_kernel(const __half* __restrict__ x, int64_t M, int64_t K,
+#ifndef QR_HEADS_HPT
+#define QR_HEADS_HPT 32
+#endif
+__global__ void __launch_bounds__(QR_HEADS_HPT == 32 ? 128 : 256, QR_HEADS_HPT == 32 ? 4 : 2) hq_heads_persist_kernel(const __half* __restrict__ x, int64_t M, int64_t K,
                                                                int64_t ld_x, int head_dim, float clip,
                                                                uint8_t* __restrict__ q, int64_t ld_q,
                                                                float* __restrict__ scale) {
@@ -765,23 +768,30 @@ cudaError_t launch_hq_heads(const void* x, int64_t M, int64_t K, int64_t ld_x, i
   const int P2 = head_dim / 2;
   const __half* xh = static_cast<const __half*>(x);
   // G groups of heads per column pair; HPT = n_h / G heads per thread (<= 32 in registers)
-  const int G = n_h > 32 ? n_h / 32 : 1;
+#ifndef QR_HEADS_HPT
+#define QR_HEADS_HPT 32
+#endif
+  const int G = n_h > QR_HEADS_HPT ? n_h / QR_HEADS_HPT : 1;
   if (G > 16) return cudaErrorInvalidValue;
   const int HPT = n_h / G;
   int threads = P2 * G;
   threads = ((threads + 31) / 32) * 32;
-  if (threads > 128) return cudaErrorInvalidValue;
+  if (threads > 256) return cudaErrorInvalidValue;
   const size_t smem = (size_t)(2 * 2 * K) + (size_t)(K / 2) + 64;
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t want = (int64_t)nsm * 6;
-  const dim3 grid((unsigned)(M < want ? M : want));
+  // persistent CTAs with a fixed row interleave: launch exactly as many as are resident, or
+  // the CTAs of a second partial wave would start late and run at reduced occupancy
 #define QR_HEADS(H, GG)                                                                                         \
   do {                                                                                                          \
     cudaError_t ee = cudaFuncSetAttribute(hq::hq_heads_persist_kernel<H, GG>,                                   \
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);              \
     if (ee != cudaSuccess) return ee;                                                                           \
+    int per_sm = 1;                                                                                             \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hq::hq_heads_persist_kernel<H, GG>, threads, smem);  \
+    const int64_t want = (int64_t)nsm * (per_sm > 0 ? per_sm : 1);                                             \
+    const dim3 grid((unsigned)(M < want ? M : want));                                                           \
     hq::hq_heads_persist_kernel<H, GG><<<grid, threads, smem, stream>>>(xh, M, K, ld_x, head_dim, clip, q, ld_q, \
                                                                         scale);                                 \
   } while (0)
@@ -796,10 +806,10 @@ cudaError_t launch_hq_heads(const void* x, int64_t M, int64_t K, int64_t ld_x, i
         default: QR_HEADS(32, 1); break;
       }
       break;
-    case 2: QR_HEADS(32, 2); break;
-    case 4: QR_HEADS(32, 4); break;
-    case 8: QR_HEADS(32, 8); break;
-    default: QR_HEADS(32, 16); break;
+    case 2: QR_HEADS(QR_HEADS_HPT, 2); break;
+    case 4: QR_HEADS(QR_HEADS_HPT, 4); break;
+    case 8: QR_HEADS(QR_HEADS_HPT, 8); break;
+    default: QR_HEADS(QR_HEADS_HPT, 16); break;
   }
 #undef QR_HEADS
   return cudaPeekAtLastError();
