@@ -826,6 +826,8 @@ cudaError_t launch_hq_full(const void* x, int64_t M, int64_t K, int64_t ld_x, in
     e = cudaFuncSetAttribute(hq::hq_full_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     hq::hq_full_kernel<1><<<grid, threads, smem, stream>>>(xh, ld_x, pow2, clip, q, ld_q, scale, nullptr);
+  } else if (m == 28 && pow2 == 1024 && g_hq_full_variant == 0) {
+    return launch_hq_full28_tc(x, M, ld_x, clip, q, ld_q, scale, stream);
   } else if (m == 28 && pow2 == 1024) {
     static bool attr[64] = {};
     int dev = 0;

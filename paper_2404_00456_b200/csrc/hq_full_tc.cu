@@ -1,0 +1,461 @@
+// hq_full_tc.cu — rows a1 + a3 for K = 1024 x 28 (the Llama-2-70B down_proj input, P:182-185,
+// P:67) with the first Kronecker factors on the tcgen05 tensor path.
+//
+// y = (H_1024 (x) H_28) x per token row (Sylvester H_1024, element i = a*28 + b, reading Z2).
+// Split a = a_hi*4 + a_lo (a_hi < 256, a_lo < 4): Sylvester gives H_1024 = H_256 (x) H_4, so
+//
+//     y[a'_hi*112 + j'] = sum_{a_hi} H_256[a'_hi][a_hi] * D[j'][a_hi],
+//     D[j'][a_hi]      = sum_j (H_4 (x) H_28)[j'][j] * x[a_hi*112 + j],   j = a_lo*28 + b.
+//
+//  * D is ONE dense fp16 contraction per row: tcgen05.mma kind::f16, M = 128 (j', 112 real rows
+//    of the constant A = H_4 (x) H_28, zero-padded), N = 256 (a_hi), K = 112 (7 MMAs of K = 16).
+//    +-1 x fp16 products are exact; the accumulation is fp32 (the paper's FP32 Hadamard).
+//    The row is TMA'd straight into the K-major SWIZZLE_128B operand layout by a 3-D tensor map
+//    [row][a_hi][j] (two 64-wide j boxes; j >= 112 is zero-filled), 3-stage ring.
+//  * D lands in TMEM (fp32, lane = j', column = a_hi), double-buffered (2 x 256 columns), so the
+//    MMA of row r+1 overlaps the epilogue of row r.
+//  * H_256 over the columns runs in registers with packed fp32x2 butterflies (FADD2): 8 epilogue
+//    warps (setmaxnreg: 224 registers each), two per TMEM lane quarter (h = 0, 1).  Pass 1: each
+//    thread loads the 128 columns with a_hi bit 5 = h and transforms bits 0-4 and 6 (pairs packed along bit 7), then stores
+//    them back to TMEM; pass 2 (after the partner warp's pass 1): the 128 columns with bit 6 = h,
+//    bits 5 and 7 (pairs packed along bit 0).  Every bit is transformed exactly once, no shuffles.
+//  * Row amax over the 8 warps (named barrier), scale (1/sqrt(K) folded in, reading Z5), RNE
+//    INT4 codes with the magic add; the two nibbles of a byte are adjacent j' = adjacent TMEM
+//    lanes, merged with one shuffle per code word.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+#include "quarot_internal.h"
+
+namespace qr {
+namespace hqtc {
+
+constexpr int MB = 28, P = 1024, K = MB * P;
+constexpr int J = 4 * MB;                    // 112: contraction (a_lo, b) per a_hi
+constexpr int NA = P / 4;                    // 256 a_hi columns
+constexpr int A_BYTES = 128 * 128 * 2;       // (H_4 (x) H_28) padded to 128 x 128 fp16, SW128 K-major
+constexpr int BOX_BYTES = NA * 128;          // 256 a_hi rows x 64 j (128 B)
+constexpr int STAGE_BYTES = 2 * BOX_BYTES;   // 64 KB per token row
+constexpr int STAGES = 3;
+constexpr int TMA_WARP = 0, MMA_WARP = 1, EPI_WARP0 = 4, NUM_EPI = 8;  // warps 2-3 idle (warpgroup 0)
+constexpr int NUM_THREADS = (EPI_WARP0 + NUM_EPI) * 32;
+constexpr uint32_t TMEM_COLS = 512;
+constexpr size_t SMEM = 1024 + A_BYTES + (size_t)STAGES * STAGE_BYTES + 256;  // + barriers
+static_assert(SMEM <= 232448, "227 KB dynamic smem");
+// kind::f16: D f32 (bits 4-5 = 1), A = B = f16 (0), both K-major, N/8 at 17, M/16 at 24
+constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(NA >> 3) << 17) | ((128u >> 4) << 24);
+
+QR_DEVICE void mma_f16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(acc));
+}
+QR_DEVICE void tma_load_3d(uint32_t dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+QR_DEVICE void expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+QR_DEVICE void bar_named(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+#define QR_TMEM_ST32(taddr, r)                                                                          \
+  asm volatile(                                                                                         \
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16," \
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),                   \
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),  \
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),      \
+      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),     \
+      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]))
+QR_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+QR_DEVICE void bfly(float2& u, float2& v) {
+  const float2 s = f2add(u, v), d = f2sub(u, v);
+  u = s;
+  v = d;
+}
+
+// 4 codes (low nibble of each byte; the byte is the two's-complement code) of a.x, a.y, b.x, b.y:
+// RNE by the 1.5 * 2^23 magic add (|v * inv| <= 7 / 0.9 < 2^22), whose low 16 bits are the
+// integer; clamp to [-7, 7] on two 16-bit lanes at a time (VIMNMX), then gather the low bytes.
+QR_DEVICE uint32_t code_word(float2 a, float2 b, float inv) {
+  const float2 i2 = make_float2(inv, inv), mg = make_float2(12582912.f, 12582912.f);
+  const float2 ma = f2add(f2mul(a, i2), mg), mb = f2add(f2mul(b, i2), mg);
+  uint32_t lo = __byte_perm(__float_as_uint(ma.x), __float_as_uint(ma.y), 0x5410);
+  uint32_t hi = __byte_perm(__float_as_uint(mb.x), __float_as_uint(mb.y), 0x5410);
+  lo = __vmaxs2(__vmins2(lo, 0x00070007u), 0xFFF9FFF9u);
+  hi = __vmaxs2(__vmins2(hi, 0x00070007u), 0xFFF9FFF9u);
+  return __byte_perm(lo, hi, 0x6420);
+}
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    hq_full28_tc_kernel(const __grid_constant__ CUtensorMap tmX, int64_t M, float clip, uint8_t* __restrict__ q,
+                        int64_t ld_q, float* __restrict__ scale, const uint4* __restrict__ a_img) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * STAGE_BYTES);  // [STAGES] TMA landed
+  uint64_t* empty = full + STAGES;                                           // [STAGES] MMA done reading
+  uint64_t* t_full = empty + STAGES;                                         // [2] D ready
+  uint64_t* t_empty = t_full + 2;                                            // [2] epilogue done reading D
+  uint64_t* pair_done = t_empty + 2;                                         // [4 quarters][2] pass 1 done
+  uint64_t* amax_done = pair_done + 8;                                       // [2] row partial amax posted
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(amax_done + 2);
+  __shared__ float red[2][NUM_EPI];                                          // per-warp partial amax
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  for (int i = threadIdx.x; i < A_BYTES / 16; i += NUM_THREADS) reinterpret_cast<uint4*>(sA)[i] = __ldg(a_img + i);
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&t_full[b], 1);
+      mbar_init(&t_empty[b], NUM_EPI);
+      mbar_init(&amax_done[b], NUM_EPI);
+    }
+    for (int i = 0; i < 8; ++i) mbar_init(&pair_done[i], 2);
+    fence_barrier_init();
+  }
+  if (warp == MMA_WARP) {
+    tmem_alloc(tmem_holder, TMEM_COLS);
+    tmem_relinquish();
+  }
+  if (warp == TMA_WARP && lane == 0)
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  const int64_t nrows = M > (int64_t)blockIdx.x ? (M - 1 - (int64_t)blockIdx.x) / gridDim.x + 1 : 0;
+
+  if (warp < EPI_WARP0) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+    if (warp == TMA_WARP) {
+      if (lane == 0) {
+        for (int64_t it = 0; it < nrows; ++it) {
+          const int s = (int)(it % STAGES);
+          mbar_wait_sleep(&empty[s], (uint32_t)((it / STAGES) & 1) ^ 1u);
+          expect_tx(&full[s], STAGE_BYTES);
+          const int row = (int)((int64_t)blockIdx.x + it * gridDim.x);
+          const uint32_t dst = smem_u32(sB + s * STAGE_BYTES);
+          tma_load_3d(dst, &tmX, 0, 0, row, &full[s]);
+          tma_load_3d(dst + BOX_BYTES, &tmX, 64, 0, row, &full[s]);
+        }
+      }
+    } else if (warp == MMA_WARP) {
+      if (lane == 0) {
+        const uint64_t a_desc = umma_desc_sw128(smem_u32(sA));
+        for (int64_t it = 0; it < nrows; ++it) {
+          const int s = (int)(it % STAGES), buf = (int)(it & 1);
+          mbar_wait_sleep(&t_empty[buf], (uint32_t)((it >> 1) & 1) ^ 1u);
+          mbar_wait_sleep(&full[s], (uint32_t)((it / STAGES) & 1));
+          tc_fence_after();
+          const uint64_t b_desc = umma_desc_sw128(smem_u32(sB + s * STAGE_BYTES));
+          const uint32_t d_tmem = tmem_base + (uint32_t)(buf * NA);
+#pragma unroll
+          for (int kk = 0; kk < J / 16; ++kk) {  // atom kk/4 (A: +16 KB, B: +32 KB), +32 B per K = 16
+            const uint64_t koff = (uint64_t)(2 * (kk & 3));
+            mma_f16(d_tmem, a_desc + (uint64_t)((kk >> 2) * (16384 >> 4)) + koff,
+                    b_desc + (uint64_t)((kk >> 2) * (BOX_BYTES >> 4)) + koff, IDESC, kk > 0 ? 1u : 0u);
+          }
+          mma_commit(&empty[s]);
+          mma_commit(&t_full[buf]);
+        }
+      }
+      __syncwarp();
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
+    // Software pipeline over rows (split-phase barriers, so no warp idles at a barrier):
+    //   pass1(r + 1) | quant(r) [after every warp posted its amax of row r] | pass2(r + 1)
+    // The pass-2 values of a row are parked in its TMEM buffer between pass 2 and quant.
+    const int e = warp - EPI_WARP0;  // 0..7
+    const int qd = warp & 3;         // TMEM lane quarter this warp may access
+    const int h = e >> 2;            // column half-set
+    const int L = qd * 32 + lane;    // TMEM lane = output j'
+    const bool lane_ok = L < J;
+    const bool odd = (lane & 1) != 0;
+    const uint32_t t_lane = tmem_base + ((uint32_t)(qd * 32) << 16);
+    const float norm_f = (float)rsqrt((double)K);
+    const float c0 = (float)((double)clip * rsqrt((double)K) / 7.0);  // scale = c0 * amax (unnormalized)
+    // merged byte of j' = 2p (low nibble, even lane) and 2p + 1 (high nibble, odd lane)
+    const uint32_t sh_keep = odd ? 4u : 0u, sh_recv = odd ? 0u : 4u;
+    const uint32_t keep_mask = odd ? 0xF0F0F0F0u : 0x0F0F0F0Fu;
+    // even lanes write the a_hi bit 7 = 0 half of the pair's bytes, odd lanes the other half
+    uint8_t* const qlane = q + (L >> 1) + (int64_t)(64 * h + 128 * (odd ? 1 : 0)) * (J / 2);
+
+    // pass 1: columns 64 i + 32 h + c; a_hi bits 0-4 = c, 5 = h, 6-7 = i; transforms bits 1-4, 6, 7
+    auto pass1 = [&](int64_t it) {
+      const int buf = (int)(it & 1);
+      mbar_wait_sleep(&t_full[buf], (uint32_t)((it >> 1) & 1));
+      tc_fence_after();
+      const uint32_t tb = t_lane + (uint32_t)(buf * NA);
+      uint32_t r[4][32];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) QR_TMEM_LD32(tb + 64u * i + 32u * h, r[i]);
+      tmem_ld_wait();
+      float2 P[4][16];  // P[i][c'] = columns (2c', 2c' + 1): adjacent registers of the load
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int c = 0; c < 16; ++c) P[i][c] = make_float2(__uint_as_float(r[i][2 * c]), __uint_as_float(r[i][2 * c + 1]));
+#pragma unroll
+      for (int st = 1; st < 16; st <<= 1)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int c = 0; c < 16; ++c)
+            if (!(c & st)) bfly(P[i][c], P[i][c + st]);
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        bfly(P[0][c], P[1][c]);  // bit 6
+        bfly(P[2][c], P[3][c]);
+        bfly(P[0][c], P[2][c]);  // bit 7
+        bfly(P[1][c], P[3][c]);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          r[i][2 * c] = __float_as_uint(P[i][c].x);
+          r[i][2 * c + 1] = __float_as_uint(P[i][c].y);
+        }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) QR_TMEM_ST32(tb + 64u * i + 32u * h, r[i]);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pair_done[qd * 2 + buf]);
+    };
+    // pass 2: columns 128 k7 + 64 h + 32 k5 + c; a_hi bits 0-4 = c, 5 = k5, 6 = h, 7 = k7;
+    // transforms bits 5 and 0 (within the register pair), posts the partial amax, parks the values
+    auto pass2 = [&](int64_t it) {
+      const int buf = (int)(it & 1);
+      mbar_wait_sleep(&pair_done[qd * 2 + buf], (uint32_t)((it >> 1) & 1));  // partner's pass 1
+      tc_fence_after();
+      const uint32_t tb = t_lane + (uint32_t)(buf * NA);
+      uint32_t u[2][2][32];
+#pragma unroll
+      for (int k7 = 0; k7 < 2; ++k7)
+#pragma unroll
+        for (int k5 = 0; k5 < 2; ++k5) QR_TMEM_LD32(tb + 128u * k7 + 64u * h + 32u * k5, u[k7][k5]);
+      tmem_ld_wait();
+      float am[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int k7 = 0; k7 < 2; ++k7)
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          float2 v0 = make_float2(__uint_as_float(u[k7][0][2 * c]), __uint_as_float(u[k7][0][2 * c + 1]));
+          float2 v1 = make_float2(__uint_as_float(u[k7][1][2 * c]), __uint_as_float(u[k7][1][2 * c + 1]));
+          bfly(v0, v1);  // bit 5
+          v0 = make_float2(v0.x + v0.y, v0.x - v0.y);  // bit 0
+          v1 = make_float2(v1.x + v1.y, v1.x - v1.y);
+          am[c & 1] = fmax_nan(am[c & 1], fmax_nan(fabsf(v0.x), fabsf(v0.y)));
+          am[2 + (c & 1)] = fmax_nan(am[2 + (c & 1)], fmax_nan(fabsf(v1.x), fabsf(v1.y)));
+          u[k7][0][2 * c] = __float_as_uint(v0.x);
+          u[k7][0][2 * c + 1] = __float_as_uint(v0.y);
+          u[k7][1][2 * c] = __float_as_uint(v1.x);
+          u[k7][1][2 * c + 1] = __float_as_uint(v1.y);
+        }
+#pragma unroll
+      for (int k7 = 0; k7 < 2; ++k7)
+#pragma unroll
+        for (int k5 = 0; k5 < 2; ++k5) QR_TMEM_ST32(tb + 128u * k7 + 64u * h + 32u * k5, u[k7][k5]);
+      float amax = lane_ok ? fmax_nan(fmax_nan(am[0], am[1]), fmax_nan(am[2], am[3])) : 0.f;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) amax = fmax_nan(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      if (lane == 0) red[buf][e] = amax;
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&amax_done[buf]);
+    };
+    // quant: row scale from the 8 partial amax values, reload the parked values, release the TMEM
+    // buffer, RNE codes, merge the nibble pairs across adjacent lanes, store
+    auto quant = [&](int64_t it) {
+      const int buf = (int)(it & 1);
+      const int64_t row = (int64_t)blockIdx.x + it * gridDim.x;
+      mbar_wait_sleep(&amax_done[buf], (uint32_t)((it >> 1) & 1));
+      tc_fence_after();
+      const uint32_t tb = t_lane + (uint32_t)(buf * NA);
+      uint32_t u[2][2][32];
+#pragma unroll
+      for (int k7 = 0; k7 < 2; ++k7)
+#pragma unroll
+        for (int k5 = 0; k5 < 2; ++k5) QR_TMEM_LD32(tb + 128u * k7 + 64u * h + 32u * k5, u[k7][k5]);
+      float amax = red[buf][0];
+#pragma unroll
+      for (int w = 1; w < NUM_EPI; ++w) amax = fmax_nan(amax, red[buf][w]);
+      // scale = fp32(clip * amax / (7 sqrt(K))) (readings Z5, Z9); zero row -> 1, non-finite -> NaN
+      float sc = 1.f, inv = 0.f;
+      if (!isfinite(amax)) {
+        sc = __int_as_float(0x7fc00000);
+      } else if (amax != 0.f) {
+        sc = c0 * amax;
+        inv = __fdiv_rn(norm_f, sc);
+      }
+      if (e == 0 && lane == 0) scale[row] = sc;
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&t_empty[buf]);  // D[buf] may be overwritten by row it + 2
+      if (inv == 0.f) {  // zero or non-finite row: all codes 0
+#pragma unroll
+        for (int k7 = 0; k7 < 2; ++k7)
+#pragma unroll
+          for (int k5 = 0; k5 < 2; ++k5)
+#pragma unroll
+            for (int c = 0; c < 32; ++c) u[k7][k5][c] = 0u;
+      }
+      uint32_t out[2][8];
+#pragma unroll
+      for (int k5 = 0; k5 < 2; ++k5)
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {  // codes of a_hi = 4m..4m+3 (+32 k5 + 64 h + 128 k7)
+          auto f2 = [&](int k7, int c) {
+            return make_float2(__uint_as_float(u[k7][k5][2 * c]), __uint_as_float(u[k7][k5][2 * c + 1]));
+          };
+          const uint32_t w0 = code_word(f2(0, 2 * m), f2(0, 2 * m + 1), inv);
+          const uint32_t w1 = code_word(f2(1, 2 * m), f2(1, 2 * m + 1), inv);
+          const uint32_t got = __shfl_xor_sync(0xffffffffu, odd ? w0 : w1, 1);
+          const uint32_t keep = odd ? w1 : w0;
+          out[k5][m] = ((keep << sh_keep) & keep_mask) | ((got << sh_recv) & ~keep_mask);
+        }
+      if (lane_ok) {
+        uint8_t* const qr = qlane + row * ld_q;
+#pragma unroll
+        for (int k5 = 0; k5 < 2; ++k5)
+#pragma unroll
+          for (int m = 0; m < 8; ++m) {
+            uint8_t* dst = qr + (int64_t)(4 * m + 32 * k5) * (J / 2);
+            const uint32_t o = out[k5][m];
+            dst[0] = (uint8_t)o;
+            dst[J / 2] = (uint8_t)(o >> 8);
+            dst[J] = (uint8_t)(o >> 16);
+            dst[3 * J / 2] = (uint8_t)(o >> 24);
+          }
+      }
+    };
+    if (nrows > 0) {
+      pass1(0);
+      pass2(0);
+    }
+    for (int64_t it = 0; it < nrows; ++it) {
+      if (it + 1 < nrows) pass1(it + 1);
+      quant(it);
+      if (it + 1 < nrows) pass2(it + 1);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == MMA_WARP) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+}  // namespace hqtc
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn_hq() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult res;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &res) == cudaSuccess &&
+        res == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// (H_4 (x) H_28)[j'][j] (j' = a'_lo*28 + b' rows, j = a_lo*28 + b columns; row i of H_28
+// dotted with x, reading Z4), zero-padded to 128 x 128 fp16 and laid out as the UMMA K-major
+// SWIZZLE_128B image: atom column k/64 at 16 KB, 8-row groups at 1024 B, 128 B rows, 16-byte
+// chunk c of row r at chunk c ^ (r & 7).
+std::vector<uint16_t> a_image_28(const int8_t* h28) {
+  std::vector<uint16_t> img(128 * 128, 0);
+  for (int m = 0; m < 128; ++m)
+    for (int k = 0; k < 128; ++k) {
+      int v = 0;
+      if (m < hqtc::J && k < hqtc::J) {
+        const int alo_o = m / 28, bo = m % 28, alo_i = k / 28, bi = k % 28;
+        const int sgn = (__builtin_popcount(alo_o & alo_i) & 1) ? -1 : 1;
+        v = sgn * h28[bo * 28 + bi];
+      }
+      const int kc = k / 64, kk = k % 64, chunk = kk / 8, within = kk % 8;
+      const size_t off = (size_t)kc * 16384 + (size_t)(m / 8) * 1024 + (size_t)(m % 8) * 128 +
+                         (size_t)((chunk ^ (m % 8)) * 16) + (size_t)within * 2;
+      img[off / 2] = v > 0 ? 0x3C00 : (v < 0 ? 0xBC00 : 0);
+    }
+  return img;
+}
+
+std::mutex g_img_mu;
+void* g_img[64];
+
+}  // namespace
+
+int g_hq_full_variant = 0;  // debug: 1 = the mma.sync kernel (hq_full28_kernel)
+
+cudaError_t launch_hq_full28_tc(const void* x, int64_t M, int64_t ld_x, float clip, uint8_t* q, int64_t ld_q,
+                                float* scale, cudaStream_t stream) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  void* img = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_img_mu);
+    if (!g_img[dev & 63]) {
+      const int8_t* h28 = base_hadamard_host(28);
+      if (!h28) return cudaErrorInvalidValue;
+      auto host = a_image_28(h28);
+      void* d = nullptr;
+      e = cudaMalloc(&d, host.size() * sizeof(uint16_t));
+      if (e != cudaSuccess) return e;
+      e = cudaMemcpy(d, host.data(), host.size() * sizeof(uint16_t), cudaMemcpyHostToDevice);
+      if (e != cudaSuccess) return e;
+      e = cudaFuncSetAttribute(hqtc::hq_full28_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)hqtc::SMEM);
+      if (e != cudaSuccess) return e;
+      g_img[dev & 63] = d;
+    }
+    img = g_img[dev & 63];
+  }
+  auto fn = encode_fn_hq();
+  if (!fn) return cudaErrorInvalidValue;
+  CUtensorMap map;
+  cuuint64_t dims[3] = {(cuuint64_t)hqtc::J, (cuuint64_t)hqtc::NA, (cuuint64_t)M};
+  cuuint64_t strides[2] = {(cuuint64_t)hqtc::J * 2, (cuuint64_t)ld_x * 2};
+  cuuint32_t box[3] = {64u, (cuuint32_t)hqtc::NA, 1u};
+  cuuint32_t estr[3] = {1u, 1u, 1u};
+  CUresult r = fn(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(x), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)(M < nsm ? M : nsm);
+  hqtc::hq_full28_tc_kernel<<<grid, hqtc::NUM_THREADS, hqtc::SMEM, stream>>>(
+      map, M, clip, q, ld_q, scale, static_cast<const uint4*>(img));
+  return cudaPeekAtLastError();
+}
+
+}  // namespace qr
+
+extern "C" void quarot_debug_hq_full_variant(int v) { qr::g_hq_full_variant = v; }

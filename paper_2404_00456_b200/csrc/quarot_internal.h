@@ -21,6 +21,10 @@ cudaError_t launch_hq_none(const void* x, int64_t M, int64_t K, int64_t ld_x, fl
                            int64_t ld_q, float* scale, cudaStream_t stream, bool rmsnorm = false);
 cudaError_t launch_hq_heads(const void* x, int64_t M, int64_t K, int64_t ld_x, int head_dim, float clip,
                             uint8_t* q, int64_t ld_q, float* scale, cudaStream_t stream);
+// hq_full_tc.cu: K = 1024 x 28 on the tcgen05 path (the default for that width)
+cudaError_t launch_hq_full28_tc(const void* x, int64_t M, int64_t ld_x, float clip, uint8_t* q, int64_t ld_q,
+                                float* scale, cudaStream_t stream);
+extern int g_hq_full_variant;
 cudaError_t launch_hq_full(const void* x, int64_t M, int64_t K, int64_t ld_x, int pow2, int m, float clip,
                            uint8_t* q, int64_t ld_q, float* scale, cudaStream_t stream);
 
