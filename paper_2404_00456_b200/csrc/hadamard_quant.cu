@@ -72,7 +72,9 @@ __global__ void __launch_bounds__(128) hq_none_kernel(const __half* __restrict__
   const int nchunk = (int)(K >> 3);
   const __half* xr = x + row * ld_x;
   uint4 v[CPT];
-  float amax = 0.f, ssq = 0.f;
+  // independent accumulator chains (the row's reductions are on the critical path of the CTA)
+  float am[4] = {0.f, 0.f, 0.f, 0.f};
+  float2 sq[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
   for (int i = 0; i < CPT; ++i) {
     const int c = threadIdx.x + i * 128;
@@ -82,11 +84,13 @@ __global__ void __launch_bounds__(128) hq_none_kernel(const __half* __restrict__
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const float2 f = __half22float2(h[e]);
-        amax = fmax_nan(amax, fmax_nan(fabsf(f.x), fabsf(f.y)));
-        if (kRms) ssq = fmaf(f.x, f.x, fmaf(f.y, f.y, ssq));
+        am[e] = fmax_nan(am[e], fmax_nan(fabsf(f.x), fabsf(f.y)));
+        if (kRms) sq[e & 1] = f2fma(f, f, sq[e & 1]);
       }
     }
   }
+  float amax = fmax_nan(fmax_nan(am[0], am[1]), fmax_nan(am[2], am[3]));
+  float ssq = (sq[0].x + sq[0].y) + (sq[1].x + sq[1].y);
   double norm = 1.0;
   if (kRms) {
 #pragma unroll
@@ -826,7 +830,7 @@ cudaError_t launch_hq_full(const void* x, int64_t M, int64_t K, int64_t ld_x, in
     e = cudaFuncSetAttribute(hq::hq_full_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     hq::hq_full_kernel<1><<<grid, threads, smem, stream>>>(xh, ld_x, pow2, clip, q, ld_q, scale, nullptr);
-  } else if (m == 28 && pow2 == 1024 && g_hq_full_variant == 0) {
+  } else if (m == 28 && pow2 == 1024 && g_hq_full_variant != 1) {
     return launch_hq_full28_tc(x, M, ld_x, clip, q, ld_q, scale, stream);
   } else if (m == 28 && pow2 == 1024) {
     static bool attr[64] = {};

@@ -14,12 +14,14 @@
 //    [row][a_hi][j] (two 64-wide j boxes; j >= 112 is zero-filled), 3-stage ring.
 //  * D lands in TMEM (fp32, lane = j', column = a_hi), double-buffered (2 x 256 columns), so the
 //    MMA of row r+1 overlaps the epilogue of row r.
-//  * H_256 over the columns runs in registers with packed fp32x2 butterflies (FADD2): 8 epilogue
-//    warps (setmaxnreg: 224 registers each), two per TMEM lane quarter (h = 0, 1).  Pass 1: each
-//    thread loads the 128 columns with a_hi bit 5 = h and transforms bits 0-4 and 6 (pairs packed along bit 7), then stores
-//    them back to TMEM; pass 2 (after the partner warp's pass 1): the 128 columns with bit 6 = h,
-//    bits 5 and 7 (pairs packed along bit 0).  Every bit is transformed exactly once, no shuffles.
-//  * Row amax over the 8 warps (named barrier), scale (1/sqrt(K) folded in, reading Z5), RNE
+//  * H_256 over the columns runs in registers with packed fp32x2 butterflies (FADD2): 16
+//    epilogue warps, four per TMEM lane quarter (g = 0..3).  Pass 1: each thread loads the 64
+//    columns with a_hi bits 6-7 = g and transforms bits 1-5 (pairs = adjacent columns), then
+//    stores them back to TMEM; pass 2 (after the lane's other three threads): the 64 columns
+//    with bits 4-5 = g, bits 6, 7 and 0 (within the register pair).  Every bit exactly once.
+//  * Rows are software-pipelined with split-phase mbarriers: pass1(r+1), then the quantization of
+//    row r once all 16 warps posted their partial amax (its values parked in TMEM), then pass2(r+1).
+//  * Scale (1/sqrt(K) folded in, reading Z5), RNE
 //    INT4 codes with the magic add; the two nibbles of a byte are adjacent j' = adjacent TMEM
 //    lanes, merged with one shuffle per code word.
 #include <cuda.h>
@@ -41,7 +43,8 @@ constexpr int A_BYTES = 128 * 128 * 2;       // (H_4 (x) H_28) padded to 128 x 1
 constexpr int BOX_BYTES = NA * 128;          // 256 a_hi rows x 64 j (128 B)
 constexpr int STAGE_BYTES = 2 * BOX_BYTES;   // 64 KB per token row
 constexpr int STAGES = 3;
-constexpr int TMA_WARP = 0, MMA_WARP = 1, EPI_WARP0 = 4, NUM_EPI = 8;  // warps 2-3 idle (warpgroup 0)
+constexpr int TMA_WARP = 0, MMA_WARP = 1, EPI_WARP0 = 4, NUM_EPI = 16;  // warps 2-3 idle (warpgroup 0)
+constexpr int TPL = NUM_EPI / 4;  // epilogue threads per TMEM lane
 constexpr int NUM_THREADS = (EPI_WARP0 + NUM_EPI) * 32;
 constexpr uint32_t TMEM_COLS = 512;
 constexpr size_t SMEM = 1024 + A_BYTES + (size_t)STAGES * STAGE_BYTES + 256;  // + barriers
@@ -68,6 +71,11 @@ QR_DEVICE void expect_tx(uint64_t* bar, uint32_t bytes) {
 }
 QR_DEVICE void bar_named(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
+#define QR_TMEM_ST16(taddr, r)                                                                          \
+  asm volatile(                                                                                         \
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr), \
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),  \
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]))
 #define QR_TMEM_ST32(taddr, r)                                                                          \
   asm volatile(                                                                                         \
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16," \
@@ -97,6 +105,7 @@ QR_DEVICE uint32_t code_word(float2 a, float2 b, float inv) {
   return __byte_perm(lo, hi, 0x6420);
 }
 
+template <bool kSpin>  // epilogue waits: spin on try_wait (true) or with a suspend-time hint
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     hq_full28_tc_kernel(const __grid_constant__ CUtensorMap tmX, int64_t M, float clip, uint8_t* __restrict__ q,
                         int64_t ld_q, float* __restrict__ scale, const uint4* __restrict__ a_img) {
@@ -126,7 +135,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&t_empty[b], NUM_EPI);
       mbar_init(&amax_done[b], NUM_EPI);
     }
-    for (int i = 0; i < 8; ++i) mbar_init(&pair_done[i], 2);
+    for (int i = 0; i < 8; ++i) mbar_init(&pair_done[i], TPL);
     fence_barrier_init();
   }
   if (warp == MMA_WARP) {
@@ -142,7 +151,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int64_t nrows = M > (int64_t)blockIdx.x ? (M - 1 - (int64_t)blockIdx.x) / gridDim.x + 1 : 0;
 
   if (warp < EPI_WARP0) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+    // register budget = launch bound (96) x 640 threads: 128 x 32 + 512 x 112 (an inc beyond the
+    // CTA's allocation would block forever)
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 32;");
     if (warp == TMA_WARP) {
       if (lane == 0) {
         for (int64_t it = 0; it < nrows; ++it) {
@@ -178,13 +189,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       __syncwarp();
     }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 112;");
     // Software pipeline over rows (split-phase barriers, so no warp idles at a barrier):
     //   pass1(r + 1) | quant(r) [after every warp posted its amax of row r] | pass2(r + 1)
     // The pass-2 values of a row are parked in its TMEM buffer between pass 2 and quant.
-    const int e = warp - EPI_WARP0;  // 0..7
+    auto epi_wait = [](uint64_t* bar, uint32_t parity) {
+      if (kSpin) mbar_wait(bar, parity);
+      else mbar_wait_sleep(bar, parity);
+    };
+    const int e = warp - EPI_WARP0;  // 0..15
     const int qd = warp & 3;         // TMEM lane quarter this warp may access
-    const int h = e >> 2;            // column half-set
+    const int g = e >> 2;            // which of the TPL = 4 threads of the lane
     const int L = qd * 32 + lane;    // TMEM lane = output j'
     const bool lane_ok = L < J;
     const bool odd = (lane & 1) != 0;
@@ -195,85 +210,77 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t sh_keep = odd ? 4u : 0u, sh_recv = odd ? 0u : 4u;
     const uint32_t keep_mask = odd ? 0xF0F0F0F0u : 0x0F0F0F0Fu;
     // even lanes write the a_hi bit 7 = 0 half of the pair's bytes, odd lanes the other half
-    uint8_t* const qlane = q + (L >> 1) + (int64_t)(64 * h + 128 * (odd ? 1 : 0)) * (J / 2);
+    uint8_t* const qlane = q + (L >> 1) + (int64_t)(16 * g + 128 * (odd ? 1 : 0)) * (J / 2);
 
-    // pass 1: columns 64 i + 32 h + c; a_hi bits 0-4 = c, 5 = h, 6-7 = i; transforms bits 1-4, 6, 7
+    // pass 1: columns 64 g + 32 i + c; a_hi bits 0-4 = c, 5 = i, 6-7 = g; transforms bits 1-5
     auto pass1 = [&](int64_t it) {
       const int buf = (int)(it & 1);
-      mbar_wait_sleep(&t_full[buf], (uint32_t)((it >> 1) & 1));
+      epi_wait(&t_full[buf], (uint32_t)((it >> 1) & 1));
       tc_fence_after();
-      const uint32_t tb = t_lane + (uint32_t)(buf * NA);
-      uint32_t r[4][32];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) QR_TMEM_LD32(tb + 64u * i + 32u * h, r[i]);
+      const uint32_t tb = t_lane + (uint32_t)(buf * NA + 64 * g);
+      uint32_t r[2][32];
+      QR_TMEM_LD32(tb, r[0]);
+      QR_TMEM_LD32(tb + 32u, r[1]);
       tmem_ld_wait();
-      float2 P[4][16];  // P[i][c'] = columns (2c', 2c' + 1): adjacent registers of the load
+      float2 P[2][16];  // P[i][c'] = columns (2c', 2c' + 1): adjacent registers of the load
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 2; ++i)
 #pragma unroll
         for (int c = 0; c < 16; ++c) P[i][c] = make_float2(__uint_as_float(r[i][2 * c]), __uint_as_float(r[i][2 * c + 1]));
 #pragma unroll
       for (int st = 1; st < 16; st <<= 1)
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 2; ++i)
 #pragma unroll
           for (int c = 0; c < 16; ++c)
             if (!(c & st)) bfly(P[i][c], P[i][c + st]);
 #pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        bfly(P[0][c], P[1][c]);  // bit 6
-        bfly(P[2][c], P[3][c]);
-        bfly(P[0][c], P[2][c]);  // bit 7
-        bfly(P[1][c], P[3][c]);
-      }
+      for (int c = 0; c < 16; ++c) bfly(P[0][c], P[1][c]);  // bit 5
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 2; ++i)
 #pragma unroll
         for (int c = 0; c < 16; ++c) {
           r[i][2 * c] = __float_as_uint(P[i][c].x);
           r[i][2 * c + 1] = __float_as_uint(P[i][c].y);
         }
-#pragma unroll
-      for (int i = 0; i < 4; ++i) QR_TMEM_ST32(tb + 64u * i + 32u * h, r[i]);
+      QR_TMEM_ST32(tb, r[0]);
+      QR_TMEM_ST32(tb + 32u, r[1]);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&pair_done[qd * 2 + buf]);
     };
-    // pass 2: columns 128 k7 + 64 h + 32 k5 + c; a_hi bits 0-4 = c, 5 = k5, 6 = h, 7 = k7;
-    // transforms bits 5 and 0 (within the register pair), posts the partial amax, parks the values
+    // pass 2: columns 64 i + 16 g + c; a_hi bits 0-3 = c, 4-5 = g, 6-7 = i; transforms bits 6, 7
+    // and 0 (within the register pair), posts the partial amax, parks the values
     auto pass2 = [&](int64_t it) {
       const int buf = (int)(it & 1);
-      mbar_wait_sleep(&pair_done[qd * 2 + buf], (uint32_t)((it >> 1) & 1));  // partner's pass 1
+      epi_wait(&pair_done[qd * 2 + buf], (uint32_t)((it >> 1) & 1));  // the lane's pass 1
       tc_fence_after();
-      const uint32_t tb = t_lane + (uint32_t)(buf * NA);
-      uint32_t u[2][2][32];
+      const uint32_t tb = t_lane + (uint32_t)(buf * NA + 16 * g);
+      uint32_t u[4][16];
 #pragma unroll
-      for (int k7 = 0; k7 < 2; ++k7)
-#pragma unroll
-        for (int k5 = 0; k5 < 2; ++k5) QR_TMEM_LD32(tb + 128u * k7 + 64u * h + 32u * k5, u[k7][k5]);
+      for (int i = 0; i < 4; ++i) QR_TMEM_LD16(tb + 64u * i, u[i]);
       tmem_ld_wait();
       float am[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int k7 = 0; k7 < 2; ++k7)
+      for (int c = 0; c < 8; ++c) {
+        float2 v[4];
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          float2 v0 = make_float2(__uint_as_float(u[k7][0][2 * c]), __uint_as_float(u[k7][0][2 * c + 1]));
-          float2 v1 = make_float2(__uint_as_float(u[k7][1][2 * c]), __uint_as_float(u[k7][1][2 * c + 1]));
-          bfly(v0, v1);  // bit 5
-          v0 = make_float2(v0.x + v0.y, v0.x - v0.y);  // bit 0
-          v1 = make_float2(v1.x + v1.y, v1.x - v1.y);
-          am[c & 1] = fmax_nan(am[c & 1], fmax_nan(fabsf(v0.x), fabsf(v0.y)));
-          am[2 + (c & 1)] = fmax_nan(am[2 + (c & 1)], fmax_nan(fabsf(v1.x), fabsf(v1.y)));
-          u[k7][0][2 * c] = __float_as_uint(v0.x);
-          u[k7][0][2 * c + 1] = __float_as_uint(v0.y);
-          u[k7][1][2 * c] = __float_as_uint(v1.x);
-          u[k7][1][2 * c + 1] = __float_as_uint(v1.y);
+        for (int i = 0; i < 4; ++i) v[i] = make_float2(__uint_as_float(u[i][2 * c]), __uint_as_float(u[i][2 * c + 1]));
+        bfly(v[0], v[1]);  // bit 6
+        bfly(v[2], v[3]);
+        bfly(v[0], v[2]);  // bit 7
+        bfly(v[1], v[3]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          v[i] = make_float2(v[i].x + v[i].y, v[i].x - v[i].y);  // bit 0
+          am[i] = fmax_nan(am[i], fmax_nan(fabsf(v[i].x), fabsf(v[i].y)));
+          u[i][2 * c] = __float_as_uint(v[i].x);
+          u[i][2 * c + 1] = __float_as_uint(v[i].y);
         }
+      }
 #pragma unroll
-      for (int k7 = 0; k7 < 2; ++k7)
-#pragma unroll
-        for (int k5 = 0; k5 < 2; ++k5) QR_TMEM_ST32(tb + 128u * k7 + 64u * h + 32u * k5, u[k7][k5]);
+      for (int i = 0; i < 4; ++i) QR_TMEM_ST16(tb + 64u * i, u[i]);
       float amax = lane_ok ? fmax_nan(fmax_nan(am[0], am[1]), fmax_nan(am[2], am[3])) : 0.f;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) amax = fmax_nan(amax, __shfl_xor_sync(0xffffffffu, amax, o));
@@ -283,19 +290,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&amax_done[buf]);
     };
-    // quant: row scale from the 8 partial amax values, reload the parked values, release the TMEM
+    // quant: row scale from the partial amax values, reload the parked values, release the TMEM
     // buffer, RNE codes, merge the nibble pairs across adjacent lanes, store
     auto quant = [&](int64_t it) {
       const int buf = (int)(it & 1);
       const int64_t row = (int64_t)blockIdx.x + it * gridDim.x;
-      mbar_wait_sleep(&amax_done[buf], (uint32_t)((it >> 1) & 1));
+      epi_wait(&amax_done[buf], (uint32_t)((it >> 1) & 1));
       tc_fence_after();
-      const uint32_t tb = t_lane + (uint32_t)(buf * NA);
-      uint32_t u[2][2][32];
+      const uint32_t tb = t_lane + (uint32_t)(buf * NA + 16 * g);
+      uint32_t u[4][16];
 #pragma unroll
-      for (int k7 = 0; k7 < 2; ++k7)
-#pragma unroll
-        for (int k5 = 0; k5 < 2; ++k5) QR_TMEM_LD32(tb + 128u * k7 + 64u * h + 32u * k5, u[k7][k5]);
+      for (int i = 0; i < 4; ++i) QR_TMEM_LD16(tb + 64u * i, u[i]);
       float amax = red[buf][0];
 #pragma unroll
       for (int w = 1; w < NUM_EPI; ++w) amax = fmax_nan(amax, red[buf][w]);
@@ -314,34 +319,33 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (lane == 0) mbar_arrive(&t_empty[buf]);  // D[buf] may be overwritten by row it + 2
       if (inv == 0.f) {  // zero or non-finite row: all codes 0
 #pragma unroll
-        for (int k7 = 0; k7 < 2; ++k7)
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int k5 = 0; k5 < 2; ++k5)
-#pragma unroll
-            for (int c = 0; c < 32; ++c) u[k7][k5][c] = 0u;
+          for (int c = 0; c < 16; ++c) u[i][c] = 0u;
       }
-      uint32_t out[2][8];
+      uint32_t out[2][4];
 #pragma unroll
-      for (int k5 = 0; k5 < 2; ++k5)
+      for (int m = 0; m < 4; ++m) {  // codes of a_hi = 64 i + 16 g + 4m .. +3
+        uint32_t w[4];
 #pragma unroll
-        for (int m = 0; m < 8; ++m) {  // codes of a_hi = 4m..4m+3 (+32 k5 + 64 h + 128 k7)
-          auto f2 = [&](int k7, int c) {
-            return make_float2(__uint_as_float(u[k7][k5][2 * c]), __uint_as_float(u[k7][k5][2 * c + 1]));
-          };
-          const uint32_t w0 = code_word(f2(0, 2 * m), f2(0, 2 * m + 1), inv);
-          const uint32_t w1 = code_word(f2(1, 2 * m), f2(1, 2 * m + 1), inv);
-          const uint32_t got = __shfl_xor_sync(0xffffffffu, odd ? w0 : w1, 1);
-          const uint32_t keep = odd ? w1 : w0;
-          out[k5][m] = ((keep << sh_keep) & keep_mask) | ((got << sh_recv) & ~keep_mask);
+        for (int i = 0; i < 4; ++i)
+          w[i] = code_word(make_float2(__uint_as_float(u[i][4 * m]), __uint_as_float(u[i][4 * m + 1])),
+                           make_float2(__uint_as_float(u[i][4 * m + 2]), __uint_as_float(u[i][4 * m + 3])), inv);
+#pragma unroll
+        for (int ii = 0; ii < 2; ++ii) {  // even lane keeps i = ii (bit 7 = 0), odd lane i = ii + 2
+          const uint32_t got = __shfl_xor_sync(0xffffffffu, odd ? w[ii] : w[ii + 2], 1);
+          const uint32_t keep = odd ? w[ii + 2] : w[ii];
+          out[ii][m] = ((keep << sh_keep) & keep_mask) | ((got << sh_recv) & ~keep_mask);
         }
+      }
       if (lane_ok) {
         uint8_t* const qr = qlane + row * ld_q;
 #pragma unroll
-        for (int k5 = 0; k5 < 2; ++k5)
+        for (int ii = 0; ii < 2; ++ii)
 #pragma unroll
-          for (int m = 0; m < 8; ++m) {
-            uint8_t* dst = qr + (int64_t)(4 * m + 32 * k5) * (J / 2);
-            const uint32_t o = out[k5][m];
+          for (int m = 0; m < 4; ++m) {
+            uint8_t* dst = qr + (int64_t)(64 * ii + 4 * m) * (J / 2);
+            const uint32_t o = out[ii][m];
             dst[0] = (uint8_t)o;
             dst[J / 2] = (uint8_t)(o >> 8);
             dst[J] = (uint8_t)(o >> 16);
@@ -411,7 +415,7 @@ void* g_img[64];
 
 }  // namespace
 
-int g_hq_full_variant = 0;  // debug: 1 = the mma.sync kernel (hq_full28_kernel)
+int g_hq_full_variant = 0;  // debug: 1 = the mma.sync kernel (hq_full28_kernel), 2 = spinning epilogue waits
 
 cudaError_t launch_hq_full28_tc(const void* x, int64_t M, int64_t ld_x, float clip, uint8_t* q, int64_t ld_q,
                                 float* scale, cudaStream_t stream) {
@@ -430,9 +434,10 @@ cudaError_t launch_hq_full28_tc(const void* x, int64_t M, int64_t ld_x, float cl
       if (e != cudaSuccess) return e;
       e = cudaMemcpy(d, host.data(), host.size() * sizeof(uint16_t), cudaMemcpyHostToDevice);
       if (e != cudaSuccess) return e;
-      e = cudaFuncSetAttribute(hqtc::hq_full28_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)hqtc::SMEM);
-      if (e != cudaSuccess) return e;
+      for (auto kern : {hqtc::hq_full28_tc_kernel<false>, hqtc::hq_full28_tc_kernel<true>}) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hqtc::SMEM);
+        if (e != cudaSuccess) return e;
+      }
       g_img[dev & 63] = d;
     }
     img = g_img[dev & 63];
@@ -451,7 +456,8 @@ cudaError_t launch_hq_full28_tc(const void* x, int64_t M, int64_t ld_x, float cl
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)(M < nsm ? M : nsm);
-  hqtc::hq_full28_tc_kernel<<<grid, hqtc::NUM_THREADS, hqtc::SMEM, stream>>>(
+  auto kern = g_hq_full_variant == 2 ? hqtc::hq_full28_tc_kernel<true> : hqtc::hq_full28_tc_kernel<false>;
+  kern<<<grid, hqtc::NUM_THREADS, hqtc::SMEM, stream>>>(
       map, M, clip, q, ld_q, scale, static_cast<const uint4*>(img));
   return cudaPeekAtLastError();
 }

@@ -89,11 +89,14 @@ def main():
             del wq, y
         del xq_big
     if "hq" in a.what:
-        for mode, K in (("none", 8192), ("across_heads", 8192), ("full", 28672), ("full", 11008), ("none", 4096)):
+        cases = [c.split(":") for c in os.environ.get("HQ_CASES", "none:8192,none_rms:8192,across_heads:8192,full:28672,full:11008,none:4096").split(",")]
+        for mode, K in cases:
+            K = int(K)
             x = synth.activations(M, K, "outlier", 5, dev)
             qb = torch.empty(M, K // 2, dtype=torch.uint8, device=dev)
             sb = torch.empty(M, dtype=torch.float32, device=dev)
-            ms = timeit(lambda: q.hadamard_quant(x, mode, 128, 0.9, q=qb, scale=sb), a.iters)
+            rms = mode == "none_rms"
+            ms = timeit(lambda: q.hadamard_quant(x, "none" if rms else mode, 128, 0.9, q=qb, scale=sb, rmsnorm=rms), a.iters)
             gbs = M * (2.5 * K + 4) / ms / 1e6
             res[f"hq_{mode}_{K}"] = {"ms": ms, "gbs": gbs, "frac_hbm": gbs / 6536}
             print(mode, K, json.dumps(res[f"hq_{mode}_{K}"]), flush=True)
