@@ -766,8 +766,12 @@ cudaError_t launch_hq_none_q8(const void* x, int64_t M, int64_t K, int64_t ld_x,
   return cudaPeekAtLastError();
 }
 
+int g_hq_heads_variant = 0;  // debug: 1 = the CUDA-core butterfly kernel for every width
+
 cudaError_t launch_hq_heads(const void* x, int64_t M, int64_t K, int64_t ld_x, int head_dim, float clip,
                             uint8_t* q, int64_t ld_q, float* scale, cudaStream_t stream) {
+  if (g_hq_heads_variant == 0 && hq_heads_tc_supported(K, head_dim))
+    return launch_hq_heads_tc(x, M, K, ld_x, head_dim, clip, q, ld_q, scale, stream);
   const int n_h = (int)(K / head_dim);
   const int P2 = head_dim / 2;
   const __half* xh = static_cast<const __half*>(x);
@@ -862,6 +866,8 @@ cudaError_t launch_hq_full(const void* x, int64_t M, int64_t K, int64_t ld_x, in
 }
 
 }  // namespace qr
+
+extern "C" void quarot_debug_hq_heads_variant(int v) { qr::g_hq_heads_variant = v; }
 
 #ifdef QR_F28_PROF
 extern "C" void quarot_debug_f28_prof(unsigned long long* out) {

@@ -1,0 +1,347 @@
+// hq_heads_tc.cu — rows a2 + a3, ACROSS_HEADS ("Hadamard heads", Eq. 9) on the
+// tcgen05 tensor path, for head_dim = 128 and n_h in {16, 32, 64} (Llama-2-7B: 32, 70B: 64).
+//
+// y = (H_{n_h} (x) I_{d_h}) z per token row, z[h*128 + d] (head-major concat).  As a matrix
+// product per row: D[d][h'] = sum_h Z[h][d] * H[h'][h], i.e. one kind::f16 MMA per row with
+//  * A = Z^T: M = d (128), K = h (n_h), taken MN-major straight from the row as TMA'd (3-D map
+//    [row][h][d], two 64-wide d boxes, SWIZZLE_128B: the canonical MN-major SW128 layout with
+//    SBO = 1024 B between 8-head groups and LBO = the 64-d box);
+//  * B = H_{n_h} (Sylvester, +-1 exact in fp16): N = h', K = h, K-major SW128 constant image;
+//  * D: fp32 in TMEM, lane = d, column = h' (n_h columns).  fp16 x +-1 products are exact and
+//    the accumulation is fp32 (FP32 Hadamard).
+// The transform needs no CUDA-core butterflies at all; the epilogue is amax + RNE INT4 codes +
+// nibble packing (pairs d, d+1 = adjacent lanes, merged with one shuffle per code word).
+// 16 epilogue warps = 4 groups of 4 (one warp per TMEM lane quarter); group g takes the CTA's
+// rows it = g (mod 4), each with two TMEM buffers, so one group's row-amax barrier never stalls
+// the others.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+#include "quarot_internal.h"
+
+namespace qr {
+namespace hqh {
+
+constexpr int DH = 128;                     // head_dim (M)
+constexpr int MAXH = 64;                    // max n_h (TMEM: 4 groups x 2 buffers x n_h columns)
+constexpr int STAGES = 6;
+constexpr int STAGE_BYTES = 2 * 64 * MAXH * 2;  // two 64-d boxes of n_h rows x 128 B
+constexpr int B_BYTES = MAXH * 128;         // H_{n_h}: n_h rows x (n_h fp16 <= 128 B), SW128 K-major
+constexpr int NG = 4, NUM_EPI = 4 * NG;
+constexpr int TMA_WARP = 0, MMA_WARP = 1, EPI_WARP0 = 4;
+constexpr int NUM_THREADS = (EPI_WARP0 + NUM_EPI) * 32;  // 640
+constexpr uint32_t TMEM_COLS = 512;
+constexpr size_t SMEM = 1024 + B_BYTES + (size_t)STAGES * STAGE_BYTES + 512;
+static_assert(SMEM <= 232448, "227 KB dynamic smem");
+
+// kind::f16: D f32, A = B = f16, A MN-major (bit 15), B K-major, N/8 at 17, M/16 at 24
+__host__ __device__ constexpr uint32_t idesc(uint32_t n) {
+  return (1u << 4) | (1u << 15) | ((n >> 3) << 17) | ((uint32_t)(DH >> 4) << 24);
+}
+// MN-major SWIZZLE_128B: 64-element (128 B) MN rows, 8 K rows per 1024-B atom; LBO = stride
+// between MN atoms (the second 64-d box), SBO = stride between 8-row K groups (1024 B)
+QR_DEVICE uint64_t desc_mn_sw128(uint32_t addr, uint32_t lbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+QR_DEVICE void mma_f16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(id), "r"(acc));
+}
+QR_DEVICE void tma_load_3d(uint32_t dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+QR_DEVICE void expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+QR_DEVICE void bar_named(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// 4 codes (low nibble of each byte) of a.x, a.y, b.x, b.y: RNE by the 1.5 * 2^23 magic add,
+// clamp to [-7, 7] on 16-bit lanes (VIMNMX), gather the low bytes
+QR_DEVICE uint32_t code_word(float2 a, float2 b, float inv) {
+  const float2 i2 = make_float2(inv, inv), mg = make_float2(12582912.f, 12582912.f);
+  const float2 ma = f2fma(a, i2, mg), mb = f2fma(b, i2, mg);
+  uint32_t lo = __byte_perm(__float_as_uint(ma.x), __float_as_uint(ma.y), 0x5410);
+  uint32_t hi = __byte_perm(__float_as_uint(mb.x), __float_as_uint(mb.y), 0x5410);
+  lo = __vmaxs2(__vmins2(lo, 0x00070007u), 0xFFF9FFF9u);
+  hi = __vmaxs2(__vmins2(hi, 0x00070007u), 0xFFF9FFF9u);
+  return __byte_perm(lo, hi, 0x6420);
+}
+
+template <int NH>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    hq_heads_tc_kernel(const __grid_constant__ CUtensorMap tmZ, int64_t M, float clip, uint8_t* __restrict__ q,
+                       int64_t ld_q, float* __restrict__ scale, const uint4* __restrict__ b_img) {
+  constexpr int ROW_BYTES = 2 * 64 * NH * 2;  // two 64-d boxes
+  constexpr int BOX_BYTES = 64 * NH * 2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sB = smem;
+  uint8_t* sA = smem + B_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sA + STAGES * STAGE_BYTES);  // [STAGES]
+  uint64_t* empty = full + STAGES;                                           // [STAGES]
+  uint64_t* t_full = empty + STAGES;                                         // [NG * 2]
+  uint64_t* t_empty = t_full + 2 * NG;                                       // [NG * 2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(t_empty + 2 * NG);
+  __shared__ float red[NG][2][4];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  for (int i = threadIdx.x; i < NH * 128 / 16; i += NUM_THREADS) reinterpret_cast<uint4*>(sB)[i] = __ldg(b_img + i);
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2 * NG; ++b) {
+      mbar_init(&t_full[b], 1);
+      mbar_init(&t_empty[b], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == MMA_WARP) {
+    tmem_alloc(tmem_holder, TMEM_COLS);
+    tmem_relinquish();
+  }
+  if (warp == TMA_WARP && lane == 0)
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmZ)) : "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  const int64_t nrows = M > (int64_t)blockIdx.x ? (M - 1 - (int64_t)blockIdx.x) / gridDim.x + 1 : 0;
+
+  if (warp < EPI_WARP0) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 32;");  // 128 x 32 + 512 x 112 = 640 x 96
+    if (warp == TMA_WARP) {
+      if (lane == 0) {
+        for (int64_t it = 0; it < nrows; ++it) {
+          const int s = (int)(it % STAGES);
+          mbar_wait_sleep(&empty[s], (uint32_t)((it / STAGES) & 1) ^ 1u);
+          expect_tx(&full[s], ROW_BYTES);
+          const int row = (int)((int64_t)blockIdx.x + it * gridDim.x);
+          const uint32_t dst = smem_u32(sA + s * STAGE_BYTES);
+          tma_load_3d(dst, &tmZ, 0, 0, row, &full[s]);
+          tma_load_3d(dst + BOX_BYTES, &tmZ, 64, 0, row, &full[s]);
+        }
+      }
+    } else if (warp == MMA_WARP) {
+      if (lane == 0) {
+        const uint64_t b_desc = umma_desc_sw128(smem_u32(sB));
+        for (int64_t it = 0; it < nrows; ++it) {
+          const int s = (int)(it % STAGES);
+          const int g = (int)(it % NG), b = (int)((it / NG) & 1), tb = g * 2 + b;
+          mbar_wait_sleep(&t_empty[tb], (uint32_t)((it / (2 * NG)) & 1) ^ 1u);
+          mbar_wait_sleep(&full[s], (uint32_t)((it / STAGES) & 1));
+          tc_fence_after();
+          const uint64_t a_desc = desc_mn_sw128(smem_u32(sA + s * STAGE_BYTES), BOX_BYTES);
+          const uint32_t d_tmem = tmem_base + (uint32_t)(tb * NH);
+#pragma unroll
+          for (int kk = 0; kk < NH / 16; ++kk)  // A: 16 heads = two 8-row K groups (2048 B); B: +32 B
+            mma_f16(d_tmem, a_desc + (uint64_t)(kk * (2048 >> 4)), b_desc + (uint64_t)(2 * kk), idesc(NH),
+                    kk > 0 ? 1u : 0u);
+          mma_commit(&empty[s]);
+          mma_commit(&t_full[tb]);
+        }
+      }
+      __syncwarp();
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 112;");
+    const int e = warp - EPI_WARP0;  // 0..15
+    const int qd = warp & 3;         // TMEM lane quarter
+    const int g = e >> 2;            // row group
+    const int d = qd * 32 + lane;    // TMEM lane = head dimension index
+    const bool odd = (lane & 1) != 0;
+    const uint32_t t_lane = tmem_base + ((uint32_t)(qd * 32) << 16);
+    const float norm_f = (float)rsqrt((double)NH);
+    const float c0 = (float)((double)clip * rsqrt((double)NH) / 7.0);
+    const uint32_t sh_keep = odd ? 4u : 0u, sh_recv = odd ? 0u : 4u;
+    const uint32_t keep_mask = odd ? 0xF0F0F0F0u : 0x0F0F0F0Fu;
+    constexpr int HALF = NH / 2;  // even lane writes h' < HALF, odd lane h' >= HALF
+    uint8_t* const qlane = q + (d >> 1) + (int64_t)(odd ? HALF : 0) * (DH / 2);
+    for (int64_t it = g; it < nrows; it += NG) {
+      const int b = (int)((it / NG) & 1), tb = g * 2 + b;
+      const int64_t row = (int64_t)blockIdx.x + it * gridDim.x;
+      mbar_wait_sleep(&t_full[tb], (uint32_t)((it / (2 * NG)) & 1));
+      tc_fence_after();
+      uint32_t u[NH];
+      if constexpr (NH >= 32) {
+#pragma unroll
+        for (int c = 0; c < NH; c += 32) QR_TMEM_LD32(t_lane + (uint32_t)(tb * NH + c), (u + c));
+      } else {
+        QR_TMEM_LD16(t_lane + (uint32_t)(tb * NH), u);
+      }
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&t_empty[tb]);
+      float am[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int c = 0; c < NH; c += 2)
+        am[(c >> 1) & 3] = fmax_nan(am[(c >> 1) & 3], fmax_nan(fabsf(__uint_as_float(u[c])), fabsf(__uint_as_float(u[c + 1]))));
+      float amax = fmax_nan(fmax_nan(am[0], am[1]), fmax_nan(am[2], am[3]));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) amax = fmax_nan(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      if (lane == 0) red[g][b][qd] = amax;
+      bar_named(1 + g, 128);
+      amax = fmax_nan(fmax_nan(red[g][b][0], red[g][b][1]), fmax_nan(red[g][b][2], red[g][b][3]));
+      // scale = fp32(clip * amax / (7 sqrt(n_h))) (readings Z5, Z9); zero row -> 1, non-finite -> NaN
+      float sc = 1.f, inv = 0.f;
+      if (!isfinite(amax)) {
+        sc = __int_as_float(0x7fc00000);
+      } else if (amax != 0.f) {
+        sc = c0 * amax;
+        inv = __fdiv_rn(norm_f, sc);
+      }
+      if (qd == 0 && lane == 0) scale[row] = sc;
+      if (inv == 0.f) {
+#pragma unroll
+        for (int c = 0; c < NH; ++c) u[c] = 0u;
+      }
+      uint32_t out[NH / 8];
+#pragma unroll
+      for (int m = 0; m < NH / 8; ++m) {  // words of h' = 4m..4m+3 (even lane) / HALF + 4m.. (odd)
+        const uint32_t w0 = code_word(make_float2(__uint_as_float(u[4 * m]), __uint_as_float(u[4 * m + 1])),
+                                      make_float2(__uint_as_float(u[4 * m + 2]), __uint_as_float(u[4 * m + 3])), inv);
+        const uint32_t w1 = code_word(
+            make_float2(__uint_as_float(u[HALF + 4 * m]), __uint_as_float(u[HALF + 4 * m + 1])),
+            make_float2(__uint_as_float(u[HALF + 4 * m + 2]), __uint_as_float(u[HALF + 4 * m + 3])), inv);
+        const uint32_t got = __shfl_xor_sync(0xffffffffu, odd ? w0 : w1, 1);
+        const uint32_t keep = odd ? w1 : w0;
+        out[m] = ((keep << sh_keep) & keep_mask) | ((got << sh_recv) & ~keep_mask);
+      }
+      uint8_t* const qr = qlane + row * ld_q;
+#pragma unroll
+      for (int m = 0; m < NH / 8; ++m) {
+        uint8_t* dst = qr + (int64_t)(4 * m) * (DH / 2);
+        const uint32_t o = out[m];
+        dst[0] = (uint8_t)o;
+        dst[DH / 2] = (uint8_t)(o >> 8);
+        dst[DH] = (uint8_t)(o >> 16);
+        dst[3 * DH / 2] = (uint8_t)(o >> 24);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == MMA_WARP) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+}  // namespace hqh
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn_heads() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult res;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &res) == cudaSuccess &&
+        res == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// Sylvester H_{n}[h'][h] = (-1)^popcount(h' & h) as the UMMA K-major SWIZZLE_128B image:
+// rows h' at 128 B (8-row groups at 1024 B), 16-byte chunk c of row r at chunk c ^ (r & 7);
+// columns h >= n are zero (a row holds 64 fp16 slots).
+std::vector<uint16_t> b_image(int n) {
+  std::vector<uint16_t> img((size_t)n * 64, 0);
+  for (int r = 0; r < n; ++r)
+    for (int k = 0; k < n; ++k) {
+      const int chunk = k / 8, within = k % 8;
+      const size_t off = (size_t)(r / 8) * 1024 + (size_t)(r % 8) * 128 + (size_t)((chunk ^ (r % 8)) * 16) + within * 2;
+      img[off / 2] = (__builtin_popcount(r & k) & 1) ? 0xBC00 : 0x3C00;
+    }
+  return img;
+}
+
+std::mutex g_mu;
+void* g_img[64][3];  // n_h = 16, 32, 64
+
+template <int NH>
+cudaError_t launch_nh(const void* x, int64_t M, int64_t ld_x, float clip, uint8_t* q, int64_t ld_q, float* scale,
+                      cudaStream_t stream, int dev, void* img) {
+  auto fn = encode_fn_heads();
+  if (!fn) return cudaErrorInvalidValue;
+  CUtensorMap map;
+  cuuint64_t dims[3] = {(cuuint64_t)hqh::DH, (cuuint64_t)NH, (cuuint64_t)M};
+  cuuint64_t strides[2] = {(cuuint64_t)hqh::DH * 2, (cuuint64_t)ld_x * 2};
+  cuuint32_t box[3] = {64u, (cuuint32_t)NH, 1u};
+  cuuint32_t estr[3] = {1u, 1u, 1u};
+  CUresult r = fn(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(x), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  static bool attr[64] = {};
+  if (!attr[dev & 63]) {
+    cudaError_t e = cudaFuncSetAttribute(hqh::hq_heads_tc_kernel<NH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)hqh::SMEM);
+    if (e != cudaSuccess) return e;
+    attr[dev & 63] = true;
+  }
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)(M < nsm ? M : nsm);
+  hqh::hq_heads_tc_kernel<NH><<<grid, hqh::NUM_THREADS, hqh::SMEM, stream>>>(map, M, clip, q, ld_q, scale,
+                                                                          static_cast<const uint4*>(img));
+  return cudaPeekAtLastError();
+}
+
+}  // namespace
+
+bool hq_heads_tc_supported(int64_t K, int head_dim) {
+  const int64_t nh = K / head_dim;
+  return head_dim == hqh::DH && (nh == 16 || nh == 32 || nh == 64);
+}
+
+cudaError_t launch_hq_heads_tc(const void* x, int64_t M, int64_t K, int64_t ld_x, int head_dim, float clip, uint8_t* q,
+                               int64_t ld_q, float* scale, cudaStream_t stream) {
+  if (!hq_heads_tc_supported(K, head_dim)) return cudaErrorInvalidValue;
+  const int nh = (int)(K / head_dim);
+  const int slot = nh == 16 ? 0 : (nh == 32 ? 1 : 2);
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  void* img = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g_img[dev & 63][slot]) {
+      auto host = b_image(nh);
+      void* dptr = nullptr;
+      e = cudaMalloc(&dptr, host.size() * sizeof(uint16_t));
+      if (e != cudaSuccess) return e;
+      e = cudaMemcpy(dptr, host.data(), host.size() * sizeof(uint16_t), cudaMemcpyHostToDevice);
+      if (e != cudaSuccess) return e;
+      g_img[dev & 63][slot] = dptr;
+    }
+    img = g_img[dev & 63][slot];
+  }
+  if (nh == 16) return launch_nh<16>(x, M, ld_x, clip, q, ld_q, scale, stream, dev, img);
+  if (nh == 32) return launch_nh<32>(x, M, ld_x, clip, q, ld_q, scale, stream, dev, img);
+  return launch_nh<64>(x, M, ld_x, clip, q, ld_q, scale, stream, dev, img);
+}
+
+}  // namespace qr
