@@ -856,6 +856,8 @@ cudaError_t launch_hq_full(const void* x, int64_t M, int64_t K, int64_t ld_x, in
     if (e != cudaSuccess) return e;
     hq::hq_full_kernel<28><<<grid, threads, smem, stream>>>(xh, ld_x, pow2, clip, q, ld_q, scale,
                                                            device_bfrag_table(28));
+  } else if (m == 172 && pow2 == 64 && g_hq_full_variant != 1) {
+    return launch_hq_full172_tc(x, M, ld_x, clip, q, ld_q, scale, stream);
   } else {
     e = cudaFuncSetAttribute(hq::hq_full_kernel<172>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

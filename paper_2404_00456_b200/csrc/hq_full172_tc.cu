@@ -1,0 +1,359 @@
+// hq_full172_tc.cu — rows a1 + a3 for K = 64 x 172 (the Llama-2-7B down_proj input, P:182-185,
+// P:67) with H_172 on the tcgen05 tensor path.
+//
+// y = (H_64 (x) H_172) x per token row, element i = a*172 + b (reading Z2), H_172 the stored
+// Williamson matrix (reading Z3), row i of H dotted with x (reading Z4):
+//
+//     y[a'*172 + j'] = sum_a H_64[a'][a] * D[j'][a],   D[j'][a] = sum_b H_172[j'][b] * x[a*172 + b].
+//
+//  * D is one dense fp16 contraction per row: two tcgen05.mma kind::f16 M = 128 halves (j' < 172
+//    real rows of the constant A = H_172, zero-padded to 256 x 192), N = 64 (a), K = 192 (b,
+//    zero-padded), 12 MMAs of K = 16 per half.  +-1 x fp16 products are exact; fp32 accumulation.
+//  * A row's a-pitch is 344 B, which no TMA tensor map can describe (strides must be multiples of
+//    16 B): the row is bulk-copied raw into shared memory and two "relayout" warps rewrite it as the
+//    K-major SWIZZLE_128B operand [a][b] (8-byte loads, 16-byte stores; the zero padding b >= 172
+//    is written once).
+//  * D lands in TMEM (lane = j', 64 columns = a; 4 buffers).  H_64 over the columns runs in
+//    registers: each thread holds all 64 a of its j' (bits 1-5 as packed fp32x2 butterflies, bit 0
+//    within the register pair).  16 epilogue warps = 2 row groups of 8 (4 lane quarters x 2
+//    M-halves); a group's row-amax barrier never stalls the other group.
+//  * Scale (1/sqrt(K) folded in, reading Z5), RNE INT4 codes with the magic add; the two nibbles
+//    of a byte are adjacent j' = adjacent TMEM lanes, merged with one shuffle per code word.
+#include <cuda.h>
+
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+#include "quarot_internal.h"
+
+namespace qr {
+namespace hq172 {
+
+constexpr int MB = 172, P = 64, K = MB * P;  // 11008
+constexpr int KP = 192;                       // contraction padded to 3 SW128 atoms
+constexpr int RAW_BYTES = K * 2;              // 22016 (a multiple of 16)
+constexpr int B_BYTES = P * KP * 2;           // 24 KB: [3 atoms][64 rows][128 B]
+constexpr int A_BYTES = 2 * 3 * 16384;        // 96 KB: [M-half][atom][128 rows][128 B]
+constexpr int RSTAGES = 2, BSTAGES = 3;
+constexpr int NG = 2, NUM_EPI = 8 * NG;
+constexpr int TMA_WARP = 0, MMA_WARP = 1, RL_WARP0 = 2, NUM_RL = 2, EPI_WARP0 = 4;
+constexpr int NUM_THREADS = (EPI_WARP0 + NUM_EPI) * 32;  // 640
+constexpr int TBUF = 4;                                   // TMEM row buffers of 128 columns
+constexpr uint32_t TMEM_COLS = 512;
+constexpr size_t SMEM = 1024 + A_BYTES + (size_t)BSTAGES * B_BYTES + (size_t)RSTAGES * RAW_BYTES + 512;
+static_assert(SMEM <= 232448, "227 KB dynamic smem");
+// kind::f16: D f32, A = B = f16, both K-major, N = 64, M = 128
+constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(P >> 3) << 17) | ((128u >> 4) << 24);
+
+QR_DEVICE void mma_f16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(id), "r"(acc));
+}
+QR_DEVICE void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+QR_DEVICE bool elect_one() {
+  uint32_t p;
+  asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\tselp.u32 %0, 1, 0, e;\n\t}" : "=r"(p));
+  return p != 0;
+}
+QR_DEVICE void bar_named(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+QR_DEVICE void bfly(float2& u, float2& v) {
+  const float2 s = f2add(u, v), d = f2sub(u, v);
+  u = s;
+  v = d;
+}
+QR_DEVICE uint32_t code_word(float2 a, float2 b, float inv) {
+  const float2 i2 = make_float2(inv, inv), mg = make_float2(12582912.f, 12582912.f);
+  const float2 ma = f2fma(a, i2, mg), mb = f2fma(b, i2, mg);
+  uint32_t lo = __byte_perm(__float_as_uint(ma.x), __float_as_uint(ma.y), 0x5410);
+  uint32_t hi = __byte_perm(__float_as_uint(mb.x), __float_as_uint(mb.y), 0x5410);
+  lo = __vmaxs2(__vmins2(lo, 0x00070007u), 0xFFF9FFF9u);
+  hi = __vmaxs2(__vmins2(hi, 0x00070007u), 0xFFF9FFF9u);
+  return __byte_perm(lo, hi, 0x6420);
+}
+// SW128 K-major byte offset of (row, 16-byte chunk c of atom kc) in a [atom][rows][128 B] image
+__host__ __device__ constexpr uint32_t sw128_off(int rows, int kc, int row, int c) {
+  return (uint32_t)(kc * rows * 128 + (row >> 3) * 1024 + (row & 7) * 128 + ((c ^ (row & 7)) << 4));
+}
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    hq_full172_tc_kernel(const __half* __restrict__ x, int64_t M, int64_t ld_x, float clip, uint8_t* __restrict__ q,
+                         int64_t ld_q, float* __restrict__ scale, const uint4* __restrict__ a_img) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + A_BYTES;
+  uint8_t* sR = sB + BSTAGES * B_BYTES;
+  uint64_t* r_full = reinterpret_cast<uint64_t*>(sR + RSTAGES * RAW_BYTES);  // [RSTAGES] raw row landed
+  uint64_t* r_empty = r_full + RSTAGES;                                       // [RSTAGES] relayout done reading
+  uint64_t* b_full = r_empty + RSTAGES;                                       // [BSTAGES] operand written
+  uint64_t* b_empty = b_full + BSTAGES;                                       // [BSTAGES] MMA done reading
+  uint64_t* t_full = b_empty + BSTAGES;                                       // [TBUF]
+  uint64_t* t_empty = t_full + TBUF;                                          // [TBUF]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(t_empty + TBUF);
+  __shared__ float red[NG][2][8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  for (int i = threadIdx.x; i < A_BYTES / 16; i += NUM_THREADS) reinterpret_cast<uint4*>(sA)[i] = __ldg(a_img + i);
+  for (int i = threadIdx.x; i < BSTAGES * P * 2; i += NUM_THREADS) {  // constant zero chunks b >= 176
+    const int st = i / (2 * P), a = (i / 2) % P, c = 6 + (i & 1);
+    *reinterpret_cast<uint4*>(sB + st * B_BYTES + sw128_off(P, 2, a, c)) = make_uint4(0u, 0u, 0u, 0u);
+  }
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < RSTAGES; ++s) {
+      mbar_init(&r_full[s], 1);
+      mbar_init(&r_empty[s], NUM_RL);
+    }
+    for (int s = 0; s < BSTAGES; ++s) {
+      mbar_init(&b_full[s], NUM_RL);
+      mbar_init(&b_empty[s], 1);
+    }
+    for (int b = 0; b < TBUF; ++b) {
+      mbar_init(&t_full[b], 1);
+      mbar_init(&t_empty[b], 8);
+    }
+    fence_barrier_init();
+  }
+  if (warp == MMA_WARP) {
+    tmem_alloc(tmem_holder, TMEM_COLS);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  const int64_t nrows = M > (int64_t)blockIdx.x ? (M - 1 - (int64_t)blockIdx.x) / gridDim.x + 1 : 0;
+
+  if (warp < EPI_WARP0) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");  // 128 x 64 + 512 x 104 = 640 x 96
+    if (warp == TMA_WARP) {
+      if (lane == 0) {
+        for (int64_t it = 0; it < nrows; ++it) {
+          const int s = (int)(it % RSTAGES);
+          mbar_wait(&r_empty[s], (uint32_t)((it / RSTAGES) & 1) ^ 1u);
+          const int64_t row = (int64_t)blockIdx.x + it * gridDim.x;
+          bulk_load(smem_u32(sR + s * RAW_BYTES), x + row * ld_x, RAW_BYTES, &r_full[s]);
+        }
+      }
+    } else if (warp == MMA_WARP) {
+      // the whole warp runs the loop (descriptors stay warp-uniform: uniform registers, no R2UR per
+      // MMA); one elected lane issues
+      const uint32_t sa = smem_u32(sA), sb = smem_u32(sB);
+      for (int64_t it = 0; it < nrows; ++it) {
+        const int s = (int)(it % BSTAGES), tb = (int)(it % TBUF);
+        mbar_wait(&t_empty[tb], (uint32_t)((it / TBUF) & 1) ^ 1u);
+        mbar_wait(&b_full[s], (uint32_t)((it / BSTAGES) & 1));
+        tc_fence_after();
+        const uint64_t b_desc = umma_desc_sw128(sb + (uint32_t)(s * B_BYTES));
+        const uint32_t d0 = tmem_base + (uint32_t)(tb * 2 * P);
+        if (elect_one()) {
+#pragma unroll
+          for (int mh = 0; mh < 2; ++mh) {
+            const uint64_t a_desc = umma_desc_sw128(sa + (uint32_t)(mh * 3 * 16384));
+#pragma unroll
+            for (int kk = 0; kk < KP / 16; ++kk) {  // atom kk/4 (A: +16 KB, B: +8 KB), +32 B per K = 16
+              const uint64_t koff = (uint64_t)(2 * (kk & 3));
+              mma_f16(d0 + (uint32_t)(mh * P), a_desc + (uint64_t)((kk >> 2) * (16384 >> 4)) + koff,
+                      b_desc + (uint64_t)((kk >> 2) * (P * 128 >> 4)) + koff, IDESC, kk > 0 ? 1u : 0u);
+            }
+          }
+          mma_commit(&b_empty[s]);
+          mma_commit(&t_full[tb]);
+        }
+        __syncwarp();
+      }
+    } else {  // relayout warps: raw row [a][172] -> K-major SW128 operand [a][192]
+      // thread = row a (64 rows over the two warps), loop over the 22 chunks of 8 b: the 8-byte
+      // loads of a warp cover all 32 banks twice (a-pitch 344 B = 86 words), the swizzled 16-byte
+      // stores cover them four times: no bank conflicts, no index arithmetic in the loop
+      const int a = (warp - RL_WARP0) * 32 + lane;
+      const uint32_t dst_row = (uint32_t)((a >> 3) * 1024 + (a & 7) * 128);
+      for (int64_t it = 0; it < nrows; ++it) {
+        const int rs = (int)(it % RSTAGES), bs = (int)(it % BSTAGES);
+        mbar_wait(&r_full[rs], (uint32_t)((it / RSTAGES) & 1));
+        mbar_wait(&b_empty[bs], (uint32_t)((it / BSTAGES) & 1) ^ 1u);
+        const uint32_t src = smem_u32(sR + rs * RAW_BYTES) + (uint32_t)(a * 344);
+        const uint32_t dst = smem_u32(sB + bs * B_BYTES) + dst_row;
+#pragma unroll
+        for (int j = 0; j < 22; ++j) {  // chunk j: b = 8j .. 8j + 7 (b >= 172 zero)
+          uint32_t v0, v1, v2 = 0u, v3 = 0u;
+          asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v0), "=r"(v1) : "r"(src + 16u * j));
+          if (j < 21) asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v2), "=r"(v3) : "r"(src + 16u * j + 8u));
+          sts_v4(dst + (uint32_t)((j >> 3) * (P * 128)) + (uint32_t)(((j & 7) ^ (a & 7)) << 4), make_uint4(v0, v1, v2, v3));
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&r_empty[rs]);
+          mbar_arrive(&b_full[bs]);
+        }
+      }
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 104;");
+    const int e = warp - EPI_WARP0;  // 0..15
+    const int g = e >> 3;            // row group
+    const int qd = warp & 3;         // TMEM lane quarter
+    const int mh = (e >> 2) & 1;     // M-half
+    const int jp = mh * 128 + qd * 32 + lane;  // output j'
+    const bool warp_ok = mh * 128 + qd * 32 < MB;
+    const bool lane_ok = jp < MB;
+    const bool odd = (lane & 1) != 0;
+    const uint32_t t_lane = tmem_base + ((uint32_t)(qd * 32) << 16) + (uint32_t)(mh * P);
+    const float norm_f = (float)rsqrt((double)K);
+    const float c0 = (float)((double)clip * rsqrt((double)K) / 7.0);
+    const uint32_t sh_keep = odd ? 4u : 0u, sh_recv = odd ? 0u : 4u;
+    const uint32_t keep_mask = odd ? 0xF0F0F0F0u : 0x0F0F0F0Fu;
+    // byte (a, p = j'/2) at a * 86 + p; even lane writes a < 32, odd lane a >= 32
+    uint8_t* const qlane = q + (jp >> 1) + (int64_t)(odd ? 32 : 0) * (MB / 2);
+    for (int64_t it = g; it < nrows; it += NG) {
+      const int tb = (int)(it % TBUF), pb = (int)((it / NG) & 1);
+      const int64_t row = (int64_t)blockIdx.x + it * gridDim.x;
+      mbar_wait_sleep(&t_full[tb], (uint32_t)((it / TBUF) & 1));
+      tc_fence_after();
+      float2 v[32];
+      float amax = 0.f;
+      if (warp_ok) {
+        uint32_t r[2][32];
+        QR_TMEM_LD32(t_lane + (uint32_t)(tb * 2 * P), r[0]);
+        QR_TMEM_LD32(t_lane + (uint32_t)(tb * 2 * P + 32), r[1]);
+        tmem_ld_wait();
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          v[c] = make_float2(__uint_as_float(r[0][2 * c]), __uint_as_float(r[0][2 * c + 1]));
+          v[16 + c] = make_float2(__uint_as_float(r[1][2 * c]), __uint_as_float(r[1][2 * c + 1]));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&t_empty[tb]);
+      if (warp_ok) {
+#pragma unroll
+        for (int st = 1; st < 32; st <<= 1)  // a bits 1-5
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            if (!(c & st)) bfly(v[c], v[c + st]);
+        float am[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {  // a bit 0: within the register pair
+          v[c] = make_float2(v[c].x + v[c].y, v[c].x - v[c].y);
+          am[c & 3] = fmax_nan(am[c & 3], fmax_nan(fabsf(v[c].x), fabsf(v[c].y)));
+        }
+        amax = lane_ok ? fmax_nan(fmax_nan(am[0], am[1]), fmax_nan(am[2], am[3])) : 0.f;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) amax = fmax_nan(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      if (lane == 0) red[g][pb][e & 7] = amax;
+      bar_named(1 + g, 256);
+      amax = red[g][pb][0];
+#pragma unroll
+      for (int w = 1; w < 8; ++w) amax = fmax_nan(amax, red[g][pb][w]);
+      float sc = 1.f, inv = 0.f;
+      if (!isfinite(amax)) {
+        sc = __int_as_float(0x7fc00000);
+      } else if (amax != 0.f) {
+        sc = c0 * amax;
+        inv = __fdiv_rn(norm_f, sc);
+      }
+      if (e == (g << 3) && lane == 0) scale[row] = sc;
+      if (!warp_ok) continue;
+      if (inv == 0.f) {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) v[c] = make_float2(0.f, 0.f);
+      }
+      uint32_t out[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {  // codes of a = 4m..4m+3 (even lane keeps) / 32 + 4m.. (odd)
+        const uint32_t w0 = code_word(v[2 * m], v[2 * m + 1], inv);
+        const uint32_t w1 = code_word(v[16 + 2 * m], v[16 + 2 * m + 1], inv);
+        const uint32_t got = __shfl_xor_sync(0xffffffffu, odd ? w0 : w1, 1);
+        const uint32_t keep = odd ? w1 : w0;
+        out[m] = ((keep << sh_keep) & keep_mask) | ((got << sh_recv) & ~keep_mask);
+      }
+      if (lane_ok) {
+        uint8_t* const qr = qlane + row * ld_q;
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          uint8_t* dst = qr + (int64_t)(4 * m) * (MB / 2);
+          const uint32_t o = out[m];
+          dst[0] = (uint8_t)o;
+          dst[MB / 2] = (uint8_t)(o >> 8);
+          dst[MB] = (uint8_t)(o >> 16);
+          dst[3 * MB / 2] = (uint8_t)(o >> 24);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == MMA_WARP) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+}  // namespace hq172
+
+namespace {
+
+// H_172[j'][b] (rows j' = outputs), zero-padded to 256 x 192, as [M-half][atom][128 rows][128 B]
+// UMMA K-major SWIZZLE_128B images
+std::vector<uint16_t> a_image_172(const int8_t* h) {
+  std::vector<uint16_t> img(hq172::A_BYTES / 2, 0);
+  for (int m = 0; m < 256; ++m)
+    for (int k = 0; k < hq172::KP; ++k) {
+      int v = (m < 172 && k < 172) ? h[m * 172 + k] : 0;
+      const int mh = m >> 7, r = m & 127, kc = k / 64, c = (k % 64) / 8, within = k % 8;
+      const size_t off = (size_t)mh * 3 * 16384 + hq172::sw128_off(128, kc, r, c) + (size_t)within * 2;
+      img[off / 2] = v > 0 ? 0x3C00 : (v < 0 ? 0xBC00 : 0);
+    }
+  return img;
+}
+
+std::mutex g_mu172;
+void* g_img172[64];
+
+}  // namespace
+
+cudaError_t launch_hq_full172_tc(const void* x, int64_t M, int64_t ld_x, float clip, uint8_t* q, int64_t ld_q,
+                                 float* scale, cudaStream_t stream) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  void* img = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_mu172);
+    if (!g_img172[dev & 63]) {
+      const int8_t* h = base_hadamard_host(172);
+      if (!h) return cudaErrorInvalidValue;
+      auto host = a_image_172(h);
+      void* d = nullptr;
+      e = cudaMalloc(&d, host.size() * sizeof(uint16_t));
+      if (e != cudaSuccess) return e;
+      e = cudaMemcpy(d, host.data(), host.size() * sizeof(uint16_t), cudaMemcpyHostToDevice);
+      if (e != cudaSuccess) return e;
+      e = cudaFuncSetAttribute(hq172::hq_full172_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)hq172::SMEM);
+      if (e != cudaSuccess) return e;
+      g_img172[dev & 63] = d;
+    }
+    img = g_img172[dev & 63];
+  }
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)(M < nsm ? M : nsm);
+  hq172::hq_full172_tc_kernel<<<grid, hq172::NUM_THREADS, hq172::SMEM, stream>>>(
+      static_cast<const __half*>(x), M, ld_x, clip, q, ld_q, scale, static_cast<const uint4*>(img));
+  return cudaPeekAtLastError();
+}
+
+}  // namespace qr
