@@ -380,248 +380,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
 }  // namespace hqtc
 
-// ---------------------------------------------------------------------------------------------
-// Variant with H_8 (x) H_28 in the MMA (quarot_debug_hq_full_variant(3)): a = a_hi*8 + a_lo,
-// j = a_lo*28 + b (K = 224 = 7 SWIZZLE_64B atoms of 32), two M = 128 halves (224 real rows of
-// A = H_8 (x) H_28), N = 128 (a_hi).  Each epilogue thread then holds all 128 a_hi of its j' and
-// does H_128 in ONE pass (bits 1-6 packed, bit 0 within the register pair): no TMEM round trip
-// and no partner barrier, at twice the MMA work and a 112 KB constant A.
-namespace hqtc8 {
-using namespace hqtc;
-constexpr int J8 = 8 * MB;                   // 224
-constexpr int NA8 = P / 8;                   // 128
-constexpr int A8_BYTES = 2 * 7 * 128 * 64;   // [M-half][K atom][128 rows][64 B] = 112 KB
-constexpr int BOX8 = NA8 * 64;               // one 32-wide j box: 128 a_hi rows x 64 B = 8 KB
-constexpr int STAGE8 = 7 * BOX8;             // 56 KB per token row
-constexpr int STAGES8 = 2;
-constexpr int NUM_EPI8 = 8;
-constexpr int NUM_THREADS8 = (EPI_WARP0 + NUM_EPI8) * 32;  // 384
-constexpr size_t SMEM8 = 1024 + A8_BYTES + (size_t)STAGES8 * STAGE8 + 256;
-static_assert(SMEM8 <= 232448, "227 KB dynamic smem");
-constexpr uint32_t IDESC8 = (1u << 4) | ((uint32_t)(NA8 >> 3) << 17) | ((128u >> 4) << 24);
-
-// UMMA descriptor, K-major SWIZZLE_64B: 8-row x 64-byte atoms stacked at 512 B (SBO)
-QR_DEVICE uint64_t desc_sw64(uint32_t addr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((addr >> 4) & 0x3FFF);
-  d |= (uint64_t)1 << 16;
-  d |= (uint64_t)(512 >> 4) << 32;
-  d |= (uint64_t)1 << 46;
-  d |= (uint64_t)4 << 61;  // SWIZZLE_64B
-  return d;
-}
-
-__global__ void __launch_bounds__(NUM_THREADS8, 1)
-    hq_full28_tc8_kernel(const __grid_constant__ CUtensorMap tmX, int64_t M, float clip, uint8_t* __restrict__ q,
-                         int64_t ld_q, float* __restrict__ scale, const uint4* __restrict__ a_img) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + A8_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES8 * STAGE8);
-  uint64_t* empty = full + STAGES8;
-  uint64_t* t_full = empty + STAGES8;  // [2]
-  uint64_t* t_empty = t_full + 2;      // [2]
-  uint64_t* amax_done = t_empty + 2;   // [2]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(amax_done + 2);
-  __shared__ float red[2][NUM_EPI8];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  for (int i = threadIdx.x; i < A8_BYTES / 16; i += NUM_THREADS8) reinterpret_cast<uint4*>(sA)[i] = __ldg(a_img + i);
-  fence_proxy_async_smem();
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES8; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&t_full[b], 1);
-      mbar_init(&t_empty[b], NUM_EPI8);
-      mbar_init(&amax_done[b], NUM_EPI8);
-    }
-    fence_barrier_init();
-  }
-  if (warp == MMA_WARP) {
-    tmem_alloc(tmem_holder, TMEM_COLS);
-    tmem_relinquish();
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_holder;
-  const int64_t nrows = M > (int64_t)blockIdx.x ? (M - 1 - (int64_t)blockIdx.x) / gridDim.x + 1 : 0;
-
-  if (warp < EPI_WARP0) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");  // 128 x 72 + 256 x 216 = 384 x 168
-    if (warp == TMA_WARP) {
-      if (lane == 0) {
-        for (int64_t it = 0; it < nrows; ++it) {
-          const int s = (int)(it % STAGES8);
-          mbar_wait_sleep(&empty[s], (uint32_t)((it / STAGES8) & 1) ^ 1u);
-          expect_tx(&full[s], STAGE8);
-          const int row = (int)((int64_t)blockIdx.x + it * gridDim.x);
-          const uint32_t dst = smem_u32(sB + s * STAGE8);
-#pragma unroll
-          for (int t = 0; t < 7; ++t) tma_load_3d(dst + t * BOX8, &tmX, 32 * t, 0, row, &full[s]);
-        }
-      }
-    } else if (warp == MMA_WARP) {
-      const uint32_t sa = smem_u32(sA), sb = smem_u32(sB);
-      for (int64_t it = 0; it < nrows; ++it) {
-        const int s = (int)(it % STAGES8), buf = (int)(it & 1);
-        mbar_wait_sleep(&t_empty[buf], (uint32_t)((it >> 1) & 1) ^ 1u);
-        mbar_wait_sleep(&full[s], (uint32_t)((it / STAGES8) & 1));
-        tc_fence_after();
-        const uint64_t b_desc = desc_sw64(sb + (uint32_t)(s * STAGE8));
-        const uint32_t d0 = tmem_base + (uint32_t)(buf * 2 * NA8);
-        if (elect_one()) {
-#pragma unroll
-          for (int mh = 0; mh < 2; ++mh) {
-            const uint64_t a_desc = desc_sw64(sa + (uint32_t)(mh * 7 * 8192));
-#pragma unroll
-            for (int kk = 0; kk < J8 / 16; ++kk) {  // atom kk/2 (+8 KB), +32 B per K = 16
-              const uint64_t koff = (uint64_t)((kk >> 1) * (8192 >> 4) + 2 * (kk & 1));
-              mma_f16(d0 + (uint32_t)(mh * NA8), a_desc + koff, b_desc + koff, IDESC8, kk > 0 ? 1u : 0u);
-            }
-          }
-          mma_commit(&empty[s]);
-          mma_commit(&t_full[buf]);
-        }
-        __syncwarp();
-      }
-    }
-  } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 216;");
-    const int e = warp - EPI_WARP0;  // 0..7
-    const int qd = warp & 3;
-    const int mh = e >> 2;
-    const int jp = mh * 128 + qd * 32 + lane;  // output j'
-    const bool warp_ok = mh * 128 + qd * 32 < J8;
-    const bool odd = (lane & 1) != 0;
-    const uint32_t t_lane = tmem_base + ((uint32_t)(qd * 32) << 16) + (uint32_t)(mh * NA8);
-    const float norm_f = (float)rsqrt((double)K);
-    const float c0 = (float)((double)clip * rsqrt((double)K) / 7.0);
-    const uint32_t sh_keep = odd ? 4u : 0u, sh_recv = odd ? 0u : 4u;
-    const uint32_t keep_mask = odd ? 0xF0F0F0F0u : 0x0F0F0F0Fu;
-    // byte (a_hi, p = j'/2) at a_hi * 112 + p; even lane writes a_hi < 64, odd lane a_hi >= 64
-    uint8_t* const qlane = q + (jp >> 1) + (int64_t)(odd ? 64 : 0) * (J8 / 2);
-    // transform: H over the 128 a_hi columns (bits 1-6 packed, bit 0 within the pair), partial
-    // amax posted, values parked in TMEM until the row scale is known
-    auto transform = [&](int64_t it) {
-      const int buf = (int)(it & 1);
-      mbar_wait_sleep(&t_full[buf], (uint32_t)((it >> 1) & 1));
-      tc_fence_after();
-      const uint32_t tb = t_lane + (uint32_t)(buf * 2 * NA8);
-      float amax = 0.f;
-      if (warp_ok) {
-        uint32_t r[128];  // column c of the row buffer; pairs (2c', 2c' + 1) are fp32x2 operands
-        auto ld2 = [&](int c) { return make_float2(__uint_as_float(r[2 * c]), __uint_as_float(r[2 * c + 1])); };
-        auto st2 = [&](int c, float2 v) {
-          r[2 * c] = __float_as_uint(v.x);
-          r[2 * c + 1] = __float_as_uint(v.y);
-        };
-#pragma unroll
-        for (int i = 0; i < 4; ++i) QR_TMEM_LD32(tb + 32u * i, (r + 32 * i));
-        tmem_ld_wait();
-#pragma unroll
-        for (int st = 1; st < 64; st <<= 1)
-#pragma unroll
-          for (int c = 0; c < 64; ++c)
-            if (!(c & st)) {
-              float2 a = ld2(c), b = ld2(c + st);
-              bfly(a, b);
-              st2(c, a);
-              st2(c + st, b);
-            }
-        float am[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int c = 0; c < 64; ++c) {
-          const float2 t = ld2(c);
-          const float2 v = make_float2(t.x + t.y, t.x - t.y);
-          st2(c, v);
-          am[c & 3] = fmax_nan(am[c & 3], fmax_nan(fabsf(v.x), fabsf(v.y)));
-        }
-        amax = jp < J8 ? fmax_nan(fmax_nan(am[0], am[1]), fmax_nan(am[2], am[3])) : 0.f;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) QR_TMEM_ST32(tb + 32u * i, (r + 32 * i));
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) amax = fmax_nan(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-      if (lane == 0) red[buf][e] = amax;
-      tmem_st_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&amax_done[buf]);
-    };
-    auto quant = [&](int64_t it) {
-      const int buf = (int)(it & 1);
-      const int64_t row = (int64_t)blockIdx.x + it * gridDim.x;
-      mbar_wait_sleep(&amax_done[buf], (uint32_t)((it >> 1) & 1));
-      tc_fence_after();
-      const uint32_t tb = t_lane + (uint32_t)(buf * 2 * NA8);
-      uint32_t u[128];
-      if (warp_ok) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) QR_TMEM_LD32(tb + 32u * i, (u + 32 * i));
-      }
-      float amax = red[buf][0];
-#pragma unroll
-      for (int w = 1; w < NUM_EPI8; ++w) amax = fmax_nan(amax, red[buf][w]);
-      float sc = 1.f, inv = 0.f;
-      if (!isfinite(amax)) {
-        sc = __int_as_float(0x7fc00000);
-      } else if (amax != 0.f) {
-        sc = c0 * amax;
-        inv = __fdiv_rn(norm_f, sc);
-      }
-      if (e == 0 && lane == 0) scale[row] = sc;
-      if (warp_ok) tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&t_empty[buf]);
-      if (!warp_ok) return;
-      if (inv == 0.f) {
-#pragma unroll
-        for (int c = 0; c < 128; ++c) u[c] = 0u;
-      }
-      auto f2 = [&](int a) { return make_float2(__uint_as_float(u[a]), __uint_as_float(u[a + 1])); };
-      uint32_t out[16];
-#pragma unroll
-      for (int m = 0; m < 16; ++m) {  // a_hi = 4m..4m+3 (even lane keeps) / 64 + 4m.. (odd)
-        const uint32_t w0 = code_word(f2(4 * m), f2(4 * m + 2), inv);
-        const uint32_t w1 = code_word(f2(64 + 4 * m), f2(64 + 4 * m + 2), inv);
-        const uint32_t got = __shfl_xor_sync(0xffffffffu, odd ? w0 : w1, 1);
-        const uint32_t keep = odd ? w1 : w0;
-        out[m] = ((keep << sh_keep) & keep_mask) | ((got << sh_recv) & ~keep_mask);
-      }
-      if (jp < J8) {
-        uint8_t* const qr = qlane + row * ld_q;
-#pragma unroll
-        for (int m = 0; m < 16; ++m) {
-          uint8_t* dst = qr + (int64_t)(4 * m) * (J8 / 2);
-          const uint32_t o = out[m];
-          dst[0] = (uint8_t)o;
-          dst[J8 / 2] = (uint8_t)(o >> 8);
-          dst[J8] = (uint8_t)(o >> 16);
-          dst[3 * J8 / 2] = (uint8_t)(o >> 24);
-        }
-      }
-    };
-    if (nrows > 0) transform(0);
-    for (int64_t it = 0; it < nrows; ++it) {
-      if (it + 1 < nrows) transform(it + 1);
-      quant(it);
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == MMA_WARP) {
-    tc_fence_after();
-    tmem_dealloc(tmem_base, TMEM_COLS);
-  }
-}
-}  // namespace hqtc8
-
 namespace {
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn_hq() {
@@ -662,77 +420,12 @@ std::vector<uint16_t> a_image_28(const int8_t* h28) {
 std::mutex g_img_mu;
 void* g_img[64];
 
-// (H_8 (x) H_28)[j'][j] (j' = a'_lo*28 + b', j = a_lo*28 + b, 224 x 224), rows padded to 256, as
-// [M-half][K atom of 32][128 rows][64 B] UMMA K-major SWIZZLE_64B images (16-byte chunk c of row
-// r at chunk c ^ ((r >> 1) & 3))
-std::vector<uint16_t> a_image_28x8(const int8_t* h28) {
-  std::vector<uint16_t> img(hqtc8::A8_BYTES / 2, 0);
-  for (int m = 0; m < 256; ++m)
-    for (int k = 0; k < hqtc8::J8; ++k) {
-      int v = 0;
-      if (m < hqtc8::J8) {
-        const int alo_o = m / 28, bo = m % 28, alo_i = k / 28, bi = k % 28;
-        v = ((__builtin_popcount(alo_o & alo_i) & 1) ? -1 : 1) * h28[bo * 28 + bi];
-      }
-      const int mh = m >> 7, r = m & 127, ka = k / 32, kk = k % 32, c = kk / 8, within = kk % 8;
-      const size_t off = (size_t)(mh * 7 + ka) * 8192 + (size_t)(r / 8) * 512 + (size_t)(r % 8) * 64 +
-                         (size_t)((c ^ ((r >> 1) & 3)) * 16) + (size_t)within * 2;
-      img[off / 2] = v > 0 ? 0x3C00 : (v < 0 ? 0xBC00 : 0);
-    }
-  return img;
-}
-void* g_img8[64];
-
 }  // namespace
-
-static cudaError_t launch_hq_full28_tc8(const void* x, int64_t M, int64_t ld_x, float clip, uint8_t* q, int64_t ld_q,
-                                       float* scale, cudaStream_t stream) {
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return e;
-  void* img = nullptr;
-  {
-    std::lock_guard<std::mutex> lk(g_img_mu);
-    if (!g_img8[dev & 63]) {
-      const int8_t* h28 = base_hadamard_host(28);
-      if (!h28) return cudaErrorInvalidValue;
-      auto host = a_image_28x8(h28);
-      void* d = nullptr;
-      e = cudaMalloc(&d, host.size() * sizeof(uint16_t));
-      if (e != cudaSuccess) return e;
-      e = cudaMemcpy(d, host.data(), host.size() * sizeof(uint16_t), cudaMemcpyHostToDevice);
-      if (e != cudaSuccess) return e;
-      e = cudaFuncSetAttribute(hqtc8::hq_full28_tc8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)hqtc8::SMEM8);
-      if (e != cudaSuccess) return e;
-      g_img8[dev & 63] = d;
-    }
-    img = g_img8[dev & 63];
-  }
-  auto fn = encode_fn_hq();
-  if (!fn) return cudaErrorInvalidValue;
-  CUtensorMap map;
-  cuuint64_t dims[3] = {(cuuint64_t)hqtc8::J8, (cuuint64_t)hqtc8::NA8, (cuuint64_t)M};
-  cuuint64_t strides[2] = {(cuuint64_t)hqtc8::J8 * 2, (cuuint64_t)ld_x * 2};
-  cuuint32_t box[3] = {32u, (cuuint32_t)hqtc8::NA8, 1u};
-  cuuint32_t estr[3] = {1u, 1u, 1u};
-  CUresult r = fn(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(x), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-  int nsm = 148;
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = (int)(M < nsm ? M : nsm);
-  hqtc8::hq_full28_tc8_kernel<<<grid, hqtc8::NUM_THREADS8, hqtc8::SMEM8, stream>>>(
-      map, M, clip, q, ld_q, scale, static_cast<const uint4*>(img));
-  return cudaPeekAtLastError();
-}
 
 int g_hq_full_variant = 0;  // debug: 1 = the mma.sync kernel (hq_full28_kernel), 2 = spinning epilogue waits
 
 cudaError_t launch_hq_full28_tc(const void* x, int64_t M, int64_t ld_x, float clip, uint8_t* q, int64_t ld_q,
                                 float* scale, cudaStream_t stream) {
-  if (g_hq_full_variant == 3) return launch_hq_full28_tc8(x, M, ld_x, clip, q, ld_q, scale, stream);
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
