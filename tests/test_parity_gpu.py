@@ -95,6 +95,31 @@ def test_hadamard_quant_strided_and_split_invariance(q):
         assert torch.equal(torch.cat([a1, a2]), xq) and torch.equal(torch.cat([s1, s2]), xs)
 
 
+@pytest.mark.parametrize("mode,K", [("full", 28672), ("full", 11008), ("across_heads", 8192), ("across_heads", 4096)])
+def test_hadamard_quant_tcgen05_paths(q, mode, K):
+    """The tcgen05 quantizers (FULL 1024x28 / 64x172, ACROSS_HEADS n_h 32/64) on what the small
+    parity cases do not reach: several rows per persistent CTA (the TMEM / smem rings wrap),
+    a leading dimension > K, row splits, and non-finite rows."""
+    M = 3 * 148 + 5
+    big = synth.activations(M, K + 64, "swiglu" if mode == "full" else "normal", seed=K, device=DEV)
+    big[7, 11] = float("nan")
+    big[300, 5] = float("inf")
+    x = big[:, :K]
+    xq, xs = q.hadamard_quant(x, mode)
+    xq2, xs2 = q.hadamard_quant(x.contiguous(), mode)
+    bits = lambda t: t.view(torch.int32)  # NaN scales compare bitwise
+    assert torch.equal(xq, xq2) and torch.equal(bits(xs), bits(xs2))
+    a1, s1 = q.hadamard_quant(x[:151], mode)
+    a2, s2 = q.hadamard_quant(x[151:], mode)
+    assert torch.equal(torch.cat([a1, a2]), xq) and torch.equal(bits(torch.cat([s1, s2])), bits(xs))
+    s = xs.cpu().numpy()
+    assert np.isnan(s[7]) and np.isnan(s[300]) and np.isfinite(np.delete(s, [7, 300])).all()
+    codes = P.unpack_signed(xq.cpu().numpy())
+    assert np.all(codes[7] == 0) and np.all(codes[300] == 0)
+    rows = [0, 1, 147, 148, 149, 296, 297, 444, 447, M - 1]  # CTA 0 rows 0..3, tail rows
+    _hq_compare(q, x.contiguous(), mode, rows=rows)
+
+
 def _rand_codes_packed(rows, k, seed):
     return synth.packed_weight_codes(rows, k, seed, device=DEV)
 
