@@ -65,21 +65,14 @@ QR_DEVICE void fwht_lanes(float (&v)[EPL], int sub) {
 template <int LPG>
 QR_DEVICE float group_min(float x) {
 #pragma unroll
-  for (int o = 1; o < LPG; o <<= 1) x = fminf(x, __shfl_xor_sync(0xffffffffu, x, o));
+  for (int o = 1; o < LPG; o <<= 1) x = fmin_nan(x, __shfl_xor_sync(0xffffffffu, x, o));
   return x;
 }
 template <int LPG>
 QR_DEVICE float group_max(float x) {
 #pragma unroll
-  for (int o = 1; o < LPG; o <<= 1) x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, o));
+  for (int o = 1; o < LPG; o <<= 1) x = fmax_nan(x, __shfl_xor_sync(0xffffffffu, x, o));
   return x;
-}
-template <int LPG>
-QR_DEVICE bool group_all(bool b) {
-  const unsigned m = __ballot_sync(0xffffffffu, b);
-  const int lane = threadIdx.x & 31;
-  const unsigned gm = ((1u << LPG) - 1u) << (lane & ~(LPG - 1));
-  return (m & gm) == gm;
 }
 
 // RoPE parameters of the fused variant (kRope): position = (pos0 + t) % seq_len; the cos/sin
@@ -174,17 +167,20 @@ __global__ void __launch_bounds__(256) kv_quant_kernel(const __half* __restrict_
       for (int j = 0; j < EPL; ++j) x[j] = y[j];
     }
     // ---- K / V: asymmetric 4-bit group quantization (Z14), scale / zero per group
-    float mn = x[0], mx = x[0];
-    bool finite = true;
+    // NaN-propagating min / max in four independent chains (a serial 32-deep chain put the
+    // reduction on the item's critical path); a NaN or +-Inf in the group makes mn or mx
+    // non-finite, which is the group's non-finite test
+    float mn4[4] = {x[0], x[1], x[2], x[3]}, mx4[4] = {x[0], x[1], x[2], x[3]};
 #pragma unroll
-    for (int j = 0; j < EPL; ++j) {
-      mn = fminf(mn, x[j]);
-      mx = fmaxf(mx, x[j]);
-      finite = finite && isfinite(x[j]);
+    for (int j = 4; j < EPL; ++j) {
+      mn4[j & 3] = fmin_nan(mn4[j & 3], x[j]);
+      mx4[j & 3] = fmax_nan(mx4[j & 3], x[j]);
     }
+    float mn = fmin_nan(fmin_nan(mn4[0], mn4[1]), fmin_nan(mn4[2], mn4[3]));
+    float mx = fmax_nan(fmax_nan(mx4[0], mx4[1]), fmax_nan(mx4[2], mx4[3]));
     mn = group_min<LPG>(mn);
     mx = group_max<LPG>(mx);
-    finite = group_all<LPG>(finite);
+    const bool finite = isfinite(mn) && isfinite(mx);
     if (!ok) return;
     if (!is_q) {
       const double norm = rot ? rnorm : 1.0;
