@@ -50,7 +50,7 @@ typedef enum {
   QUAROT_OK = 0,
   QUAROT_ERR_NULL = 1,             /* a required pointer is NULL                        */
   QUAROT_ERR_DIM = 2,              /* non-positive / inconsistent dimension, ld < width */
-  QUAROT_ERR_UNSUPPORTED_SIZE = 3, /* K not 2^n * m with m in {1, 28, 172}; heads not 2^n */
+  QUAROT_ERR_UNSUPPORTED_SIZE = 3, /* K not 2^n * m with m in {1, 20, 28, 108, 172}; heads not 2^n */
   QUAROT_ERR_ALIGN = 4,            /* pointer / leading dimension misaligned (16 B) or a
                                       width not a multiple of the kernel granularity    */
   QUAROT_ERR_ARG = 5,              /* clip ratio outside (0, 1], bad mode or flags       */
@@ -61,8 +61,8 @@ typedef enum {
   /* QKV / gate-up input: quantize only (the global rotation Q is fused into W). */
   QUAROT_HAD_NONE = 0,
   /* down_proj input: y = H^_K x, H^_K = (H_{2^n} (x) H_m) / sqrt(K), K = 2^n m,
-   * m in {1, 28, 172}.  Element i = a*m + b: H_m acts on the contiguous index b,
-   * H_{2^n} (Sylvester / natural order, Eq. 1) on a.  y_i = sum_j H^_ij x_j. */
+   * m in {1, 20, 28, 108, 172} (20 and 108 serve the Llama-2-13B widths).
+   * Element i = a*m + b: H_m acts on the contiguous index b, H_{2^n} (Sylvester / natural order, Eq. 1) on a.  y_i = sum_j H^_ij x_j. */
   QUAROT_HAD_FULL = 1,
   /* out_proj input, "Hadamard heads" (Eq. 9): y = (H_{n_h} (x) I_{d_h}) z / sqrt(n_h),
    * n_h = K / head_dim; n_h and head_dim powers of two. */
@@ -239,7 +239,7 @@ quarot_status quarot_swiglu(const void* gate_up, int64_t M, int64_t F, int64_t l
 /* Host-side utilities (no GPU work). */
 const char* quarot_status_string(int32_t status);
 int32_t quarot_abi_version(void);
-/* Copies the library's stored base Hadamard H_m (m in {28, 172}) as int8 +-1, row-major,
+/* Copies the library's stored base Hadamard H_m (m in {20, 28, 108, 172}) as int8 +-1, row-major,
  * into host buffer out[m*m].  Lets tests compare the library's independently built table
  * with the oracle's.  Returns QUAROT_ERR_UNSUPPORTED_SIZE for other m. */
 quarot_status quarot_base_hadamard(int32_t m, int8_t* out);

@@ -16,7 +16,7 @@ algorithms (FWHT butterflies, fused kernels) live only in the CUDA path.
 
 Readings: Z1 Sylvester/natural order; Z2 Kronecker order
 H_{2^n} (x) H_m exactly as P:67 writes it (index i = a*m + b, H_m acting on the
-contiguous b); Z3 the specific H_28 / H_172 instances below; Z4 y = H x (row i of
+contiguous b); Z3 the specific H_20 / H_28 / H_108 / H_172 instances below; Z4 y = H x (row i of
 H dotted with x); Z5 orthonormal scaling 1/sqrt(d).
 """
 from __future__ import annotations
@@ -80,6 +80,32 @@ def h28() -> np.ndarray:
     return h
 
 
+def _paley1(q: int) -> np.ndarray:
+    """Paley's first construction, q prime with q = 3 mod 4: Jacobsthal Q_ij = chi(j - i) is
+    antisymmetric; S = [[0, 1^T], [-1, Q]] (skew conference matrix of order q + 1); H = I + S."""
+    chi = _quadratic_character(q)
+    jac = np.array([[chi[(j - i) % q] for j in range(q)] for i in range(q)], dtype=np.int64)
+    s = np.zeros((q + 1, q + 1), dtype=np.int64)
+    s[0, 1:] = 1
+    s[1:, 0] = -1
+    s[1:, 1:] = jac
+    h = (np.eye(q + 1, dtype=np.int64) + s).astype(np.int64)
+    h.setflags(write=False)
+    return h
+
+
+@lru_cache(maxsize=None)
+def h20() -> np.ndarray:
+    """H_20 by Paley I with q = 19 (Llama-2-13B hidden 5120 = 256 x 20).  Not symmetric."""
+    return _paley1(19)
+
+
+@lru_cache(maxsize=None)
+def h108() -> np.ndarray:
+    """H_108 by Paley I with q = 107 (Llama-2-13B FFN 13824 = 128 x 108).  Not symmetric."""
+    return _paley1(107)
+
+
 # Williamson quadruple of order 43 from the cyclotomic classes of index 7 of GF(43),
 # generator 3.  Each of A, B, C, D is the symmetric circulant with first row
 # v[0] = a0 and v[j] = -1 iff j lies in the union of the classes selected by `mask`
@@ -113,15 +139,19 @@ def h172() -> np.ndarray:
     return h
 
 
-BASE_SIZES = (1, 28, 172)
+BASE_SIZES = (1, 20, 28, 108, 172)
 
 
 def base_matrix(m: int) -> np.ndarray:
     """The stored small Hadamard H_m, m in BASE_SIZES (int64 +-1)."""
     if m == 1:
         return np.ones((1, 1), dtype=np.int64)
+    if m == 20:
+        return h20()
     if m == 28:
         return h28()
+    if m == 108:
+        return h108()
     if m == 172:
         return h172()
     raise ValueError(f"no stored Hadamard matrix of order {m}; supported {BASE_SIZES}")

@@ -6,7 +6,7 @@
 //
 //   NONE          quantize only (QKV / gate-up inputs; global Q fused into W)
 //   ACROSS_HEADS  y = (H_{n_h} (x) I_{d_h}) z   ("Hadamard heads", Eq. 9)
-//   FULL          y = (H_{2^n} (x) H_m) x, m in {1, 28, 172}   (down_proj input)
+//   FULL          y = (H_{2^n} (x) H_m) x, m in {1, 20, 28, 108, 172}   (down_proj input)
 //
 // The orthonormal factor 1/sqrt(size) (reading Z5) is folded into the per-row scale: codes
 // are invariant to positive scaling of y, so the kernels transform unnormalized and scale
@@ -856,6 +856,11 @@ cudaError_t launch_hq_full(const void* x, int64_t M, int64_t K, int64_t ld_x, in
     if (e != cudaSuccess) return e;
     hq::hq_full_kernel<28><<<grid, threads, smem, stream>>>(xh, ld_x, pow2, clip, q, ld_q, scale,
                                                            device_bfrag_table(28));
+  } else if (m == 20 || m == 108) {  // Llama-2-13B widths: the smem kernel
+    auto kern = m == 20 ? hq::hq_full_kernel<20> : hq::hq_full_kernel<108>;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, threads, smem, stream>>>(xh, ld_x, pow2, clip, q, ld_q, scale, device_bfrag_table(m));
   } else if (m == 172 && pow2 == 64 && g_hq_full_variant != 1) {
     return launch_hq_full172_tc(x, M, ld_x, clip, q, ld_q, scale, stream);
   } else {

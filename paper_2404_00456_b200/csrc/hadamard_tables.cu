@@ -28,10 +28,14 @@ namespace {
 
 constexpr int KS28 = 2, NT28 = 4;     // pad 28 -> 32 (k), 32 (n)
 constexpr int KS172 = 11, NT172 = 22; // pad 172 -> 176
+constexpr int KS20 = 2, NT20 = 3;     // pad 20 -> 32 (k), 24 (n)
+constexpr int KS108 = 7, NT108 = 14;  // pad 108 -> 112
 
 __device__ uint32_t g_bfrag28[KS28 * NT28 * 64];
 __device__ uint32_t g_bfrag172[KS172 * NT172 * 64];
 __device__ uint32_t g_afrag28[2 * 2 * 32 * 4];
+__device__ uint32_t g_bfrag20[KS20 * NT20 * 64];
+__device__ uint32_t g_bfrag108[KS108 * NT108 * 64];
 
 std::vector<int8_t> build_h28() {
   const int q = 13;
@@ -54,6 +58,25 @@ std::vector<int8_t> build_h28() {
       for (int u = 0; u < 2; ++u)
         for (int v = 0; v < 2; ++v)
           h[(2 * i + u) * 28 + (2 * j + v)] = (int8_t)(S[i][j] * A[u][v] + (i == j ? B[u][v] : 0));
+  return h;
+}
+
+// Paley I (q prime, q = 3 mod 4): H = I + [[0, 1^T], [-1, Q]], Q_ij = chi(j - i) (antisymmetric)
+std::vector<int8_t> build_paley1(int q) {
+  std::vector<int> chi(q, -1);
+  chi[0] = 0;
+  for (int x = 1; x < q; ++x) chi[(x * x) % q] = 1;
+  const int n = q + 1;
+  std::vector<int8_t> h((size_t)n * n);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      int v;
+      if (i == 0 && j == 0) v = 0;
+      else if (i == 0) v = 1;
+      else if (j == 0) v = -1;
+      else v = chi[((j - 1) - (i - 1) + q) % q];
+      h[(size_t)i * n + j] = (int8_t)(v + (i == j ? 1 : 0));
+    }
   return h;
 }
 
@@ -98,8 +121,8 @@ bool is_hadamard(const std::vector<int8_t>& h, int m) {
 }
 
 struct Tables {
-  std::vector<int8_t> h28, h172;
-  bool ok28 = false, ok172 = false;
+  std::vector<int8_t> h28, h172, h20, h108;
+  bool ok28 = false, ok172 = false, ok20 = false, ok108 = false;
 };
 
 Tables& tables() {
@@ -110,6 +133,10 @@ Tables& tables() {
     t.h172 = build_h172();
     t.ok28 = is_hadamard(t.h28, 28);
     t.ok172 = is_hadamard(t.h172, 172);
+    t.h20 = build_paley1(19);
+    t.h108 = build_paley1(107);
+    t.ok20 = is_hadamard(t.h20, 20);
+    t.ok108 = is_hadamard(t.h108, 108);
   });
   return t;
 }
@@ -164,6 +191,8 @@ const int8_t* base_hadamard_host(int m) {
   Tables& t = tables();
   if (m == 28) return t.ok28 ? t.h28.data() : nullptr;
   if (m == 172) return t.ok172 ? t.h172.data() : nullptr;
+  if (m == 20) return t.ok20 ? t.h20.data() : nullptr;
+  if (m == 108) return t.ok108 ? t.h108.data() : nullptr;
   return nullptr;
 }
 
@@ -187,6 +216,16 @@ cudaError_t ensure_device_tables() {
     e = cudaMemcpyToSymbol(g_bfrag172, f.data(), f.size() * sizeof(uint32_t));
     if (e != cudaSuccess) return e;
   }
+  if (t.ok20) {
+    auto f = bfrag(t.h20, 20, KS20, NT20);
+    e = cudaMemcpyToSymbol(g_bfrag20, f.data(), f.size() * sizeof(uint32_t));
+    if (e != cudaSuccess) return e;
+  }
+  if (t.ok108) {
+    auto f = bfrag(t.h108, 108, KS108, NT108);
+    e = cudaMemcpyToSymbol(g_bfrag108, f.data(), f.size() * sizeof(uint32_t));
+    if (e != cudaSuccess) return e;
+  }
   g_dev_ready[dev & 63] = true;
   return cudaSuccess;
 }
@@ -201,6 +240,8 @@ const uint32_t* device_bfrag_table(int m) {
   void* p = nullptr;
   if (m == 28) cudaGetSymbolAddress(&p, g_bfrag28);
   else if (m == 172) cudaGetSymbolAddress(&p, g_bfrag172);
+  else if (m == 20) cudaGetSymbolAddress(&p, g_bfrag20);
+  else if (m == 108) cudaGetSymbolAddress(&p, g_bfrag108);
   return static_cast<const uint32_t*>(p);
 }
 

@@ -21,9 +21,9 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 bool pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
 bool clip_ok(float c) { return c > 0.f && c <= 1.f; }  // NaN fails both
 
-// K = 2^n * m with m in {1, 28, 172}; smallest admissible m (largest power of two).
+// K = 2^n * m with m in {1, 20, 28, 108, 172}; smallest admissible m (largest power of two).
 bool factorize(int64_t K, int64_t& p, int& m) {
-  const int cands[3] = {1, 28, 172};
+  const int cands[5] = {1, 20, 28, 108, 172};
   for (int c : cands) {
     if (K % c == 0 && pow2(K / c)) {
       p = K / c;
@@ -44,7 +44,7 @@ const char* quarot_status_string(int32_t s) {
     case QUAROT_ERR_NULL: return "null pointer argument";
     case QUAROT_ERR_DIM: return "dimension error (non-positive, odd, inconsistent or ld < width)";
     case QUAROT_ERR_UNSUPPORTED_SIZE:
-      return "unsupported size: FULL needs K = 2^n * m with m in {1, 28, 172} and 2^n >= 2; "
+      return "unsupported size: FULL needs K = 2^n * m with m in {1, 20, 28, 108, 172} and 2^n >= 2; "
              "ACROSS_HEADS needs K / head_dim and head_dim powers of two (head_dim >= 64); "
              "KV needs head_dim in {64, 128, 256}";
     case QUAROT_ERR_ALIGN: return "alignment error (16-byte pointers / leading dimensions, width granularity)";

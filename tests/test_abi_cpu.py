@@ -48,7 +48,7 @@ def test_abi_version_and_status_strings(q):
         assert q.lib().quarot_status_string(s)
 
 
-@pytest.mark.parametrize("m", [28, 172])
+@pytest.mark.parametrize("m", [20, 28, 108, 172])
 def test_library_tables_match_oracle(m):
     # two independent constructions of the same instance (reading Z3) must agree exactly
     from paper_2404_00456_b200 import quarot

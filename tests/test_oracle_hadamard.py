@@ -25,7 +25,7 @@ def test_h2_definition():
     assert np.allclose(had.hadamard(2) * math.sqrt(2), np.array(g["dense_times_sqrt2"]), atol=1e-15)
 
 
-@pytest.mark.parametrize("m", [28, 172])
+@pytest.mark.parametrize("m", [20, 28, 108, 172])
 def test_base_matrices_are_hadamard(m):
     # P1 / P:59: entries +-1 and H H^T = m I exactly (int64).
     h = had.base_matrix(m)
@@ -45,13 +45,18 @@ def test_base_checksums_recorded():
 
 
 def test_h28_symmetric_h172_not():
-    # Z4: orientation only matters for the non-symmetric H_172.
+    # Z4: orientation only matters for the non-symmetric H_172 (and the Paley I H_20 / H_108,
+    # which are I + skew: H + H^T = 2 I).
     assert np.array_equal(had.h28(), had.h28().T)
     assert not np.array_equal(had.h172(), had.h172().T)
+    for m in (20, 108):
+        h = had.base_matrix(m)
+        assert np.array_equal(h + h.T, 2 * np.eye(m, dtype=np.int64))
 
 
 @pytest.mark.parametrize("d,expect", [(256, (256, 1)), (4096, (4096, 1)), (8192, (8192, 1)),
-                                      (11008, (64, 172)), (28672, (1024, 28)), (128, (128, 1))])
+                                      (11008, (64, 172)), (28672, (1024, 28)), (128, (128, 1)),
+                                      (5120, (256, 20)), (13824, (128, 108))])
 def test_factorize_llama_sizes(d, expect):
     # d = 2^n m; Llama-2 FFN widths (BASELINE configs).
     assert had.factorize(d) == expect

@@ -57,7 +57,7 @@ def _hq_compare(q, x16: torch.Tensor, mode: str, head_dim: int = 128, clip=0.9, 
 @pytest.mark.parametrize("mode,K,hd", [
     ("none", 256, 128), ("none", 4096, 128), ("none", 8192, 128), ("none", 11008, 128),
     ("full", 256, 128), ("full", 448, 128), ("full", 688, 128), ("full", 4096, 128),
-    ("full", 11008, 128), ("full", 28672, 128),
+    ("full", 11008, 128), ("full", 28672, 128), ("full", 640, 128), ("full", 5120, 128), ("full", 13824, 128),
     ("across_heads", 512, 128), ("across_heads", 4096, 128), ("across_heads", 8192, 128),
     ("across_heads", 8192, 64),
 ])
