@@ -275,6 +275,8 @@ __global__ void __launch_bounds__(256) kv_quant_kernel(const __half* __restrict_
 
 }  // namespace kvq
 
+int g_kv_variant = 0;  // debug: 1 = the CUDA-core kernel for every shape
+
 cudaError_t launch_kv_quant(const void* k, int64_t ld_k, const void* v, int64_t ld_v, int64_t T, int n_kv,
                             int head_dim, void* q, int64_t ld_q, int n_q, uint32_t flags, float clip,
                             uint8_t* k_codes, float* k_scale, uint8_t* k_zero, uint8_t* v_codes, float* v_scale,
@@ -282,6 +284,9 @@ cudaError_t launch_kv_quant(const void* k, int64_t ld_k, const void* v, int64_t 
   const int nq = q ? n_q : 0;
   const int64_t groups = T * (2 * (int64_t)n_kv + nq);
   if (groups == 0) return cudaSuccess;
+  if (g_kv_variant == 0 && kv_tc_supported(n_kv, head_dim, nq, flags, nullptr))
+    return launch_kv_tc(k, ld_k, v, ld_v, T, n_kv, q, ld_q, nq, clip, false, 0, 1, 0.f, k_codes, k_scale, k_zero,
+                        v_codes, v_scale, v_zero, stream);
   const int threads = 256;
   const int lpg = head_dim / 32;
   const int64_t warps_needed = (groups + (32 / lpg) - 1) / (32 / lpg);
@@ -310,6 +315,9 @@ cudaError_t launch_kv_quant_rope(const void* k, int64_t ld_k, const void* v, int
   const int nq = q ? n_q : 0;
   const int G = 2 * n_kv + nq;
   if (T == 0 || G == 0) return cudaSuccess;
+  if (g_kv_variant == 0 && kv_tc_supported(n_kv, head_dim, nq, flags, positions))
+    return launch_kv_tc(k, ld_k, v, ld_v, T, n_kv, q, ld_q, nq, clip, true, pos0, seq_len, theta, k_codes, k_scale,
+                        k_zero, v_codes, v_scale, v_zero, stream);
   const int threads = 256;
   const int lpg = head_dim / 32;
   const int gpb = (threads / 32) * (32 / lpg);  // items one pass of the block covers
@@ -337,3 +345,5 @@ cudaError_t launch_kv_quant_rope(const void* k, int64_t ld_k, const void* v, int
 }
 
 }  // namespace qr
+
+extern "C" void quarot_debug_kv_variant(int v) { qr::g_kv_variant = v; }

@@ -1,0 +1,480 @@
+// kv_quant_tc.cu — rows a6 + a7 (KV-cache Init) with the per-head Hadamard on the
+// tcgen05 tensor path, for head_dim 128, n_kv in {4, 8, 16, 32, 64, 128}, n_q a multiple of
+// n_kv, K rotated and V not (flags = KV_ROTATE_K), optionally with RoPE fused in front (§8 f1).
+//
+// Per-head H_128 (Eqs. 13-14) on a head vector is a row times H^T; 128 head vectors
+// at once are one kind::f16 MMA: A = the rows (M = 128, K = d), B = H_128 (N = 128), D = fp32
+// in TMEM (lane = row, column = d').  The inputs are fp16 (post-RoPE rounded to fp16, reading
+// Z22), so the +-1 products are exact and the sums fp32, like the butterflies they replace.
+//  * Work = token blocks of B_t = 128 / n_kv tokens: n_q / n_kv Q tiles, one K tile and one V
+//    tile of 128 rows each (V goes through the MMA with B = I, exact, to share the epilogue).
+//  * A TMA warp loads each tile (3-D maps [token][head][d], two 64-wide d boxes) straight into
+//    the K-major SWIZZLE_128B operand layout, 3-stage ring.  With RoPE fused, eight warps rotate
+//    the Q / K rows in place in shared memory (two threads per row) from a per-block cos/sin table
+//    (fp64 sincos rounded to fp32, as quarot_rope) and round to fp16; otherwise they only hand
+//    the stage to the MMA.
+//  * Epilogue warps (thread = TMEM lane = row): Q rows scaled by 1/sqrt(128), rounded to fp16
+//    and written back in place; K / V rows quantized asymmetrically (clip 0.95, group = the
+//    row, reading Z14) entirely in-thread: min / max, scale / zero, 64 code bytes in four
+//    16-byte stores.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+#include "quarot_internal.h"
+
+namespace qr {
+namespace kvtc {
+
+constexpr int HD = 128;
+constexpr int TILE_BYTES = 128 * HD * 2;  // 32 KB: 128 rows x 128 fp16, two SW128 atoms
+constexpr int STAGES = 3;
+constexpr int NUM_EPI = 4, NUM_PROD = 8;  // two RoPE threads per tile row
+constexpr int EPI_WARP0 = 0, PROD_WARP0 = 4, MMA_WARP = 12, TMA_WARP = 13;
+constexpr int NUM_THREADS = 14 * 32;
+constexpr int TBUF = 4;
+constexpr uint32_t TMEM_COLS = 512;
+constexpr int MAX_BT = 32;                                 // tokens per block (n_kv >= 4)
+constexpr int TAB_BYTES = MAX_BT * (HD / 2) * 8;           // (cos, sin) per token and pair
+constexpr size_t SMEM = 1024 + 2 * TILE_BYTES + (size_t)STAGES * TILE_BYTES + TAB_BYTES + 512 + (HD / 2) * 8;
+static_assert(SMEM <= 232448, "227 KB dynamic smem");
+constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(HD >> 3) << 17) | ((128u >> 4) << 24);
+
+struct Args {
+  const __half* k;
+  int64_t ld_k;
+  const __half* v;
+  int64_t ld_v;
+  __half* q;
+  int64_t ld_q;
+  int64_t T;
+  int n_kv, n_q;
+  float clip;
+  uint8_t *k_codes, *k_zero, *v_codes, *v_zero;
+  float *k_scale, *v_scale;
+  int64_t pos0;
+  int seq_len;
+  float theta;
+};
+
+QR_DEVICE void mma_f16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(id), "r"(acc));
+}
+QR_DEVICE bool elect_one() {
+  uint32_t p;
+  asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\tselp.u32 %0, 1, 0, e;\n\t}" : "=r"(p));
+  return p != 0;
+}
+QR_DEVICE void tma_load_3d(uint32_t dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+QR_DEVICE void bar_named(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+QR_DEVICE uint32_t sw128(int row, int d) {  // byte offset of element d of tile row `row`
+  const int atom = d >> 6, chunk = (d & 63) >> 3;
+  return (uint32_t)(atom * 16384 + (row >> 3) * 1024 + (row & 7) * 128 + ((chunk ^ (row & 7)) << 4) + (d & 7) * 2);
+}
+
+// tile j of a token block: 0 .. nQ-1 = Q tiles, nQ = K tile, nQ + 1 = V tile
+struct TileInfo {
+  int type;  // 0 Q, 1 K, 2 V
+  int row0;  // first row within the block's rows of that type
+};
+QR_DEVICE TileInfo tile_info(int j, int nQ) {
+  if (j < nQ) return {0, j * 128};
+  return {j == nQ ? 1 : 2, 0};
+}
+
+template <bool kRope>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    kv_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                 const __grid_constant__ CUtensorMap tmV, const Args a, const uint4* __restrict__ b_img) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sB = smem;                   // [H_128 | I_128] K-major SW128 images
+  uint8_t* sA = sB + 2 * TILE_BYTES;    // [STAGES] tiles
+  float2* tab = reinterpret_cast<float2*>(sA + STAGES * TILE_BYTES);  // [B_t][64] (cos, sin)
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(tab) + TAB_BYTES);
+  uint64_t* a_empty = a_full + STAGES;
+  uint64_t* x_full = a_empty + STAGES;  // [STAGES] TMA landed
+  uint64_t* t_full = x_full + STAGES;
+  uint64_t* t_empty = t_full + TBUF;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(t_empty + TBUF);
+  double* inv_freq = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(a_full) + 512);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int BT = 128 / a.n_kv;          // tokens per block
+  const int nQ = a.n_q / a.n_kv;        // Q tiles per block
+  const int tpb = nQ + 2;               // tiles per block
+  const int64_t nblocks = (a.T + BT - 1) / BT;
+  const int64_t my_blocks = nblocks > (int64_t)blockIdx.x ? (nblocks - 1 - (int64_t)blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t ntiles = my_blocks * tpb;
+
+  for (int i = threadIdx.x; i < 2 * TILE_BYTES / 16; i += NUM_THREADS) reinterpret_cast<uint4*>(sB)[i] = __ldg(b_img + i);
+  if (kRope)
+    for (int i = threadIdx.x; i < HD / 2; i += NUM_THREADS) inv_freq[i] = pow((double)a.theta, -2.0 * (double)i / (double)HD);
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&a_full[s], NUM_PROD);
+      mbar_init(&a_empty[s], 1);
+      mbar_init(&x_full[s], 1);
+    }
+    for (int b = 0; b < TBUF; ++b) {
+      mbar_init(&t_full[b], 1);
+      mbar_init(&t_empty[b], NUM_EPI);
+    }
+    fence_barrier_init();
+  }
+  if (warp == MMA_WARP) {
+    tmem_alloc(tmem_holder, TMEM_COLS);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == TMA_WARP) {
+    // ---------------------------------------------------------------- TMA: tile -> operand layout
+    if (lane == 0) {
+      for (int64_t it = 0; it < ntiles; ++it) {
+        const int s = (int)(it % STAGES);
+        const int64_t bi = it / tpb;
+        const TileInfo ti = tile_info((int)(it % tpb), nQ);
+        const int nh = ti.type == 0 ? a.n_q : a.n_kv;
+        const int tok = (int)(((int64_t)blockIdx.x + bi * gridDim.x) * BT + ti.row0 / nh);
+        const CUtensorMap* map = ti.type == 0 ? &tmQ : (ti.type == 1 ? &tmK : &tmV);
+        mbar_wait_sleep(&a_empty[s], (uint32_t)((it / STAGES) & 1) ^ 1u);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&x_full[s])),
+                     "r"(TILE_BYTES)
+                     : "memory");
+        const uint32_t dst = smem_u32(sA + s * TILE_BYTES);
+        tma_load_3d(dst, map, 0, 0, tok, &x_full[s]);
+        tma_load_3d(dst + 16384, map, 64, 0, tok, &x_full[s]);
+      }
+    }
+  } else if (warp >= PROD_WARP0 && warp < PROD_WARP0 + NUM_PROD) {
+    // ---------------------------------------------------------------- RoPE in place (Q, K rows)
+    const int pt = (warp - PROD_WARP0) * 32 + lane;
+    const int r = pt & 127, half = pt >> 7;  // tile row; pairs (i, i + 64) with i in [32 half, 32 half + 32)
+    int64_t it = 0;
+    for (int64_t bi = 0; bi < my_blocks; ++bi) {
+      const int64_t t0 = ((int64_t)blockIdx.x + bi * gridDim.x) * BT;
+      if (kRope) {
+        bar_named(1, NUM_PROD * 32);  // every producer is done with the previous block's table
+        for (int i = pt; i < BT * (HD / 2); i += NUM_PROD * 32) {
+          const int tt = i / (HD / 2), ii = i - tt * (HD / 2);
+          const int64_t pos = (a.pos0 + t0 + tt) % a.seq_len;
+          double sn, cn;
+          sincos((double)pos * inv_freq[ii], &sn, &cn);  // == quarot_rope's table
+          tab[i] = make_float2((float)cn, (float)sn);
+        }
+        bar_named(1, NUM_PROD * 32);
+      }
+      for (int j = 0; j < tpb; ++j, ++it) {
+        const int s = (int)(it % STAGES);
+        const TileInfo ti = tile_info(j, nQ);
+        mbar_wait(&x_full[s], (uint32_t)((it / STAGES) & 1));
+        if (kRope && ti.type != 2) {
+          // RoPE rotate-half pairs (i, i + 64), rounded to fp16 (reading Z22)
+          const int nh = ti.type == 0 ? a.n_q : a.n_kv;
+          const int tl = (ti.row0 + r) / nh;  // token within the block
+          const float2* cs = tab + tl * (HD / 2);
+          const uint32_t row = smem_u32(sA + s * TILE_BYTES);
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            const int c = 4 * half + cc;
+            const uint32_t plo = row + sw128(r, 8 * c), phi = row + sw128(r, 64 + 8 * c);
+            uint4 lo4, hi4;
+            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(lo4.x), "=r"(lo4.y), "=r"(lo4.z), "=r"(lo4.w) : "r"(plo));
+            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(hi4.x), "=r"(hi4.y), "=r"(hi4.z), "=r"(hi4.w) : "r"(phi));
+            __half2* lo = reinterpret_cast<__half2*>(&lo4);
+            __half2* hi = reinterpret_cast<__half2*>(&hi4);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 x1 = __half22float2(lo[e]), x2 = __half22float2(hi[e]);
+              const float4 c2 = *reinterpret_cast<const float4*>(cs + 8 * c + 2 * e);  // pairs i, i + 1
+              lo[e] = __floats2half2_rn(rope_first(x1.x, x2.x, c2.x, c2.y), rope_first(x1.y, x2.y, c2.z, c2.w));
+              hi[e] = __floats2half2_rn(rope_second(x1.x, x2.x, c2.x, c2.y), rope_second(x1.y, x2.y, c2.z, c2.w));
+            }
+            sts_v4(plo, lo4);
+            sts_v4(phi, hi4);
+          }
+          fence_proxy_async_smem();
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&a_full[s]);
+      }
+    }
+  } else if (warp == MMA_WARP) {
+    // ---------------------------------------------------------------- MMA: D = rows x B^T
+    const uint32_t sa = smem_u32(sA), sb = smem_u32(sB);
+    for (int64_t it = 0; it < ntiles; ++it) {
+      const int s = (int)(it % STAGES), tb = (int)(it % TBUF);
+      const TileInfo ti = tile_info((int)(it % tpb), nQ);
+      mbar_wait(&t_empty[tb], (uint32_t)((it / TBUF) & 1) ^ 1u);
+      mbar_wait(&a_full[s], (uint32_t)((it / STAGES) & 1));
+      tc_fence_after();
+      const uint64_t a_desc = umma_desc_sw128(sa + (uint32_t)(s * TILE_BYTES));
+      const uint64_t b_desc = umma_desc_sw128(sb + (uint32_t)(ti.type == 2 ? TILE_BYTES : 0));
+      const uint32_t d_tmem = tmem_base + (uint32_t)(tb * HD);
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {  // atom kk/4 at +16 KB, +32 B per K = 16
+          const uint64_t koff = (uint64_t)((kk >> 2) * (16384 >> 4) + 2 * (kk & 3));
+          mma_f16(d_tmem, a_desc + koff, b_desc + koff, IDESC, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(&a_empty[s]);
+        mma_commit(&t_full[tb]);
+      }
+      __syncwarp();
+    }
+  } else if (warp < EPI_WARP0 + NUM_EPI) {
+    // ---------------------------------------------------------------- epilogue: thread = row
+    const int r = warp * 32 + lane;
+    const uint32_t t_lane = tmem_base + ((uint32_t)(warp * 32) << 16);
+    const double rnorm = rsqrt((double)HD);
+    const float rn = (float)rnorm;
+    for (int64_t it = 0; it < ntiles; ++it) {
+      const int tb = (int)(it % TBUF);
+      const int64_t bi = it / tpb;
+      const TileInfo ti = tile_info((int)(it % tpb), nQ);
+      const int64_t t0 = ((int64_t)blockIdx.x + bi * gridDim.x) * BT;
+      const int nh = ti.type == 0 ? a.n_q : a.n_kv;
+      const int rr = ti.row0 + r;
+      const int tl = rr / nh, h = rr - tl * nh;
+      const int64_t t = t0 + tl;
+      const bool ok = t < a.T;
+      mbar_wait_sleep(&t_full[tb], (uint32_t)((it / TBUF) & 1));
+      tc_fence_after();
+      const uint32_t tcol = t_lane + (uint32_t)(tb * HD);
+      // every lane runs the (warp-collective) TMEM loads; rows past T only skip their stores
+      uint32_t u[HD / 2];  // one 64-column half of the row at a time (register budget)
+      if (ti.type == 0) {  // Q: rotated in place, rounded to fp16 (Eq. 13)
+        uint4* dst = reinterpret_cast<uint4*>(a.q + t * a.ld_q + h * HD);
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          QR_TMEM_LD32(tcol + 64u * hf, u);
+          QR_TMEM_LD32(tcol + 64u * hf + 32u, (u + 32));
+          tmem_ld_wait();
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            uint4 w;
+            __half2* hw = reinterpret_cast<__half2*>(&w);
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              hw[e] = __floats2half2_rn(__uint_as_float(u[8 * c + 2 * e]) * rn, __uint_as_float(u[8 * c + 2 * e + 1]) * rn);
+            if (ok) dst[8 * hf + c] = w;
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&t_empty[tb]);
+        continue;
+      }
+      // K / V: asymmetric 4-bit quantization of the row (group = head_dim, reading Z14)
+      float mn4[4], mx4[4];
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        QR_TMEM_LD32(tcol + 64u * hf, u);
+        QR_TMEM_LD32(tcol + 64u * hf + 32u, (u + 32));
+        tmem_ld_wait();
+        if (hf == 0) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) mn4[j] = mx4[j] = __uint_as_float(u[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < HD / 2; ++j) {
+          mn4[j & 3] = fmin_nan(mn4[j & 3], __uint_as_float(u[j]));
+          mx4[j & 3] = fmax_nan(mx4[j & 3], __uint_as_float(u[j]));
+        }
+      }
+      const float mn = fmin_nan(fmin_nan(mn4[0], mn4[1]), fmin_nan(mn4[2], mn4[3]));
+      const float mx = fmax_nan(fmax_nan(mx4[0], mx4[1]), fmax_nan(mx4[2], mx4[3]));
+      const double norm = ti.type == 1 ? rnorm : 1.0;
+      const double lo = (double)a.clip * (double)fminf(mn, 0.f) * norm;
+      const double hi = (double)a.clip * (double)fmaxf(mx, 0.f) * norm;
+      float sc = 1.f, inv = 0.f;
+      int z = 0;
+      if (!(isfinite(mn) && isfinite(mx))) {
+        sc = __int_as_float(0x7fc00000);
+      } else if (hi != lo) {
+        sc = (float)((hi - lo) / 15.0);
+        const double zr = rint(-lo / (double)sc);
+        z = (int)(zr < 0.0 ? 0.0 : (zr > 15.0 ? 15.0 : zr));
+        inv = (float)(norm / (double)sc);
+      }
+      const int64_t gi = t * a.n_kv + h;
+      uint8_t* codes = (ti.type == 1 ? a.k_codes : a.v_codes) + gi * (HD / 2);
+      const float zf = (float)z;
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {  // the first half is reloaded (TMEM reads are cheap)
+        QR_TMEM_LD32(tcol + 64u * hf, u);
+        QR_TMEM_LD32(tcol + 64u * hf + 32u, (u + 32));
+        tmem_ld_wait();
+        uint32_t w[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) w[j] = 0u;
+        if (inv != 0.f) {
+#pragma unroll
+          for (int j = 0; j < HD / 2; j += 2) {
+            // rne(x * inv) + z == rne(x * inv + z) (z integral); clamp to [0, 15]; magic-add RNE
+            float2 m = f2fma(make_float2(__uint_as_float(u[j]), __uint_as_float(u[j + 1])), make_float2(inv, inv),
+                             make_float2(zf, zf));
+            m.x = fminf(fmaxf(m.x, 0.f), 15.f);
+            m.y = fminf(fmaxf(m.y, 0.f), 15.f);
+            m = f2add(m, make_float2(12582912.f, 12582912.f));
+            const uint32_t byte = (__float_as_uint(m.x) & 0xFu) | ((__float_as_uint(m.y) & 0xFu) << 4);
+            w[j >> 3] |= byte << (8 * ((j >> 1) & 3));
+          }
+        }
+        if (ok) {
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+            reinterpret_cast<uint4*>(codes)[2 * hf + c] = make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&t_empty[tb]);
+      if (ok) {
+        (ti.type == 1 ? a.k_scale : a.v_scale)[gi] = sc;
+        (ti.type == 1 ? a.k_zero : a.v_zero)[gi] = (uint8_t)z;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == MMA_WARP) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+}  // namespace kvtc
+
+namespace {
+
+// [H_128 | I_128] as K-major SWIZZLE_128B images (rows = output d', K = input d): two atoms of
+// 64 columns per matrix, 16-byte chunk c of row r at chunk c ^ (r & 7)
+std::vector<uint16_t> b_images() {
+  std::vector<uint16_t> img(2 * kvtc::TILE_BYTES / 2, 0);
+  for (int which = 0; which < 2; ++which)
+    for (int r = 0; r < kvtc::HD; ++r)
+      for (int k = 0; k < kvtc::HD; ++k) {
+        const int v = which == 0 ? ((__builtin_popcount(r & k) & 1) ? -1 : 1) : (r == k ? 1 : 0);
+        const int atom = k >> 6, chunk = (k & 63) >> 3;
+        const size_t off = (size_t)which * kvtc::TILE_BYTES + (size_t)atom * 16384 + (size_t)(r >> 3) * 1024 +
+                           (size_t)(r & 7) * 128 + (size_t)((chunk ^ (r & 7)) << 4) + (size_t)(k & 7) * 2;
+        img[off / 2] = v > 0 ? 0x3C00 : (v < 0 ? 0xBC00 : 0);
+      }
+  return img;
+}
+
+std::mutex g_mu;
+void* g_bimg[64];
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn_kv() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult res;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &res) == cudaSuccess &&
+        res == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+}  // namespace
+
+bool kv_tc_supported(int n_kv, int head_dim, int n_q, uint32_t flags, const int32_t* positions) {
+  auto p2 = [](int v) { return v > 0 && (v & (v - 1)) == 0; };
+  return head_dim == kvtc::HD && n_kv >= 4 && n_kv <= 128 && p2(n_kv) && (n_q == 0 || (p2(n_q) && n_q <= 128)) &&
+         n_q % n_kv == 0 && flags == 1u && positions == nullptr;
+}
+
+cudaError_t launch_kv_tc(const void* k, int64_t ld_k, const void* v, int64_t ld_v, int64_t T, int n_kv, void* q,
+                         int64_t ld_q, int n_q, float clip, bool rope, int64_t pos0, int seq_len, float theta,
+                         uint8_t* k_codes, float* k_scale, uint8_t* k_zero, uint8_t* v_codes, float* v_scale,
+                         uint8_t* v_zero, cudaStream_t stream) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  void* img = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g_bimg[dev & 63]) {
+      auto host = b_images();
+      void* d = nullptr;
+      e = cudaMalloc(&d, host.size() * sizeof(uint16_t));
+      if (e != cudaSuccess) return e;
+      e = cudaMemcpy(d, host.data(), host.size() * sizeof(uint16_t), cudaMemcpyHostToDevice);
+      if (e != cudaSuccess) return e;
+      for (auto kern : {kvtc::kv_tc_kernel<false>, kvtc::kv_tc_kernel<true>}) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kvtc::SMEM);
+        if (e != cudaSuccess) return e;
+      }
+      g_bimg[dev & 63] = d;
+    }
+    img = g_bimg[dev & 63];
+  }
+  kvtc::Args a;
+  a.k = static_cast<const __half*>(k);
+  a.ld_k = ld_k;
+  a.v = static_cast<const __half*>(v);
+  a.ld_v = ld_v;
+  a.q = static_cast<__half*>(q);
+  a.ld_q = ld_q;
+  a.T = T;
+  a.n_kv = n_kv;
+  a.n_q = q ? n_q : 0;
+  a.clip = clip;
+  a.k_codes = k_codes;
+  a.k_scale = k_scale;
+  a.k_zero = k_zero;
+  a.v_codes = v_codes;
+  a.v_scale = v_scale;
+  a.v_zero = v_zero;
+  a.pos0 = pos0;
+  a.seq_len = seq_len;
+  a.theta = theta;
+  auto fn = encode_fn_kv();
+  if (!fn) return cudaErrorInvalidValue;
+  // 3-D maps [token][head][d] (token stride ld, head stride 256 B), box {64 d, heads, tokens}
+  auto make = [&](CUtensorMap* m, const void* base, int nh, int64_t ld) -> bool {
+    const int nh_eff = nh > 0 ? nh : 1;
+    cuuint64_t dims[3] = {(cuuint64_t)kvtc::HD, (cuuint64_t)nh_eff, (cuuint64_t)T};
+    cuuint64_t strides[2] = {(cuuint64_t)kvtc::HD * 2, (cuuint64_t)(ld > 0 ? ld : kvtc::HD) * 2};
+    cuuint32_t box[3] = {64u, (cuuint32_t)nh_eff, (cuuint32_t)(128 / nh_eff)};
+    cuuint32_t estr[3] = {1u, 1u, 1u};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  };
+  CUtensorMap mq, mk, mv;
+  if (!make(&mk, k, n_kv, ld_k) || !make(&mv, v, n_kv, ld_v) || !make(&mq, q ? q : k, q ? n_q : n_kv, q ? ld_q : ld_k))
+    return cudaErrorInvalidValue;
+  const int BT = 128 / n_kv;
+  const int64_t nblocks = (T + BT - 1) / BT;
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)(nblocks < nsm ? nblocks : nsm);
+  if (grid == 0) return cudaSuccess;
+  auto kern = rope ? kvtc::kv_tc_kernel<true> : kvtc::kv_tc_kernel<false>;
+  kern<<<grid, kvtc::NUM_THREADS, kvtc::SMEM, stream>>>(mq, mk, mv, a, static_cast<const uint4*>(img));
+  return cudaPeekAtLastError();
+}
+
+}  // namespace qr

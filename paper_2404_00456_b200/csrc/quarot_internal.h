@@ -44,6 +44,14 @@ cudaError_t launch_kv_quant_rope(const void* k, int64_t ld_k, const void* v, int
                                  int64_t pos0, int seq_len, float theta, uint8_t* k_codes, float* k_scale,
                                  uint8_t* k_zero, uint8_t* v_codes, float* v_scale, uint8_t* v_zero,
                                  cudaStream_t stream, const int32_t* positions = nullptr, int64_t s_max = 0);
+// kv_quant_tc.cu: KV Init (± RoPE) on the tcgen05 path (head_dim 128, n_kv power of two >= 4,
+// n_q % n_kv == 0, K rotated / V not, no per-sequence positions)
+bool kv_tc_supported(int n_kv, int head_dim, int n_q, uint32_t flags, const int32_t* positions);
+cudaError_t launch_kv_tc(const void* k, int64_t ld_k, const void* v, int64_t ld_v, int64_t T, int n_kv, void* q,
+                         int64_t ld_q, int n_q, float clip, bool rope, int64_t pos0, int seq_len, float theta,
+                         uint8_t* k_codes, float* k_scale, uint8_t* k_zero, uint8_t* v_codes, float* v_scale,
+                         uint8_t* v_zero, cudaStream_t stream);
+extern int g_kv_variant;
 // A8W8: int8 per-token quantizer (mode NONE, optional RMSNorm) and the
 // int8 x int8 GEMM with the same epilogues
 cudaError_t launch_hq_none_q8(const void* x, int64_t M, int64_t K, int64_t ld_x, float clip, int8_t* q, int64_t ld_q,
