@@ -18,6 +18,7 @@
  *   quarot_kv_append        routine "Append": one new token per sequence into the cache
  *   quarot_kv_decode        routine "Decode": attention over the INT4 cache
  *   quarot_hadamard_quant8, quarot_int8_linear   A8W8 (8-bit RTN configuration)
+ *   quarot_hadamard_quant_group                  group-wise INT4 quantizer (§8 f3)
  *
  * Conventions (all entry points)
  *  - Tensor pointers are CUDA DEVICE pointers owned by the caller.  The library never
@@ -169,6 +170,21 @@ quarot_status quarot_kv_quant_rope(const void* k, int64_t ld_k, const void* v, i
                                    uint32_t flags, float clip_ratio, int64_t pos0, int32_t seq_len,
                                    float theta, uint8_t* k_codes, float* k_scale, uint8_t* k_zero,
                                    uint8_t* v_codes, float* v_scale, uint8_t* v_zero, void* stream);
+
+/* group-wise symmetric INT4 ("group-wise quantization", group size 128
+ * in tab:group_wise_ablation), mode NONE (the global rotation is fused into W).
+ * quarot_hadamard_quant_group: every run of `group` consecutive elements of a row is quantized
+ *   by the rule of quarot_hadamard_quant (scale = fp32(clip * max|x_g| / 7), codes RNE, clamp
+ *   [-7, 7]; zero group: scale 1, codes 0; non-finite group: scale NaN, codes 0).
+ *   x      fp16 [M][ld_x] device, K elements used per row
+ *   q      uint8 [M][ld_q] device, K/2 packed bytes (low nibble = even element)
+ *   scale  fp32 [M][ld_s] device, K/group scales per row (ld_s >= K/group)
+ *   group  64, 128 or 256 (QUAROT_ERR_UNSUPPORTED_SIZE otherwise); K % group == 0 (QUAROT_ERR_DIM)
+ * Errors as quarot_hadamard_quant; x and q 16-byte aligned, ld_x % 8 == 0, ld_q % 4 == 0.
+ * The group-wise GEMM is not built yet. */
+quarot_status quarot_hadamard_quant_group(const void* x, int64_t M, int64_t K, int64_t ld_x, int32_t group,
+                                         float clip_ratio, uint8_t* q, int64_t ld_q, float* scale, int64_t ld_s,
+                                         void* stream);
 
 /* A8W8 QuaRot ("lossless" 8-bit RTN, P:6, tab:rtn_results): the native
  * kind::i8 tensor path with no unpacking, the comparison point for the INT4 unpack cost.

@@ -54,3 +54,18 @@ def dequant_epilogue(acc: np.ndarray, x_scale: np.ndarray, w_scale: np.ndarray) 
     y = np.asarray(acc, dtype=np.float64) * np.asarray(x_scale, dtype=np.float64)[:, None] \
         * np.asarray(w_scale, dtype=np.float64)[None, :]
     return y.astype(np.float16)
+
+
+def group_linear(cx: np.ndarray, sx: np.ndarray, cw: np.ndarray, sw: np.ndarray) -> np.ndarray:
+    """Group-wise W4A4 linear: y[m, n] = fp16_RNE( sum_g sx[m, g] sw[n, g]
+    sum_{k in g} cx[m, k] cw[n, k] ), the per-group integer dot products exact (int64), the
+    scaled sum in fp64.  sx [M, K/G], sw [N, K/G]."""
+    cx = np.asarray(cx, dtype=np.int64)
+    cw = np.asarray(cw, dtype=np.int64)
+    ng = sx.shape[1]
+    g = cx.shape[1] // ng
+    y = np.zeros((cx.shape[0], cw.shape[0]), dtype=np.float64)
+    for j in range(ng):
+        acc = int_matmul(cx[:, j * g:(j + 1) * g], cw[:, j * g:(j + 1) * g]).astype(np.float64)
+        y += acc * np.asarray(sx[:, j], dtype=np.float64)[:, None] * np.asarray(sw[:, j], dtype=np.float64)[None, :]
+    return y.astype(np.float16)

@@ -61,6 +61,26 @@ def quantize_sym_rows(y: np.ndarray, clip_ratio: float = 0.9, qmax: int = QMAX_S
     return codes, scale
 
 
+def quantize_sym_groups(y: np.ndarray, group: int = 128, clip_ratio: float = 0.9, qmax: int = QMAX_SYM4):
+    """Group-wise symmetric RTN ("group-wise quantization ... group size
+    128"): every run of `group` consecutive elements of a row is quantized by the rule of
+    quantize_sym_rows with its own scale.  Returns (codes int64 [rows, K], scale float32
+    [rows, K / group])."""
+    y = np.asarray(y, dtype=np.float64)
+    rows, k = y.shape
+    if group <= 0 or k % group:
+        raise ValueError(f"group {group} must divide K = {k}")
+    codes, scale = quantize_sym_rows(y.reshape(rows * (k // group), group), clip_ratio, qmax)
+    return codes.reshape(rows, k), scale.reshape(rows, k // group)
+
+
+def dequantize_sym_groups(codes: np.ndarray, scale: np.ndarray) -> np.ndarray:
+    """x^ = c * s_g for the group g of each element."""
+    codes = np.asarray(codes, dtype=np.float64)
+    g = codes.shape[1] // scale.shape[1]
+    return codes * np.repeat(np.asarray(scale, dtype=np.float64), g, axis=1)
+
+
 def dequantize_sym_rows(codes: np.ndarray, scale: np.ndarray) -> np.ndarray:
     """x^ = c * s (P:233)."""
     return np.asarray(codes, dtype=np.float64) * np.asarray(scale, dtype=np.float64)[:, None]

@@ -133,6 +133,41 @@ __global__ void __launch_bounds__(128) hq_none_kernel(const __half* __restrict__
   }
 }
 
+// ------------------------------------------------------------------ NONE, group-wise (§8 f3)
+// Group-wise symmetric INT4 (group size 128): every run of G consecutive elements of a
+// row gets its own scale.  Thread = one 8-element chunk; a group is G/8 consecutive lanes
+// (8, 16 or 32), reduced with shuffles; scale [row][K/G].
+template <int LPG>  // lanes per group = G / 8
+__global__ void __launch_bounds__(128) hq_none_group_kernel(const __half* __restrict__ x, int64_t K, int64_t ld_x,
+                                                            float clip, uint8_t* __restrict__ q, int64_t ld_q,
+                                                            float* __restrict__ scale, int64_t ld_s) {
+  const int64_t row = blockIdx.y;
+  const int64_t c = (int64_t)blockIdx.x * 128 + threadIdx.x;  // chunk (all lanes of a group exist: K % G == 0)
+  const bool ok = c < (K >> 3);
+  uint4 v = make_uint4(0u, 0u, 0u, 0u);
+  if (ok) v = ldg_nc_v4(x + row * ld_x + c * 8);
+  const __half2* h = reinterpret_cast<const __half2*>(&v);
+  float f[8];
+  float am = 0.f;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 t = __half22float2(h[e]);
+    f[2 * e] = t.x;
+    f[2 * e + 1] = t.y;
+    am = fmax_nan(am, fmax_nan(fabsf(t.x), fabsf(t.y)));
+  }
+#pragma unroll
+  for (int o = 1; o < LPG; o <<= 1) am = fmax_nan(am, __shfl_xor_sync(0xffffffffu, am, o));
+  float s, inv;
+  row_scale(am, 1.0, clip, s, inv);
+  if (!ok) return;
+  if ((threadIdx.x & (LPG - 1)) == 0) scale[row * ld_s + c / LPG] = s;
+  uint32_t packed = 0;
+#pragma unroll
+  for (int e = 0; e < 8; e += 2) packed |= (nib(code_of(f[e], inv)) | (nib(code_of(f[e + 1], inv)) << 4)) << (4 * e);
+  *reinterpret_cast<uint32_t*>(q + row * ld_q + c * 4) = packed;
+}
+
 // ------------------------------------------------------------------ ACROSS_HEADS
 // Thread (p, g): column pair j = 2p, 2p+1 of head_dim (one float2), heads h = g*HPT + r.
 // Lane = g + G * p_lo: the FWHT over r runs in registers on fp32x2 pairs (FADD2), over g
@@ -741,6 +776,16 @@ cudaError_t launch_hq_none(const void* x, int64_t M, int64_t K, int64_t ld_x, fl
   else if (cpt <= 16) QR_NONE(16);
   else QR_NONE(32);
 #undef QR_NONE
+  return cudaPeekAtLastError();
+}
+
+cudaError_t launch_hq_none_group(const void* x, int64_t M, int64_t K, int64_t ld_x, int group, float clip,
+                                 uint8_t* q, int64_t ld_q, float* scale, int64_t ld_s, cudaStream_t stream) {
+  const dim3 grid((unsigned)((K / 8 + 127) / 128), (unsigned)M);
+  const __half* xh = static_cast<const __half*>(x);
+  if (group == 64) hq::hq_none_group_kernel<8><<<grid, 128, 0, stream>>>(xh, K, ld_x, clip, q, ld_q, scale, ld_s);
+  else if (group == 128) hq::hq_none_group_kernel<16><<<grid, 128, 0, stream>>>(xh, K, ld_x, clip, q, ld_q, scale, ld_s);
+  else hq::hq_none_group_kernel<32><<<grid, 128, 0, stream>>>(xh, K, ld_x, clip, q, ld_q, scale, ld_s);
   return cudaPeekAtLastError();
 }
 

@@ -214,6 +214,25 @@ quarot_status quarot_int4_matmul_s32(const uint8_t* xq, int64_t M, int64_t K, in
 }
 
 // ---- A8W8
+quarot_status quarot_hadamard_quant_group(const void* x, int64_t M, int64_t K, int64_t ld_x, int32_t group,
+                                         float clip_ratio, uint8_t* q, int64_t ld_q, float* scale, int64_t ld_s,
+                                         void* stream) {
+  g_last_launches = 0;
+  if (!clip_ok(clip_ratio)) return QUAROT_ERR_ARG;
+  if (!(group == 64 || group == 128 || group == 256)) return QUAROT_ERR_UNSUPPORTED_SIZE;
+  if (M < 0 || K <= 0 || K % 2 || ld_x < K || ld_q < K / 2 || ld_s < K / group) return QUAROT_ERR_DIM;
+  if (K % group) return QUAROT_ERR_DIM;
+  if (M > 0xffffLL * 1024) return QUAROT_ERR_DIM;
+  if (M == 0) return QUAROT_OK;
+  if (!x || !q || !scale) return QUAROT_ERR_NULL;
+  if (!aligned16(x) || !aligned16(q) || (ld_x % 8) || (ld_q % 4)) return QUAROT_ERR_ALIGN;
+  cudaError_t e = qr::launch_hq_none_group(x, M, K, ld_x, group, clip_ratio, q, ld_q, scale, ld_s,
+                                           static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e);
+  g_last_launches = 1;
+  return QUAROT_OK;
+}
+
 quarot_status quarot_hadamard_quant8(const void* x, int64_t M, int64_t K, int64_t ld_x, int32_t mode,
                                      int32_t head_dim, float clip_ratio, int8_t* q, int64_t ld_q, float* scale,
                                      void* stream) {

@@ -17,6 +17,9 @@ cudaError_t launch_int4_gemm_s32(const uint8_t* xq, int64_t M, int64_t K, int64_
                                  int64_t N, int64_t ld_wq, int32_t* acc, int64_t ld_acc, cudaStream_t stream);
 
 // hadamard_quant.cu
+// group-wise symmetric INT4, mode NONE: group in {64, 128, 256}, scale [M][K/group]
+cudaError_t launch_hq_none_group(const void* x, int64_t M, int64_t K, int64_t ld_x, int group, float clip,
+                                 uint8_t* q, int64_t ld_q, float* scale, int64_t ld_s, cudaStream_t stream);
 cudaError_t launch_hq_none(const void* x, int64_t M, int64_t K, int64_t ld_x, float clip, uint8_t* q,
                            int64_t ld_q, float* scale, cudaStream_t stream, bool rmsnorm = false);
 cudaError_t launch_hq_heads(const void* x, int64_t M, int64_t K, int64_t ld_x, int head_dim, float clip,

@@ -41,6 +41,7 @@ _SIGS = {
     "quarot_kv_decode": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_i64, _c_i32, _c_i32, _c_i32, _c_i64, _c_f32,
                          _vp, _vp, _c_i64, _vp],
     "quarot_kv_decode_workspace_bytes": [_c_i64, _c_i32, _c_i32, _c_i64],
+    "quarot_hadamard_quant_group": [_vp, _c_i64, _c_i64, _c_i64, _c_i32, _c_f32, _vp, _c_i64, _vp, _c_i64, _vp],
     "quarot_hadamard_quant8": [_vp, _c_i64, _c_i64, _c_i64, _c_i32, _c_i32, _c_f32, _vp, _c_i64, _vp, _vp],
     "quarot_int8_linear": [_vp, _vp, _c_i64, _c_i64, _c_i64, _vp, _vp, _c_i64, _c_i64, _vp, _c_i64, _vp],
     "quarot_int8_matmul_s32": [_vp, _c_i64, _c_i64, _c_i64, _vp, _c_i64, _c_i64, _vp, _c_i64, _vp],
@@ -257,6 +258,19 @@ def kv_quant(k: torch.Tensor, v: torch.Tensor, q: torch.Tensor | None = None, fl
         pos0, seq_len, theta = rope
         _check("quarot_kv_quant_rope", lib().quarot_kv_quant_rope(*head, int(pos0), int(seq_len), float(theta), *outs))
     return out
+
+
+def hadamard_quant_group(x: torch.Tensor, group: int = 128, clip_ratio: float = 0.9, q: torch.Tensor | None = None,
+                         scale: torch.Tensor | None = None, stream=None):
+    """quarot_hadamard_quant_group (§8 f3, mode NONE): packed INT4 [M, K/2] and fp32 scales [M, K/group]."""
+    M, K = x.shape
+    q = torch.empty(M, K // 2, dtype=torch.uint8, device=x.device) if q is None else q
+    scale = torch.empty(M, max(K // group, 1), dtype=torch.float32, device=x.device) if scale is None else scale
+    st = lib().quarot_hadamard_quant_group(_dev(x, "x", torch.float16), M, K, x.stride(0), group, clip_ratio,
+                                           _dev(q, "q", torch.uint8), q.stride(0), _dev(scale, "scale", torch.float32),
+                                           scale.stride(0), _stream(stream))
+    _check("quarot_hadamard_quant_group", st)
+    return q, scale
 
 
 def hadamard_quant8(x: torch.Tensor, clip_ratio: float = 0.9, rmsnorm: bool = False, q: torch.Tensor | None = None,

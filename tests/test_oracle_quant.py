@@ -246,3 +246,63 @@ def test_int8_matmul_exactness_bound():
     a = rng.integers(-127, 128, (5, 3000))
     b = rng.integers(-127, 128, (4, 3000))
     assert np.array_equal(gemm.int_matmul_exact_f64(a, b), a @ b.T)
+
+
+# ---------------------------------------------------------------------------- group-wise (§8 f3)
+
+def test_group_equal_to_row_when_group_is_k():
+    # a single group per row is exactly the per-token rule (special case)
+    rng = np.random.default_rng(5)
+    y = rng.standard_normal((6, 256))
+    c1, s1 = quant.quantize_sym_groups(y, 256)
+    c2, s2 = quant.quantize_sym_rows(y)
+    assert np.array_equal(c1, c2) and np.array_equal(s1[:, 0], s2)
+
+
+def test_group_brute_force_nearest_level_and_bound():
+    # P7 per group: every unclipped element's code is the nearest level of its own group's
+    # scale (ties to even), |y - c s_g| <= s_g / 2, and no group's scale exceeds the row scale
+    rng = np.random.default_rng(6)
+    y = rng.standard_normal((4, 64)) * np.repeat(rng.uniform(0.01, 10, (4, 4)), 16, axis=1)
+    y[1, 5] = 300.0  # one group with an outlier
+    codes, scale = quant.quantize_sym_groups(y, 16)
+    _, srow = quant.quantize_sym_rows(y)
+    assert np.all(scale <= srow[:, None] * (1 + 1e-7))
+    for r in range(4):
+        for k in range(64):
+            s = float(scale[r, k // 16])
+            levels = np.arange(-7, 8)
+            d = np.abs(y[r, k] - levels * s)
+            best = levels[d == d.min()]
+            c = codes[r, k]
+            if abs(y[r, k]) <= 7 * s:
+                assert c in best and (len(best) == 1 or c % 2 == 0)
+                assert abs(y[r, k] - c * s) <= s / 2 * (1 + 1e-12)
+            else:
+                assert c == np.sign(y[r, k]) * 7
+
+
+def test_group_zero_and_nonfinite_groups():
+    y = np.zeros((1, 32))
+    y[0, 20] = np.nan
+    codes, scale = quant.quantize_sym_groups(y, 16)
+    assert scale[0, 0] == 1.0 and np.isnan(scale[0, 1]) and not codes.any()
+
+
+def test_group_linear_reduces_and_brute_force():
+    from oracle import gemm as G
+    rng = np.random.default_rng(7)
+    cx = rng.integers(-7, 8, (3, 32))
+    cw = rng.integers(-7, 8, (5, 32))
+    sx = rng.uniform(0.1, 2, (3, 4)).astype(np.float32)
+    sw = rng.uniform(0.1, 2, (5, 4)).astype(np.float32)
+    y = G.group_linear(cx, sx, cw, sw)
+    ref = np.zeros((3, 5))
+    for m in range(3):  # triple loop by definition
+        for n in range(5):
+            for k in range(32):
+                ref[m, n] += float(cx[m, k]) * float(cw[n, k]) * float(sx[m, k // 8]) * float(sw[n, k // 8])
+    assert np.array_equal(y, ref.astype(np.float16))
+    # equal scales in every group reduce to the per-token / per-channel epilogue
+    y2 = G.group_linear(cx, np.repeat(sx[:, :1], 4, 1), cw, np.repeat(sw[:, :1], 4, 1))
+    assert np.array_equal(y2, G.dequant_epilogue(G.int_matmul(cx, cw), sx[:, 0], sw[:, 0]))

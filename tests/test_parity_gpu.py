@@ -249,3 +249,25 @@ def test_kv_quant_from_fused_qkv_views(q):
     assert P.max_fp16_ulp(qv.cpu().numpy(), ref["q_rot"]) <= 1
     # K and V regions of the fused buffer are untouched
     assert np.array_equal(kv_.cpu().numpy(), k_ref) and np.array_equal(vv.cpu().numpy(), v_ref)
+
+
+@pytest.mark.parametrize("K,group", [(8192, 128), (4096, 64), (11008, 256), (256, 128)])
+def test_hadamard_quant_group_parity(q, K, group):
+    """group-wise INT4 quantizer against the oracle (codes within one step on
+    <= 1e-4 of elements, scales 1e-5), with the adversarial rows and a non-finite group."""
+    if K % group:
+        pytest.skip("group must divide K")
+    M = 37
+    x = synth.activations(M, K, "outlier", seed=K + group, device=DEV)
+    x = torch.cat([x, torch.from_numpy(_adversarial_rows(K)).to(DEV)], 0).contiguous()
+    x[3, group + 1] = float("nan")
+    xq, xs = q.hadamard_quant_group(x, group)
+    torch.cuda.synchronize()
+    ref_c, ref_s = oquant.quantize_sym_groups(x.float().cpu().numpy().astype(np.float64), group)
+    got = P.unpack_signed(xq.cpu().numpy())
+    P.assert_codes(got, ref_c, f"group {group} K={K}")
+    s = xs.cpu().numpy()
+    assert np.isnan(s[3, 1]) and np.all(got[3, group:2 * group] == 0)
+    fin = np.isfinite(ref_s)
+    assert np.array_equal(fin, np.isfinite(s))
+    P.assert_scales(s[fin], ref_s[fin], f"group {group} K={K}")
