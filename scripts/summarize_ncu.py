@@ -14,7 +14,7 @@ from collections import defaultdict
 # launch order of runtime.DecoderLayerStep (fused SwiGLU, RoPE fused into the KV pass): the
 # library's kernels only
 CHAIN = ["hq_qkv", "gemm_qkv", "kv_quant", "hq_o", "gemm_o", "hq_gate_up", "gemm_gate_up", "hq_down", "gemm_down"]
-OURS = ("int4_gemm", "hq_", "kv_quant", "rope_kernel", "swiglu_kernel")
+OURS = ("int4_gemm", "hq_", "kv_quant", "kv_tc", "rope_kernel", "swiglu_kernel")
 
 
 def read_csv(path):
