@@ -80,6 +80,21 @@ def test_hadamard_quant_validation_without_gpu(q):
     assert _hq(q, mode=2, K=256, hd=32) == 3                           # head_dim < 64
 
 
+def _hqg(q, x=16, M=4, K=256, ld_x=256, group=128, clip=0.9, qp=32, ld_q=128, sp=48, ld_s=2):
+    return q.lib().quarot_hadamard_quant_group(x, M, K, ld_x, group, clip, qp, ld_q, sp, ld_s, None)
+
+
+def test_hadamard_quant_group_validation_without_gpu(q):
+    # quarot_hadamard_quant_group (§8 f3): every rejection happens before any CUDA call
+    assert _hqg(q, group=100) == 3 and _hqg(q, group=32) == 3           # ERR_UNSUPPORTED_SIZE
+    assert _hqg(q, K=192, ld_x=192, ld_q=96, group=128) == 2            # K % group
+    assert _hqg(q, ld_s=1) == 2 and _hqg(q, ld_x=100) == 2 and _hqg(q, M=-1) == 2  # ERR_DIM
+    assert _hqg(q, clip=0.0) == 5                                       # ERR_ARG
+    assert _hqg(q, M=0) == 0                                            # no-op
+    assert _hqg(q, x=None) == 1 and _hqg(q, sp=None) == 1               # ERR_NULL
+    assert _hqg(q, x=16 * 7 + 2) == 4                                   # misaligned pointer
+
+
 def _lin(q, M=128, K=256, N=256, ld_xq=128, ld_wq=128, ld_y=256, xp=16, wp=16, yp=16):
     return q.lib().quarot_int4_linear(xp, 16, M, K, ld_xq, wp, 16, N, ld_wq, yp, ld_y, None)
 
