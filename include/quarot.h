@@ -18,7 +18,7 @@
  *   quarot_kv_append        routine "Append": one new token per sequence into the cache
  *   quarot_kv_decode        routine "Decode": attention over the INT4 cache
  *   quarot_hadamard_quant8, quarot_int8_linear   A8W8 (8-bit RTN configuration)
- *   quarot_hadamard_quant_group                  group-wise INT4 quantizer (§8 f3)
+ *   quarot_hadamard_quant_group(8), quarot_int4_linear_group   group-wise W4A4 (§8 f3)
  *
  * Conventions (all entry points)
  *  - Tensor pointers are CUDA DEVICE pointers owned by the caller.  The library never
@@ -181,10 +181,26 @@ quarot_status quarot_kv_quant_rope(const void* k, int64_t ld_k, const void* v, i
  *   scale  fp32 [M][ld_s] device, K/group scales per row (ld_s >= K/group)
  *   group  64, 128 or 256 (QUAROT_ERR_UNSUPPORTED_SIZE otherwise); K % group == 0 (QUAROT_ERR_DIM)
  * Errors as quarot_hadamard_quant; x and q 16-byte aligned, ld_x % 8 == 0, ld_q % 4 == 0.
- * The group-wise GEMM is not built yet. */
+ * quarot_hadamard_quant_group8: the same codes, one per int8 byte (q int8 [M][ld_q], ld_q >= K,
+ *   ld_q % 8 == 0) — the operand format of quarot_int4_linear_group. */
 quarot_status quarot_hadamard_quant_group(const void* x, int64_t M, int64_t K, int64_t ld_x, int32_t group,
                                          float clip_ratio, uint8_t* q, int64_t ld_q, float* scale, int64_t ld_s,
                                          void* stream);
+quarot_status quarot_hadamard_quant_group8(const void* x, int64_t M, int64_t K, int64_t ld_x, int32_t group,
+                                          float clip_ratio, int8_t* q, int64_t ld_q, float* scale, int64_t ld_s,
+                                          void* stream);
+/* quarot_int4_linear_group: group-wise W4A4 linear (§8 f3), group 128:
+ *   y[m][n] = fp16( sum_g x_scale[m][g] * w_scale_t[g][n] * sum_{k in g} xq[m][k] * wq[n][k] ),
+ *   the per-group integer sums exact (int32 on the tensor cores), the scaled sum in fp32.
+ *   xq int8 [M][ld_xq] and wq int8 [N][ld_wq]: INT4 codes in [-7, 7], one per byte (the 4-bit
+ *   values take the native kind::i8 path); x_scale fp32 [M][ld_sx] (K/128 per row,
+ *   as quarot_hadamard_quant_group8 writes them); w_scale_t fp32 [K/128][ld_sw] (transposed,
+ *   prepared offline); y fp16 [M][ld_y].  K % 256 == 0, N % 8 == 0, ld_xq / ld_wq % 16 == 0,
+ *   ld_y % 8 == 0, 16-byte aligned xq / wq / y (QUAROT_ERR_ALIGN); group != 128:
+ *   QUAROT_ERR_UNSUPPORTED_SIZE. */
+quarot_status quarot_int4_linear_group(const int8_t* xq, const float* x_scale, int64_t ld_sx, int64_t M, int64_t K,
+                                       int64_t ld_xq, const int8_t* wq, const float* w_scale_t, int64_t ld_sw,
+                                       int64_t N, int64_t ld_wq, int32_t group, void* y, int64_t ld_y, void* stream);
 
 /* A8W8 QuaRot ("lossless" 8-bit RTN, P:6, tab:rtn_results): the native
  * kind::i8 tensor path with no unpacking, the comparison point for the INT4 unpack cost.

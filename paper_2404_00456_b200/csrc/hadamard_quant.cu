@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(128) hq_none_kernel(const __half* __restrict__
 // Group-wise symmetric INT4 (group size 128): every run of G consecutive elements of a
 // row gets its own scale.  Thread = one 8-element chunk; a group is G/8 consecutive lanes
 // (8, 16 or 32), reduced with shuffles; scale [row][K/G].
-template <int LPG>  // lanes per group = G / 8
+template <int LPG, bool kQ8 = false>  // lanes per group = G / 8; kQ8: int8 codes, one per byte
 __global__ void __launch_bounds__(128) hq_none_group_kernel(const __half* __restrict__ x, int64_t K, int64_t ld_x,
                                                             float clip, uint8_t* __restrict__ q, int64_t ld_q,
                                                             float* __restrict__ scale, int64_t ld_s) {
@@ -162,10 +162,17 @@ __global__ void __launch_bounds__(128) hq_none_group_kernel(const __half* __rest
   row_scale(am, 1.0, clip, s, inv);
   if (!ok) return;
   if ((threadIdx.x & (LPG - 1)) == 0) scale[row * ld_s + c / LPG] = s;
-  uint32_t packed = 0;
+  if constexpr (kQ8) {
+    uint32_t w[2] = {0u, 0u};
 #pragma unroll
-  for (int e = 0; e < 8; e += 2) packed |= (nib(code_of(f[e], inv)) | (nib(code_of(f[e + 1], inv)) << 4)) << (4 * e);
-  *reinterpret_cast<uint32_t*>(q + row * ld_q + c * 4) = packed;
+    for (int e = 0; e < 8; ++e) w[e >> 2] |= ((uint32_t)code_of(f[e], inv) & 0xFFu) << (8 * (e & 3));
+    *reinterpret_cast<uint2*>(q + row * ld_q + c * 8) = make_uint2(w[0], w[1]);
+  } else {
+    uint32_t packed = 0;
+#pragma unroll
+    for (int e = 0; e < 8; e += 2) packed |= (nib(code_of(f[e], inv)) | (nib(code_of(f[e + 1], inv)) << 4)) << (4 * e);
+    *reinterpret_cast<uint32_t*>(q + row * ld_q + c * 4) = packed;
+  }
 }
 
 // ------------------------------------------------------------------ ACROSS_HEADS
@@ -780,12 +787,18 @@ cudaError_t launch_hq_none(const void* x, int64_t M, int64_t K, int64_t ld_x, fl
 }
 
 cudaError_t launch_hq_none_group(const void* x, int64_t M, int64_t K, int64_t ld_x, int group, float clip,
-                                 uint8_t* q, int64_t ld_q, float* scale, int64_t ld_s, cudaStream_t stream) {
+                                 uint8_t* q, int64_t ld_q, float* scale, int64_t ld_s, cudaStream_t stream, bool q8) {
   const dim3 grid((unsigned)((K / 8 + 127) / 128), (unsigned)M);
   const __half* xh = static_cast<const __half*>(x);
-  if (group == 64) hq::hq_none_group_kernel<8><<<grid, 128, 0, stream>>>(xh, K, ld_x, clip, q, ld_q, scale, ld_s);
-  else if (group == 128) hq::hq_none_group_kernel<16><<<grid, 128, 0, stream>>>(xh, K, ld_x, clip, q, ld_q, scale, ld_s);
-  else hq::hq_none_group_kernel<32><<<grid, 128, 0, stream>>>(xh, K, ld_x, clip, q, ld_q, scale, ld_s);
+#define QR_G(L)                                                                                                \
+  do {                                                                                                         \
+    if (q8) hq::hq_none_group_kernel<L, true><<<grid, 128, 0, stream>>>(xh, K, ld_x, clip, q, ld_q, scale, ld_s); \
+    else hq::hq_none_group_kernel<L, false><<<grid, 128, 0, stream>>>(xh, K, ld_x, clip, q, ld_q, scale, ld_s);  \
+  } while (0)
+  if (group == 64) QR_G(8);
+  else if (group == 128) QR_G(16);
+  else QR_G(32);
+#undef QR_G
   return cudaPeekAtLastError();
 }
 

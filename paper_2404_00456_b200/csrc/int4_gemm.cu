@@ -696,6 +696,220 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(i8::NUM_THREADS, 1)
   }
 }
 
+
+// ============================================================================ group-wise (§8 f3)
+// W4A4 with one scale per 128-k group on both operands (tab:group_wise_ablation):
+//   y[m, n] = fp16( sum_g sx[m, g] sw[n, g] acc_g[m, n] ),  acc_g = sum_{k in g} cx cw (exact int32).
+// Codes are stored one per int8 byte (values in [-7, 7]), so both operands take the A8W8 TMA /
+// SS-MMA path unchanged; the MMA warp starts a fresh accumulator for every group (4 MMAs of
+// K = 32) in alternating TMEM buffers, and the epilogue folds each group into fp32 registers
+// (128 accumulators per thread) with the group's row scale and the tile's 256 column scales,
+// staged per group in smem from the transposed weight-scale layout [K/G][N] (coalesced).
+namespace gq {
+constexpr int G = 128;
+constexpr size_t SMEM_BYTES = i8::STAGES * i8::STAGE_BYTES + 1024 + 512 + 2 * BN * 4;
+static_assert(SMEM_BYTES <= 232448, "227 KB dynamic smem");
+}  // namespace gq
+
+struct GParams {
+  const float* x_scale;    // [M][ld_sx], K / G per row
+  const float* w_scale_t;  // [K / G][ld_sw]
+  __half* out;
+  int64_t M, N, K, ld_out, ld_sx, ld_sw;
+  int num_m, num_n, num_kb, num_tiles, group_m;
+};
+
+QR_DEVICE void gtile_coords(const GParams& p, int t, int& mb, int& nb) {
+  const int per_group = p.group_m * p.num_n;
+  const int group = t / per_group;
+  const int first_m = group * p.group_m;
+  const int gm = min(p.num_m - first_m, p.group_m);
+  const int within = t - group * per_group;
+  mb = first_m + within % gm;
+  nb = within / gm;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(i8::NUM_THREADS, 1)
+    int8_group_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                           const GParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + i8::STAGES * i8::STAGE_BYTES);
+  uint64_t* full = bars;
+  uint64_t* ready = full + i8::STAGES;
+  uint64_t* empty = ready + i8::STAGES;
+  uint64_t* t_full = empty + i8::STAGES;  // [2]
+  uint64_t* t_empty = t_full + 2;         // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(t_empty + 2);
+  float* ws_smem = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 512);  // [2][BN]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int pair = (int)blockIdx.x >> 1;
+  const int num_pairs = (int)gridDim.x >> 1;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < i8::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&ready[s], 2);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&t_full[b], 1);
+      mbar_init(&t_empty[b], 2 * NUM_EPI_WARPS);
+    }
+    fence_barrier_init();
+  }
+  if (warp == i8::MMA_WARP) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  const int my_tiles = (p.num_tiles > pair) ? (p.num_tiles - 1 - pair) / num_pairs + 1 : 0;
+  const int total = my_tiles * p.num_kb;
+  const int ngroups = (int)(p.K / gq::G);
+
+  if (warp >= NUM_EPI_WARPS) {
+    QR_SETMAXNREG_DEC(56);  // 128 x 56 + 256 x 224 = 384 x 168
+    if (warp == i8::TMA_WARP) {
+      if (lane == 0) {
+        for (int it = 0; it < total; ++it) {
+          const int tl = it / p.num_kb, kb = it - tl * p.num_kb;
+          int mb, nb;
+          gtile_coords(p, pair + tl * num_pairs, mb, nb);
+          const int s = it % i8::STAGES;
+          mbar_wait_sleep(&empty[s], ((it / i8::STAGES) & 1) ^ 1);
+          mbar_expect_tx(&full[s], i8::STAGE_BYTES);
+          const uint32_t dst = smem_u32(smem + s * i8::STAGE_BYTES);
+          const int ya = mb * BM + (int)rank * BMC, yb = nb * BN + (int)rank * BNC;
+          tma_load_2d(dst, &tmA, kb * BK, ya, &full[s]);
+          tma_load_2d(dst + BMC * 128, &tmA, kb * BK + 128, ya, &full[s]);
+          tma_load_2d(dst + i8::A_BYTES, &tmB, kb * BK, yb, &full[s]);
+          tma_load_2d(dst + i8::A_BYTES + BNC * 128, &tmB, kb * BK + 128, yb, &full[s]);
+        }
+      }
+    } else if (warp == i8::RELAY_WARP) {
+      if (lane == 0) {
+        const uint32_t ready_leader = map_to_rank(&ready[0], 0);
+        for (int it = 0; it < total; ++it) {
+          const int s = it % i8::STAGES;
+          mbar_wait(&full[s], (it / i8::STAGES) & 1);
+          mbar_arrive_cluster(ready_leader + (uint32_t)s * 8u);
+        }
+      }
+    } else if (warp == i8::MMA_WARP) {
+      if (rank == 0 && lane == 0) {
+        int it = 0, gc = 0;
+        for (int tl = 0; tl < my_tiles; ++tl) {
+          for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
+            const int s = it % i8::STAGES;
+            mbar_wait(&ready[s], (it / i8::STAGES) & 1);
+            tc_fence_after();
+            const uint32_t base = smem_u32(smem + s * i8::STAGE_BYTES);
+            const uint64_t a_desc = umma_desc_sw128(base), b_desc = umma_desc_sw128(base + i8::A_BYTES);
+#pragma unroll
+            for (int hg = 0; hg < BK / gq::G; ++hg, ++gc) {  // a fresh accumulator per 128-k group
+              const int ab = gc & 1;
+              mbar_wait(&t_empty[ab], ((gc >> 1) & 1) ^ 1);
+              tc_fence_after();
+              const uint32_t d_tmem = tmem_base + (uint32_t)(ab * BN);
+#pragma unroll
+              for (int k = 4 * hg; k < 4 * hg + 4; ++k) {  // atom k/4 at +16 KB, 32 bytes along K within it
+                const uint64_t off = (uint64_t)((k >> 2) * (BMC * 128 / 16) + 2 * (k & 3));
+                mma_i8_ss_2sm(d_tmem, a_desc + off, b_desc + off, IDESC, k != 4 * hg ? 1u : 0u);
+              }
+              mma_commit_pair(&t_full[ab]);
+            }
+            mma_commit_pair(&empty[s]);
+          }
+        }
+      }
+      __syncwarp();
+    }
+  } else {
+    QR_SETMAXNREG_INC(224);
+    const uint32_t tempty_leader = map_to_rank(&t_empty[0], 0);
+    const int quarter = warp & 3, chalf = warp >> 2;
+    const int row_in_tile = (int)rank * BMC + quarter * 32 + lane;
+    const int et = threadIdx.x;  // 0..255: the tile column whose scale this thread stages
+    int gc = 0;
+    for (int tl = 0; tl < my_tiles; ++tl) {
+      int mb, nb;
+      gtile_coords(p, pair + tl * num_pairs, mb, nb);
+      const int64_t m = (int64_t)mb * BM + row_in_tile;
+      const bool row_ok = m < p.M;
+      const int64_t n_st = (int64_t)nb * BN + et;
+      float2 acc[64];  // columns (2c, 2c + 1) of the thread's 128
+#pragma unroll
+      for (int c = 0; c < 64; ++c) acc[c] = make_float2(0.f, 0.f);
+      // the scales of group g + 1 are loaded while group g is folded (their L2 latency would
+      // otherwise sit on every group's critical path)
+      float ws_next = n_st < p.N ? __ldg(p.w_scale_t + n_st) : 0.f;
+      float sx_next = row_ok ? __ldg(p.x_scale + m * p.ld_sx) : 0.f;
+      for (int g = 0; g < ngroups; ++g, ++gc) {
+        const int ab = gc & 1;
+        ws_smem[ab * BN + et] = ws_next;
+        const float sx = sx_next;
+        if (g + 1 < ngroups) {
+          ws_next = n_st < p.N ? __ldg(p.w_scale_t + (int64_t)(g + 1) * p.ld_sw + n_st) : 0.f;
+          sx_next = row_ok ? __ldg(p.x_scale + m * p.ld_sx + g + 1) : 0.f;
+        }
+        epi_bar_sync();
+        mbar_wait(&t_full[ab], (gc >> 1) & 1);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(ab * BN) + (uint32_t)(chalf * 128);
+        const float* wsc = ws_smem + ab * BN + chalf * 128;
+        const float2 sx2 = make_float2(sx, sx), mg = make_float2(-12582912.f, -12582912.f);
+#pragma unroll
+        for (int cc = 0; cc < 4; cc += 2) {  // two 32-column chunks per TMEM round trip
+          uint32_t rc[2][32];
+          QR_TMEM_LD32(taddr + 32u * cc, rc[0]);
+          QR_TMEM_LD32(taddr + 32u * cc + 32u, rc[1]);
+          tmem_ld_wait();
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int c = 0; c < 32; c += 4) {
+              const float4 w4 = *reinterpret_cast<const float4*>(wsc + 32 * (cc + h) + c);
+              // int32 -> fp32 exactly by the 1.5 * 2^23 magic (|acc_g| <= 128 * 49 < 2^22): an
+              // integer add and a packed add instead of the quarter-rate I2F
+              const float2 d0 = f2add(make_float2(__int_as_float((int)rc[h][c] + 0x4B400000),
+                                                  __int_as_float((int)rc[h][c + 1] + 0x4B400000)), mg);
+              const float2 d1 = f2add(make_float2(__int_as_float((int)rc[h][c + 2] + 0x4B400000),
+                                                  __int_as_float((int)rc[h][c + 3] + 0x4B400000)), mg);
+              const int j = (32 * (cc + h) + c) >> 1;
+              acc[j] = f2fma(d0, f2mul(sx2, make_float2(w4.x, w4.y)), acc[j]);
+              acc[j + 1] = f2fma(d1, f2mul(sx2, make_float2(w4.z, w4.w)), acc[j + 1]);
+            }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty_leader + (uint32_t)ab * 8u);
+      }
+      if (row_ok) {
+        __half* dst = p.out + m * p.ld_out + (int64_t)nb * BN + chalf * 128;
+        const int64_t n0 = (int64_t)nb * BN + chalf * 128;
+#pragma unroll
+        for (int c = 0; c < 128; c += 8) {
+          if (n0 + c < p.N)
+            *reinterpret_cast<uint4*>(dst + c) =
+                make_uint4(pack_half2(acc[c / 2].x, acc[c / 2].y), pack_half2(acc[c / 2 + 1].x, acc[c / 2 + 1].y),
+                           pack_half2(acc[c / 2 + 2].x, acc[c / 2 + 2].y), pack_half2(acc[c / 2 + 3].x, acc[c / 2 + 3].y));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == i8::MMA_WARP) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+  }
+}
+
 }  // namespace gemm
 
 namespace {
@@ -876,6 +1090,50 @@ cudaError_t launch_int8_gemm(const int8_t* xq, const float* xs, int64_t M, int64
 cudaError_t launch_int8_gemm_s32(const int8_t* xq, int64_t M, int64_t K, int64_t ld_xq, const int8_t* wq, int64_t N,
                                  int64_t ld_wq, int32_t* acc, int64_t ld_acc, cudaStream_t stream) {
   return launch_i8_impl<true>(xq, nullptr, M, K, ld_xq, wq, nullptr, N, ld_wq, acc, ld_acc, stream, nullptr, 0);
+}
+
+
+cudaError_t launch_int8_group_gemm(const int8_t* xq, const float* xs, int64_t ld_sx, int64_t M, int64_t K,
+                                   int64_t ld_xq, const int8_t* wq, const float* ws_t, int64_t ld_sw, int64_t N,
+                                   int64_t ld_wq, void* y, int64_t ld_y, cudaStream_t stream) {
+  using namespace gemm;
+  static bool attr_set[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!attr_set[dev & 63]) {
+    cudaError_t e = cudaFuncSetAttribute(int8_group_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)gq::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set[dev & 63] = true;
+  }
+  CUtensorMap ma, mb;
+  if (!make_i8_map(&ma, reinterpret_cast<const uint8_t*>(xq), M, K, ld_xq) ||
+      !make_i8_map(&mb, reinterpret_cast<const uint8_t*>(wq), N, K, ld_wq))
+    return cudaErrorInvalidValue;
+  GParams p;
+  p.x_scale = xs;
+  p.w_scale_t = ws_t;
+  p.out = static_cast<__half*>(y);
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.ld_out = ld_y;
+  p.ld_sx = ld_sx;
+  p.ld_sw = ld_sw;
+  p.num_m = (int)((M + BM - 1) / BM);
+  p.num_n = (int)((N + BN - 1) / BN);
+  p.num_kb = (int)(K / BK);
+  p.num_tiles = p.num_m * p.num_n;
+  {
+    const int64_t a_tile_bytes = (int64_t)BM * K;
+    int g = (int)((64ll << 20) / (a_tile_bytes > 0 ? a_tile_bytes : 1));
+    g = g < 8 ? 8 : (g > 32 ? 32 : g);
+    p.group_m = g > p.num_m ? p.num_m : g;
+  }
+  const int max_pairs = num_sms_current() / 2;
+  const int pairs = p.num_tiles < max_pairs ? p.num_tiles : max_pairs;
+  int8_group_gemm_kernel<<<2 * pairs, i8::NUM_THREADS, gq::SMEM_BYTES, stream>>>(ma, mb, p);
+  return cudaPeekAtLastError();
 }
 
 // Debug / roofline probe (not in the public header): mode 1 = MMA issue only.

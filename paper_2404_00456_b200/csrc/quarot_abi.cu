@@ -214,20 +214,50 @@ quarot_status quarot_int4_matmul_s32(const uint8_t* xq, int64_t M, int64_t K, in
 }
 
 // ---- A8W8
-quarot_status quarot_hadamard_quant_group(const void* x, int64_t M, int64_t K, int64_t ld_x, int32_t group,
-                                         float clip_ratio, uint8_t* q, int64_t ld_q, float* scale, int64_t ld_s,
-                                         void* stream) {
+static quarot_status hq_group_impl(const void* x, int64_t M, int64_t K, int64_t ld_x, int32_t group, float clip_ratio,
+                                   uint8_t* q, int64_t ld_q, float* scale, int64_t ld_s, void* stream, bool q8) {
   g_last_launches = 0;
   if (!clip_ok(clip_ratio)) return QUAROT_ERR_ARG;
   if (!(group == 64 || group == 128 || group == 256)) return QUAROT_ERR_UNSUPPORTED_SIZE;
-  if (M < 0 || K <= 0 || K % 2 || ld_x < K || ld_q < K / 2 || ld_s < K / group) return QUAROT_ERR_DIM;
+  if (M < 0 || K <= 0 || K % 2 || ld_x < K || ld_q < (q8 ? K : K / 2) || ld_s < K / group) return QUAROT_ERR_DIM;
   if (K % group) return QUAROT_ERR_DIM;
   if (M > 0xffffLL * 1024) return QUAROT_ERR_DIM;
   if (M == 0) return QUAROT_OK;
   if (!x || !q || !scale) return QUAROT_ERR_NULL;
-  if (!aligned16(x) || !aligned16(q) || (ld_x % 8) || (ld_q % 4)) return QUAROT_ERR_ALIGN;
+  if (!aligned16(x) || !aligned16(q) || (ld_x % 8) || (ld_q % (q8 ? 8 : 4))) return QUAROT_ERR_ALIGN;
   cudaError_t e = qr::launch_hq_none_group(x, M, K, ld_x, group, clip_ratio, q, ld_q, scale, ld_s,
-                                           static_cast<cudaStream_t>(stream));
+                                           static_cast<cudaStream_t>(stream), q8);
+  if (e != cudaSuccess) return cuda_fail(e);
+  g_last_launches = 1;
+  return QUAROT_OK;
+}
+
+quarot_status quarot_hadamard_quant_group(const void* x, int64_t M, int64_t K, int64_t ld_x, int32_t group,
+                                         float clip_ratio, uint8_t* q, int64_t ld_q, float* scale, int64_t ld_s,
+                                         void* stream) {
+  return hq_group_impl(x, M, K, ld_x, group, clip_ratio, q, ld_q, scale, ld_s, stream, false);
+}
+
+quarot_status quarot_hadamard_quant_group8(const void* x, int64_t M, int64_t K, int64_t ld_x, int32_t group,
+                                          float clip_ratio, int8_t* q, int64_t ld_q, float* scale, int64_t ld_s,
+                                          void* stream) {
+  return hq_group_impl(x, M, K, ld_x, group, clip_ratio, reinterpret_cast<uint8_t*>(q), ld_q, scale, ld_s, stream,
+                       true);
+}
+
+quarot_status quarot_int4_linear_group(const int8_t* xq, const float* x_scale, int64_t ld_sx, int64_t M, int64_t K,
+                                       int64_t ld_xq, const int8_t* wq, const float* w_scale_t, int64_t ld_sw,
+                                       int64_t N, int64_t ld_wq, int32_t group, void* y, int64_t ld_y, void* stream) {
+  g_last_launches = 0;
+  if (group != 128) return QUAROT_ERR_UNSUPPORTED_SIZE;
+  if (M < 0 || N <= 0 || K <= 0 || ld_xq < K || ld_wq < K || ld_y < N || ld_sx < K / 128 || ld_sw < N)
+    return QUAROT_ERR_DIM;
+  if (M == 0) return QUAROT_OK;
+  if (!xq || !x_scale || !wq || !w_scale_t || !y) return QUAROT_ERR_NULL;
+  if (K % 256 || N % 8 || ld_xq % 16 || ld_wq % 16 || ld_y % 8 || !aligned16(xq) || !aligned16(wq) || !aligned16(y))
+    return QUAROT_ERR_ALIGN;
+  cudaError_t e = qr::launch_int8_group_gemm(xq, x_scale, ld_sx, M, K, ld_xq, wq, w_scale_t, ld_sw, N, ld_wq, y, ld_y,
+                                             static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e);
   g_last_launches = 1;
   return QUAROT_OK;

@@ -19,7 +19,13 @@ cudaError_t launch_int4_gemm_s32(const uint8_t* xq, int64_t M, int64_t K, int64_
 // hadamard_quant.cu
 // group-wise symmetric INT4, mode NONE: group in {64, 128, 256}, scale [M][K/group]
 cudaError_t launch_hq_none_group(const void* x, int64_t M, int64_t K, int64_t ld_x, int group, float clip,
-                                 uint8_t* q, int64_t ld_q, float* scale, int64_t ld_s, cudaStream_t stream);
+                                 uint8_t* q, int64_t ld_q, float* scale, int64_t ld_s, cudaStream_t stream,
+                                 bool q8 = false);
+// group-wise W4A4 GEMM (§8 f3): codes one per int8 byte, x scales [M][ld_sx], weight scales
+// transposed [K/128][ld_sw]; y fp16
+cudaError_t launch_int8_group_gemm(const int8_t* xq, const float* xs, int64_t ld_sx, int64_t M, int64_t K,
+                                   int64_t ld_xq, const int8_t* wq, const float* ws_t, int64_t ld_sw, int64_t N,
+                                   int64_t ld_wq, void* y, int64_t ld_y, cudaStream_t stream);
 cudaError_t launch_hq_none(const void* x, int64_t M, int64_t K, int64_t ld_x, float clip, uint8_t* q,
                            int64_t ld_q, float* scale, cudaStream_t stream, bool rmsnorm = false);
 cudaError_t launch_hq_heads(const void* x, int64_t M, int64_t K, int64_t ld_x, int head_dim, float clip,

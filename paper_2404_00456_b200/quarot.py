@@ -42,6 +42,9 @@ _SIGS = {
                          _vp, _vp, _c_i64, _vp],
     "quarot_kv_decode_workspace_bytes": [_c_i64, _c_i32, _c_i32, _c_i64],
     "quarot_hadamard_quant_group": [_vp, _c_i64, _c_i64, _c_i64, _c_i32, _c_f32, _vp, _c_i64, _vp, _c_i64, _vp],
+    "quarot_hadamard_quant_group8": [_vp, _c_i64, _c_i64, _c_i64, _c_i32, _c_f32, _vp, _c_i64, _vp, _c_i64, _vp],
+    "quarot_int4_linear_group": [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _vp, _vp, _c_i64, _c_i64, _c_i64, _c_i32,
+                                 _vp, _c_i64, _vp],
     "quarot_hadamard_quant8": [_vp, _c_i64, _c_i64, _c_i64, _c_i32, _c_i32, _c_f32, _vp, _c_i64, _vp, _vp],
     "quarot_int8_linear": [_vp, _vp, _c_i64, _c_i64, _c_i64, _vp, _vp, _c_i64, _c_i64, _vp, _c_i64, _vp],
     "quarot_int8_matmul_s32": [_vp, _c_i64, _c_i64, _c_i64, _vp, _c_i64, _c_i64, _vp, _c_i64, _vp],
@@ -271,6 +274,33 @@ def hadamard_quant_group(x: torch.Tensor, group: int = 128, clip_ratio: float = 
                                            scale.stride(0), _stream(stream))
     _check("quarot_hadamard_quant_group", st)
     return q, scale
+
+
+def hadamard_quant_group8(x: torch.Tensor, group: int = 128, clip_ratio: float = 0.9, stream=None):
+    """quarot_hadamard_quant_group8 (§8 f3): int8 codes [M, K] (one per byte) and fp32 scales [M, K/group]."""
+    M, K = x.shape
+    q = torch.empty(M, K, dtype=torch.int8, device=x.device)
+    scale = torch.empty(M, max(K // group, 1), dtype=torch.float32, device=x.device)
+    st = lib().quarot_hadamard_quant_group8(_dev(x, "x", torch.float16), M, K, x.stride(0), group, clip_ratio,
+                                            q.data_ptr(), q.stride(0), _dev(scale, "scale", torch.float32),
+                                            scale.stride(0), _stream(stream))
+    _check("quarot_hadamard_quant_group8", st)
+    return q, scale
+
+
+def int4_linear_group(xq: torch.Tensor, x_scale: torch.Tensor, wq: torch.Tensor, w_scale_t: torch.Tensor,
+                      y: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """quarot_int4_linear_group (§8 f3, group 128): int8-stored codes xq [M, K], wq [N, K];
+    x_scale [M, K/128]; w_scale_t [K/128, N]; y fp16 [M, N]."""
+    M, K = xq.shape
+    N = wq.shape[0]
+    y = torch.empty(M, N, dtype=torch.float16, device=xq.device) if y is None else y
+    st = lib().quarot_int4_linear_group(xq.data_ptr(), _dev(x_scale, "x_scale", torch.float32), x_scale.stride(0), M, K,
+                                        xq.stride(0), wq.data_ptr(), _dev(w_scale_t, "w_scale_t", torch.float32),
+                                        w_scale_t.stride(0), N, wq.stride(0), 128, _dev(y, "y", torch.float16),
+                                        y.stride(0), _stream(stream))
+    _check("quarot_int4_linear_group", st)
+    return y
 
 
 def hadamard_quant8(x: torch.Tensor, clip_ratio: float = 0.9, rmsnorm: bool = False, q: torch.Tensor | None = None,

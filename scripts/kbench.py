@@ -143,6 +143,21 @@ def main():
                             "frac_hbm": byts / ms_dec / 1e6 / 6536}
                 print(key, json.dumps(res[key]), flush=True)
                 del cache
+    if "gemm_group" in a.what:
+        # group-wise (G = 128) W4A4 GEMM, codes one per int8 byte; same shapes
+        xq_big = torch.randint(-7, 8, (M, 28672), dtype=torch.int8, device=dev)
+        for name, N, K in (("qkv", 10240, 8192), ("o", 8192, 8192), ("gate_up", 57344, 8192), ("down", 8192, 28672)):
+            xq = xq_big[:, :K]
+            wq = torch.randint(-7, 8, (N, K), dtype=torch.int8, device=dev)
+            xs = torch.rand(M, K // 128, device=dev) * 0.01 + 0.001
+            ws = torch.rand(K // 128, N, device=dev) * 0.01 + 0.001
+            y = torch.empty(M, N, dtype=torch.float16, device=dev)
+            ms = timeit(lambda: q.int4_linear_group(xq, xs, wq, ws, y=y), a.iters)
+            tops = 2 * M * N * K / ms / 1e9
+            res[f"gemm_group_{name}"] = {"ms": ms, "tops": tops, "frac_int8_2x_bf16_sustained": tops / 2765.6}
+            print("group", name, json.dumps(res[f"gemm_group_{name}"]), flush=True)
+            del wq, y
+        del xq_big
     if "gemm8" in a.what:
         # A8W8: the native kind::i8 path, same shapes as the W4A4 bench; the
         # difference to "gemm" is the cost of unpacking INT4 on B200

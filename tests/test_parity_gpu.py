@@ -271,3 +271,46 @@ def test_hadamard_quant_group_parity(q, K, group):
     fin = np.isfinite(ref_s)
     assert np.array_equal(fin, np.isfinite(s))
     P.assert_scales(s[fin], ref_s[fin], f"group {group} K={K}")
+
+
+@pytest.mark.parametrize("M,N,K", [(300, 520, 512), (128, 256, 256), (513, 1032, 1024), (64, 256, 4096)])
+def test_int4_linear_group_parity(q, M, N, K):
+    """group-wise W4A4 GEMM (group 128) against the oracle's group_linear on the
+    same codes and scales: fp16 outputs within 1e-2 relative Frobenius and 2 fp16 ulp."""
+    from oracle import gemm as og
+    rng = np.random.default_rng(M + N + K)
+    cx = rng.integers(-7, 8, (M, K)).astype(np.int8)
+    cw = rng.integers(-7, 8, (N, K)).astype(np.int8)
+    sx = rng.uniform(0.001, 0.02, (M, K // 128)).astype(np.float32)
+    sw = rng.uniform(0.001, 0.02, (N, K // 128)).astype(np.float32)
+    y = q.int4_linear_group(torch.from_numpy(cx).to(DEV), torch.from_numpy(sx).to(DEV),
+                            torch.from_numpy(cw).to(DEV), torch.from_numpy(sw.T.copy()).to(DEV))
+    torch.cuda.synchronize()
+    ref = og.group_linear(cx, sx, cw, sw)
+    got = y.cpu().numpy()
+    assert P.frob_rel(got, ref) <= 1e-2
+    ulp = np.abs(got.astype(np.float32) - ref.astype(np.float32)) / np.maximum(
+        np.abs(np.spacing(ref.astype(np.float16))).astype(np.float32), 1e-30)
+    assert np.quantile(ulp, 0.999) <= 2.0
+
+
+def test_group_pipeline_quant8_then_linear(q):
+    """quarot_hadamard_quant_group8 -> quarot_int4_linear_group against the oracle pipeline
+    (quantize_sym_groups on x, group_linear), and quant8 codes equal the packed quantizer's."""
+    from oracle import gemm as og
+    M, K, N = 200, 1024, 264
+    x = synth.activations(M, K, "outlier", seed=11, device=DEV)
+    xq8, xs = q.hadamard_quant_group8(x, 128)
+    xq4, xs4 = q.hadamard_quant_group(x, 128)
+    torch.cuda.synchronize()
+    assert np.array_equal(P.unpack_signed(xq4.cpu().numpy()), xq8.cpu().numpy().astype(np.int64))
+    assert torch.equal(xs, xs4)
+    rng = np.random.default_rng(12)
+    cw = rng.integers(-7, 8, (N, K)).astype(np.int8)
+    sw = rng.uniform(0.001, 0.02, (N, K // 128)).astype(np.float32)
+    y = q.int4_linear_group(xq8, xs, torch.from_numpy(cw).to(DEV), torch.from_numpy(sw.T.copy()).to(DEV))
+    torch.cuda.synchronize()
+    rc, rs = oquant.quantize_sym_groups(x.float().cpu().numpy().astype(np.float64), 128)
+    P.assert_codes(xq8.cpu().numpy().astype(np.int64), rc, "group8 codes")
+    ref = og.group_linear(rc, rs, cw, sw)
+    assert P.frob_rel(y.cpu().numpy(), ref) <= 1e-2
