@@ -196,7 +196,7 @@ quarot_status quarot_hadamard_quant_group8(const void* x, int64_t M, int64_t K, 
  *   values take the native kind::i8 path); x_scale fp32 [M][ld_sx] (K/128 per row,
  *   as quarot_hadamard_quant_group8 writes them); w_scale_t fp32 [K/128][ld_sw] (transposed,
  *   prepared offline); y fp16 [M][ld_y].  K % 256 == 0, N % 8 == 0, ld_xq / ld_wq % 16 == 0,
- *   ld_y % 8 == 0, 16-byte aligned xq / wq / y (QUAROT_ERR_ALIGN); group != 128:
+ *   ld_y % 8 == 0, ld_sw % 4 == 0, 16-byte aligned xq / wq / y / w_scale_t (QUAROT_ERR_ALIGN); group != 128:
  *   QUAROT_ERR_UNSUPPORTED_SIZE. */
 quarot_status quarot_int4_linear_group(const int8_t* xq, const float* x_scale, int64_t ld_sx, int64_t M, int64_t K,
                                        int64_t ld_xq, const int8_t* wq, const float* w_scale_t, int64_t ld_sw,

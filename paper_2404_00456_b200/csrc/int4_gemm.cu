@@ -707,7 +707,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(i8::NUM_THREADS, 1)
 // staged per group in smem from the transposed weight-scale layout [K/G][N] (coalesced).
 namespace gq {
 constexpr int G = 128;
-constexpr size_t SMEM_BYTES = i8::STAGES * i8::STAGE_BYTES + 1024 + 512 + 2 * BN * 4;
+constexpr size_t SMEM_BYTES = i8::STAGES * i8::STAGE_BYTES + 1024 + 512 + NUM_EPI_WARPS * 2 * 128 * 4;
 static_assert(SMEM_BYTES <= 232448, "227 KB dynamic smem");
 }  // namespace gq
 
@@ -741,7 +741,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(i8::NUM_THREADS, 1)
   uint64_t* t_full = empty + i8::STAGES;  // [2]
   uint64_t* t_empty = t_full + 2;         // [2]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(t_empty + 2);
-  float* ws_smem = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 512);  // [2][BN]
+  float* ws_smem = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 512);  // [warp][2][128]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
@@ -834,34 +834,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(i8::NUM_THREADS, 1)
     const uint32_t tempty_leader = map_to_rank(&t_empty[0], 0);
     const int quarter = warp & 3, chalf = warp >> 2;
     const int row_in_tile = (int)rank * BMC + quarter * 32 + lane;
-    const int et = threadIdx.x;  // 0..255: the tile column whose scale this thread stages
     int gc = 0;
     for (int tl = 0; tl < my_tiles; ++tl) {
       int mb, nb;
       gtile_coords(p, pair + tl * num_pairs, mb, nb);
       const int64_t m = (int64_t)mb * BM + row_in_tile;
       const bool row_ok = m < p.M;
-      const int64_t n_st = (int64_t)nb * BN + et;
       float2 acc[64];  // columns (2c, 2c + 1) of the thread's 128
 #pragma unroll
       for (int c = 0; c < 64; ++c) acc[c] = make_float2(0.f, 0.f);
       // the scales of group g + 1 are loaded while group g is folded (their L2 latency would
-      // otherwise sit on every group's critical path)
-      float ws_next = n_st < p.N ? __ldg(p.w_scale_t + n_st) : 0.f;
+      // otherwise sit on every group's critical path); each warp stages its own 128 column
+      // scales in a private smem slice (no block-wide barrier per group)
+      const int64_t n4 = (int64_t)nb * BN + chalf * 128 + 4 * lane;
+      auto ld_ws = [&](int g) {
+        return n4 < p.N ? __ldg(reinterpret_cast<const float4*>(p.w_scale_t + (int64_t)g * p.ld_sw + n4))
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+      };
+      float4 ws_next = ld_ws(0);
       float sx_next = row_ok ? __ldg(p.x_scale + m * p.ld_sx) : 0.f;
       for (int g = 0; g < ngroups; ++g, ++gc) {
         const int ab = gc & 1;
-        ws_smem[ab * BN + et] = ws_next;
+        float* wsw = ws_smem + (warp * 2 + ab) * 128;
+        reinterpret_cast<float4*>(wsw)[lane] = ws_next;
         const float sx = sx_next;
         if (g + 1 < ngroups) {
-          ws_next = n_st < p.N ? __ldg(p.w_scale_t + (int64_t)(g + 1) * p.ld_sw + n_st) : 0.f;
+          ws_next = ld_ws(g + 1);
           sx_next = row_ok ? __ldg(p.x_scale + m * p.ld_sx + g + 1) : 0.f;
         }
-        epi_bar_sync();
+        __syncwarp();
         mbar_wait(&t_full[ab], (gc >> 1) & 1);
         tc_fence_after();
         const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(ab * BN) + (uint32_t)(chalf * 128);
-        const float* wsc = ws_smem + ab * BN + chalf * 128;
+        const float* wsc = wsw;
         const float2 sx2 = make_float2(sx, sx), mg = make_float2(-12582912.f, -12582912.f);
 #pragma unroll
         for (int cc = 0; cc < 4; cc += 2) {  // two 32-column chunks per TMEM round trip

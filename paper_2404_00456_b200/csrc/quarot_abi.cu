@@ -254,7 +254,8 @@ quarot_status quarot_int4_linear_group(const int8_t* xq, const float* x_scale, i
     return QUAROT_ERR_DIM;
   if (M == 0) return QUAROT_OK;
   if (!xq || !x_scale || !wq || !w_scale_t || !y) return QUAROT_ERR_NULL;
-  if (K % 256 || N % 8 || ld_xq % 16 || ld_wq % 16 || ld_y % 8 || !aligned16(xq) || !aligned16(wq) || !aligned16(y))
+  if (K % 256 || N % 8 || ld_xq % 16 || ld_wq % 16 || ld_y % 8 || ld_sw % 4 || !aligned16(xq) || !aligned16(wq) ||
+      !aligned16(y) || !aligned16(w_scale_t))
     return QUAROT_ERR_ALIGN;
   cudaError_t e = qr::launch_int8_group_gemm(xq, x_scale, ld_sx, M, K, ld_xq, wq, w_scale_t, ld_sw, N, ld_wq, y, ld_y,
                                              static_cast<cudaStream_t>(stream));
