@@ -205,9 +205,11 @@ quarot_status quarot_int4_linear_group(const int8_t* xq, const float* x_scale, i
 /* A8W8 QuaRot ("lossless" 8-bit RTN, P:6, tab:rtn_results): the native
  * kind::i8 tensor path with no unpacking, the comparison point for the INT4 unpack cost.
  * quarot_hadamard_quant8: as quarot_hadamard_quant but codes are int8 in [-127, 127], one byte
- *   per element (q int8 [M][ld_q], ld_q >= K, % 8), scale = fp32(clip * amax / 127).  Only
- *   mode QUAROT_HAD_NONE (optionally | QUAROT_HAD_RMSNORM) is built; FULL / ACROSS_HEADS return
- *   QUAROT_ERR_UNSUPPORTED_SIZE.
+ *   per element (q int8 [M][ld_q], ld_q >= K, % 8), scale = fp32(clip * amax / 127).  Modes:
+ *   NONE (optionally | QUAROT_HAD_RMSNORM, any K <= 32768); FULL for K = 1024 x 28 (the 70B
+ *   down_proj input); ACROSS_HEADS for head_dim 128 and 16, 32 or 64 heads.  Other FULL /
+ *   ACROSS_HEADS widths return QUAROT_ERR_UNSUPPORTED_SIZE; RMSNORM with FULL / ACROSS_HEADS
+ *   returns QUAROT_ERR_ARG.
  * quarot_int8_linear: y[m,n] = fp16_rn(fp32(acc) * x_scale[m] * w_scale[n]),
  *   acc = sum_k xq[m,k] * wq[n,k] (int8 x int8 -> exact int32).  xq int8 [M][ld_xq], wq int8
  *   [N][ld_wq] (nn.Linear layout), ld % 16 == 0, K % 128 == 0, K <= 131072, N % 8 == 0.

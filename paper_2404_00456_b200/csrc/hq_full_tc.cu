@@ -110,7 +110,9 @@ QR_DEVICE uint32_t code_word(float2 a, float2 b, float inv) {
   return __byte_perm(lo, hi, 0x6420);
 }
 
-template <bool kSpin>  // epilogue waits: spin on try_wait (true) or with a suspend-time hint
+// kSpin: epilogue waits spin on try_wait (true) or with a suspend-time hint; kQ8: int8 codes in
+// [-127, 127], one byte per element (A8, §8 f4)
+template <bool kSpin, bool kQ8 = false>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     hq_full28_tc_kernel(const __grid_constant__ CUtensorMap tmX, int64_t M, float clip, uint8_t* __restrict__ q,
                         int64_t ld_q, float* __restrict__ scale, const uint4* __restrict__ a_img) {
@@ -212,7 +214,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const bool odd = (lane & 1) != 0;
     const uint32_t t_lane = tmem_base + ((uint32_t)(qd * 32) << 16);
     const float norm_f = (float)rsqrt((double)K);
-    const float c0 = (float)((double)clip * rsqrt((double)K) / 7.0);  // scale = c0 * amax (unnormalized)
+    const float c0 = (float)((double)clip * rsqrt((double)K) / (kQ8 ? 127.0 : 7.0));  // scale = c0 * amax
     // merged byte of j' = 2p (low nibble, even lane) and 2p + 1 (high nibble, odd lane)
     const uint32_t sh_keep = odd ? 4u : 0u, sh_recv = odd ? 0u : 4u;
     const uint32_t keep_mask = odd ? 0xF0F0F0F0u : 0x0F0F0F0Fu;
@@ -330,6 +332,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int c = 0; c < 16; ++c) u[i][c] = 0u;
       }
+      if constexpr (kQ8) {  // element (a_hi, j') at byte a_hi * 112 + j': a warp store covers 32 bytes
+        if (lane_ok) {
+          int8_t* const q8 = reinterpret_cast<int8_t*>(q) + row * ld_q + L;
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int c = 0; c < 16; c += 2) {
+              const float2 m = f2fma(make_float2(__uint_as_float(u[i][c]), __uint_as_float(u[i][c + 1])),
+                                     make_float2(inv, inv), make_float2(12582912.f, 12582912.f));
+              const uint32_t w = __vmaxs2(__vmins2(__byte_perm(__float_as_uint(m.x), __float_as_uint(m.y), 0x5410),
+                                                   0x007F007Fu), 0xFF81FF81u);
+              const int a = 64 * i + 16 * g + c;
+              q8[(int64_t)a * J] = (int8_t)(w & 0xFFu);
+              q8[(int64_t)(a + 1) * J] = (int8_t)((w >> 16) & 0xFFu);
+            }
+        }
+        return;
+      }
       uint32_t out[2][4];
 #pragma unroll
       for (int m = 0; m < 4; ++m) {  // codes of a_hi = 64 i + 16 g + 4m .. +3
@@ -425,7 +445,7 @@ void* g_img[64];
 int g_hq_full_variant = 0;  // debug: 1 = the mma.sync kernel (hq_full28_kernel), 2 = spinning epilogue waits
 
 cudaError_t launch_hq_full28_tc(const void* x, int64_t M, int64_t ld_x, float clip, uint8_t* q, int64_t ld_q,
-                                float* scale, cudaStream_t stream) {
+                                float* scale, cudaStream_t stream, bool q8) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -441,7 +461,8 @@ cudaError_t launch_hq_full28_tc(const void* x, int64_t M, int64_t ld_x, float cl
       if (e != cudaSuccess) return e;
       e = cudaMemcpy(d, host.data(), host.size() * sizeof(uint16_t), cudaMemcpyHostToDevice);
       if (e != cudaSuccess) return e;
-      for (auto kern : {hqtc::hq_full28_tc_kernel<false>, hqtc::hq_full28_tc_kernel<true>}) {
+      for (auto kern : {hqtc::hq_full28_tc_kernel<false>, hqtc::hq_full28_tc_kernel<true>,
+                        hqtc::hq_full28_tc_kernel<false, true>}) {
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hqtc::SMEM);
         if (e != cudaSuccess) return e;
       }
@@ -463,7 +484,8 @@ cudaError_t launch_hq_full28_tc(const void* x, int64_t M, int64_t ld_x, float cl
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)(M < nsm ? M : nsm);
-  auto kern = g_hq_full_variant == 2 ? hqtc::hq_full28_tc_kernel<true> : hqtc::hq_full28_tc_kernel<false>;
+  auto kern = q8 ? hqtc::hq_full28_tc_kernel<false, true>
+                 : (g_hq_full_variant == 2 ? hqtc::hq_full28_tc_kernel<true> : hqtc::hq_full28_tc_kernel<false>);
   kern<<<grid, hqtc::NUM_THREADS, hqtc::SMEM, stream>>>(
       map, M, clip, q, ld_q, scale, static_cast<const uint4*>(img));
   return cudaPeekAtLastError();

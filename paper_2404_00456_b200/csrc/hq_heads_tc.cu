@@ -84,7 +84,15 @@ QR_DEVICE uint32_t code_word(float2 a, float2 b, float inv) {
   return __byte_perm(lo, hi, 0x6420);
 }
 
-template <int NH>
+// 8-bit codes (A8, §8 f4) of a pair: clamp(RNE(v * inv), -127, 127) in the low bytes of two
+// 16-bit lanes
+QR_DEVICE uint32_t code_pair8(float a, float b, float inv) {
+  const float2 m = f2fma(make_float2(a, b), make_float2(inv, inv), make_float2(12582912.f, 12582912.f));
+  const uint32_t w = __byte_perm(__float_as_uint(m.x), __float_as_uint(m.y), 0x5410);
+  return __vmaxs2(__vmins2(w, 0x007F007Fu), 0xFF81FF81u);
+}
+
+template <int NH, bool kQ8 = false>  // kQ8: int8 codes in [-127, 127], one byte per element
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     hq_heads_tc_kernel(const __grid_constant__ CUtensorMap tmZ, int64_t M, float clip, uint8_t* __restrict__ q,
                        int64_t ld_q, float* __restrict__ scale, const uint4* __restrict__ b_img) {
@@ -171,7 +179,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const bool odd = (lane & 1) != 0;
     const uint32_t t_lane = tmem_base + ((uint32_t)(qd * 32) << 16);
     const float norm_f = (float)rsqrt((double)NH);
-    const float c0 = (float)((double)clip * rsqrt((double)NH) / 7.0);
+    const float c0 = (float)((double)clip * rsqrt((double)NH) / (kQ8 ? 127.0 : 7.0));
     const uint32_t sh_keep = odd ? 4u : 0u, sh_recv = odd ? 0u : 4u;
     const uint32_t keep_mask = odd ? 0xF0F0F0F0u : 0x0F0F0F0Fu;
     constexpr int HALF = NH / 2;  // even lane writes h' < HALF, odd lane h' >= HALF
@@ -214,6 +222,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (inv == 0.f) {
 #pragma unroll
         for (int c = 0; c < NH; ++c) u[c] = 0u;
+      }
+      if constexpr (kQ8) {  // element (h', d) at byte h' * 128 + d: each store covers 32 contiguous bytes
+        int8_t* const q8 = reinterpret_cast<int8_t*>(q) + row * ld_q + d;
+#pragma unroll
+        for (int c = 0; c < NH; c += 2) {
+          const uint32_t w = code_pair8(__uint_as_float(u[c]), __uint_as_float(u[c + 1]), inv);
+          q8[c * DH] = (int8_t)(w & 0xFFu);
+          q8[(c + 1) * DH] = (int8_t)((w >> 16) & 0xFFu);
+        }
+        continue;
       }
       uint32_t out[NH / 8];
 #pragma unroll
@@ -281,7 +299,7 @@ std::vector<uint16_t> b_image(int n) {
 std::mutex g_mu;
 void* g_img[64][3];  // n_h = 16, 32, 64
 
-template <int NH>
+template <int NH, bool kQ8>
 cudaError_t launch_nh(const void* x, int64_t M, int64_t ld_x, float clip, uint8_t* q, int64_t ld_q, float* scale,
                       cudaStream_t stream, int dev, void* img) {
   auto fn = encode_fn_heads();
@@ -297,16 +315,16 @@ cudaError_t launch_nh(const void* x, int64_t M, int64_t ld_x, float clip, uint8_
   if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
   static bool attr[64] = {};
   if (!attr[dev & 63]) {
-    cudaError_t e = cudaFuncSetAttribute(hqh::hq_heads_tc_kernel<NH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)hqh::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(hqh::hq_heads_tc_kernel<NH, kQ8>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hqh::SMEM);
     if (e != cudaSuccess) return e;
     attr[dev & 63] = true;
   }
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)(M < nsm ? M : nsm);
-  hqh::hq_heads_tc_kernel<NH><<<grid, hqh::NUM_THREADS, hqh::SMEM, stream>>>(map, M, clip, q, ld_q, scale,
-                                                                          static_cast<const uint4*>(img));
+  hqh::hq_heads_tc_kernel<NH, kQ8><<<grid, hqh::NUM_THREADS, hqh::SMEM, stream>>>(map, M, clip, q, ld_q, scale,
+                                                                               static_cast<const uint4*>(img));
   return cudaPeekAtLastError();
 }
 
@@ -318,7 +336,7 @@ bool hq_heads_tc_supported(int64_t K, int head_dim) {
 }
 
 cudaError_t launch_hq_heads_tc(const void* x, int64_t M, int64_t K, int64_t ld_x, int head_dim, float clip, uint8_t* q,
-                               int64_t ld_q, float* scale, cudaStream_t stream) {
+                               int64_t ld_q, float* scale, cudaStream_t stream, bool q8) {
   if (!hq_heads_tc_supported(K, head_dim)) return cudaErrorInvalidValue;
   const int nh = (int)(K / head_dim);
   const int slot = nh == 16 ? 0 : (nh == 32 ? 1 : 2);
@@ -339,9 +357,14 @@ cudaError_t launch_hq_heads_tc(const void* x, int64_t M, int64_t K, int64_t ld_x
     }
     img = g_img[dev & 63][slot];
   }
-  if (nh == 16) return launch_nh<16>(x, M, ld_x, clip, q, ld_q, scale, stream, dev, img);
-  if (nh == 32) return launch_nh<32>(x, M, ld_x, clip, q, ld_q, scale, stream, dev, img);
-  return launch_nh<64>(x, M, ld_x, clip, q, ld_q, scale, stream, dev, img);
+  if (q8) {
+    if (nh == 16) return launch_nh<16, true>(x, M, ld_x, clip, q, ld_q, scale, stream, dev, img);
+    if (nh == 32) return launch_nh<32, true>(x, M, ld_x, clip, q, ld_q, scale, stream, dev, img);
+    return launch_nh<64, true>(x, M, ld_x, clip, q, ld_q, scale, stream, dev, img);
+  }
+  if (nh == 16) return launch_nh<16, false>(x, M, ld_x, clip, q, ld_q, scale, stream, dev, img);
+  if (nh == 32) return launch_nh<32, false>(x, M, ld_x, clip, q, ld_q, scale, stream, dev, img);
+  return launch_nh<64, false>(x, M, ld_x, clip, q, ld_q, scale, stream, dev, img);
 }
 
 }  // namespace qr

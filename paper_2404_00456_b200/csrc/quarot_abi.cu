@@ -267,21 +267,35 @@ quarot_status quarot_int4_linear_group(const int8_t* xq, const float* x_scale, i
 quarot_status quarot_hadamard_quant8(const void* x, int64_t M, int64_t K, int64_t ld_x, int32_t mode,
                                      int32_t head_dim, float clip_ratio, int8_t* q, int64_t ld_q, float* scale,
                                      void* stream) {
-  (void)head_dim;
   g_last_launches = 0;
   const bool rms = (mode & QUAROT_HAD_RMSNORM) != 0;
   mode &= ~QUAROT_HAD_RMSNORM;
   if (mode < QUAROT_HAD_NONE || mode > QUAROT_HAD_ACROSS_HEADS) return QUAROT_ERR_ARG;
-  if (mode != QUAROT_HAD_NONE) return QUAROT_ERR_UNSUPPORTED_SIZE;  // 8-bit FULL / ACROSS_HEADS: not built
+  if (rms && mode != QUAROT_HAD_NONE) return QUAROT_ERR_ARG;
   if (!clip_ok(clip_ratio)) return QUAROT_ERR_ARG;
   if (M < 0 || K <= 0 || ld_x < K || ld_q < K) return QUAROT_ERR_DIM;
   if (M > 0x7fffffffLL) return QUAROT_ERR_DIM;
+  // 8-bit FULL / ACROSS_HEADS: the tcgen05 quantizers' widths (K = 1024 x 28; head_dim 128, n_h 16-64)
+  if (mode == QUAROT_HAD_FULL && K != 28672) return QUAROT_ERR_UNSUPPORTED_SIZE;
+  if (mode == QUAROT_HAD_ACROSS_HEADS && (head_dim <= 0 || K % head_dim || !qr::hq_heads_tc_supported(K, head_dim)))
+    return QUAROT_ERR_UNSUPPORTED_SIZE;
   if (M == 0) return QUAROT_OK;
   if (!x || !q || !scale) return QUAROT_ERR_NULL;
   if (!aligned16(x) || !aligned16(q) || (ld_x % 8) || (ld_q % 8) || (K % 16)) return QUAROT_ERR_ALIGN;
   if (K > 32768) return QUAROT_ERR_UNSUPPORTED_SIZE;
-  cudaError_t e = qr::launch_hq_none_q8(x, M, K, ld_x, clip_ratio, q, ld_q, scale, static_cast<cudaStream_t>(stream),
-                                        rms);
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  if (mode == QUAROT_HAD_NONE) {
+    e = qr::launch_hq_none_q8(x, M, K, ld_x, clip_ratio, q, ld_q, scale, st, rms);
+  } else {
+    e = qr::ensure_device_tables();
+    if (e == cudaSuccess) {
+      uint8_t* qb = reinterpret_cast<uint8_t*>(q);
+      e = mode == QUAROT_HAD_FULL ? qr::launch_hq_full28_tc(x, M, ld_x, clip_ratio, qb, ld_q, scale, st, true)
+                                  : qr::launch_hq_heads_tc(x, M, K, ld_x, head_dim, clip_ratio, qb, ld_q, scale, st,
+                                                           true);
+    }
+  }
   if (e != cudaSuccess) return cuda_fail(e);
   g_last_launches = 1;
   return QUAROT_OK;

@@ -32,7 +32,7 @@ cudaError_t launch_hq_heads(const void* x, int64_t M, int64_t K, int64_t ld_x, i
                             uint8_t* q, int64_t ld_q, float* scale, cudaStream_t stream);
 // hq_full_tc.cu: K = 1024 x 28 on the tcgen05 path (the default for that width)
 cudaError_t launch_hq_full28_tc(const void* x, int64_t M, int64_t ld_x, float clip, uint8_t* q, int64_t ld_q,
-                                float* scale, cudaStream_t stream);
+                                float* scale, cudaStream_t stream, bool q8 = false);
 extern int g_hq_full_variant;
 // hq_full172_tc.cu: K = 64 x 172 on the tcgen05 path (the default for that width)
 cudaError_t launch_hq_full172_tc(const void* x, int64_t M, int64_t ld_x, float clip, uint8_t* q, int64_t ld_q,
@@ -40,7 +40,7 @@ cudaError_t launch_hq_full172_tc(const void* x, int64_t M, int64_t ld_x, float c
 // hq_heads_tc.cu: ACROSS_HEADS on the tcgen05 path (head_dim 128, n_h in {16, 32, 64})
 bool hq_heads_tc_supported(int64_t K, int head_dim);
 cudaError_t launch_hq_heads_tc(const void* x, int64_t M, int64_t K, int64_t ld_x, int head_dim, float clip, uint8_t* q,
-                               int64_t ld_q, float* scale, cudaStream_t stream);
+                               int64_t ld_q, float* scale, cudaStream_t stream, bool q8 = false);
 cudaError_t launch_hq_full(const void* x, int64_t M, int64_t K, int64_t ld_x, int pow2, int m, float clip,
                            uint8_t* q, int64_t ld_q, float* scale, cudaStream_t stream);
 

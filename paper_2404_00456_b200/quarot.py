@@ -304,15 +304,17 @@ def int4_linear_group(xq: torch.Tensor, x_scale: torch.Tensor, wq: torch.Tensor,
 
 
 def hadamard_quant8(x: torch.Tensor, clip_ratio: float = 0.9, rmsnorm: bool = False, q: torch.Tensor | None = None,
-                    scale: torch.Tensor | None = None, stream=None):
-    """quarot_hadamard_quant8 (A8W8, §8 f4; mode NONE): int8 codes [M, K] and fp32 scales [M]."""
+                    scale: torch.Tensor | None = None, stream=None, mode="none", head_dim: int = 128):
+    """quarot_hadamard_quant8 (A8W8, §8 f4): int8 codes [M, K] and fp32 scales [M]; mode NONE
+    (± RMSNorm), FULL (K = 28672) or ACROSS_HEADS (head_dim 128, 16-64 heads)."""
     M, K = x.shape
     if x.stride(1) != 1:
         raise ValueError("x rows must be contiguous")
     q = torch.empty(M, K, dtype=torch.int8, device=x.device) if q is None else q
     scale = torch.empty(M, dtype=torch.float32, device=x.device) if scale is None else scale
-    st = lib().quarot_hadamard_quant8(_dev(x, "x", torch.float16), M, K, x.stride(0), NONE | (RMSNORM if rmsnorm else 0),
-                                      128, clip_ratio, q.data_ptr(), q.stride(0), scale.data_ptr(), _stream(stream))
+    mode_i = MODES[mode] if isinstance(mode, str) else int(mode)
+    st = lib().quarot_hadamard_quant8(_dev(x, "x", torch.float16), M, K, x.stride(0), mode_i | (RMSNORM if rmsnorm else 0),
+                                      head_dim, clip_ratio, q.data_ptr(), q.stride(0), scale.data_ptr(), _stream(stream))
     _check("quarot_hadamard_quant8", st)
     return q, scale
 

@@ -37,11 +37,32 @@ def test_quant8_parity(q, K, rms):
     rc, rs = oquant.quantize_sym_rows(y, 0.9, qmax=127)
     P.assert_codes(xq.cpu().numpy().astype(np.int64), rc, "int8 codes")
     P.assert_scales(xs.cpu().numpy(), rs, "int8 scales")
-    with pytest.raises(q.QuarotError):  # only mode NONE is built in 8 bits
+    with pytest.raises(q.QuarotError):  # 8-bit FULL exists only for K = 28672
         q.lib()
         st = q.lib().quarot_hadamard_quant8(x.data_ptr(), 67, K, K, q.FULL, 128, 0.9, xq.data_ptr(), K,
                                             xs.data_ptr(), None)
         q.quarot._check("quarot_hadamard_quant8", st)
+
+
+@pytest.mark.parametrize("mode,K", [("full", 28672), ("across_heads", 8192), ("across_heads", 4096)])
+def test_quant8_transform_parity(q, mode, K):
+    """8-bit FULL / ACROSS_HEADS quantizers (the tcgen05 transforms with qmax = 127) against the
+    oracle's dense transform + RTN, including a zero row, a non-finite row and multi-row CTAs."""
+    from oracle import layer as olayer
+    M = 2 * 148 + 7
+    x = synth.activations(M, K, "swiglu" if mode == "full" else "normal", seed=K + 3, device=DEV)
+    x[5] = 0
+    x[9, 3] = float("inf")
+    xq, xs = q.hadamard_quant8(x, mode=mode)
+    torch.cuda.synchronize()
+    rows = [0, 1, 5, 147, 148, 149, 296, M - 1]
+    xh = x[rows].float().cpu().numpy().astype(np.float64)
+    rc, rs = oquant.quantize_sym_rows(olayer.online_transform(xh, mode, 128), 0.9, qmax=127)
+    P.assert_codes(xq[rows].cpu().numpy().astype(np.int64), rc, f"int8 {mode} codes")
+    P.assert_scales(xs[rows].cpu().numpy(), rs, f"int8 {mode} scales")
+    s9 = xs[9].item()
+    assert s9 != s9 and not xq[9].any()  # non-finite row: scale NaN, codes 0
+    assert int(xq.abs().max()) <= 127
 
 
 @pytest.mark.parametrize("M,N,K", [(128, 256, 128), (300, 776, 512), (129, 264, 4096), (600, 1024, 8192),
