@@ -13,7 +13,7 @@ CSRC = os.path.join(PKG, "csrc")
 OUT = os.path.join(PKG, "libquarot.so")
 BUILD = os.path.join(PKG, "_build")
 
-SOURCES = ["quarot_abi.cu", "hadamard_tables.cu", "hadamard_quant.cu", "hq_full_tc.cu", "hq_heads_tc.cu", "hq_full172_tc.cu", "int4_gemm.cu", "kv_quant.cu", "kv_quant_tc.cu", "kv_decode.cu", "glue.cu"]
+SOURCES = ["quarot_abi.cu", "hadamard_tables.cu", "hadamard_quant.cu", "hq_full_tc.cu", "hq_heads_tc.cu", "hq_full172_tc.cu", "hq_full_small_tc.cu", "int4_gemm.cu", "kv_quant.cu", "kv_quant_tc.cu", "kv_decode.cu", "glue.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-v", "-I", os.path.join(ROOT, "include")]

@@ -914,7 +914,9 @@ cudaError_t launch_hq_full(const void* x, int64_t M, int64_t K, int64_t ld_x, in
     if (e != cudaSuccess) return e;
     hq::hq_full_kernel<28><<<grid, threads, smem, stream>>>(xh, ld_x, pow2, clip, q, ld_q, scale,
                                                            device_bfrag_table(28));
-  } else if (m == 20 || m == 108) {  // Llama-2-13B widths: the smem kernel
+  } else if (hq_full_small_tc_supported(pow2, m) && g_hq_full_variant != 1) {  // 13B widths, tcgen05
+    return launch_hq_full_small_tc(x, M, ld_x, pow2, m, clip, q, ld_q, scale, stream);
+  } else if (m == 20 || m == 108) {  // other 2^n x {20, 108}: the smem kernel
     auto kern = m == 20 ? hq::hq_full_kernel<20> : hq::hq_full_kernel<108>;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

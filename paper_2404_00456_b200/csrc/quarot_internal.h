@@ -34,6 +34,10 @@ cudaError_t launch_hq_heads(const void* x, int64_t M, int64_t K, int64_t ld_x, i
 cudaError_t launch_hq_full28_tc(const void* x, int64_t M, int64_t ld_x, float clip, uint8_t* q, int64_t ld_q,
                                 float* scale, cudaStream_t stream, bool q8 = false);
 extern int g_hq_full_variant;
+// hq_full_small_tc.cu: the Llama-2-13B widths K = 128 x 108 and 256 x 20 on the tcgen05 path
+bool hq_full_small_tc_supported(int64_t pow2, int m);
+cudaError_t launch_hq_full_small_tc(const void* x, int64_t M, int64_t ld_x, int64_t pow2, int m, float clip,
+                                    uint8_t* q, int64_t ld_q, float* scale, cudaStream_t stream);
 // hq_full172_tc.cu: K = 64 x 172 on the tcgen05 path (the default for that width)
 cudaError_t launch_hq_full172_tc(const void* x, int64_t M, int64_t ld_x, float clip, uint8_t* q, int64_t ld_q,
                                  float* scale, cudaStream_t stream);

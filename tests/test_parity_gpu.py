@@ -95,7 +95,8 @@ def test_hadamard_quant_strided_and_split_invariance(q):
         assert torch.equal(torch.cat([a1, a2]), xq) and torch.equal(torch.cat([s1, s2]), xs)
 
 
-@pytest.mark.parametrize("mode,K", [("full", 28672), ("full", 11008), ("across_heads", 8192), ("across_heads", 4096)])
+@pytest.mark.parametrize("mode,K", [("full", 28672), ("full", 11008), ("full", 13824), ("full", 5120),
+                                    ("across_heads", 8192), ("across_heads", 4096)])
 def test_hadamard_quant_tcgen05_paths(q, mode, K):
     """The tcgen05 quantizers (FULL 1024x28 / 64x172, ACROSS_HEADS n_h 32/64) on what the small
     parity cases do not reach: several rows per persistent CTA (the TMEM / smem rings wrap),
