@@ -11,8 +11,8 @@
 //  * A TMA warp loads each tile (3-D maps [token][head][d], two 64-wide d boxes) straight into
 //    the K-major SWIZZLE_128B operand layout, 3-stage ring.  With RoPE fused, eight warps rotate
 //    the Q / K rows in place in shared memory (two threads per row) from a per-block cos/sin table
-//    (fp64 sincos rounded to fp32, as quarot_rope) and round to fp16; otherwise they only hand
-//    the stage to the MMA.
+//    (fp64 sincos rounded to fp32, as quarot_rope; two table warps build it a block ahead into a
+//    double buffer) and round to fp16; otherwise they only hand the stage to the MMA.
 //  * Epilogue warps (thread = TMEM lane = row): Q rows scaled by 1/sqrt(128), rounded to fp16
 //    and written back in place; K / V rows quantized asymmetrically (clip 0.95, group = the
 //    row, reading Z14) entirely in-thread: min / max, scale / zero, 64 code bytes in four
@@ -33,13 +33,13 @@ constexpr int HD = 128;
 constexpr int TILE_BYTES = 128 * HD * 2;  // 32 KB: 128 rows x 128 fp16, two SW128 atoms
 constexpr int STAGES = 3;
 constexpr int NUM_EPI = 4, NUM_PROD = 8;  // two RoPE threads per tile row
-constexpr int EPI_WARP0 = 0, PROD_WARP0 = 4, MMA_WARP = 12, TMA_WARP = 13;
-constexpr int NUM_THREADS = 14 * 32;
+constexpr int EPI_WARP0 = 0, PROD_WARP0 = 4, MMA_WARP = 12, TMA_WARP = 13, TAB_WARP0 = 14, NUM_TAB = 2;
+constexpr int NUM_THREADS = 16 * 32;
 constexpr int TBUF = 4;
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int MAX_BT = 32;                                 // tokens per block (n_kv >= 4)
 constexpr int TAB_BYTES = MAX_BT * (HD / 2) * 8;           // (cos, sin) per token and pair
-constexpr size_t SMEM = 1024 + 2 * TILE_BYTES + (size_t)STAGES * TILE_BYTES + TAB_BYTES + 512 + (HD / 2) * 8;
+constexpr size_t SMEM = 1024 + 2 * TILE_BYTES + (size_t)STAGES * TILE_BYTES + 2 * TAB_BYTES + 512 + (HD / 2) * 8;
 static_assert(SMEM <= 232448, "227 KB dynamic smem");
 constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(HD >> 3) << 17) | ((128u >> 4) << 24);
 
@@ -103,13 +103,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sB = smem;                   // [H_128 | I_128] K-major SW128 images
   uint8_t* sA = sB + 2 * TILE_BYTES;    // [STAGES] tiles
-  float2* tab = reinterpret_cast<float2*>(sA + STAGES * TILE_BYTES);  // [B_t][64] (cos, sin)
-  uint64_t* a_full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(tab) + TAB_BYTES);
+  float2* tab = reinterpret_cast<float2*>(sA + STAGES * TILE_BYTES);  // [2][B_t][64] (cos, sin)
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(tab) + 2 * TAB_BYTES);
   uint64_t* a_empty = a_full + STAGES;
   uint64_t* x_full = a_empty + STAGES;  // [STAGES] TMA landed
   uint64_t* t_full = x_full + STAGES;
   uint64_t* t_empty = t_full + TBUF;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(t_empty + TBUF);
+  uint64_t* tab_full = t_empty + TBUF;  // [2] table warps -> RoPE warps
+  uint64_t* tab_empty = tab_full + 2;   // [2] RoPE warps -> table warps
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tab_empty + 2);
   double* inv_freq = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(a_full) + 512);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int BT = 128 / a.n_kv;          // tokens per block
@@ -132,6 +134,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int b = 0; b < TBUF; ++b) {
       mbar_init(&t_full[b], 1);
       mbar_init(&t_empty[b], NUM_EPI);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tab_full[b], NUM_TAB);
+      mbar_init(&tab_empty[b], NUM_PROD);
     }
     fence_barrier_init();
   }
@@ -170,17 +176,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int64_t it = 0;
     for (int64_t bi = 0; bi < my_blocks; ++bi) {
       const int64_t t0 = ((int64_t)blockIdx.x + bi * gridDim.x) * BT;
-      if (kRope) {
-        bar_named(1, NUM_PROD * 32);  // every producer is done with the previous block's table
-        for (int i = pt; i < BT * (HD / 2); i += NUM_PROD * 32) {
-          const int tt = i / (HD / 2), ii = i - tt * (HD / 2);
-          const int64_t pos = (a.pos0 + t0 + tt) % a.seq_len;
-          double sn, cn;
-          sincos((double)pos * inv_freq[ii], &sn, &cn);  // == quarot_rope's table
-          tab[i] = make_float2((float)cn, (float)sn);
-        }
-        bar_named(1, NUM_PROD * 32);
-      }
+      const float2* btab = tab + (bi & 1) * (TAB_BYTES / 8);  // this block's cos/sin table
+      if (kRope) mbar_wait(&tab_full[bi & 1], (uint32_t)((bi >> 1) & 1));
       for (int j = 0; j < tpb; ++j, ++it) {
         const int s = (int)(it % STAGES);
         const TileInfo ti = tile_info(j, nQ);
@@ -189,7 +186,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           // RoPE rotate-half pairs (i, i + 64), rounded to fp16 (reading Z22)
           const int nh = ti.type == 0 ? a.n_q : a.n_kv;
           const int tl = (ti.row0 + r) / nh;  // token within the block
-          const float2* cs = tab + tl * (HD / 2);
+          const float2* cs = btab + tl * (HD / 2);
           const uint32_t row = smem_u32(sA + s * TILE_BYTES);
 #pragma unroll
           for (int cc = 0; cc < 4; ++cc) {
@@ -214,6 +211,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&a_full[s]);
+      }
+      if (kRope && lane == 0) mbar_arrive(&tab_empty[bi & 1]);  // this warp is done with the table
+    }
+  } else if (warp >= TAB_WARP0 && warp < TAB_WARP0 + NUM_TAB) {
+    // ---------------------------------------------------------------- cos/sin tables, a block ahead
+    if (kRope) {
+      const int tt0 = (warp - TAB_WARP0) * 32 + lane;
+      for (int64_t bi = 0; bi < my_blocks; ++bi) {
+        const int64_t t0 = ((int64_t)blockIdx.x + bi * gridDim.x) * BT;
+        float2* btab = tab + (bi & 1) * (TAB_BYTES / 8);
+        mbar_wait_sleep(&tab_empty[bi & 1], (uint32_t)((bi >> 1) & 1) ^ 1u);
+        for (int i = tt0; i < BT * (HD / 2); i += NUM_TAB * 32) {
+          const int tt = i / (HD / 2), ii = i - tt * (HD / 2);
+          const int64_t pos = (a.pos0 + t0 + tt) % a.seq_len;
+          double sn, cn;
+          sincos((double)pos * inv_freq[ii], &sn, &cn);  // == quarot_rope's table
+          btab[i] = make_float2((float)cn, (float)sn);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tab_full[bi & 1]);
       }
     }
   } else if (warp == MMA_WARP) {
