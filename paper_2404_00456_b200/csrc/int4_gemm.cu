@@ -796,7 +796,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(i8::NUM_THREADS, 1)
         const uint32_t ready_leader = map_to_rank(&ready[0], 0);
         for (int it = 0; it < total; ++it) {
           const int s = it % i8::STAGES;
-          mbar_wait(&full[s], (it / i8::STAGES) & 1);
+          mbar_wait_sleep(&full[s], (it / i8::STAGES) & 1);
           mbar_arrive_cluster(ready_leader + (uint32_t)s * 8u);
         }
       }
@@ -806,14 +806,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(i8::NUM_THREADS, 1)
         for (int tl = 0; tl < my_tiles; ++tl) {
           for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
             const int s = it % i8::STAGES;
-            mbar_wait(&ready[s], (it / i8::STAGES) & 1);
+            mbar_wait_sleep(&ready[s], (it / i8::STAGES) & 1);
             tc_fence_after();
             const uint32_t base = smem_u32(smem + s * i8::STAGE_BYTES);
             const uint64_t a_desc = umma_desc_sw128(base), b_desc = umma_desc_sw128(base + i8::A_BYTES);
 #pragma unroll
             for (int hg = 0; hg < BK / gq::G; ++hg, ++gc) {  // a fresh accumulator per 128-k group
               const int ab = gc & 1;
-              mbar_wait(&t_empty[ab], ((gc >> 1) & 1) ^ 1);
+              mbar_wait_sleep(&t_empty[ab], ((gc >> 1) & 1) ^ 1);
               tc_fence_after();
               const uint32_t d_tmem = tmem_base + (uint32_t)(ab * BN);
 #pragma unroll
