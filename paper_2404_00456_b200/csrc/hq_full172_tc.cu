@@ -321,6 +321,8 @@ std::vector<uint16_t> a_image_172(const int8_t* h) {
 
 std::mutex g_mu172;
 void* g_img172[64];
+// the constant A image lives in static device memory (the library allocates none)
+__device__ uint4 g_a172_img[hq172::A_BYTES / 16];
 
 }  // namespace
 
@@ -337,7 +339,7 @@ cudaError_t launch_hq_full172_tc(const void* x, int64_t M, int64_t ld_x, float c
       if (!h) return cudaErrorInvalidValue;
       auto host = a_image_172(h);
       void* d = nullptr;
-      e = cudaMalloc(&d, host.size() * sizeof(uint16_t));
+      e = cudaGetSymbolAddress(&d, g_a172_img);
       if (e != cudaSuccess) return e;
       e = cudaMemcpy(d, host.data(), host.size() * sizeof(uint16_t), cudaMemcpyHostToDevice);
       if (e != cudaSuccess) return e;

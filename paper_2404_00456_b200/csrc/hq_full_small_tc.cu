@@ -308,6 +308,9 @@ std::vector<uint16_t> a_image_small(const int8_t* h) {
 
 std::mutex g_mu_small;
 void* g_img_small[64][2];
+// the constant A images live in static device memory (the library allocates none)
+__device__ uint4 g_small_img108[hqs::Cfg<108, 1>::A_BYTES / 16];
+__device__ uint4 g_small_img20[hqs::Cfg<20, 2>::A_BYTES / 16];
 
 template <int MB, int LLO>
 cudaError_t launch_small(const void* x, int64_t M, int64_t ld_x, float clip, uint8_t* q, int64_t ld_q, float* scale,
@@ -324,7 +327,7 @@ cudaError_t launch_small(const void* x, int64_t M, int64_t ld_x, float clip, uin
       if (!h) return cudaErrorInvalidValue;
       auto host = a_image_small<MB, LLO>(h);
       void* d = nullptr;
-      e = cudaMalloc(&d, host.size() * sizeof(uint16_t));
+      e = MB == 108 ? cudaGetSymbolAddress(&d, g_small_img108) : cudaGetSymbolAddress(&d, g_small_img20);
       if (e != cudaSuccess) return e;
       e = cudaMemcpy(d, host.data(), host.size() * sizeof(uint16_t), cudaMemcpyHostToDevice);
       if (e != cudaSuccess) return e;

@@ -439,6 +439,8 @@ std::vector<uint16_t> a_image_28(const int8_t* h28) {
 
 std::mutex g_img_mu;
 void* g_img[64];
+// the constant A image lives in static device memory (the library allocates none)
+__device__ uint4 g_a28_img[hqtc::A_BYTES / 16];
 
 }  // namespace
 
@@ -457,7 +459,7 @@ cudaError_t launch_hq_full28_tc(const void* x, int64_t M, int64_t ld_x, float cl
       if (!h28) return cudaErrorInvalidValue;
       auto host = a_image_28(h28);
       void* d = nullptr;
-      e = cudaMalloc(&d, host.size() * sizeof(uint16_t));
+      e = cudaGetSymbolAddress(&d, g_a28_img);
       if (e != cudaSuccess) return e;
       e = cudaMemcpy(d, host.data(), host.size() * sizeof(uint16_t), cudaMemcpyHostToDevice);
       if (e != cudaSuccess) return e;

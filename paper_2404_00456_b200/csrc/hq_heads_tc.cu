@@ -298,6 +298,10 @@ std::vector<uint16_t> b_image(int n) {
 
 std::mutex g_mu;
 void* g_img[64][3];  // n_h = 16, 32, 64
+// the constant B images live in static device memory (the library allocates none)
+__device__ uint4 g_heads_img16[16 * 128 / 16];
+__device__ uint4 g_heads_img32[32 * 128 / 16];
+__device__ uint4 g_heads_img64[64 * 128 / 16];
 
 template <int NH, bool kQ8>
 cudaError_t launch_nh(const void* x, int64_t M, int64_t ld_x, float clip, uint8_t* q, int64_t ld_q, float* scale,
@@ -349,7 +353,8 @@ cudaError_t launch_hq_heads_tc(const void* x, int64_t M, int64_t K, int64_t ld_x
     if (!g_img[dev & 63][slot]) {
       auto host = b_image(nh);
       void* dptr = nullptr;
-      e = cudaMalloc(&dptr, host.size() * sizeof(uint16_t));
+      e = nh == 16 ? cudaGetSymbolAddress(&dptr, g_heads_img16)
+                   : (nh == 32 ? cudaGetSymbolAddress(&dptr, g_heads_img32) : cudaGetSymbolAddress(&dptr, g_heads_img64));
       if (e != cudaSuccess) return e;
       e = cudaMemcpy(dptr, host.data(), host.size() * sizeof(uint16_t), cudaMemcpyHostToDevice);
       if (e != cudaSuccess) return e;

@@ -400,6 +400,8 @@ std::vector<uint16_t> b_images() {
 
 std::mutex g_mu;
 void* g_bimg[64];
+// the constant B images live in static device memory (the library allocates none)
+__device__ uint4 g_kv_bimg[2 * kvtc::TILE_BYTES / 16];
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn_kv() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -435,7 +437,7 @@ cudaError_t launch_kv_tc(const void* k, int64_t ld_k, const void* v, int64_t ld_
     if (!g_bimg[dev & 63]) {
       auto host = b_images();
       void* d = nullptr;
-      e = cudaMalloc(&d, host.size() * sizeof(uint16_t));
+      e = cudaGetSymbolAddress(&d, g_kv_bimg);
       if (e != cudaSuccess) return e;
       e = cudaMemcpy(d, host.data(), host.size() * sizeof(uint16_t), cudaMemcpyHostToDevice);
       if (e != cudaSuccess) return e;
