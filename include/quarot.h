@@ -25,7 +25,8 @@
  *    allocates device memory; its only state is immutable per-device tables in static
  *    __device__ storage: the stored Hadamard matrices H_20, H_28, H_108, H_172 (built and
  *    verified H H^T = m I on first use) and the constant MMA operand images derived from them
- *    (written once per device, on the first call that needs them).
+ *    (written once per device by a synchronous copy on the first call that needs them: make
+ *    that call outside CUDA graph capture).
  *  - `stream` is a cudaStream_t (NULL = legacy default stream).  All work is enqueued
  *    on it; no entry point synchronizes the host.  Calls are reentrant across streams.
  *  - Arguments are validated before any launch; a failing call launches nothing and
