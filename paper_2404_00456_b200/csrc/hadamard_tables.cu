@@ -226,6 +226,8 @@ cudaError_t ensure_device_tables() {
     e = cudaMemcpyToSymbol(g_bfrag108, f.data(), f.size() * sizeof(uint32_t));
     if (e != cudaSuccess) return e;
   }
+  e = cudaDeviceSynchronize();  // one-time: the tables are complete before any stream reads them
+  if (e != cudaSuccess) return e;
   g_dev_ready[dev & 63] = true;
   return cudaSuccess;
 }

@@ -343,6 +343,8 @@ cudaError_t launch_hq_full172_tc(const void* x, int64_t M, int64_t ld_x, float c
       if (e != cudaSuccess) return e;
       e = cudaMemcpy(d, host.data(), host.size() * sizeof(uint16_t), cudaMemcpyHostToDevice);
       if (e != cudaSuccess) return e;
+      e = cudaDeviceSynchronize();  // one-time: the image is complete before any stream reads it
+      if (e != cudaSuccess) return e;
       e = cudaFuncSetAttribute(hq172::hq_full172_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)hq172::SMEM);
       if (e != cudaSuccess) return e;

@@ -331,6 +331,8 @@ cudaError_t launch_small(const void* x, int64_t M, int64_t ld_x, float clip, uin
       if (e != cudaSuccess) return e;
       e = cudaMemcpy(d, host.data(), host.size() * sizeof(uint16_t), cudaMemcpyHostToDevice);
       if (e != cudaSuccess) return e;
+      e = cudaDeviceSynchronize();  // one-time: the image is complete before any stream reads it
+      if (e != cudaSuccess) return e;
       e = cudaFuncSetAttribute(hqs::hq_full_small_tc_kernel<MB, LLO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)C::SMEM);
       if (e != cudaSuccess) return e;

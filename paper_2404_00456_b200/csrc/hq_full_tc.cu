@@ -463,6 +463,8 @@ cudaError_t launch_hq_full28_tc(const void* x, int64_t M, int64_t ld_x, float cl
       if (e != cudaSuccess) return e;
       e = cudaMemcpy(d, host.data(), host.size() * sizeof(uint16_t), cudaMemcpyHostToDevice);
       if (e != cudaSuccess) return e;
+      e = cudaDeviceSynchronize();  // one-time: the image is complete before any stream reads it
+      if (e != cudaSuccess) return e;
       for (auto kern : {hqtc::hq_full28_tc_kernel<false>, hqtc::hq_full28_tc_kernel<true>,
                         hqtc::hq_full28_tc_kernel<false, true>}) {
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hqtc::SMEM);

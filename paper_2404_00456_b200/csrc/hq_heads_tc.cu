@@ -358,6 +358,8 @@ cudaError_t launch_hq_heads_tc(const void* x, int64_t M, int64_t K, int64_t ld_x
       if (e != cudaSuccess) return e;
       e = cudaMemcpy(dptr, host.data(), host.size() * sizeof(uint16_t), cudaMemcpyHostToDevice);
       if (e != cudaSuccess) return e;
+      e = cudaDeviceSynchronize();  // one-time: the image is complete before any stream reads it
+      if (e != cudaSuccess) return e;
       g_img[dev & 63][slot] = dptr;
     }
     img = g_img[dev & 63][slot];

@@ -441,6 +441,8 @@ cudaError_t launch_kv_tc(const void* k, int64_t ld_k, const void* v, int64_t ld_
       if (e != cudaSuccess) return e;
       e = cudaMemcpy(d, host.data(), host.size() * sizeof(uint16_t), cudaMemcpyHostToDevice);
       if (e != cudaSuccess) return e;
+      e = cudaDeviceSynchronize();  // one-time: the image is complete before any stream reads it
+      if (e != cudaSuccess) return e;
       for (auto kern : {kvtc::kv_tc_kernel<false>, kvtc::kv_tc_kernel<true>}) {
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kvtc::SMEM);
         if (e != cudaSuccess) return e;
