@@ -306,3 +306,16 @@ def test_group_linear_reduces_and_brute_force():
     # equal scales in every group reduce to the per-token / per-channel epilogue
     y2 = G.group_linear(cx, np.repeat(sx[:, :1], 4, 1), cw, np.repeat(sw[:, :1], 4, 1))
     assert np.array_equal(y2, G.dequant_epilogue(G.int_matmul(cx, cw), sx[:, 0], sw[:, 0]))
+
+
+def test_group_dequantize_matches_codes_times_group_scale():
+    # x^ = c * s_g for the element's own group; with one group per row it is the per-row rule
+    rng = np.random.default_rng(8)
+    y = rng.standard_normal((3, 48))
+    c, s = quant.quantize_sym_groups(y, 16)
+    d = quant.dequantize_sym_groups(c, s)
+    for r in range(3):
+        for k in range(48):
+            assert d[r, k] == c[r, k] * float(s[r, k // 16])
+    c1, s1 = quant.quantize_sym_groups(y, 48)
+    assert np.array_equal(quant.dequantize_sym_groups(c1, s1), quant.dequantize_sym_rows(c1, s1[:, 0]))
