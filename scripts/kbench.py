@@ -16,6 +16,19 @@ import synth  # noqa: E402
 import paper_2404_00456_b200 as q  # noqa: E402
 
 
+def _peaks():
+    """HBM GB/s and the INT8 TOPS denominator (2 x sustained bf16) from MEASURED_PEAKS.json."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), 2.0 * float(p.get("bf16_tflops_sustained", p["bf16_tflops"]))
+    except (OSError, KeyError, ValueError):
+        return 6536.0, 2765.6
+
+
+HBM_GBS, INT8_TOPS = _peaks()
+
+
 def timeit(fn, iters=10, warm=3):
     for _ in range(warm):
         fn()
@@ -84,7 +97,7 @@ def main():
             y = torch.empty(M, N, dtype=torch.float16, device=dev)
             ms = timeit(lambda: q.int4_linear(xq, xs, wq, ws, y=y), a.iters)
             tops = 2 * M * N * K / ms / 1e9
-            res[f"gemm_{name}"] = {"ms": ms, "tops": tops, "frac_int8_2x_bf16_sustained": tops / 2765.6}
+            res[f"gemm_{name}"] = {"ms": ms, "tops": tops, "frac_int8_2x_bf16_sustained": tops / INT8_TOPS}
             print(name, json.dumps(res[f"gemm_{name}"]), flush=True)
             del wq, y
         del xq_big
@@ -98,7 +111,7 @@ def main():
             rms = mode == "none_rms"
             ms = timeit(lambda: q.hadamard_quant(x, "none" if rms else mode, 128, 0.9, q=qb, scale=sb, rmsnorm=rms), a.iters)
             gbs = M * (2.5 * K + 4) / ms / 1e6
-            res[f"hq_{mode}_{K}"] = {"ms": ms, "gbs": gbs, "frac_hbm": gbs / 6536}
+            res[f"hq_{mode}_{K}"] = {"ms": ms, "gbs": gbs, "frac_hbm": gbs / HBM_GBS}
             print(mode, K, json.dumps(res[f"hq_{mode}_{K}"]), flush=True)
             del x
     if "kv" in a.what:
@@ -110,10 +123,10 @@ def main():
         out = q.kv_quant(kv_, vv, qv)
         ms = timeit(lambda: q.kv_quant(kv_, vv, qv, out=out), a.iters)
         byts = 2 * T * 8 * (2 * d + d // 2 + 5) + T * 64 * d * 4
-        res["kv"] = {"ms": ms, "gbs": byts / ms / 1e6, "frac_hbm": byts / ms / 1e6 / 6536}
+        res["kv"] = {"ms": ms, "gbs": byts / ms / 1e6, "frac_hbm": byts / ms / 1e6 / HBM_GBS}
         print("kv", json.dumps(res["kv"]), flush=True)
         ms = timeit(lambda: q.kv_quant(kv_, vv, qv, out=out, rope=(0, 2048, 10000.0)), a.iters)
-        res["kv_rope"] = {"ms": ms, "gbs": byts / ms / 1e6, "frac_hbm": byts / ms / 1e6 / 6536}
+        res["kv_rope"] = {"ms": ms, "gbs": byts / ms / 1e6, "frac_hbm": byts / ms / 1e6 / HBM_GBS}
         print("kv_rope", json.dumps(res["kv_rope"]), flush=True)
         ms = timeit(lambda: q.rope(fused[:, :9216].view(T, 72, d)), a.iters)
         print("rope", json.dumps({"ms": ms}), flush=True)
@@ -140,7 +153,7 @@ def main():
                 byts = B * n_kv * L * (2 * d // 2 + 10)
                 key = f"decode_{n_q}x{n_kv}_b{B}"
                 res[key] = {"ms_append_decode": ms, "ms_decode": ms_dec, "gbs_decode": byts / ms_dec / 1e6,
-                            "frac_hbm": byts / ms_dec / 1e6 / 6536}
+                            "frac_hbm": byts / ms_dec / 1e6 / HBM_GBS}
                 print(key, json.dumps(res[key]), flush=True)
                 del cache
     if "gemm_group" in a.what:
@@ -154,7 +167,7 @@ def main():
             y = torch.empty(M, N, dtype=torch.float16, device=dev)
             ms = timeit(lambda: q.int4_linear_group(xq, xs, wq, ws, y=y), a.iters)
             tops = 2 * M * N * K / ms / 1e9
-            res[f"gemm_group_{name}"] = {"ms": ms, "tops": tops, "frac_int8_2x_bf16_sustained": tops / 2765.6}
+            res[f"gemm_group_{name}"] = {"ms": ms, "tops": tops, "frac_int8_2x_bf16_sustained": tops / INT8_TOPS}
             print("group", name, json.dumps(res[f"gemm_group_{name}"]), flush=True)
             del wq, y
         del xq_big
@@ -170,7 +183,7 @@ def main():
             y = torch.empty(M, N, dtype=torch.float16, device=dev)
             ms = timeit(lambda: q.int8_linear(xq, xs, wq, ws, y=y), a.iters)
             tops = 2 * M * N * K / ms / 1e9
-            res[f"gemm8_{name}"] = {"ms": ms, "tops": tops, "frac_int8_2x_bf16_sustained": tops / 2765.6}
+            res[f"gemm8_{name}"] = {"ms": ms, "tops": tops, "frac_int8_2x_bf16_sustained": tops / INT8_TOPS}
             print("a8w8", name, json.dumps(res[f"gemm8_{name}"]), flush=True)
             del wq, y
         del xq_big
