@@ -128,3 +128,27 @@ def test_kv_validation_without_gpu(q):
     assert f(*bad) == 2                                 # ld_k < n_kv * head_dim
     bad = list(args); bad[1] = 1028
     assert f(*bad) == 4                                 # ld_k % 8
+
+
+def _lg(q, xp=16, sx=16, ld_sx=2, M=128, K=256, ld_xq=256, wp=16, sw=16, ld_sw=256, N=256, ld_wq=256, group=128,
+        yp=16, ld_y=256):
+    return q.lib().quarot_int4_linear_group(xp, sx, ld_sx, M, K, ld_xq, wp, sw, ld_sw, N, ld_wq, group, yp, ld_y, None)
+
+
+def test_int4_linear_group_validation_without_gpu(q):
+    # quarot_int4_linear_group (§8 f3): rejected before any CUDA call
+    assert _lg(q, group=64) == 3                                        # only group 128
+    assert _lg(q, K=384, ld_xq=384, ld_wq=384, ld_sx=3) == 4           # K % 256
+    assert _lg(q, ld_sx=1) == 2 and _lg(q, ld_sw=100) == 2 and _lg(q, ld_y=100) == 2  # ERR_DIM
+    assert _lg(q, N=260, ld_sw=260, ld_y=264) == 4                      # N % 8
+    assert _lg(q, ld_sw=258) == 4                                       # ld_sw % 4
+    assert _lg(q, M=0) == 0                                             # no-op
+    assert _lg(q, xp=None) == 1 and _lg(q, sw=None) == 1                # ERR_NULL
+
+
+def test_hadamard_quant8_validation_without_gpu(q):
+    lib = q.lib()
+    f = lambda mode, K, hd=128: lib.quarot_hadamard_quant8(16, 4, K, K, mode, hd, 0.9, 16, K, 16, None)
+    assert f(q.FULL, 8192) == 3                      # 8-bit FULL only for K = 1024 x 28
+    assert f(q.ACROSS_HEADS, 512) == 3               # 4 heads: not on the 8-bit path
+    assert f(q.FULL | q.RMSNORM, 28672) == 5         # RMSNorm only with mode NONE
