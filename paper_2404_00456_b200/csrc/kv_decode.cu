@@ -298,11 +298,24 @@ __global__ void __launch_bounds__(WARPS * 32) kv_decode_kernel(Args a) {
                                          __uint_as_float(__byte_perm(hi, 0x4B000000u, 0x7540))), two23);
     const float2 c23 = f2sub(make_float2(__uint_as_float(__byte_perm(lo, 0x4B000000u, 0x7541)),
                                          __uint_as_float(__byte_perm(hi, 0x4B000000u, 0x7541))), two23);
+    if constexpr (G % 4 == 0) {  // the row's p of four heads in one 16-byte load
 #pragma unroll
-    for (int r = 0; r < G; ++r) {
-      const float pv = p_w[rl][r];
-      o2[r][0] = f2fma(make_float2(pv, pv), c01, o2[r][0]);
-      o2[r][1] = f2fma(make_float2(pv, pv), c23, o2[r][1]);
+      for (int r4 = 0; r4 < G; r4 += 4) {
+        const float4 p4 = *reinterpret_cast<const float4*>(&p_w[rl][r4]);
+        const float pp[4] = {p4.x, p4.y, p4.z, p4.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          o2[r4 + e][0] = f2fma(make_float2(pp[e], pp[e]), c01, o2[r4 + e][0]);
+          o2[r4 + e][1] = f2fma(make_float2(pp[e], pp[e]), c23, o2[r4 + e][1]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < G; ++r) {
+        const float pv = p_w[rl][r];
+        o2[r][0] = f2fma(make_float2(pv, pv), c01, o2[r][0]);
+        o2[r][1] = f2fma(make_float2(pv, pv), c23, o2[r][1]);
+      }
     }
   }
   // ---- merge the 4 warps: each writes (o - zsum, m, l) per head over its own (now idle)
