@@ -6,7 +6,7 @@ A step = one pass of every SURVEY §8(a) row over one batch: one Llama-2-70B dec
 tokens per GPU, as the chain of runtime.DecoderLayerStep (attention core excluded):
 RMSNorm+quantize -> INT4 QKV GEMM -> RoPE -> KV-cache Init (+Q rotation) ; Hadamard-heads +
 quantize -> INT4 O GEMM + residual ; RMSNorm+quantize -> INT4 gate/up GEMM -> SwiGLU ;
-Hadamard (1024 x H_28) + quantize -> INT4 down GEMM + residual (11 kernel launches, all ours).
+Hadamard (1024 x H_28) + quantize -> INT4 down GEMM + residual (9 kernel launches, all ours).
 `--step linears` times rows a1-a7 alone on independent inputs (9 launches).
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
@@ -283,7 +283,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--profile-steps", type=int, default=0, help="run N untimed steps and exit (ncu)")
     ap.add_argument("--step", default="chain", choices=["chain", "linears"],
-                    help="chain: the decoder-layer chain (a1-a8, 11 launches); linears: a1-a7 on independent inputs")
+                    help="chain: the decoder-layer chain (a1-a8, 9 launches); linears: a1-a7 on independent inputs")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

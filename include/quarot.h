@@ -92,8 +92,13 @@ typedef enum {
  *   else scale = fp32(clip * a / 7), code_k = clamp(round_half_even(y_k / scale), -7, 7)
  *   ("dividing the maximum absolute value of each token by 7 ... round the
  *   result to its nearest integer").  x^ = code * scale approximates y.
- * Granularity: K % 16 == 0 (NONE); K % 32 == 0 and K / head_dim a power of two
- * (ACROSS_HEADS, head_dim % 2 == 0); K = 2^n m with 2^n >= 2 (FULL).            */
+ * Granularity / limits (QUAROT_ERR_ALIGN / QUAROT_ERR_UNSUPPORTED_SIZE otherwise):
+ *   NONE: K % 16 == 0, K <= 32768.
+ *   ACROSS_HEADS: K % 32 == 0; head_dim a power of two >= 64; n_h = K / head_dim a power of
+ *     two.  head_dim 128 with n_h in {16, 32, 64} runs on the tensor cores; every other
+ *     shape on the CUDA-core kernel, which needs (head_dim / 2) * max(1, n_h / 32) <= 256
+ *     and K <= 32768.
+ *   FULL: K = 2^n m with 2^n >= 2, K % 16 == 0, K <= 32768.                          */
 quarot_status quarot_hadamard_quant(const void* x, int64_t M, int64_t K, int64_t ld_x,
                                     int32_t mode, int32_t head_dim, float clip_ratio,
                                     uint8_t* q, int64_t ld_q, float* scale, void* stream);
@@ -106,7 +111,9 @@ quarot_status quarot_hadamard_quant(const void* x, int64_t M, int64_t K, int64_t
  *   x_scale fp32 [M], w_scale fp32 [N] (per output channel, "per-column").
  *   y      fp16 [M][ld_y].
  * Requirements: K % 128 == 0; N % 8 == 0; ld_xq, ld_wq % 16 == 0; ld_y % 8 == 0; all
- * pointers 16-B aligned.  Ragged M and N tails are handled. */
+ * pointers 16-B aligned.  Ragged M and N tails are handled.  Activation codes must lie in
+ * [-7, 7] (quarot_hadamard_quant never writes -8), weight codes in [-8, 7]: the accumulator
+ * is then exact for K <= 149796 (larger K: QUAROT_ERR_UNSUPPORTED_SIZE). */
 quarot_status quarot_int4_linear(const uint8_t* xq, const float* x_scale, int64_t M, int64_t K,
                                  int64_t ld_xq, const uint8_t* wq, const float* w_scale,
                                  int64_t N, int64_t ld_wq, void* y, int64_t ld_y, void* stream);
@@ -181,7 +188,8 @@ quarot_status quarot_kv_quant_rope(const void* k, int64_t ld_k, const void* v, i
  *   x      fp16 [M][ld_x] device, K elements used per row
  *   q      uint8 [M][ld_q] device, K/2 packed bytes (low nibble = even element)
  *   scale  fp32 [M][ld_s] device, K/group scales per row (ld_s >= K/group)
- *   group  64, 128 or 256 (QUAROT_ERR_UNSUPPORTED_SIZE otherwise); K % group == 0 (QUAROT_ERR_DIM)
+ *   group  64, 128 or 256 (QUAROT_ERR_UNSUPPORTED_SIZE otherwise); K % group == 0 (QUAROT_ERR_DIM);
+ *          M < 2^31, K <= 65535 * 1024
  * Errors as quarot_hadamard_quant; x and q 16-byte aligned, ld_x % 8 == 0, ld_q % 4 == 0.
  * quarot_hadamard_quant_group8: the same codes, one per int8 byte (q int8 [M][ld_q], ld_q >= K,
  *   ld_q % 8 == 0) — the operand format of quarot_int4_linear_group. */
@@ -250,7 +258,8 @@ quarot_status quarot_kv_append(const void* k, int64_t ld_k, const void* v, int64
  * h -> KV head h / (n_q / n_kv).  q fp16 [B][n_q][head_dim] contiguous; out fp16
  * [B][n_q][head_dim] contiguous (o is in V's space: V is not rotated online).
  * workspace fp32, quarot_kv_decode_workspace_bytes(B, n_q, head_dim, s_max) bytes, caller-owned.
- * Requirements: head_dim == 128; n_q / n_kv in {1, 2, 4, 8}; sm_scale finite (the standard
+ * Requirements: head_dim == 128; n_q / n_kv in {1, 2, 4, 8}; B, n_kv <= 65535 (ERR_DIM);
+ * sm_scale finite (the standard
  * 1/sqrt(head_dim) is reading Z24); 16-B aligned pointers.  Two kernel launches. */
 quarot_status quarot_kv_decode(const void* q, const uint8_t* k_codes, const float* k_scale,
                                const uint8_t* k_zero, const uint8_t* v_codes, const float* v_scale,

@@ -141,8 +141,8 @@ template <int LPG, bool kQ8 = false>  // lanes per group = G / 8; kQ8: int8 code
 __global__ void __launch_bounds__(128) hq_none_group_kernel(const __half* __restrict__ x, int64_t K, int64_t ld_x,
                                                             float clip, uint8_t* __restrict__ q, int64_t ld_q,
                                                             float* __restrict__ scale, int64_t ld_s) {
-  const int64_t row = blockIdx.y;
-  const int64_t c = (int64_t)blockIdx.x * 128 + threadIdx.x;  // chunk (all lanes of a group exist: K % G == 0)
+  const int64_t row = blockIdx.x;  // rows on x (up to 2^31 - 1), chunk blocks on y
+  const int64_t c = (int64_t)blockIdx.y * 128 + threadIdx.x;  // chunk (all lanes of a group exist: K % G == 0)
   const bool ok = c < (K >> 3);
   uint4 v = make_uint4(0u, 0u, 0u, 0u);
   if (ok) v = ldg_nc_v4(x + row * ld_x + c * 8);
@@ -788,7 +788,7 @@ cudaError_t launch_hq_none(const void* x, int64_t M, int64_t K, int64_t ld_x, fl
 
 cudaError_t launch_hq_none_group(const void* x, int64_t M, int64_t K, int64_t ld_x, int group, float clip,
                                  uint8_t* q, int64_t ld_q, float* scale, int64_t ld_s, cudaStream_t stream, bool q8) {
-  const dim3 grid((unsigned)((K / 8 + 127) / 128), (unsigned)M);
+  const dim3 grid((unsigned)M, (unsigned)((K / 8 + 127) / 128));
   const __half* xh = static_cast<const __half*>(x);
 #define QR_G(L)                                                                                                \
   do {                                                                                                         \

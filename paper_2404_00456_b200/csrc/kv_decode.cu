@@ -384,9 +384,9 @@ __global__ void __launch_bounds__(HD) kv_decode_combine(const float* __restrict_
 
 }  // namespace kvd
 
-size_t kv_decode_workspace_bytes(int B, int n_q, int head_dim, int s_max) {
-  const int nsplit = (s_max + kvd::CHUNK - 1) / kvd::CHUNK;
-  return (size_t)B * n_q * nsplit * (head_dim + 2) * sizeof(float);
+int64_t kv_decode_workspace_bytes(int64_t B, int64_t n_q, int64_t head_dim, int64_t s_max) {
+  const int64_t nsplit = (s_max + kvd::CHUNK - 1) / kvd::CHUNK;
+  return B * n_q * nsplit * (head_dim + 2) * (int64_t)sizeof(float);
 }
 
 cudaError_t launch_kv_decode(const void* q, const uint8_t* k_codes, const float* k_scale, const uint8_t* k_zero,

@@ -93,6 +93,12 @@ quarot_status quarot_hadamard_quant(const void* x, int64_t M, int64_t K, int64_t
     if (!pow2(head_dim) || head_dim < 64 || !pow2(K / head_dim) || K / head_dim > 512)
       return QUAROT_ERR_UNSUPPORTED_SIZE;
     if (K % 32) return QUAROT_ERR_ALIGN;
+    if (!qr::hq_heads_tc_supported(K, head_dim)) {
+      // CUDA-core fallback limits: (head_dim / 2) x G threads <= 256 with G = max(1, n_h / 32)
+      // head groups, and the row staged in shared memory (4.5 K bytes)
+      const int64_t nh = K / head_dim, G = nh > 32 ? nh / 32 : 1;
+      if (head_dim / 2 * G > 256 || K > 32768) return QUAROT_ERR_UNSUPPORTED_SIZE;
+    }
     e = qr::launch_hq_heads(x, M, K, ld_x, head_dim, clip_ratio, q, ld_q, scale, st);
   } else {
     int64_t p = 0;
@@ -119,7 +125,9 @@ static quarot_status check_gemm(const uint8_t* xq, int64_t M, int64_t K, int64_t
   if (!xq || !wq || !out) return QUAROT_ERR_NULL;
   if (K % 128 || N % 8 || ld_xq % 16 || ld_wq % 16 || ld_out % out_elems_align) return QUAROT_ERR_ALIGN;
   if (!aligned16(xq) || !aligned16(wq) || !aligned16(out)) return QUAROT_ERR_ALIGN;
-  if (K > 171196) return QUAROT_ERR_UNSUPPORTED_SIZE;  // 256 * 49 * K must fit int32
+  // the MMA accumulates 256 * acc with |acc| <= 7 * 8 * K (activation codes in [-7, 7], weight
+  // codes in [-8, 7]): exact in int32 for K <= 149796
+  if (K > 149796) return QUAROT_ERR_UNSUPPORTED_SIZE;
   return QUAROT_OK;
 }
 
@@ -221,7 +229,8 @@ static quarot_status hq_group_impl(const void* x, int64_t M, int64_t K, int64_t 
   if (!(group == 64 || group == 128 || group == 256)) return QUAROT_ERR_UNSUPPORTED_SIZE;
   if (M < 0 || K <= 0 || K % 2 || ld_x < K || ld_q < (q8 ? K : K / 2) || ld_s < K / group) return QUAROT_ERR_DIM;
   if (K % group) return QUAROT_ERR_DIM;
-  if (M > 0xffffLL * 1024) return QUAROT_ERR_DIM;
+  if (M > 0x7fffffffLL) return QUAROT_ERR_DIM;              // rows on gridDim.x
+  if (K > 0xffffLL * 1024) return QUAROT_ERR_UNSUPPORTED_SIZE;  // 1024-element blocks on gridDim.y
   if (M == 0) return QUAROT_OK;
   if (!x || !q || !scale) return QUAROT_ERR_NULL;
   if (!aligned16(x) || !aligned16(q) || (ld_x % 8) || (ld_q % (q8 ? 8 : 4))) return QUAROT_ERR_ALIGN;
@@ -424,8 +433,8 @@ quarot_status quarot_kv_append(const void* k, int64_t ld_k, const void* v, int64
 }
 
 int64_t quarot_kv_decode_workspace_bytes(int64_t B, int32_t n_q, int32_t head_dim, int64_t s_max) {
-  if (B <= 0 || n_q <= 0 || head_dim <= 0 || s_max <= 0) return 0;
-  return (int64_t)qr::kv_decode_workspace_bytes((int)B, n_q, head_dim, (int)s_max);
+  if (B <= 0 || n_q <= 0 || head_dim <= 0 || s_max <= 0 || B > 65535 || s_max > (1 << 30)) return 0;
+  return qr::kv_decode_workspace_bytes(B, n_q, head_dim, s_max);
 }
 
 quarot_status quarot_kv_decode(const void* q, const uint8_t* k_codes, const float* k_scale,
@@ -435,6 +444,7 @@ quarot_status quarot_kv_decode(const void* q, const uint8_t* k_codes, const floa
                                float* workspace, int64_t workspace_bytes, void* stream) {
   g_last_launches = 0;
   if (B < 0 || n_q <= 0 || n_kv <= 0 || head_dim <= 0 || s_max <= 0 || s_max > (1 << 30)) return QUAROT_ERR_DIM;
+  if (B > 65535 || n_kv > 65535) return QUAROT_ERR_DIM;  // grid (split, n_kv, B)
   if (n_q % n_kv) return QUAROT_ERR_DIM;
   const int G = n_q / n_kv;
   if (head_dim != 128 || !(G == 1 || G == 2 || G == 4 || G == 8)) return QUAROT_ERR_UNSUPPORTED_SIZE;

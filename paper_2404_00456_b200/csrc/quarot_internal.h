@@ -75,7 +75,7 @@ cudaError_t launch_int8_gemm(const int8_t* xq, const float* xs, int64_t M, int64
 cudaError_t launch_int8_gemm_s32(const int8_t* xq, int64_t M, int64_t K, int64_t ld_xq, const int8_t* wq, int64_t N,
                                  int64_t ld_wq, int32_t* acc, int64_t ld_acc, cudaStream_t stream);
 // KV Decode: split-sequence flash decoding over the INT4 cache + the combine pass.
-size_t kv_decode_workspace_bytes(int B, int n_q, int head_dim, int s_max);
+int64_t kv_decode_workspace_bytes(int64_t B, int64_t n_q, int64_t head_dim, int64_t s_max);
 cudaError_t launch_kv_decode(const void* q, const uint8_t* k_codes, const float* k_scale, const uint8_t* k_zero,
                              const uint8_t* v_codes, const float* v_scale, const uint8_t* v_zero,
                              const int32_t* seq_lens, int B, int n_q, int n_kv, int head_dim, int s_max,

@@ -136,7 +136,7 @@ def hadamard_quant(x: torch.Tensor, mode="none", head_dim: int = 128, clip_ratio
         scale = torch.empty(M, dtype=torch.float32, device=x.device)
     st = lib().quarot_hadamard_quant(_dev(x, "x", torch.float16), M, K, x.stride(0), mode_i, head_dim,
                                      clip_ratio, _dev(q, "q", torch.uint8), q.stride(0),
-                                     _dev(scale, "scale", torch.float32), None, _stream(stream))
+                                     _dev(scale, "scale", torch.float32), _stream(stream))
     _check("quarot_hadamard_quant", st)
     return q, scale
 

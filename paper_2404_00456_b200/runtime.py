@@ -11,7 +11,7 @@ prefill uses them (Fig. ffn_quarot, Fig. attn_quarot, App. P
 
 = 9 kernel launches through the C ABI (`PrefillStep`, rows a1-a7 with independent synthetic
 inputs per linear).  `DecoderLayerStep` adds the a8 glue and chains the linears into a real
-decoder layer (attention core excluded): 11 launches, the bench default.
+decoder layer (attention core excluded): 9 launches with every fusion on, the bench default.
 
 `run_device` enqueues a step on one stream with inputs resident in HBM.  `run_host` is
 the end-to-end path for callers whose activations live in (pinned) host memory: the

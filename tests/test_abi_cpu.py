@@ -152,3 +152,101 @@ def test_hadamard_quant8_validation_without_gpu(q):
     assert f(q.FULL, 8192) == 3                      # 8-bit FULL only for K = 1024 x 28
     assert f(q.ACROSS_HEADS, 512) == 3               # 4 heads: not on the 8-bit path
     assert f(q.FULL | q.RMSNORM, 28672) == 5         # RMSNorm only with mode NONE
+
+
+# ---------------------------------------------------------------- binding marshalling
+
+_CTYPE = {"int64_t": "c_int64", "int32_t": "c_int", "uint32_t": "c_uint", "float": "c_float"}
+
+
+def declared_signatures():
+    """name -> list of ctypes type names, parsed from include/quarot.h."""
+    src = re.sub(r"/\*.*?\*/", "", open(HEADER).read(), flags=re.S)
+    sigs = {}
+    for m in re.finditer(r"\b(?:quarot_status|int64_t|int32_t|const char\*)\s+(quarot_[a-z0-9_]+)\s*\(([^)]*)\)\s*;",
+                         src):
+        params = [p.strip() for p in m.group(2).split(",") if p.strip() and p.strip() != "void"]
+        types = []
+        for p in params:
+            t = p.rsplit(None, 1)[0] if "*" not in p else "ptr"
+            types.append("c_void_p" if t == "ptr" else _CTYPE[t.replace("const ", "").strip()])
+        sigs[m.group(1)] = types
+    return sigs
+
+
+def test_binding_argtypes_match_header(q):
+    """Every ctypes signature in quarot.py has the header's parameter count and types."""
+    import ctypes as ct
+    decl = declared_signatures()
+    assert set(decl) == set(q.EXPORTS)
+    for name, args in q._SIGS.items():
+        got = [a.__name__ for a in args]
+        want = decl[name]
+        norm = {"c_long": "c_int64", "c_longlong": "c_int64", "c_int32": "c_int", "c_uint32": "c_uint"}
+        got = [norm.get(g, g) for g in got]
+        want = [norm.get(w, w) for w in want]
+        assert got == want, f"{name}: binding {got} vs header {want}"
+    assert ct.sizeof(ct.c_int) == 4
+
+
+class _FakeLib:
+    """Records calls and checks each one passes exactly the declared number of arguments
+    (ctypes itself silently accepts extra trailing arguments for cdecl functions)."""
+
+    def __init__(self, sigs):
+        self.sigs, self.calls = sigs, []
+
+    def __getattr__(self, name):
+        def fn(*args):
+            assert len(args) == len(self.sigs[name]), f"{name}: {len(args)} args, header has {len(self.sigs[name])}"
+            self.calls.append((name, args))
+            if name == "quarot_kv_decode_workspace_bytes":
+                return 64
+            return 0
+        return fn
+
+
+def test_every_wrapper_passes_declared_arity_and_stream(monkeypatch):
+    """Call every Python wrapper against a fake library (CPU tensors stand in for device ones):
+    each call has the header's arity and its LAST argument is the caller's stream handle."""
+    import torch
+    from paper_2404_00456_b200 import quarot as qq
+    fake = _FakeLib(declared_signatures())
+    monkeypatch.setattr(qq, "lib", lambda: fake)
+    monkeypatch.setattr(qq, "_dev", lambda t, name, dtype=None: t.data_ptr())
+    STREAM = 0xABC0
+    u8 = lambda *s: torch.zeros(*s, dtype=torch.uint8)
+    f16 = lambda *s: torch.zeros(*s, dtype=torch.float16)
+    f32 = lambda *s: torch.zeros(*s, dtype=torch.float32)
+    i8 = lambda *s: torch.zeros(*s, dtype=torch.int8)
+    dev = torch.device("cpu")
+    x = f16(4, 256)
+    qq.hadamard_quant(x, "full", stream=STREAM)
+    qq.hadamard_quant(x, "none", rmsnorm=True, stream=STREAM)
+    xq, xs, wq, ws = u8(4, 128), f32(4), u8(16, 128), f32(16)
+    qq.int4_linear(xq, xs, wq, ws, stream=STREAM)
+    qq.int4_linear(xq, xs, wq, ws, residual=f16(4, 16), stream=STREAM)
+    qq.int4_linear_swiglu(xq, xs, wq, ws, stream=STREAM)
+    qq.int4_matmul_s32(xq, wq, stream=STREAM)
+    qq.rope(f16(4, 2, 128), stream=STREAM)
+    qq.swiglu(f16(4, 32), stream=STREAM)
+    k, v, qh = f16(4, 2, 128), f16(4, 2, 128), f16(4, 4, 128)
+    out = {n: u8(4, 2, 64) if "codes" in n else (f32(4, 2) if "scale" in n else u8(4, 2))
+           for n in ("k_codes", "k_scale", "k_zero", "v_codes", "v_scale", "v_zero")}
+    qq.kv_quant(k, v, qh, out=out, stream=STREAM)
+    qq.kv_quant(k, v, qh, out=out, rope=(0, 2048, 1e4), stream=STREAM)
+    qq.hadamard_quant_group(x, stream=STREAM)
+    qq.hadamard_quant_group8(x, stream=STREAM)
+    qq.int4_linear_group(i8(4, 256), f32(4, 2), i8(16, 256), f32(2, 16), stream=STREAM)
+    qq.hadamard_quant8(x, stream=STREAM)
+    qq.int8_linear(i8(4, 256), f32(4), i8(16, 256), f32(16), stream=STREAM)
+    qq.int8_matmul_s32(i8(4, 256), i8(16, 256), stream=STREAM)
+    cache = qq.kv_cache_empty(2, 8, 2, 128, device=dev)
+    pos = torch.zeros(2, dtype=torch.int32)
+    monkeypatch.setattr(torch.Tensor, "device", property(lambda self: dev), raising=False)
+    qq.kv_append(f16(2, 2, 128), f16(2, 2, 128), f16(2, 4, 128), pos, cache, stream=STREAM)
+    qq.kv_decode(f16(2, 4, 128), cache, pos, stream=STREAM)
+    launched = [c for c in fake.calls if c[0] != "quarot_kv_decode_workspace_bytes"]
+    assert len(launched) >= 18
+    for name, args in launched:
+        assert args[-1] == STREAM, f"{name}: stream not forwarded (last arg {args[-1]!r})"
