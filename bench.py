@@ -2,19 +2,23 @@
 """QuaRot hot-path benchmark (driver contract).
 
 A step = one pass of every SURVEY §8(a) row over one batch: one Llama-2-70B decoder layer
-(hidden 8192, FFN 28672 = 1024 x H_28, 64 Q / 8 KV heads x 128) prefilling 64 x 2048 = 131072
-tokens per GPU, as the chain of runtime.DecoderLayerStep (attention core excluded):
-RMSNorm+quantize -> INT4 QKV GEMM -> RoPE -> KV-cache Init (+Q rotation) ; Hadamard-heads +
-quantize -> INT4 O GEMM + residual ; RMSNorm+quantize -> INT4 gate/up GEMM -> SwiGLU ;
+(hidden 8192, FFN 28672 = 1024 x H_28, 64 Q / 8 KV heads x 128) prefilling the 64 x 2048 =
+131072-token batch, as the chain of runtime.DecoderLayerStep (attention core excluded):
+RMSNorm+quantize -> INT4 QKV GEMM -> RoPE + KV-cache Init (+Q rotation) ; Hadamard-heads +
+quantize -> INT4 O GEMM + residual ; RMSNorm+quantize -> INT4 gate/up GEMM + SwiGLU ;
 Hadamard (1024 x H_28) + quantize -> INT4 down GEMM + residual (9 kernel launches, all ours).
-`--step linears` times rows a1-a7 alone on independent inputs (9 launches).
+`--step linears` times rows a1-a7 alone on independent inputs (9 launches); `--config 7b` runs
+BASELINE config 2 (Llama-2-7B, 8 x 2048 tokens, down_proj K = 64 x H_172).
 
-  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+  python bench.py [--gpus N --steps K --warmup W] [--config 70b|7b] [--impl reference]
 
-N > 1 runs under torchrun, one process per GPU; each rank processes its own 64 x 2048
-batch (token sharding, weak scaling, no collective on the data path); rank 0 prints one
-JSON line with the whole-job tokens/s = N * tokens / max-over-ranks time.
-`--impl reference` times the CPU oracle (the parity reference) on a bounded token sample.
+N > 1 runs one process per GPU (under torchrun; `--gpus N` without WORLD_SIZE self-spawns that
+launch).  Strong scaling (default): the fixed global batch is split into N
+contiguous row shards, no collective on the data path; rank 0 prints one JSON line with the
+whole-job tokens/s = global tokens / max-over-ranks time, after an NCCL all_gather of every
+rank's layer output and KV cache checked bitwise against an unsharded run.  `--scaling weak`
+gives every rank the whole batch.  `--impl reference` times the CPU oracle (the parity
+reference) on a bounded token sample.
 """
 from __future__ import annotations
 
@@ -37,7 +41,6 @@ import synth  # noqa: E402
 
 METRIC = "llama2-70b layer prefill tokens/s (QuaRot W4A4 hot path)"
 UNIT = "tokens/s"
-WORKLOAD = "llama2-70b-layer-prefill-64x2048"
 
 
 def _peaks():
@@ -107,28 +110,67 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def make_layer(device, seed_base=1000):
+CONFIGS = {  # BASELINE.json configs served by the bench: name -> (shapes, global batch, seq_len, workload)
+    "70b": (synth.inputs.LLAMA2_70B, 64, 2048, "llama2-70b-layer-prefill-64x2048"),   # configs 3 / 5
+    "7b": (synth.inputs.LLAMA2_7B, 8, 2048, "llama2-7b-layer-prefill-8x2048"),        # config 2
+}
+
+
+def make_layer(device, seed_base=1000, shapes=None):
     from paper_2404_00456_b200.runtime import QuaRotLayer
-    S = synth.inputs.LLAMA2_70B
-    shapes = {"qkv": (S.qkv_out, S.hidden), "o": (S.hidden, S.hidden), "gate_up": (2 * S.ffn, S.hidden),
-              "down": (S.hidden, S.ffn)}
+    S = shapes or synth.inputs.LLAMA2_70B
+    dims = {"qkv": (S.qkv_out, S.hidden), "o": (S.hidden, S.hidden), "gate_up": (2 * S.ffn, S.hidden),
+            "down": (S.hidden, S.ffn)}
     weights = {}
-    for i, (name, (n, k)) in enumerate(shapes.items()):
+    for i, (name, (n, k)) in enumerate(dims.items()):
         weights[name] = (synth.packed_weight_codes(n, k, seed_base + i, device=device),
                          synth.weight_scales(n, seed_base + 10 + i, device=device))
     return QuaRotLayer(S.hidden, S.ffn, S.n_heads, S.n_kv_heads, S.head_dim, weights)
 
 
-def make_inputs(tokens, device, rank, step="chain"):
-    S = synth.inputs.LLAMA2_70B
-    base = 100 + 10 * rank
+def make_inputs(tokens, device, rank, step="chain", shapes=None, rows=None):
+    """Seeded synthetic inputs of `tokens` rows.  rows = (r0, r1): strong scaling — the rows
+    [r0, r1) of the one global batch every rank generates identically (so a sharded run can be
+    checked bitwise against the unsharded one); rows = None: weak scaling, a rank-seeded batch."""
+    S = shapes or synth.inputs.LLAMA2_70B
+    base = 100 + (0 if rows is not None else 10 * rank)
     if step == "chain":
-        return {"x": synth.activations(tokens, S.hidden, "outlier", base + 0, device),
-                "attn_out": synth.activations(tokens, S.hidden, "normal", base + 1, device)}
-    return {"attn_in": synth.activations(tokens, S.hidden, "outlier", base + 0, device),
-            "attn_out": synth.activations(tokens, S.hidden, "normal", base + 1, device),
-            "ffn_in": synth.activations(tokens, S.hidden, "outlier", base + 2, device),
-            "ffn_act": synth.activations(tokens, S.ffn, "swiglu", base + 3, device)}
+        spec = {"x": (S.hidden, "outlier", 0), "attn_out": (S.hidden, "normal", 1)}
+    else:
+        spec = {"attn_in": (S.hidden, "outlier", 0), "attn_out": (S.hidden, "normal", 1),
+                "ffn_in": (S.hidden, "outlier", 2), "ffn_act": (S.ffn, "swiglu", 3)}
+    out = {}
+    for name, (k, kind, off) in spec.items():
+        t = synth.activations(tokens, k, kind, base + off, device)
+        out[name] = t if rows is None else t[rows[0]:rows[1]].contiguous()
+        del t
+    return out
+
+
+def plan_shard(global_tokens: int, world: int, rank: int, scaling: str):
+    """(r0, r1, local_tokens, job_tokens): strong scaling splits the fixed global batch into
+    contiguous row shards (GPU g takes sequences [g*B/G, (g+1)*B/G)); weak scaling
+    gives every rank the whole batch."""
+    from paper_2404_00456_b200 import dist as qd
+    if scaling == "strong":
+        r0, r1 = qd.shard_bounds(global_tokens, world, rank)
+        return r0, r1, r1 - r0, global_tokens
+    return 0, global_tokens, global_tokens, global_tokens * world
+
+
+def torchrun_cmd(gpus: int, argv: list, port: int) -> list:
+    """The launch the driver uses for N > 1 (one process per GPU over NCCL), for self-spawning."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *argv]
+
+
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
 
 
 def load_traffic():
@@ -166,19 +208,19 @@ def oracle_step(host_in: dict, host_w: dict, layer_dims: dict) -> None:
     return outs
 
 
-def _block_linear(cx, sx, wq, ws, residual=None):
-    """Oracle int4 linear with the packed weights unpacked in row blocks (memory bound)."""
+def _block_linear(cx, sx, wq, ws, residual=None, rows=None):
+    """Oracle int4 linear (fp16 output) with the packed weights unpacked in row blocks
+    (memory bound); `rows` selects weight rows; residual: the FP16 model's add."""
+    from oracle import glue as oglue
     from oracle import layer as olayer
     from oracle import quant as oquant
+    rows = np.arange(wq.shape[0]) if rows is None else np.asarray(rows)
     ys = []
-    for r0 in range(0, wq.shape[0], 2048):
-        cw = oquant.unpack_int4_signed(wq[r0:r0 + 2048])
-        acc = olayer.int4_linear(cx, sx, cw, ws[r0:r0 + 2048])[0]
-        ys.append(acc * sx.astype(np.float64)[:, None] * ws[r0:r0 + 2048].astype(np.float64)[None, :])
+    for r0 in range(0, len(rows), 2048):
+        sel = rows[r0:r0 + 2048]
+        ys.append(olayer.int4_linear(cx, sx, oquant.unpack_int4_signed(wq[sel]), ws[sel])[1])
     y = np.concatenate(ys, axis=1)
-    if residual is not None:
-        y = y + residual.astype(np.float64)
-    return y.astype(np.float16)
+    return y if residual is None else oglue.add_fp16(residual, y)
 
 
 def oracle_chain_step(host_in: dict, host_w: dict, dims: dict, positions) -> dict:
@@ -198,14 +240,8 @@ def oracle_chain_step(host_in: dict, host_w: dict, dims: dict, positions) -> dic
     cz, _, sz = olayer.hadamard_quant(host_in["attn_out"].astype(np.float64), "across_heads", d)
     o = _block_linear(cz, sz, *host_w["o"], residual=x)
     co, _, so = oglue.rmsnorm_quant(o.astype(np.float64))
-    wq_gu, ws_gu = host_w["gate_up"]
-    acts = []
-    for f0 in range(0, F, 1024):  # gate/up rows in blocks (memory bound), SwiGLU on fp64 values
-        from oracle import quant as oquant
-        f1 = min(F, f0 + 1024)
-        rows_blk = np.concatenate([np.arange(f0, f1), F + np.arange(f0, f1)])
-        acts.append(oglue.linear_swiglu(co, so, oquant.unpack_int4_signed(wq_gu[rows_blk]), ws_gu[rows_blk], f1 - f0))
-    act = np.concatenate(acts, axis=1)
+    gu = _block_linear(co, so, *host_w["gate_up"])            # fp16 [gate | up]
+    act = oglue.swiglu_fp16(gu[:, :F], gu[:, F:])
     ca, _, sa = olayer.hadamard_quant(act.astype(np.float64), "full", d)
     return {"out": _block_linear(ca, sa, *host_w["down"], residual=o), "cache": cache}
 
@@ -242,9 +278,10 @@ def run_reference(args):
     if rank != 0:
         return 0
     device = "cuda" if torch.cuda.is_available() else "cpu"
-    layer = make_layer(device)
+    shapes, batch, seq_len, workload = CONFIGS[args.config]
+    layer = make_layer(device, shapes=shapes)
     sample = args.ref_tokens
-    inputs = make_inputs(sample * 16, device, 0, args.step)
+    inputs = make_inputs(sample * 16, device, 0, args.step, shapes)
     host_in, host_w, rows = host_sample(inputs, layer, sample)
     for _ in range(args.warmup):
         run_oracle(args, host_in, host_w, layer, rows)
@@ -254,12 +291,13 @@ def run_reference(args):
     dt = (time.perf_counter() - t0) / args.steps
     cores, blas = cpu_threads()
     value = sample / dt
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "step": args.step, "tokens_per_step": sample,
-                       "sample": f"{sample} tokens of the 64x2048 batch through the whole {args.step} step "
-                                 "(full-width layer, dense fp64 Hadamard, int64 GEMM)"},
+    line = {"impl": "reference", "metric": metric_for(args.config), "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": workload, "step": args.step, "tokens_per_step": sample,
+                       "sample": f"{sample} tokens of the {batch}x{seq_len} batch through the whole {args.step} "
+                                 "step (full-width layer, dense fp64 Hadamard, int64 GEMM)"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "blas_threads": blas,
                              "kind": "oracle", "sample": f"{sample} tokens per step"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -270,21 +308,36 @@ def run_reference(args):
 
 # ----------------------------------------------------------------------------- ours
 
+def metric_for(config: str) -> str:
+    return METRIC if config == "70b" else f"llama2-{config} layer prefill tokens/s (QuaRot W4A4 hot path)"
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--tokens", type=int, default=64 * 2048, help="tokens per GPU per step")
+    ap.add_argument("--config", default="70b", choices=sorted(CONFIGS),
+                    help="70b: BASELINE configs 3/5 (64 x 2048 tokens); 7b: config 2 (8 x 2048 tokens)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong (SURVEY §8e): the fixed global batch split into row shards; weak: every GPU "
+                         "runs the whole batch")
+    ap.add_argument("--tokens", type=int, default=0, help="global batch tokens (default: the config's B x 2048)")
     ap.add_argument("--ref-tokens", type=int, default=2, help="oracle sample tokens per step")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-verify", action="store_true", help="N > 1: skip the NCCL gather + bitwise check")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--profile-steps", type=int, default=0, help="run N untimed steps and exit (ncu)")
     ap.add_argument("--step", default="chain", choices=["chain", "linears"],
                     help="chain: the decoder-layer chain (a1-a8, 9 launches); linears: a1-a7 on independent inputs")
     args = ap.parse_args()
+    shapes, batch, seq_len, workload = CONFIGS[args.config]
+    global_tokens = args.tokens or batch * seq_len
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # self-spawn the driver's launch: one process per GPU (torchrun, 127.0.0.1 rendezvous)
+        return subprocess.call(torchrun_cmd(args.gpus, sys.argv[1:], _free_port()))
     if args.impl == "reference":
         return run_reference(args)
 
@@ -301,10 +354,17 @@ def main():
     from paper_2404_00456_b200 import dist as qd
     from paper_2404_00456_b200.runtime import DecoderLayerStep, HostPipeline, PrefillStep
     q.lib()
-    layer = make_layer(dev)
-    T = args.tokens
-    inputs = make_inputs(T, dev, rank, args.step)
-    step = DecoderLayerStep(layer, T, dev) if args.step == "chain" else PrefillStep(layer, T, dev)
+    layer = make_layer(dev, shapes=shapes)
+    r0, r1, T, job_tokens = plan_shard(global_tokens, world, rank, args.scaling)
+    strong = args.scaling == "strong"
+    inputs = make_inputs(global_tokens, dev, rank, args.step, shapes, rows=(r0, r1) if strong else None)
+
+    def new_step(tokens, row_offset):
+        if args.step == "chain":
+            return DecoderLayerStep(layer, tokens, dev, seq_len=seq_len, row_offset=row_offset)
+        return PrefillStep(layer, tokens, dev)
+
+    step = new_step(T, r0 if strong else 0)
     stream = torch.cuda.current_stream()
     if args.profile_steps:
         for _ in range(args.profile_steps):
@@ -337,12 +397,12 @@ def main():
         t_end.record(stream)
         torch.cuda.synchronize()
     barrier()
-    ms = t_start.elapsed_time(t_end) / args.steps
+    ms_local = t_start.elapsed_time(t_end) / args.steps
     for evs in all_events:
         for (_, a), (name, b) in zip(evs[:-1], evs[1:]):
             per_kernel.setdefault(name, []).append(a.elapsed_time(b))
     kern_ms = {k: sum(v) / len(v) for k, v in per_kernel.items()}
-    ms = qd.max_over_ranks(ms, dev)  # max over ranks (no-op at N = 1)
+    ms = qd.max_over_ranks(ms_local, dev)  # max over ranks (no-op at N = 1)
     clocks = clk.summary()
 
     # ---- roofline of the dominant kernel (the INT4 GEMM) and the HBM-bound kernels
@@ -354,12 +414,11 @@ def main():
     hq_gbs = layer.hq_bytes(T) / (hq_ms * 1e-3) / 1e9
     kv_gbs = layer.kv_bytes(T) / (kern_ms["kv_quant"] * 1e-3) / 1e9
     glue_bytes = {"rope": T * (layer.n_heads + layer.n_kv) * layer.head_dim * 4, "swiglu": T * layer.ffn * 6}
-    if args.step == "chain" and step.fuse_swiglu:  # the gate/up GEMM writes act (F wide), not gate|up
-        kernels_note = "gate/up GEMM epilogue computes SwiGLU (writes act)"
     traffic = load_traffic()
     kernels = {}
     for s in layer.specs:
-        kernels[f"gemm_{s.name}"] = {"ms": kern_ms[f"gemm_{s.name}"], "tops": 2 * T * s.n * s.k / (kern_ms[f"gemm_{s.name}"] * 1e-3) / 1e12}
+        kernels[f"gemm_{s.name}"] = {"ms": kern_ms[f"gemm_{s.name}"],
+                                     "tops": 2 * T * s.n * s.k / (kern_ms[f"gemm_{s.name}"] * 1e-3) / 1e12}
         kernels[f"hq_{s.name}"] = {"ms": kern_ms[f"hq_{s.name}"], "mode": s.mode,
                                    "gbs": T * (2.5 * s.k + 4) / (kern_ms[f"hq_{s.name}"] * 1e-3) / 1e9}
         kernels[f"hq_{s.name}"]["frac_hbm"] = kernels[f"hq_{s.name}"]["gbs"] / peaks["hbm_gbs"]
@@ -370,14 +429,14 @@ def main():
             g_gbs = gb / (kern_ms[gname] * 1e-3) / 1e9
             kernels[gname] = {"ms": kern_ms[gname], "gbs": g_gbs, "frac_hbm": g_gbs / peaks["hbm_gbs"]}
 
-    tokens_total = T * world
     line = {
-        "metric": METRIC, "value": qd.aggregate_throughput(T, ms, world), "unit": UNIT, "n_gpus": world,
+        "metric": metric_for(args.config), "value": job_tokens / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int4xint4->int32 (fp16 io, fp32 transform)",
-        "data": "synthetic (seeded; random INT4 weight codes, Llama-2-70B shapes)",
-        "config": {"workload": WORKLOAD, "step": args.step, "tokens_per_gpu": T, "global_batch": 64 * world,
-                   "seq_len": 2048,
+        "scaling": "strong" if strong else "weak", "vs_baseline": None,
+        "dtype": "int4xint4->int32 (fp16 io, fp32 transform)",
+        "data": f"synthetic (seeded; random INT4 weight codes, {shapes.name} shapes)",
+        "config": {"workload": workload, "step": args.step, "global_batch": batch if strong else batch * world,
+                   "seq_len": seq_len, "tokens_per_gpu": T, "job_tokens": job_tokens, "rows": [r0, r1],
                    "hidden": layer.hidden, "ffn": layer.ffn, "heads": [layer.n_heads, layer.n_kv, layer.head_dim],
                    "parallelism": f"token-shard x{world} (no data-path collective)",
                    "l2": "inputs larger than L2 (GB-scale activations per step)",
@@ -397,6 +456,8 @@ def main():
         "gpu_launches": step.LAUNCHES * args.steps,
         "clocks": clocks,
     }
+    if world > 1:
+        line["per_rank_ms"] = _gather_floats(ms_local, world, dev)
 
     # ---- end to end through the public API with pinned host buffers
     if not args.no_e2e:
@@ -416,12 +477,30 @@ def main():
             torch.cuda.synchronize()
             e_ms = e0.elapsed_time(e1) / args.e2e_steps
             e_ms = qd.max_over_ranks(e_ms, dev)
-            line["e2e"] = {"value": qd.aggregate_throughput(T, e_ms, world), "unit": UNIT,
+            line["e2e"] = {"value": job_tokens / (e_ms * 1e-3), "unit": UNIT,
                            "h2d_bytes_per_step": pipe.h2d_bytes(), "d2h_bytes_per_step": pipe.d2h_bytes(),
                            "ms_per_step": e_ms, "chunks": 8, "steps": args.e2e_steps}
             del pipe, host_in
         except Exception as exc:  # noqa: BLE001
             line["e2e"] = {"value": None, "unit": UNIT, "error": repr(exc)[:200]}
+
+    # ---- N > 1: gather the sharded results over NCCL and check them bitwise against an
+    #      unsharded run of the whole batch on rank 0 (outside every timed region)
+    if world > 1 and strong and not args.no_verify:
+        local_res = {k: t for k, t in step.result_tensors().items()}
+        ref = None
+        if rank == 0:
+            full_in = make_inputs(global_tokens, dev, 0, args.step, shapes, rows=(0, global_tokens))
+            ref_step = new_step(global_tokens, 0)
+            ref_step.run_device(full_in, stream)
+            torch.cuda.synchronize()
+            ref = ref_step.result_tensors()
+        res = qd.gather_and_compare(local_res, global_tokens, ref)
+        if rank == 0:
+            line["verify"] = {"gathered": sorted(res), "bitwise_equal_to_1gpu": all(res.values()),
+                              "how": "NCCL all_gather of every rank's layer output and KV cache rows vs one "
+                                     "unsharded run of the whole batch on rank 0"}
+        del ref
 
     # ---- CPU oracle baseline (rank 0, N == 1 only)
     if not args.no_cpu_baseline and world == 1 and rank == 0:
@@ -442,6 +521,14 @@ def main():
     if rank == 0:
         print(json.dumps(line), flush=True)
     return 0
+
+
+def _gather_floats(v: float, world: int, dev) -> list:
+    import torch.distributed as dist
+    t = torch.tensor([float(v)], dtype=torch.float64, device=dev)
+    outs = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(outs, t)
+    return [float(o.item()) for o in outs]
 
 
 if __name__ == "__main__":

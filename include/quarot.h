@@ -119,7 +119,9 @@ quarot_status quarot_int4_linear(const uint8_t* xq, const float* x_scale, int64_
                                  int64_t N, int64_t ld_wq, void* y, int64_t ld_y, void* stream);
 
 /* quarot_int4_linear with the residual add of the decoder layer fused into the epilogue
- * (SURVEY §8 a8): y = fp16_rn( (fp32)acc * x_scale[m] * w_scale[n] + (fp32)residual[m][n] ).
+ * (SURVEY §8 a8): y = fp16_rn( (fp32)fp16_rn((fp32)acc * x_scale[m] * w_scale[n]) + (fp32)residual[m][n] )
+ *   — the linear output is cast to FP16 first ("immediately cast (and scale) to FP16"), then
+ *   the FP16 model's residual add; bitwise equal to quarot_int4_linear followed by an fp16 add.
  *   residual fp16 [M][ld_r] (ld_r % 8 == 0, 16-B aligned); it may alias y (in-place add). */
 quarot_status quarot_int4_linear_residual(const uint8_t* xq, const float* x_scale, int64_t M, int64_t K,
                                           int64_t ld_xq, const uint8_t* wq, const float* w_scale,
@@ -130,9 +132,11 @@ quarot_status quarot_int4_linear_residual(const uint8_t* xq, const float* x_scal
  * the N2 = 2F rows of wq / w_scale are the gate and up rows interleaved in blocks of 8 —
  * row 16j + i is gate feature 8j + i and row 16j + 8 + i is up feature 8j + i (i < 8), an
  * offline layout choice (quarot.interleave_gate_up) — and the output is
- *   act[m][f] = fp16_rn( silu(g) * u ),  g = acc_gate * x_scale[m] * w_scale[gate row],
- *   u = acc_up * x_scale[m] * w_scale[up row]  (fp32; the gate/up products are never rounded
- *   to fp16).  act fp16 [M][ld_act], ld_act >= N2/2, % 8 == 0.  N2 % 16 == 0. */
+ *   act[m][f] = fp16_rn( fp16_rn(silu(g)) * u ),  g = fp16_rn(acc_gate * x_scale[m] * w_scale[gate row]),
+ *   u = fp16_rn(acc_up * x_scale[m] * w_scale[up row])  — the fp16 linear outputs through
+ *   the FP16 model's SiLU and multiply (reading Z23); bitwise equal to quarot_int4_linear on the
+ *   de-interleaved weights followed by quarot_swiglu.
+ *   act fp16 [M][ld_act], ld_act >= N2/2, % 8 == 0.  N2 % 16 == 0. */
 quarot_status quarot_int4_linear_swiglu(const uint8_t* xq, const float* x_scale, int64_t M, int64_t K,
                                         int64_t ld_xq, const uint8_t* wq, const float* w_scale, int64_t N2,
                                         int64_t ld_wq, void* act, int64_t ld_act, void* stream);
@@ -274,7 +278,7 @@ int64_t quarot_kv_decode_workspace_bytes(int64_t B, int32_t n_q, int32_t head_di
  *   angle = pos * theta^(-2i/d), pos = (pos0 + t) % seq_len; fp32 math, fp16 RNE result.
  *   head_dim even and <= 256; ld_x % 8 == 0; x 16-B aligned.  Apply it to the Q|K block of a
  *   fused QKV output (n_heads = n_q + n_kv) before quarot_kv_quant.
- * quarot_swiglu: act[m][f] = fp16(silu(gu[m][f]) * gu[m][F + f]) — the gated FFN activation of
+ * quarot_swiglu: act[m][f] = fp16(fp16(silu(gu[m][f])) * gu[m][F + f]) — the gated FFN activation of
  *   Fig. ffn_orig with [gate | up] column halves; F % 8 == 0, ld % 8 == 0, 16-B aligned. */
 quarot_status quarot_rope(void* x, int64_t T, int32_t n_heads, int32_t head_dim, int64_t ld_x,
                           int64_t pos0, int32_t seq_len, float theta, void* stream);

@@ -10,6 +10,13 @@ Fig. attn_quarot), fp64:
   half"), inv_freq_i = theta^(-2i/d), theta = 10000, position = index within the sequence.
 * SwiGLU: act = silu(gate) * up (Fig. ffn_orig, sigma = SiLU in Llama).
 * residual add.
+
+Precision (Fig. ffn_quarot caption): "The result of the matmul between the INT4 weights
+and activations on a TensorCore is INT32, which we immediately cast (and scale) to FP16 which is
+the default precision of the model."  Every linear output is therefore an fp16 tensor before
+the next op, and the elementwise glue runs as the FP16 model's ops (reading Z23): each op's
+result is rounded to fp16, i.e. act = fp16(fp16(silu(g)) * u) and x + fp16(y) -> fp16, with the
+arithmetic of each op exact (fp64) before its one rounding.
 """
 from __future__ import annotations
 
@@ -40,17 +47,29 @@ def rope(x: np.ndarray, positions: np.ndarray, theta: float = ROPE_THETA) -> np.
 
 
 def swiglu(gate: np.ndarray, up: np.ndarray) -> np.ndarray:
+    """silu(g) * u in fp64 (the full-precision definition)."""
     g = np.asarray(gate, dtype=np.float64)
     return g / (1.0 + np.exp(-g)) * np.asarray(up, dtype=np.float64)
 
 
-def linear_swiglu(cx, sx, cw_gate_up, sw_gate_up, ffn: int):
-    """Gate/up INT4 linear with SwiGLU applied to the fp64 epilogue values (no fp16 rounding
-    of gate/up in between): act = fp16(silu(g) * u).  W rows [gate (ffn) ; up (ffn)]."""
-    from .gemm import int_matmul_exact_f64
-    acc = int_matmul_exact_f64(cx, cw_gate_up).astype(np.float64)
-    y = acc * np.asarray(sx, np.float64)[:, None] * np.asarray(sw_gate_up, np.float64)[None, :]
-    return swiglu(y[:, :ffn], y[:, ffn:]).astype(np.float16)
+def silu_fp16(gate16: np.ndarray) -> np.ndarray:
+    """The FP16 model's activation op: fp16(silu(g)) of fp16 g (one rounding)."""
+    g = np.asarray(gate16, dtype=np.float16).astype(np.float64)
+    return (g / (1.0 + np.exp(-g))).astype(np.float16)
+
+
+def swiglu_fp16(gate16: np.ndarray, up16: np.ndarray) -> np.ndarray:
+    """SwiGLU of the FP16 model (Fig. ffn_orig, reading Z23): fp16(fp16(silu(g)) * u), g and u
+    the fp16 outputs of the gate / up linears."""
+    s = silu_fp16(gate16).astype(np.float64)
+    return (s * np.asarray(up16, dtype=np.float16).astype(np.float64)).astype(np.float16)
+
+
+def add_fp16(a16: np.ndarray, b16: np.ndarray) -> np.ndarray:
+    """The FP16 model's residual add: fp16(a + b) of two fp16 tensors (one rounding)."""
+    with np.errstate(over="ignore"):  # |a + b| > 65504 rounds to inf, as in the FP16 model
+        return (np.asarray(a16, np.float16).astype(np.float64)
+                + np.asarray(b16, np.float16).astype(np.float64)).astype(np.float16)
 
 
 def rmsnorm_quant(x: np.ndarray, clip_ratio: float = 0.9, eps: float = RMS_EPS):
@@ -81,14 +100,10 @@ def decoder_layer(x, attn_out, w, positions, shapes: dict, clip=0.9, clip_kv=0.9
     v = qkv64[:, nq + nk:].reshape(T, n_kv, d)
     cache = okv.kv_init(k, v, q, clip_ratio=clip_kv)
     co, _, so = olayer.hadamard_quant(attn_out, "across_heads", d, clip)
-    acc_o = olayer.int4_linear(co, so, *w["o"], exact_f64=True)[0]
-    o = (acc_o * so.astype(np.float64)[:, None] * w["o"][1].astype(np.float64)[None, :]
-         + np.asarray(x, dtype=np.float64)).astype(np.float16)
+    o = add_fp16(x, olayer.int4_linear(co, so, *w["o"], exact_f64=True)[1])      # x + fp16 linear output
     cn, _, sn = rmsnorm_quant(o, clip)
-    gu = olayer.int4_linear(cn, sn, *w["gate_up"], exact_f64=True)[1]
-    act = linear_swiglu(cn, sn, *w["gate_up"], ffn)  # SwiGLU fused into the gate/up epilogue
+    gu = olayer.int4_linear(cn, sn, *w["gate_up"], exact_f64=True)[1]            # fp16 [gate | up]
+    act = swiglu_fp16(gu[:, :ffn], gu[:, ffn:])
     cd, _, sd = olayer.hadamard_quant(act, "full", d, clip)
-    acc_d = olayer.int4_linear(cd, sd, *w["down"], exact_f64=True)[0]
-    out = (acc_d * sd.astype(np.float64)[:, None] * w["down"][1].astype(np.float64)[None, :]
-           + o.astype(np.float64)).astype(np.float16)
+    out = add_fp16(o, olayer.int4_linear(cd, sd, *w["down"], exact_f64=True)[1])
     return {"qkv": qkv, "cache": cache, "o": o, "gate_up": gu, "act": act, "out": out}

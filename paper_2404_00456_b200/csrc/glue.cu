@@ -4,7 +4,7 @@
 // RoPE ("Pos", Eqs. 10-12): Llama-2 rotate-half form, pair (i, i + d/2) rotated by
 // pos * theta^(-2i/d).  One CTA iteration per token: the d/2 (cos, sin) values are computed once
 // in double precision into smem and reused by every head of the token.
-// SwiGLU (Fig. ffn_orig): act = silu(gate) * up over [gate | up] column halves.
+// SwiGLU (Fig. ffn_orig): act = fp16(fp16(silu(gate)) * up) over [gate | up] column halves.
 #include "common.cuh"
 #include "quarot_internal.h"
 
@@ -66,7 +66,10 @@ __global__ void __launch_bounds__(256) swiglu_kernel(const __half* __restrict__ 
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const float2 g = __half22float2(g2[e]), u = __half22float2(u2[e]);
-      o2[e] = __floats2half2_rn(g.x / (1.f + __expf(-g.x)) * u.x, g.y / (1.f + __expf(-g.y)) * u.y);
+      // the FP16 model's ops (reading Z23): fp16(silu(g)), then fp16(that * u)
+      const float sx = __half2float(__float2half_rn(g.x / (1.f + __expf(-g.x))));
+      const float sy = __half2float(__float2half_rn(g.y / (1.f + __expf(-g.y))));
+      o2[e] = __floats2half2_rn(sx * u.x, sy * u.y);
     }
     *reinterpret_cast<uint4*>(act + m * ld_act + c) = o;
   }

@@ -180,9 +180,12 @@ QR_DEVICE void mma_commit_pair(uint64_t* bar) {
       : "memory")
 
 // Converts and stores one 32-column accumulator chunk of one row (columns n0 .. n0 + 31;
-// wsc = their 32 weight scales in smem).  fp16: y = fp16_rn(fp32(acc) * s_x * s_w [+ r]);
-// s32: raw accumulators; SwiGLU: the chunk is [8 gate | 8 up] x 2 (interleaved weight rows)
-// and 16 act = silu(g) * u values go to column n0 / 2.
+// wsc = their 32 weight scales in smem).  fp16: y = fp16_rn(fp32(acc) * s_x * s_w); with a
+// residual, fp16_rn(fp32(y) + fp32(r)); s32: raw accumulators; SwiGLU: the chunk is
+// [8 gate | 8 up] x 2 (interleaved weight rows) and 16 act = fp16_rn(fp16_rn(silu(g)) * u)
+// values go to column n0 / 2, g and u the fp16 linear outputs (the FP16 model's ops, Z23).  The INT32 result is "immediately cast (and
+// scale[d]) to FP16" before any further op, so the fused epilogues equal the unfused
+// GEMM -> fp16 -> residual add / quarot_swiglu chain bit for bit.
 template <bool kS32, int kDbg, int kShift = 8>  // kShift: the x16 nibble scaling of both operands (A4W4)
 QR_DEVICE void epi_chunk(const Params& p, const uint32_t (&rc)[32], int64_t m, bool row_ok, int64_t n0, float sx,
                          const float* wsc) {
@@ -208,9 +211,10 @@ QR_DEVICE void epi_chunk(const Params& p, const uint32_t (&rc)[32], int64_t m, b
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
             const int c = 2 * e + j;
-            const float gv = ((float)((int32_t)rc[16 * hgrp + c] >> kShift) * sx) * sg[c];
-            const float uv = ((float)((int32_t)rc[16 * hgrp + 8 + c] >> kShift) * sx) * sg[8 + c];
-            a[j] = gv / (1.f + __expf(-gv)) * uv;
+            const float gv = __half2float(__float2half_rn(((float)((int32_t)rc[16 * hgrp + c] >> kShift) * sx) * sg[c]));
+            const float uv =
+                __half2float(__float2half_rn(((float)((int32_t)rc[16 * hgrp + 8 + c] >> kShift) * sx) * sg[8 + c]));
+            a[j] = __half2float(__float2half_rn(gv / (1.f + __expf(-gv)))) * uv;  // fp16(silu(g)) * u
           }
           h[e] = pack_half2(a[0], a[1]);
         }
@@ -241,9 +245,9 @@ QR_DEVICE void epi_chunk(const Params& p, const uint32_t (&rc)[32], int64_t m, b
         for (int e = 0; e < 4; ++e) {
           float v0 = ((float)((int32_t)rc[8 * g + 2 * e] >> kShift) * sx) * swv[2 * e];
           float v1 = ((float)((int32_t)rc[8 * g + 2 * e + 1] >> kShift) * sx) * swv[2 * e + 1];
-          if (p.residual) {
-            v0 += __half2float(__ushort_as_half((unsigned short)(rw[e] & 0xFFFFu)));
-            v1 += __half2float(__ushort_as_half((unsigned short)(rw[e] >> 16)));
+          if (p.residual) {  // the linear output is fp16 before the residual add
+            v0 = __half2float(__float2half_rn(v0)) + __half2float(__ushort_as_half((unsigned short)(rw[e] & 0xFFFFu)));
+            v1 = __half2float(__float2half_rn(v1)) + __half2float(__ushort_as_half((unsigned short)(rw[e] >> 16)));
           }
           h[e] = pack_half2(v0, v1);
         }

@@ -1,8 +1,10 @@
 """Multi-GPU plumbing for token-sharded prefill (one process per GPU, torch.distributed).
 
 The hot path has no collective: every step is row-independent, so each rank
-processes its own token slice with the full replicated INT4 weights.  The only
-communication is outside the timed region:
+processes its own token slice with the full replicated INT4 weights.  Strong scaling (§8e,
+BASELINE config 3/5): the fixed 64 x 2048-token batch is split into contiguous row shards,
+GPU g taking sequences [g*64/G, (g+1)*64/G).  The only communication is outside the timed
+region:
   * `max_over_ranks` — the step time every rank reports is the max over ranks;
   * `gather_rows` — verification gather of per-rank outputs (NCCL all_gather over
     NVLink on GPUs, gloo in the CPU tests), to check that a sharded run equals the
@@ -49,3 +51,29 @@ def gather_rows(local: torch.Tensor, total_rows: int) -> torch.Tensor:
     outs = [torch.empty_like(buf) for _ in range(world)]
     dist.all_gather(outs, buf)
     return torch.cat([o[: b - a] for o, (a, b) in zip(outs, sizes)], 0)
+
+
+def shard_plan(total: int, world: int) -> list[tuple[int, int]]:
+    """Every rank's [r0, r1) (shard_bounds for ranks 0..world-1)."""
+    return [shard_bounds(total, world, r) for r in range(world)]
+
+
+def gather_and_compare(local: dict, total_rows: int, reference=None) -> dict:
+    """Verification (outside the timed region): all-gather every per-rank row shard in `local`
+    (name -> tensor whose first dim is this rank's rows) into the full batch, then, on the
+    ranks holding `reference` (name -> full tensor of an unsharded run, or None), compare
+    bitwise.  Returns {name: True/False} on ranks with a reference, {} elsewhere.  Collective:
+    every rank must call it with the same names in the same order."""
+    result = {}
+    for name in sorted(local):
+        full = gather_rows(local[name].contiguous(), total_rows)
+        if reference is not None:
+            ref = reference[name].contiguous()
+            result[name] = bool(full.shape == ref.shape and full.dtype == ref.dtype
+                                and torch.equal(_bits(full), _bits(ref.to(full.device))))
+    return result
+
+
+def _bits(t: torch.Tensor) -> torch.Tensor:
+    """Byte view (bitwise comparison: NaN payloads and signed zeros count)."""
+    return t.reshape(-1).view(torch.uint8)

@@ -192,9 +192,12 @@ class DecoderLayerStep:
     gu, then SwiGLU)."""
 
     def __init__(self, layer: QuaRotLayer, tokens: int, device="cuda", seq_len: int = 2048, theta: float = 10000.0,
-                 fuse_swiglu: bool = True, fuse_rope: bool = True):
+                 fuse_swiglu: bool = True, fuse_rope: bool = True, row_offset: int = 0):
+        """tokens: rows this step processes; row_offset: their first row in the global batch (a
+        token shard of a multi-GPU job, dist.shard_bounds): RoPE positions are
+        (row_offset + t) % seq_len, so a sharded run equals the unsharded one bit for bit."""
         self.layer, self.tokens, self.device = layer, tokens, torch.device(device)
-        self.seq_len, self.theta = seq_len, theta
+        self.seq_len, self.theta, self.row_offset = seq_len, theta, row_offset
         self.fuse_swiglu, self.fuse_rope = fuse_swiglu, fuse_rope
         self.LAUNCHES = 9 + (not fuse_swiglu) + (not fuse_rope)
         if fuse_swiglu:  # offline: gate/up rows interleaved in blocks of 8 for the fused epilogue
@@ -226,7 +229,7 @@ class DecoderLayerStep:
 
     def run_rows(self, inputs: dict, r0: int, r1: int, stream=None, events=None):
         """inputs: 'x' residual stream [T, hidden] fp16, 'attn_out' [T, hidden] fp16 stand-in for
-        the attention core's output.  Rows [r0, r1); positions (r0 + t) % seq_len."""
+        the attention core's output.  Rows [r0, r1); positions (row_offset + r0 + t) % seq_len."""
         x, attn_out = inputs["x"], inputs["attn_out"]
         L = self.layer
         stream = torch.cuda.current_stream() if stream is None else stream
@@ -253,13 +256,13 @@ class DecoderLayerStep:
         linear(qkv_s, xr, True, qkv)
         nq, nkv = L.n_heads * d, L.n_kv * d
         if not self.fuse_rope:
-            q.rope(qkv[:, : nq + nkv].view(T, L.n_heads + L.n_kv, d), pos0=r0, seq_len=self.seq_len,
+            q.rope(qkv[:, : nq + nkv].view(T, L.n_heads + L.n_kv, d), pos0=self.row_offset + r0, seq_len=self.seq_len,
                    theta=self.theta, stream=stream)
             mark("rope")
         q.kv_quant(qkv[:, nq:nq + nkv].view(T, L.n_kv, d), qkv[:, nq + nkv:].view(T, L.n_kv, d),
                    qkv[:, :nq].view(T, L.n_heads, d), flags=q.KV_ROTATE_K, clip_ratio=L.clip_kv,
                    out={k: t[r0:r1] for k, t in self.kv.items()}, stream=stream,
-                   rope=(r0, self.seq_len, self.theta) if self.fuse_rope else None)
+                   rope=(self.row_offset + r0, self.seq_len, self.theta) if self.fuse_rope else None)
         mark("kv_quant")
         o = self.o[r0:r1]
         linear(o_s, attn_out[r0:r1], False, o, residual=xr)

@@ -47,6 +47,28 @@ def _no_nibble8(packed: torch.Tensor) -> bool:
     return not bool(((lo == 8) | (hi == 8)).any().item())
 
 
+def test_full_m_down_gemm_blocks_bit_exact():
+    """The bench's down_proj launch shape (M = 131072, N = 8192, K = 28672: 512 x 32 tiles over
+    74 CTA pairs, 112 k-blocks each): whole 256-row x 256-column tile blocks at the first, a
+    middle and the last M / N tiles compared element-exactly with the oracle's int64 GEMM."""
+    import paper_2404_00456_b200 as q
+    M, N, K = 131072, 8192, 28672
+
+    def codes(rows, seed):  # uniform packed codes in [-7, 7] (nibble 0x8 = -8 mapped to 0x9 = -7)
+        g = torch.Generator(device=DEV).manual_seed(seed)
+        b = torch.randint(0, 256, (rows, K // 2), dtype=torch.uint8, device=DEV, generator=g)
+        b = torch.where((b & 0xF) == 8, b + 1, b)
+        return torch.where((b >> 4) == 8, b + 16, b)
+    xq, wq = codes(M, 501), codes(N, 502)
+    acc = q.int4_matmul_s32(xq, wq)
+    torch.cuda.synchronize()
+    for (m0, n0) in ((0, 0), (M // 2 + 256 * 37, N // 2 + 256 * 5), (M - 256, N - 256), (256 * 300, 0)):
+        r = torch.arange(m0, m0 + 256, device=DEV)
+        c = torch.arange(n0, n0 + 256, device=DEV)
+        ref = ogemm.int_matmul_exact_f64(P.unpack_signed(xq[r].cpu().numpy()), P.unpack_signed(wq[c].cpu().numpy()))
+        assert np.array_equal(acc[r][:, c].cpu().numpy().astype(np.int64), ref), (m0, n0)
+
+
 @pytest.mark.parametrize("cfg", [1, 2])
 def test_full_size_step_sampled_parity(cfg):
     import paper_2404_00456_b200 as q
@@ -67,7 +89,13 @@ def test_full_size_step_sampled_parity(cfg):
         xq, xs = q.hadamard_quant(x, spec_lin.mode, layer.head_dim, layer.clip_act)
         wq, ws = layer.weights[spec_lin.name]
         y = q.int4_linear(xq, xs, wq, ws)
-        acc = q.int4_matmul_s32(xq[rows_t].contiguous(), wq)  # accumulators of the sampled rows
+        cols = np.sort(rng.choice(spec_lin.n, size=min(256, spec_lin.n), replace=False))
+        cols[-1] = spec_lin.n - 1  # the last N tile
+        cols_t = torch.as_tensor(cols, device=DEV)
+        # accumulators of the FULL-M launch (the bench's M, every tile of the grid), sampled blocks
+        acc_full = q.int4_matmul_s32(xq, wq)
+        acc = acc_full[rows_t][:, cols_t].contiguous()
+        del acc_full
         torch.cuda.synchronize()
         # full-tensor properties
         assert torch.isfinite(xs).all() and (xs > 0).all()
@@ -78,15 +106,16 @@ def test_full_size_step_sampled_parity(cfg):
         gc = P.unpack_signed(xq[rows_t].cpu().numpy())
         P.assert_codes(gc, rc, f"{S.name} {spec_lin.name} codes")
         P.assert_scales(xs[rows_t].cpu().numpy(), rs, f"{S.name} {spec_lin.name} scales")
-        # sampled (row, column) block: accumulators bit-exact, fp16 outputs within tolerance
-        cols = np.sort(rng.choice(spec_lin.n, size=min(256, spec_lin.n), replace=False))
-        cw = oquant.unpack_int4_signed(wq[torch.as_tensor(cols, device=DEV)].cpu().numpy())
+        # sampled (row, column) block of the full launch: accumulators bit-exact, and the bench
+        # launch's fp16 outputs within 2 ulp of the oracle epilogue on the same codes / scales
+        cw = oquant.unpack_int4_signed(wq[cols_t].cpu().numpy())
         ref_acc = ogemm.int_matmul_exact_f64(gc, cw)
-        got_acc = acc[:, torch.as_tensor(cols, device=DEV)].cpu().numpy().astype(np.int64)
+        got_acc = acc.cpu().numpy().astype(np.int64)
         assert np.array_equal(got_acc, ref_acc), f"{S.name} {spec_lin.name}: accumulators differ"
         ref_y = ogemm.dequant_epilogue(ref_acc, xs[rows_t].cpu().numpy(), ws.cpu().numpy()[cols])
-        got_y = y[rows_t][:, torch.as_tensor(cols, device=DEV)].cpu().numpy()
+        got_y = y[rows_t][:, cols_t].cpu().numpy()
         assert P.frob_rel(got_y, ref_y) <= P.FROB_REL
+        assert P.max_fp16_ulp(got_y, ref_y) <= 2, f"{S.name} {spec_lin.name}: fp16 outputs"
         del xq, xs, y, acc
     # the timed step itself (same launches as bench.py) reproduces the per-call results
     step.run_device(inputs)

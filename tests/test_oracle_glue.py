@@ -95,3 +95,67 @@ def test_decoder_layer_close_to_full_precision():
     bad = glue.decoder_layer(x, z, w_bad, np.arange(T), shapes)
     rel_bad = np.linalg.norm(bad["out"].astype(np.float64) - ref) / np.linalg.norm(ref)
     assert rel_bad > 2 * rel, (rel, rel_bad)
+
+
+def _ulp16(a, b):
+    a = np.asarray(a, np.float16).view(np.int16).astype(np.int64)
+    b = np.asarray(b, np.float16).view(np.int16).astype(np.int64)
+    a = np.where(a < 0, -(a & 0x7FFF), a)
+    b = np.where(b < 0, -(b & 0x7FFF), b)
+    return np.abs(a - b)
+
+
+def test_fp16_glue_ops_match_torch_half():
+    """Pin of reading Z23 (every linear output is FP16, the model's default precision):
+    the oracle's FP16 ops equal PyTorch's own fp16 CPU kernels — F.silu on a half tensor, the
+    half product, the half add — an independent implementation of the same FP16 model ops."""
+    import torch
+    rng = np.random.default_rng(5)
+    g = (rng.standard_normal(200000) * 4).astype(np.float16)
+    u = (rng.standard_normal(200000) * 2).astype(np.float16)
+    g[:6] = [0.0, -0.0, 65504.0, -65504.0, 6e-8, -20.0]
+    tg, tu = torch.from_numpy(g), torch.from_numpy(u)
+    s_t = torch.nn.functional.silu(tg).numpy()
+    s_o = glue.silu_fp16(g)
+    d = _ulp16(s_o, s_t)
+    # torch evaluates silu in fp32 before its one rounding; fp64 vs fp32 may straddle a rounding
+    # boundary only in rare near-tie cases
+    assert d.max() <= 1 and np.count_nonzero(d) <= 2e-3 * d.size, (d.max(), np.count_nonzero(d))
+    # with the same fp16 silu output, the product and the add are single correctly rounded ops
+    a_t = (torch.from_numpy(s_o) * tu).numpy()
+    assert np.array_equal(glue.swiglu_fp16(g, u).view(np.int16), a_t.view(np.int16))
+    r = (rng.standard_normal(200000) * 3).astype(np.float16)
+    assert np.array_equal(glue.add_fp16(r, u).view(np.int16), (torch.from_numpy(r) + tu).numpy().view(np.int16))
+
+
+def test_fp16_glue_special_cases():
+    # silu(0) = 0; large positive g: silu(g) = g exactly in fp16; large negative: -0/0
+    assert glue.silu_fp16(np.float16([0.0]))[0] == 0
+    assert glue.silu_fp16(np.float16([30.0]))[0] == np.float16(30.0)
+    assert glue.silu_fp16(np.float16([-30.0]))[0] == 0
+    # up = 1: the SwiGLU is the fp16 SiLU itself; residual add of 0 is the identity
+    g = np.float16([0.5, -1.25, 3.0, 7.5])
+    assert np.array_equal(glue.swiglu_fp16(g, np.ones(4, np.float16)), glue.silu_fp16(g))
+    assert np.array_equal(glue.add_fp16(g, np.zeros(4, np.float16)), g)
+    # fp16 overflow of the add saturates to inf like the FP16 model
+    assert np.isinf(glue.add_fp16(np.float16([65504.0]), np.float16([65504.0]))[0])
+
+
+def test_decoder_layer_outputs_are_fp16_model_ops():
+    """decoder_layer's intermediates are fp16 and its act is the FP16 model's SwiGLU of the fp16
+    gate/up linear output, recomputed here with PyTorch's own half kernels (within 1 ulp)."""
+    rng = np.random.default_rng(6)
+    T, D, F, nh, nkv, d = 4, 256, 448, 2, 1, 128
+    shapes = {"n_heads": nh, "n_kv": nkv, "head_dim": d, "ffn": F}
+    x = (rng.standard_normal((T, D)) * 0.5).astype(np.float16)
+    z = rng.standard_normal((T, D)).astype(np.float16)
+    w = {"qkv": (rng.integers(-7, 8, ((nh + 2 * nkv) * d, D)), np.full((nh + 2 * nkv) * d, 0.02, np.float32)),
+         "o": (rng.integers(-7, 8, (D, D)), np.full(D, 0.02, np.float32)),
+         "gate_up": (rng.integers(-7, 8, (2 * F, D)), np.full(2 * F, 0.02, np.float32)),
+         "down": (rng.integers(-7, 8, (D, F)), np.full(D, 0.02, np.float32))}
+    out = glue.decoder_layer(x, z, w, np.arange(T), shapes)
+    assert out["o"].dtype == out["act"].dtype == out["out"].dtype == out["gate_up"].dtype == np.float16
+    import torch
+    gu = torch.from_numpy(out["gate_up"])
+    act_t = (torch.nn.functional.silu(gu[:, :F]) * gu[:, F:]).numpy()
+    assert _ulp16(out["act"], act_t).max() <= 1

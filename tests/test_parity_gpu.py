@@ -138,7 +138,7 @@ def test_int4_gemm_s32_bit_exact(q, M, N, K):
     assert np.array_equal(acc.cpu().numpy().astype(np.int64), ref)
 
 
-@pytest.mark.parametrize("M,N,K", [(2085, 4120, 4096), (1100, 8200, 2176)])
+@pytest.mark.parametrize("M,N,K", [(2085, 4120, 4096), (1100, 8200, 2176), (2085, 4120, 28672)])
 def test_int4_gemm_multi_tile_full_matrix(q, M, N, K):
     # more 256x256 tiles than CTA pairs (>= 2 tiles per persistent pair), so the staging and
     # operand rings run across tile boundaries; ragged M and N, and a K % 256 == 128 tail.
