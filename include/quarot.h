@@ -78,6 +78,18 @@ typedef enum {
  * divides the scale by the row RMS: one pass over x (SURVEY §8 a8 fused, f1). */
 #define QUAROT_HAD_RMSNORM 0x100
 
+/* Mode flag (OR-ed into `mode`, FULL only; K = 1024 x 28): write the codes in the transform's
+ * native K order instead of the natural element order.  The FULL kernel produces output element
+ * i = a * J + j' (a = the 2^n Sylvester index, j' = the H_m-side index, J = K / 256) with a warp
+ * owning 32 consecutive j'; in the native order the code of element i sits at position
+ *     p(i) = (a >> 5) * 32 J + 32 j' + (a & 31)
+ * so every thread writes 16 contiguous bytes and a warp 512 (quarot_full_kperm returns the
+ * permutation).  The INT4 GEMM's accumulator is a sum over k, so pairing these codes with
+ * weights whose columns are permuted the same way offline (W'[n][p] = W[n][i(p)]) gives
+ * bit-identical int32 accumulators and outputs.  Requires
+ * ld_q % 16 == 0 and a 16-byte aligned q (QUAROT_ERR_ALIGN); other K: QUAROT_ERR_UNSUPPORTED_SIZE. */
+#define QUAROT_HAD_KPERM 0x200
+
 /* Rows a1|a2 + a3 of the hot path: online Hadamard + per-token symmetric INT4 RTN + pack.
  *
  *   x      fp16 [M][ld_x] row-major (K used); 16-B aligned; ld_x % 8 == 0.
@@ -292,6 +304,10 @@ int32_t quarot_abi_version(void);
  * into host buffer out[m*m].  Lets tests compare the library's independently built table
  * with the oracle's.  Returns QUAROT_ERR_UNSUPPORTED_SIZE for other m. */
 quarot_status quarot_base_hadamard(int32_t m, int8_t* out);
+/* The QUAROT_HAD_KPERM permutation for width K (host, no GPU work): perm[p] = the natural element
+ * index whose code sits at position p (perm: int64 [K], caller-owned).  K = 1024 x 28 only
+ * (QUAROT_ERR_UNSUPPORTED_SIZE otherwise). */
+quarot_status quarot_full_kperm(int64_t K, int64_t* perm);
 /* Number of kernels the last successful entry point on this host thread enqueued. */
 int32_t quarot_last_launch_count(void);
 /* "cudaErrorName: description" of the last call on this host thread that returned

@@ -4,9 +4,9 @@ The compute lives in ``libquarot.so`` (hand-written CUDA, C ABI in include/quaro
 ``quarot`` is its thin ctypes binding.  See DESIGN.md."""
 
 from .quarot import (  # noqa: F401
-    ACROSS_HEADS, FULL, NONE, RMSNORM, EXPORTS, LIB_PATH, QuarotError,
+    ACROSS_HEADS, FULL, NONE, RMSNORM, KPERM, EXPORTS, LIB_PATH, QuarotError,
     abi_version, base_hadamard, hadamard_quant, int4_linear, int4_matmul_s32, kv_quant,
     last_launch_count, lib, quarot_linear, rope, swiglu, interleave_gate_up, int4_linear_swiglu,
     kv_append, kv_decode, kv_cache_empty, hadamard_quant8, int8_linear, int8_matmul_s32,
-    hadamard_quant_group, hadamard_quant_group8, int4_linear_group,
+    hadamard_quant_group, hadamard_quant_group8, int4_linear_group, full_kperm, permute_k_packed,
 )

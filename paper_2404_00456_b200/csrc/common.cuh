@@ -51,6 +51,14 @@ QR_DEVICE bool mbar_try_wait_sleep(uint32_t addr, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// try_wait + an explicit back-off: for producer warps whose waits are long (a row of epilogue
+// work), so their retries do not take issue slots from the epilogue warps on the same SMSP
+// (try_wait's suspend hint wakes on every barrier event of the CTA)
+template <int kNs>
+QR_DEVICE void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  while (!mbar_try_wait(addr, parity)) __nanosleep(kNs);
+}
 QR_DEVICE void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   while (!mbar_try_wait_sleep(addr, parity)) {
@@ -192,6 +200,11 @@ QR_DEVICE float2 f2mul(float2 a, float2 b) {
       "mul.rn.f32x2 rc, ra, rb;\n\tmov.b64 {%0,%1}, rc;\n\t}"
       : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
   return r;
+}
+// (x + y, x - y) of the pair held in one float2: ONE FFMA2 with scalar-broadcast operands
+// (SASS: y.F32 * (1, -1) + x.F32) instead of two scalar FADDs — bitwise the same results
+QR_DEVICE float2 pair_bfly(float2 p) {
+  return f2fma(make_float2(p.y, p.y), make_float2(1.f, -1.f), make_float2(p.x, p.x));
 }
 // byte = nib(rne(clamp(v.x * inv))) | nib(rne(clamp(v.y * inv))) << 4; RNE via 1.5 * 2^23
 QR_DEVICE uint32_t quant_pair(float2 v, float inv) {

@@ -89,6 +89,14 @@ QR_DEVICE void bar_named(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(
       "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),      \
       "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),     \
       "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]))
+#define QR_TMEM_LD8(taddr, r)                                                                           \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"                 \
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),    \
+                 "=r"(r[7])                                                                             \
+               : "r"(taddr))
+#define QR_TMEM_ST8(taddr, r)                                                                           \
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),    \
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]))
 QR_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 QR_DEVICE void bfly(float2& u, float2& v) {
@@ -282,7 +290,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         bfly(v[1], v[3]);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          v[i] = make_float2(v[i].x + v[i].y, v[i].x - v[i].y);  // bit 0
+          v[i] = pair_bfly(v[i]);  // bit 0
           am[i] = fmax_nan(am[i], fmax_nan(fabsf(v[i].x), fabsf(v[i].y)));
           u[i][2 * c] = __float_as_uint(v[i].x);
           u[i][2 * c + 1] = __float_as_uint(v[i].y);
@@ -400,6 +408,313 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
 }  // namespace hqtc
 
+// ============================================================================ warpgroup pair per row
+// hq_full28_wg_kernel: the same transform (MMA of H_4 (x) H_28 per row into TMEM, H_256 over the
+// a_hi columns on CUDA cores) with each of the two TMEM row buffers owned by its own pair of
+// epilogue warpgroups (8 warps), so the two rows in flight never wait on each other, and with
+// hardware named barriers (no mbarrier polling) for the two intra-row dependencies.  Round-1
+// ncu: the 16-warps-share-every-row design spent ~1.9 instructions per element polling
+// mbarriers.  Per row, thread (lane L = j', g = its warpgroup within the pair):
+//   pass A: its half (a_hi bit 7 = g) in two 64-column chunks, bits 0-5 in registers;
+//   [named barrier, the 2 warps sharing the lanes]
+//   pass B: bits 6 and 7 over the 4-tuples (c, c + 64, c + 128, c + 192), c in [32 g, 32 g + 32),
+//           + amax; parked in TMEM;
+//   [named barrier, the 8 warps: the row's amax]
+//   quant:  its half, 32 columns at a time; the half is released to the MMA after its last load.
+// The MMA runs per 64-column quarter (N = 64), one MMA warp per buffer, so a quarter of the next
+// row is multiplied as soon as its warpgroup's quant loaded it and pass A of the next row starts
+// on it while the rest of the quant runs.  Bit 0 (within a register pair) uses one FFMA2
+// with scalar-broadcast operands (pair_bfly), so all 8 stages cost 0.5 instructions / element.
+// kPerm: codes in the transform-native K order (quarot.h QUAROT_HAD_KPERM): position
+//   p = (a_hi >> 5) * 3584 + j' * 32 + (a_hi & 31) — 32 consecutive a_hi of a lane are 16
+//   contiguous bytes (one 16-byte store; a warp writes 512 contiguous bytes); otherwise the
+//   natural element order a_hi * 112 + j' (adjacent lanes merged into bytes, byte stores).
+namespace hqwg {
+using hqtc::A_BYTES;
+using hqtc::BOX_BYTES;
+using hqtc::J;
+using hqtc::K;
+using hqtc::NA;
+using hqtc::STAGE_BYTES;
+constexpr int NH = NA / 2;  // 128 columns per half (a_hi bit 7)
+constexpr int NQ = NA / 4;  // 64 columns per quarter: the MMA / release granularity
+constexpr int STAGES = 3;
+constexpr int TMA_WARP = 0, MMA_WARP0 = 1, EPI_WARP0 = 4, NUM_EPI = 16;  // MMA warps 1, 2: one per buffer
+constexpr int NUM_THREADS = (EPI_WARP0 + NUM_EPI) * 32;                    // 640
+constexpr uint32_t TMEM_COLS = 512;
+#ifndef QR_WG_BACKOFF
+#define QR_WG_BACKOFF 64  // ns between the MMA warps' barrier polls (the next row's MMA is latency-critical)
+#endif
+#ifndef QR_WG_TMA_BACKOFF
+#define QR_WG_TMA_BACKOFF 512  // ns between the TMA warp's polls (three stages of slack)
+#endif
+constexpr size_t SMEM = 1024 + A_BYTES + (size_t)STAGES * STAGE_BYTES + 256;
+static_assert(SMEM <= 232448, "227 KB dynamic smem");
+constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(NQ >> 3) << 17) | ((128u >> 4) << 24);
+
+// 8 codes -> one 32-bit word of the KPERM layout: byte t = c[2t] | c[2t+1] << 4 (a..d = pairs)
+QR_DEVICE uint32_t code_word8(float2 a, float2 b, float2 c, float2 d, float inv) {
+  const float2 i2 = make_float2(inv, inv), mg = make_float2(12582912.f, 12582912.f);
+  const float2 ma = f2fma(a, i2, mg), mb = f2fma(b, i2, mg), mc = f2fma(c, i2, mg), md = f2fma(d, i2, mg);
+  // 16-bit lanes: even codes (c0, c2) / odd codes (c1, c3) of each group of four, clamped to [-7, 7]
+  uint32_t e0 = __byte_perm(__float_as_uint(ma.x), __float_as_uint(mb.x), 0x5410);
+  uint32_t o0 = __byte_perm(__float_as_uint(ma.y), __float_as_uint(mb.y), 0x5410);
+  uint32_t e1 = __byte_perm(__float_as_uint(mc.x), __float_as_uint(md.x), 0x5410);
+  uint32_t o1 = __byte_perm(__float_as_uint(mc.y), __float_as_uint(md.y), 0x5410);
+  e0 = __vmaxs2(__vmins2(e0, 0x00070007u), 0xFFF9FFF9u);
+  o0 = __vmaxs2(__vmins2(o0, 0x00070007u), 0xFFF9FFF9u);
+  e1 = __vmaxs2(__vmins2(e1, 0x00070007u), 0xFFF9FFF9u);
+  o1 = __vmaxs2(__vmins2(o1, 0x00070007u), 0xFFF9FFF9u);
+  const uint32_t w0 = (e0 & 0x000F000Fu) | ((o0 & 0x000F000Fu) << 4);  // bytes at bits 0-7, 16-23
+  const uint32_t w1 = (e1 & 0x000F000Fu) | ((o1 & 0x000F000Fu) << 4);
+  return __byte_perm(w0, w1, 0x6420);
+}
+
+template <bool kPerm>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    hq_full28_wg_kernel(const __grid_constant__ CUtensorMap tmX, int64_t M, float clip, uint8_t* __restrict__ q,
+                        int64_t ld_q, float* __restrict__ scale, const uint4* __restrict__ a_img) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * STAGE_BYTES);  // [STAGES] TMA landed
+  uint64_t* empty = full + STAGES;                                           // [STAGES] MMA done reading
+  uint64_t* t_full = empty + STAGES;                                         // [buf][quarter] D ready
+  uint64_t* t_empty = t_full + 8;                                            // [buf][quarter] D consumed
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(t_empty + 8);
+  __shared__ float red[2][2][8];                                             // [buf][row parity][warp]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  for (int i = threadIdx.x; i < A_BYTES / 16; i += NUM_THREADS) reinterpret_cast<uint4*>(sA)[i] = __ldg(a_img + i);
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 8; ++i) {
+      mbar_init(&t_full[i], 1);
+      mbar_init(&t_empty[i], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == MMA_WARP0) {
+    tmem_alloc(tmem_holder, TMEM_COLS);
+    tmem_relinquish();
+  }
+  if (warp == TMA_WARP && lane == 0)
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  const int64_t nrows = M > (int64_t)blockIdx.x ? (M - 1 - (int64_t)blockIdx.x) / gridDim.x + 1 : 0;
+
+  if (warp < EPI_WARP0) {
+    if (warp == TMA_WARP) {
+      if (lane == 0) {
+        for (int64_t it = 0; it < nrows; ++it) {
+          const int s = (int)(it % STAGES);
+          mbar_wait_backoff<QR_WG_TMA_BACKOFF>(&empty[s], (uint32_t)((it / STAGES) & 1) ^ 1u);
+          hqtc::expect_tx(&full[s], STAGE_BYTES);
+          const int row = (int)((int64_t)blockIdx.x + it * gridDim.x);
+          const uint32_t dst = smem_u32(sB + s * STAGE_BYTES);
+          hqtc::tma_load_3d(dst, &tmX, 0, 0, row, &full[s]);
+          hqtc::tma_load_3d(dst + BOX_BYTES, &tmX, 64, 0, row, &full[s]);
+        }
+      }
+    } else if (warp < MMA_WARP0 + 2) {
+      // MMA warp b issues the rows of buffer b (it % 2 == b)
+      const int b = warp - MMA_WARP0;
+      const uint64_t a_desc = umma_desc_sw128(smem_u32(sA));
+      const uint32_t sb = smem_u32(sB);
+      for (int64_t it = b; it < nrows; it += 2) {
+        const int s = (int)(it % STAGES);
+        const uint32_t n_par = (uint32_t)((it >> 1) & 1);
+        mbar_wait_backoff<QR_WG_BACKOFF>(&full[s], (uint32_t)((it / STAGES) & 1));
+#pragma unroll 1
+        for (int h = 0; h < 4; ++h) {  // quarter h: a_hi 64 h .. 64 h + 63 (N = 64)
+          mbar_wait_backoff<QR_WG_BACKOFF>(&t_empty[4 * b + h], n_par ^ 1u);
+          tc_fence_after();
+          const uint64_t b_desc = umma_desc_sw128(sb + (uint32_t)(s * STAGE_BYTES + h * (NQ * 128)));
+          const uint32_t d_tmem = tmem_base + (uint32_t)(b * NA + h * NQ);
+          if (hqtc::elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < J / 16; ++kk) {  // atom kk/4 (A: +16 KB, B: +32 KB), +32 B per K = 16
+              const uint64_t koff = (uint64_t)(2 * (kk & 3));
+              hqtc::mma_f16(d_tmem, a_desc + (uint64_t)((kk >> 2) * (16384 >> 4)) + koff,
+                            b_desc + (uint64_t)((kk >> 2) * (BOX_BYTES >> 4)) + koff, IDESC, kk > 0 ? 1u : 0u);
+            }
+            mma_commit(&t_full[4 * b + h]);
+            if (h == 3) mma_commit(&empty[s]);
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else {
+    const int e = warp - EPI_WARP0;   // 0..15
+    const int b = e >> 3;             // row buffer (rows it % 2 == b)
+    const int g = (e >> 2) & 1;       // half of the row this warp's pass A / quant own
+    const int qd = warp & 3;          // TMEM lane quarter
+    const int w8 = e & 7;             // warp index within the buffer's 8
+    const int L = qd * 32 + lane;     // TMEM lane = output j'
+    const bool lane_ok = L < J;
+    const bool odd = (lane & 1) != 0;
+    const uint32_t t_lane = tmem_base + ((uint32_t)(qd * 32) << 16) + (uint32_t)(b * NA);
+    const uint32_t t_half = t_lane + (uint32_t)(g * NH);
+    const int bar_lanes = 1 + 4 * b + qd, bar_row = 9 + b;  // named barriers (0 = __syncthreads)
+    const float norm_f = (float)rsqrt((double)K);
+    const float c0 = (float)((double)clip * rsqrt((double)K) / 7.0);  // scale = c0 * amax
+    for (int64_t it = b; it < nrows; it += 2) {
+      const uint32_t par = (uint32_t)((it >> 1) & 1);
+      const int64_t row = (int64_t)blockIdx.x + it * gridDim.x;
+      // ---- pass A: this warp's half, one 64-column quarter at a time (as soon as its MMA landed),
+      //      bits 0-5 (pair i = columns 2i, 2i+1)
+#pragma unroll 1
+      for (int k = 0; k < 2; ++k) {
+        mbar_wait(&t_full[4 * b + 2 * g + k], par);
+        tc_fence_after();
+        uint32_t r[2][32];
+        QR_TMEM_LD32(t_half + 64u * k, r[0]);
+        QR_TMEM_LD32(t_half + 64u * k + 32u, r[1]);
+        tmem_ld_wait();
+        float2 P[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          P[i] = make_float2(__uint_as_float(r[i >> 4][2 * (i & 15)]), __uint_as_float(r[i >> 4][2 * (i & 15) + 1]));
+#pragma unroll
+        for (int st = 1; st < 32; st <<= 1)
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (!(i & st)) hqtc::bfly(P[i], P[i + st]);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          P[i] = pair_bfly(P[i]);  // bit 0
+          r[i >> 4][2 * (i & 15)] = __float_as_uint(P[i].x);
+          r[i >> 4][2 * (i & 15) + 1] = __float_as_uint(P[i].y);
+        }
+        QR_TMEM_ST32(t_half + 64u * k, r[0]);
+        QR_TMEM_ST32(t_half + 64u * k + 32u, r[1]);
+      }
+      hqtc::tmem_st_wait();
+      tc_fence_before();
+      hqtc::bar_named(bar_lanes, 64);  // both halves of these lanes done with pass A
+      tc_fence_after();
+      // ---- pass B: bits 6, 7 over (c, c + 64, c + 128, c + 192), c in [32 g, 32 g + 32); amax
+      float am = 0.f;
+#pragma unroll 1
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t tc0 = t_lane + (uint32_t)(32 * g + 8 * k);
+        uint32_t u[4][8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) QR_TMEM_LD8(tc0 + 64u * i, u[i]);
+        tmem_ld_wait();
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          float2 v[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) v[i] = make_float2(__uint_as_float(u[i][2 * c]), __uint_as_float(u[i][2 * c + 1]));
+          hqtc::bfly(v[0], v[1]);  // bit 6
+          hqtc::bfly(v[2], v[3]);
+          hqtc::bfly(v[0], v[2]);  // bit 7
+          hqtc::bfly(v[1], v[3]);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            am = fmax_nan(am, fmax_nan(fabsf(v[i].x), fabsf(v[i].y)));
+            u[i][2 * c] = __float_as_uint(v[i].x);
+            u[i][2 * c + 1] = __float_as_uint(v[i].y);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) QR_TMEM_ST8(tc0 + 64u * i, u[i]);
+      }
+      float amax = lane_ok ? am : 0.f;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) amax = fmax_nan(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      if (lane == 0) red[b][par][w8] = amax;
+      hqtc::tmem_st_wait();
+      tc_fence_before();
+      hqtc::bar_named(bar_row, 256);  // the row's amax; pass B's TMEM stores of all 8 warps done
+      tc_fence_after();
+      amax = red[b][par][0];
+#pragma unroll
+      for (int w = 1; w < 8; ++w) amax = fmax_nan(amax, red[b][par][w]);
+      // scale = fp32(clip * amax / (7 sqrt(K))) (readings Z5, Z9); zero row -> 1, non-finite -> NaN, codes 0
+      float sc = 1.f, inv = 0.f;
+      if (!isfinite(amax)) {
+        sc = __int_as_float(0x7fc00000);
+      } else if (amax != 0.f) {
+        sc = c0 * amax;
+        inv = __fdiv_rn(norm_f, sc);
+      }
+      if (w8 == 0 && lane == 0) scale[row] = sc;
+      const bool zero = inv == 0.f;  // zero / non-finite row: all codes 0
+      uint8_t* const qrow = q + row * ld_q;
+      // ---- quant: this warp's half, 32 columns (a_hi = 128 g + 32 ch + r) at a time
+#pragma unroll 1
+      for (int ch = 0; ch < 4; ++ch) {
+        uint32_t r[32];
+        QR_TMEM_LD32(t_half + 32u * ch, r);
+        tmem_ld_wait();
+        if (ch & 1) {  // quarter 2 g + ch / 2 fully loaded: release it to the MMA of row it + 2
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&t_empty[4 * b + 2 * g + (ch >> 1)]);
+        }
+        float2 V[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) V[i] = make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+        if constexpr (kPerm) {
+          uint32_t w[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            w[t] = code_word8(V[4 * t], V[4 * t + 1], V[4 * t + 2], V[4 * t + 3], inv);
+            if (zero) w[t] = 0u;
+          }
+          if (lane_ok) {
+            const int64_t byte = ((int64_t)(4 * g + ch) * (J * 32) + (int64_t)L * 32) >> 1;
+            *reinterpret_cast<uint4*>(qrow + byte) = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        } else {
+          // natural order: element (a_hi, j') at a_hi * 112 + j'; the byte of j' = 2p, 2p + 1 at
+          // a_hi * 56 + p — even lanes keep words 0..3 (a_hi + 0..15), odd lanes 4..7 (+16..31)
+          uint32_t w[8];
+#pragma unroll
+          for (int m = 0; m < 8; ++m) {
+            w[m] = hqtc::code_word(V[2 * m], V[2 * m + 1], inv);
+            if (zero) w[m] = 0u;
+          }
+          const uint32_t keep_mask = odd ? 0xF0F0F0F0u : 0x0F0F0F0Fu;
+          uint8_t* const qb = qrow + (L >> 1) + (int64_t)(NH * g + 32 * ch + (odd ? 16 : 0)) * (J / 2);
+#pragma unroll
+          for (int mm = 0; mm < 4; ++mm) {
+            const uint32_t got = __shfl_xor_sync(0xffffffffu, odd ? w[mm] : w[mm + 4], 1);
+            const uint32_t keep = odd ? w[mm + 4] : w[mm];
+            const uint32_t o = odd ? (((keep << 4) & keep_mask) | (got & 0x0F0F0F0Fu))
+                                   : ((keep & keep_mask) | ((got << 4) & 0xF0F0F0F0u));
+            if (lane_ok) {
+              uint8_t* dst = qb + (int64_t)(4 * mm) * (J / 2);
+              dst[0] = (uint8_t)o;
+              dst[J / 2] = (uint8_t)(o >> 8);
+              dst[J] = (uint8_t)(o >> 16);
+              dst[3 * J / 2] = (uint8_t)(o >> 24);
+            }
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == MMA_WARP0) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+}  // namespace hqwg
+
 namespace {
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn_hq() {
@@ -444,54 +759,78 @@ __device__ uint4 g_a28_img[hqtc::A_BYTES / 16];
 
 }  // namespace
 
-int g_hq_full_variant = 0;  // debug: 1 = the mma.sync kernel (hq_full28_kernel), 2 = spinning epilogue waits
+int g_hq_full_variant = 0;  // debug: 1 = the mma.sync kernel (hq_full28_kernel), 2 = spinning epilogue waits,
+                            // 3 = the 16-warps-per-row tcgen05 kernel (hq_full28_tc_kernel)
 
-cudaError_t launch_hq_full28_tc(const void* x, int64_t M, int64_t ld_x, float clip, uint8_t* q, int64_t ld_q,
-                                float* scale, cudaStream_t stream, bool q8) {
+namespace {
+// the (H_4 (x) H_28) operand image in device memory (uploaded once per device) and the
+// kernels' shared-memory attributes
+cudaError_t a28_image(const void** img_out) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  void* img = nullptr;
-  {
-    std::lock_guard<std::mutex> lk(g_img_mu);
-    if (!g_img[dev & 63]) {
-      const int8_t* h28 = base_hadamard_host(28);
-      if (!h28) return cudaErrorInvalidValue;
-      auto host = a_image_28(h28);
-      void* d = nullptr;
-      e = cudaGetSymbolAddress(&d, g_a28_img);
+  std::lock_guard<std::mutex> lk(g_img_mu);
+  if (!g_img[dev & 63]) {
+    const int8_t* h28 = base_hadamard_host(28);
+    if (!h28) return cudaErrorInvalidValue;
+    auto host = a_image_28(h28);
+    void* d = nullptr;
+    e = cudaGetSymbolAddress(&d, g_a28_img);
+    if (e != cudaSuccess) return e;
+    e = cudaMemcpy(d, host.data(), host.size() * sizeof(uint16_t), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return e;
+    e = cudaDeviceSynchronize();  // one-time: the image is complete before any stream reads it
+    if (e != cudaSuccess) return e;
+    for (auto kern : {hqtc::hq_full28_tc_kernel<false>, hqtc::hq_full28_tc_kernel<true>,
+                      hqtc::hq_full28_tc_kernel<false, true>}) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hqtc::SMEM);
       if (e != cudaSuccess) return e;
-      e = cudaMemcpy(d, host.data(), host.size() * sizeof(uint16_t), cudaMemcpyHostToDevice);
-      if (e != cudaSuccess) return e;
-      e = cudaDeviceSynchronize();  // one-time: the image is complete before any stream reads it
-      if (e != cudaSuccess) return e;
-      for (auto kern : {hqtc::hq_full28_tc_kernel<false>, hqtc::hq_full28_tc_kernel<true>,
-                        hqtc::hq_full28_tc_kernel<false, true>}) {
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hqtc::SMEM);
-        if (e != cudaSuccess) return e;
-      }
-      g_img[dev & 63] = d;
     }
-    img = g_img[dev & 63];
+    for (auto kern : {hqwg::hq_full28_wg_kernel<false>, hqwg::hq_full28_wg_kernel<true>}) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hqwg::SMEM);
+      if (e != cudaSuccess) return e;
+    }
+    g_img[dev & 63] = d;
   }
+  *img_out = g_img[dev & 63];
+  return cudaSuccess;
+}
+
+cudaError_t x_map_28(const void* x, int64_t M, int64_t ld_x, CUtensorMap* map) {
   auto fn = encode_fn_hq();
   if (!fn) return cudaErrorInvalidValue;
-  CUtensorMap map;
   cuuint64_t dims[3] = {(cuuint64_t)hqtc::J, (cuuint64_t)hqtc::NA, (cuuint64_t)M};
   cuuint64_t strides[2] = {(cuuint64_t)hqtc::J * 2, (cuuint64_t)ld_x * 2};
   cuuint32_t box[3] = {64u, (cuuint32_t)hqtc::NA, 1u};
   cuuint32_t estr[3] = {1u, 1u, 1u};
-  CUresult r = fn(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(x), dims, strides, box, estr,
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(x), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-  int nsm = 148;
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+}  // namespace
+
+cudaError_t launch_hq_full28_tc(const void* x, int64_t M, int64_t ld_x, float clip, uint8_t* q, int64_t ld_q,
+                                float* scale, cudaStream_t stream, bool q8, bool kperm) {
+  const void* img = nullptr;
+  cudaError_t e = a28_image(&img);
+  if (e != cudaSuccess) return e;
+  CUtensorMap map;
+  e = x_map_28(x, M, ld_x, &map);
+  if (e != cudaSuccess) return e;
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)(M < nsm ? M : nsm);
+  const uint4* a = static_cast<const uint4*>(img);
+  if (!q8 && (kperm || (g_hq_full_variant != 2 && g_hq_full_variant != 3))) {
+    auto kern = kperm ? hqwg::hq_full28_wg_kernel<true> : hqwg::hq_full28_wg_kernel<false>;
+    kern<<<grid, hqwg::NUM_THREADS, hqwg::SMEM, stream>>>(map, M, clip, q, ld_q, scale, a);
+    return cudaPeekAtLastError();
+  }
   auto kern = q8 ? hqtc::hq_full28_tc_kernel<false, true>
                  : (g_hq_full_variant == 2 ? hqtc::hq_full28_tc_kernel<true> : hqtc::hq_full28_tc_kernel<false>);
-  kern<<<grid, hqtc::NUM_THREADS, hqtc::SMEM, stream>>>(
-      map, M, clip, q, ld_q, scale, static_cast<const uint4*>(img));
+  kern<<<grid, hqtc::NUM_THREADS, hqtc::SMEM, stream>>>(map, M, clip, q, ld_q, scale, a);
   return cudaPeekAtLastError();
 }
 

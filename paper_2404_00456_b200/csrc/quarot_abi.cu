@@ -59,6 +59,15 @@ const char* quarot_last_cuda_error(void) { return g_last_cuda_error; }
 
 int32_t quarot_last_launch_count(void) { return g_last_launches; }
 
+quarot_status quarot_full_kperm(int64_t K, int64_t* perm) {
+  if (!perm) return QUAROT_ERR_NULL;
+  if (K != 28672) return QUAROT_ERR_UNSUPPORTED_SIZE;
+  const int64_t J = K / 256;  // natural element i = a * J + j', a < 256
+  for (int64_t a = 0; a < 256; ++a)
+    for (int64_t j = 0; j < J; ++j) perm[(a >> 5) * 32 * J + 32 * j + (a & 31)] = a * J + j;
+  return QUAROT_OK;
+}
+
 quarot_status quarot_base_hadamard(int32_t m, int8_t* out) {
   if (!out) return QUAROT_ERR_NULL;
   const int8_t* h = qr::base_hadamard_host(m);
@@ -72,11 +81,15 @@ quarot_status quarot_hadamard_quant(const void* x, int64_t M, int64_t K, int64_t
                                     void* stream) {
   g_last_launches = 0;
   const bool rms = (mode & QUAROT_HAD_RMSNORM) != 0;
-  mode &= ~QUAROT_HAD_RMSNORM;
+  const bool kperm = (mode & QUAROT_HAD_KPERM) != 0;
+  mode &= ~(QUAROT_HAD_RMSNORM | QUAROT_HAD_KPERM);
   if (mode < QUAROT_HAD_NONE || mode > QUAROT_HAD_ACROSS_HEADS) return QUAROT_ERR_ARG;
   if (rms && mode != QUAROT_HAD_NONE) return QUAROT_ERR_ARG;
+  if (kperm && mode != QUAROT_HAD_FULL) return QUAROT_ERR_ARG;
   if (!clip_ok(clip_ratio)) return QUAROT_ERR_ARG;
   if (M < 0 || K <= 0 || (K & 1) || ld_x < K || ld_q < K / 2) return QUAROT_ERR_DIM;
+  if (kperm && K != 28672) return QUAROT_ERR_UNSUPPORTED_SIZE;
+  if (kperm && (ld_q % 16 || (M > 0 && q && !aligned16(q)))) return QUAROT_ERR_ALIGN;
   if (M > 0x7fffffffLL) return QUAROT_ERR_DIM;
   if (M == 0) return QUAROT_OK;
   if (!x || !q || !scale) return QUAROT_ERR_NULL;
@@ -110,7 +123,8 @@ quarot_status quarot_hadamard_quant(const void* x, int64_t M, int64_t K, int64_t
       e = qr::ensure_device_tables();
       if (e != cudaSuccess) return cuda_fail(e);
     }
-    e = qr::launch_hq_full(x, M, K, ld_x, (int)p, m, clip_ratio, q, ld_q, scale, st);
+    e = kperm ? qr::launch_hq_full28_tc(x, M, ld_x, clip_ratio, q, ld_q, scale, st, false, true)
+              : qr::launch_hq_full(x, M, K, ld_x, (int)p, m, clip_ratio, q, ld_q, scale, st);
   }
   if (e != cudaSuccess) return cuda_fail(e);
   g_last_launches = 1;

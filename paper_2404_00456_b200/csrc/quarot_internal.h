@@ -31,8 +31,9 @@ cudaError_t launch_hq_none(const void* x, int64_t M, int64_t K, int64_t ld_x, fl
 cudaError_t launch_hq_heads(const void* x, int64_t M, int64_t K, int64_t ld_x, int head_dim, float clip,
                             uint8_t* q, int64_t ld_q, float* scale, cudaStream_t stream);
 // hq_full_tc.cu: K = 1024 x 28 on the tcgen05 path (the default for that width)
+// kperm: codes in the transform-native K order (quarot.h QUAROT_HAD_KPERM)
 cudaError_t launch_hq_full28_tc(const void* x, int64_t M, int64_t ld_x, float clip, uint8_t* q, int64_t ld_q,
-                                float* scale, cudaStream_t stream, bool q8 = false);
+                                float* scale, cudaStream_t stream, bool q8 = false, bool kperm = false);
 extern int g_hq_full_variant;
 // hq_full_small_tc.cu: the Llama-2-13B widths K = 128 x 108 and 256 x 20 on the tcgen05 path
 bool hq_full_small_tc_supported(int64_t pow2, int m);

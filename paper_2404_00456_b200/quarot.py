@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("QUAROT_LIB") or os.path.join(_PKG, "libquarot.so")
 
 NONE, FULL, ACROSS_HEADS = 0, 1, 2
 RMSNORM = 0x100  # mode flag: scale-free RMSNorm fused into the NONE quantizer
+KPERM = 0x200    # mode flag (FULL, K = 28672): codes in the transform-native K order
 MODES = {"none": NONE, "full": FULL, "across_heads": ACROSS_HEADS}
 KV_ROTATE_K, KV_ROTATE_V = 1, 2
 
@@ -51,6 +52,7 @@ _SIGS = {
     "quarot_status_string": [_c_i32],
     "quarot_abi_version": [],
     "quarot_base_hadamard": [_c_i32, _vp],
+    "quarot_full_kperm": [_c_i64, _vp],
     "quarot_last_launch_count": [],
     "quarot_last_cuda_error": [],
 }
@@ -123,12 +125,15 @@ def base_hadamard(m: int) -> torch.Tensor:
 
 def hadamard_quant(x: torch.Tensor, mode="none", head_dim: int = 128, clip_ratio: float = 0.9,
                    q: torch.Tensor | None = None, scale: torch.Tensor | None = None, stream=None,
-                   rmsnorm: bool = False):
+                   rmsnorm: bool = False, kperm: bool = False):
     """quarot_hadamard_quant: fp16 x [M, K] -> (packed uint8 q [M, K/2], fp32 scale [M]).
-    rmsnorm=True (NONE only): RMS-normalize each row first (scale-free RMSNorm, fused)."""
+    rmsnorm=True (NONE only): RMS-normalize each row first (scale-free RMSNorm, fused).
+    kperm=True (FULL, K = 28672): codes in the transform-native K order (full_kperm)."""
     mode_i = MODES[mode] if isinstance(mode, str) else int(mode)
     if rmsnorm:
         mode_i |= RMSNORM
+    if kperm:
+        mode_i |= KPERM
     M, K = x.shape
     if q is None:
         q = torch.empty(M, K // 2, dtype=torch.uint8, device=x.device)
@@ -139,6 +144,22 @@ def hadamard_quant(x: torch.Tensor, mode="none", head_dim: int = 128, clip_ratio
                                      _dev(scale, "scale", torch.float32), _stream(stream))
     _check("quarot_hadamard_quant", st)
     return q, scale
+
+
+def full_kperm(K: int) -> torch.Tensor:
+    """quarot_full_kperm: int64 [K] (host), perm[p] = natural element index at native position p."""
+    perm = torch.empty(K, dtype=torch.int64)
+    _check("quarot_full_kperm", lib().quarot_full_kperm(K, perm.data_ptr()))
+    return perm
+
+
+def permute_k_packed(w: torch.Tensor, perm: torch.Tensor) -> torch.Tensor:
+    """Offline: packed INT4 rows [N, K/2] reordered along K by `perm` (W'[n][p] = W[n][perm[p]]),
+    the weight layout paired with KPERM activations.  A pure nibble permutation (torch ops)."""
+    lo, hi = (w & 0xF), (w >> 4)
+    codes = torch.stack([lo, hi], -1).reshape(w.shape[0], -1)
+    codes = codes[:, perm.to(w.device)]
+    return (codes[:, 0::2] | (codes[:, 1::2] << 4)).contiguous()
 
 
 def int4_linear(xq: torch.Tensor, x_scale: torch.Tensor, wq: torch.Tensor, w_scale: torch.Tensor,

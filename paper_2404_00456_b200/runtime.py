@@ -192,13 +192,20 @@ class DecoderLayerStep:
     gu, then SwiGLU)."""
 
     def __init__(self, layer: QuaRotLayer, tokens: int, device="cuda", seq_len: int = 2048, theta: float = 10000.0,
-                 fuse_swiglu: bool = True, fuse_rope: bool = True, row_offset: int = 0):
+                 fuse_swiglu: bool = True, fuse_rope: bool = True, row_offset: int = 0, kperm: bool | None = None):
         """tokens: rows this step processes; row_offset: their first row in the global batch (a
         token shard of a multi-GPU job, dist.shard_bounds): RoPE positions are
-        (row_offset + t) % seq_len, so a sharded run equals the unsharded one bit for bit."""
+        (row_offset + t) % seq_len, so a sharded run equals the unsharded one bit for bit.
+        kperm (default: on where supported, FFN = 1024 x 28): the down_proj input is quantized in
+        the FULL kernel's native K order (quarot.h QUAROT_HAD_KPERM) against down_proj weights whose
+        columns were permuted the same way offline — bit-identical outputs, faster stores."""
         self.layer, self.tokens, self.device = layer, tokens, torch.device(device)
         self.seq_len, self.theta, self.row_offset = seq_len, theta, row_offset
         self.fuse_swiglu, self.fuse_rope = fuse_swiglu, fuse_rope
+        self.kperm = (layer.ffn == 28672) if kperm is None else kperm
+        if self.kperm:  # offline: W_down columns in the native K order of the FULL quantizer
+            wq, ws = layer.weights["down"]
+            self.down_kperm = (q.permute_k_packed(wq, q.full_kperm(layer.ffn)), ws)
         self.LAUNCHES = 9 + (not fuse_swiglu) + (not fuse_rope)
         if fuse_swiglu:  # offline: gate/up rows interleaved in blocks of 8 for the fused epilogue
             self.gate_up_il = q.interleave_gate_up(*layer.weights["gate_up"])
@@ -244,9 +251,10 @@ class DecoderLayerStep:
         def linear(spec, xin, rms, out, residual=None):
             xq = self.xq[r0:r1, : spec.k // 2]
             xs = self.xs[r0:r1]
-            q.hadamard_quant(xin, spec.mode, d, L.clip_act, q=xq, scale=xs, stream=stream, rmsnorm=rms)
+            kp = self.kperm and spec.name == "down"
+            q.hadamard_quant(xin, spec.mode, d, L.clip_act, q=xq, scale=xs, stream=stream, rmsnorm=rms, kperm=kp)
             mark(f"hq_{spec.name}")
-            wq, ws = L.weights[spec.name]
+            wq, ws = self.down_kperm if kp else L.weights[spec.name]
             q.int4_linear(xq, xs, wq, ws, y=out, stream=stream, residual=residual)
             mark(f"gemm_{spec.name}")
 

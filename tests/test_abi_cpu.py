@@ -250,3 +250,39 @@ def test_every_wrapper_passes_declared_arity_and_stream(monkeypatch):
     assert len(launched) >= 18
     for name, args in launched:
         assert args[-1] == STREAM, f"{name}: stream not forwarded (last arg {args[-1]!r})"
+
+
+def test_full_kperm_permutation_matches_header_formula(q):
+    """quarot_full_kperm (QUAROT_HAD_KPERM): a bijection, equal to the header's formula
+    p(i) = (a >> 5) * 32 J + 32 j' + (a & 31) for i = a * J + j', J = K / 256."""
+    K = 28672
+    perm = q.full_kperm(K).numpy()
+    assert np.array_equal(np.sort(perm), np.arange(K))
+    J = K // 256
+    i = np.arange(K)
+    a, j = i // J, i % J
+    p = (a >> 5) * 32 * J + 32 * j + (a & 31)
+    assert np.array_equal(perm[p], i)
+    with pytest.raises(q.QuarotError):
+        q.full_kperm(8192)
+
+
+def test_permute_k_packed_roundtrip(q):
+    import torch
+    rng = np.random.default_rng(0)
+    K = 28672
+    w = torch.from_numpy(rng.integers(0, 256, (3, K // 2), dtype=np.uint8))
+    perm = q.full_kperm(K)
+    wp = q.permute_k_packed(w, perm)
+    inv = torch.empty_like(perm)
+    inv[perm] = torch.arange(K)
+    assert torch.equal(q.permute_k_packed(wp, inv), w)
+
+
+def test_kperm_flag_validation_without_gpu(q):
+    f = lambda mode, K, ld_q=None, qp=32: q.lib().quarot_hadamard_quant(16, 4, K, K, mode, 128, 0.9, qp,
+                                                                         ld_q or K // 2, 48, None)
+    assert f(q.FULL | q.KPERM, 8192) == 3                 # KPERM only at K = 1024 x 28
+    assert f(q.NONE | q.KPERM, 28672) == 5                # FULL only
+    assert f(q.FULL | q.KPERM, 28672, ld_q=14344) == 4    # ld_q % 16
+    assert f(q.FULL | q.KPERM, 28672, qp=40) == 4         # q 16-byte aligned
