@@ -314,6 +314,20 @@ int32_t quarot_last_launch_count(void);
  * QUAROT_ERR_CUDA ("" if none); the buffer is owned by the library. */
 const char* quarot_last_cuda_error(void);
 
+/* Diagnostics: process-wide kernel-variant switches for A/B experiments and roofline probes
+ * (not thread-safe; 0 restores the default).  quarot_debug_gemm_mode: 1 = the INT4 GEMM with its
+ * producers idled (MMA issue only: the tensor-pipe probe bench.py reports as the INT8 peak), 2 =
+ * no B widening stores, 3 = no TMA, 4 = no output stores — probes 1-4 compute garbage.
+ * quarot_debug_gemm_group_m: raster group override (pair-rows).  quarot_debug_hq_full_variant:
+ * 1 = the mma.sync FULL-28 kernel, 2 / 3 = the 16-warps-per-row tcgen05 kernel (spin / sleep
+ * waits).  quarot_debug_hq_heads_variant: 1 = the CUDA-core ACROSS_HEADS kernel for every width.
+ * quarot_debug_kv_variant: 1 = the CUDA-core KV kernel for every shape. */
+void quarot_debug_gemm_mode(int32_t mode);
+void quarot_debug_gemm_group_m(int32_t group_m);
+void quarot_debug_hq_full_variant(int32_t variant);
+void quarot_debug_hq_heads_variant(int32_t variant);
+void quarot_debug_kv_variant(int32_t variant);
+
 #ifdef __cplusplus
 }
 #endif

@@ -934,7 +934,7 @@ cudaError_t launch_hq_full(const void* x, int64_t M, int64_t K, int64_t ld_x, in
 
 }  // namespace qr
 
-extern "C" void quarot_debug_hq_heads_variant(int v) { qr::g_hq_heads_variant = v; }
+extern "C" void quarot_debug_hq_heads_variant(int32_t v) { qr::g_hq_heads_variant = v; }
 
 #ifdef QR_F28_PROF
 extern "C" void quarot_debug_f28_prof(unsigned long long* out) {

@@ -836,4 +836,4 @@ cudaError_t launch_hq_full28_tc(const void* x, int64_t M, int64_t ld_x, float cl
 
 }  // namespace qr
 
-extern "C" void quarot_debug_hq_full_variant(int v) { qr::g_hq_full_variant = v; }
+extern "C" void quarot_debug_hq_full_variant(int32_t v) { qr::g_hq_full_variant = v; }

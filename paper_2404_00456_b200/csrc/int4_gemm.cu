@@ -1146,8 +1146,8 @@ cudaError_t launch_int8_group_gemm(const int8_t* xq, const float* xs, int64_t ld
 }
 
 // Debug / roofline probe (not in the public header): mode 1 = MMA issue only.
-extern "C" void quarot_debug_gemm_mode(int mode) { g_gemm_debug_mode = mode; }
-extern "C" void quarot_debug_gemm_group_m(int g) { g_gemm_group_m = g; }
+extern "C" void quarot_debug_gemm_mode(int32_t mode) { g_gemm_debug_mode = mode; }
+extern "C" void quarot_debug_gemm_group_m(int32_t g) { g_gemm_group_m = g; }
 
 cudaError_t launch_int4_gemm(const uint8_t* xq, const float* xs, int64_t M, int64_t K, int64_t ld_xq,
                              const uint8_t* wq, const float* ws, int64_t N, int64_t ld_wq, void* y,

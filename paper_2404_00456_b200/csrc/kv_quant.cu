@@ -346,4 +346,4 @@ cudaError_t launch_kv_quant_rope(const void* k, int64_t ld_k, const void* v, int
 
 }  // namespace qr
 
-extern "C" void quarot_debug_kv_variant(int v) { qr::g_kv_variant = v; }
+extern "C" void quarot_debug_kv_variant(int32_t v) { qr::g_kv_variant = v; }

@@ -55,6 +55,11 @@ _SIGS = {
     "quarot_full_kperm": [_c_i64, _vp],
     "quarot_last_launch_count": [],
     "quarot_last_cuda_error": [],
+    "quarot_debug_gemm_mode": [_c_i32],
+    "quarot_debug_gemm_group_m": [_c_i32],
+    "quarot_debug_hq_full_variant": [_c_i32],
+    "quarot_debug_hq_heads_variant": [_c_i32],
+    "quarot_debug_kv_variant": [_c_i32],
 }
 EXPORTS = tuple(_SIGS)
 
@@ -79,7 +84,8 @@ def lib() -> ctypes.CDLL:
             f = getattr(h, name)
             f.argtypes = args
             f.restype = (ctypes.c_char_p if name in ("quarot_status_string", "quarot_last_cuda_error")
-                         else ctypes.c_int64 if name == "quarot_kv_decode_workspace_bytes" else ctypes.c_int32)
+                         else ctypes.c_int64 if name == "quarot_kv_decode_workspace_bytes"
+                         else None if name.startswith("quarot_debug_") else ctypes.c_int32)
         _lib = h
     return _lib
 

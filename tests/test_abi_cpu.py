@@ -163,7 +163,7 @@ def declared_signatures():
     """name -> list of ctypes type names, parsed from include/quarot.h."""
     src = re.sub(r"/\*.*?\*/", "", open(HEADER).read(), flags=re.S)
     sigs = {}
-    for m in re.finditer(r"\b(?:quarot_status|int64_t|int32_t|const char\*)\s+(quarot_[a-z0-9_]+)\s*\(([^)]*)\)\s*;",
+    for m in re.finditer(r"\b(?:quarot_status|int64_t|int32_t|void|const char\*)\s+(quarot_[a-z0-9_]+)\s*\(([^)]*)\)\s*;",
                          src):
         params = [p.strip() for p in m.group(2).split(",") if p.strip() and p.strip() != "void"]
         types = []
