@@ -7,16 +7,18 @@
 // in TMEM (lane = row, column = d').  The inputs are fp16 (post-RoPE rounded to fp16, reading
 // Z22), so the +-1 products are exact and the sums fp32, like the butterflies they replace.
 //  * Work = token blocks of B_t = 128 / n_kv tokens: n_q / n_kv Q tiles, one K tile and one V
-//    tile of 128 rows each (V goes through the MMA with B = I, exact, to share the epilogue).
+//    tile of 128 rows each (V is not rotated: the epilogue reads it straight from the stage).
 //  * A TMA warp loads each tile (3-D maps [token][head][d], two 64-wide d boxes) straight into
 //    the K-major SWIZZLE_128B operand layout, 3-stage ring.  With RoPE fused, eight warps rotate
 //    the Q / K rows in place in shared memory (two threads per row) from a per-block cos/sin table
 //    (fp64 sincos rounded to fp32, as quarot_rope; two table warps build it a block ahead into a
 //    double buffer) and round to fp16; otherwise they only hand the stage to the MMA.
-//  * Epilogue warps (thread = TMEM lane = row): Q rows scaled by 1/sqrt(128), rounded to fp16
-//    and written back in place; K / V rows quantized asymmetrically (clip 0.95, group = the
-//    row, reading Z14) entirely in-thread: min / max, scale / zero, 64 code bytes in four
-//    16-byte stores.
+//  * Epilogue warps (thread = TMEM lane = row): Q rows scaled by 1/sqrt(128), rounded to fp16,
+//    written into the (consumed) stage in the operand's SW128 layout and TMA-stored back in place
+//    (the bulk tensor store writes whole lines; per-thread 16-byte row stores at a 256-byte lane
+//    stride touched 32 half-used sectors per instruction); K / V rows quantized asymmetrically
+//    (clip 0.95, group = the row, reading Z14) entirely in-thread: min / max, scale / zero, 64
+//    code bytes in four 16-byte stores.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -31,7 +33,7 @@ namespace kvtc {
 
 constexpr int HD = 128;
 constexpr int TILE_BYTES = 128 * HD * 2;  // 32 KB: 128 rows x 128 fp16, two SW128 atoms
-constexpr int STAGES = 3;
+constexpr int STAGES = 4;
 constexpr int NUM_EPI = 4, NUM_PROD = 8;  // two RoPE threads per tile row
 constexpr int EPI_WARP0 = 0, PROD_WARP0 = 4, MMA_WARP = 12, TMA_WARP = 13, TAB_WARP0 = 14, NUM_TAB = 2;
 constexpr int NUM_THREADS = 16 * 32;
@@ -39,7 +41,7 @@ constexpr int TBUF = 4;
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int MAX_BT = 32;                                 // tokens per block (n_kv >= 4)
 constexpr int TAB_BYTES = MAX_BT * (HD / 2) * 8;           // (cos, sin) per token and pair
-constexpr size_t SMEM = 1024 + 2 * TILE_BYTES + (size_t)STAGES * TILE_BYTES + 2 * TAB_BYTES + 512 + (HD / 2) * 8;
+constexpr size_t SMEM = 1024 + TILE_BYTES + (size_t)STAGES * TILE_BYTES + 2 * TAB_BYTES + 512 + (HD / 2) * 8;
 static_assert(SMEM <= 232448, "227 KB dynamic smem");
 constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(HD >> 3) << 17) | ((128u >> 4) << 24);
 
@@ -79,6 +81,12 @@ QR_DEVICE void tma_load_3d(uint32_t dst, const CUtensorMap* map, int x, int y, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
       : "memory");
 }
+QR_DEVICE void tma_store_3d(const CUtensorMap* map, int x, int y, int z, uint32_t src) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y), "r"(z), "r"(src)
+               : "memory");
+}
 QR_DEVICE void bar_named(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 QR_DEVICE uint32_t sw128(int row, int d) {  // byte offset of element d of tile row `row`
   const int atom = d >> 6, chunk = (d & 63) >> 3;
@@ -101,8 +109,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                  const __grid_constant__ CUtensorMap tmV, const Args a, const uint4* __restrict__ b_img) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sB = smem;                   // [H_128 | I_128] K-major SW128 images
-  uint8_t* sA = sB + 2 * TILE_BYTES;    // [STAGES] tiles
+  uint8_t* sB = smem;                   // H_128 K-major SW128 image
+  uint8_t* sA = sB + TILE_BYTES;        // [STAGES] tiles
   float2* tab = reinterpret_cast<float2*>(sA + STAGES * TILE_BYTES);  // [2][B_t][64] (cos, sin)
   uint64_t* a_full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(tab) + 2 * TAB_BYTES);
   uint64_t* a_empty = a_full + STAGES;
@@ -121,7 +129,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int64_t my_blocks = nblocks > (int64_t)blockIdx.x ? (nblocks - 1 - (int64_t)blockIdx.x) / gridDim.x + 1 : 0;
   const int64_t ntiles = my_blocks * tpb;
 
-  for (int i = threadIdx.x; i < 2 * TILE_BYTES / 16; i += NUM_THREADS) reinterpret_cast<uint4*>(sB)[i] = __ldg(b_img + i);
+  for (int i = threadIdx.x; i < TILE_BYTES / 16; i += NUM_THREADS) reinterpret_cast<uint4*>(sB)[i] = __ldg(b_img + i);
   if (kRope)
     for (int i = threadIdx.x; i < HD / 2; i += NUM_THREADS) inv_freq[i] = pow((double)a.theta, -2.0 * (double)i / (double)HD);
   fence_proxy_async_smem();
@@ -186,7 +194,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           // RoPE rotate-half pairs (i, i + 64), rounded to fp16 (reading Z22)
           const int nh = ti.type == 0 ? a.n_q : a.n_kv;
           const int tl = (ti.row0 + r) / nh;  // token within the block
-          const float2* cs = btab + tl * (HD / 2);
+          const uint32_t cs = smem_u32(btab + tl * (HD / 2));  // ld.shared (a generic load takes the L1 tag path)
           const uint32_t row = smem_u32(sA + s * TILE_BYTES);
 #pragma unroll
           for (int cc = 0; cc < 4; ++cc) {
@@ -200,7 +208,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const float2 x1 = __half22float2(lo[e]), x2 = __half22float2(hi[e]);
-              const float4 c2 = *reinterpret_cast<const float4*>(cs + 8 * c + 2 * e);  // pairs i, i + 1
+              float4 c2;  // (cos, sin) of pairs i, i + 1
+              asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                           : "=f"(c2.x), "=f"(c2.y), "=f"(c2.z), "=f"(c2.w)
+                           : "r"(cs + (uint32_t)((8 * c + 2 * e) * 8)));
               lo[e] = __floats2half2_rn(rope_first(x1.x, x2.x, c2.x, c2.y), rope_first(x1.y, x2.y, c2.z, c2.w));
               hi[e] = __floats2half2_rn(rope_second(x1.x, x2.x, c2.x, c2.y), rope_second(x1.y, x2.y, c2.z, c2.w));
             }
@@ -234,16 +245,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp == MMA_WARP) {
-    // ---------------------------------------------------------------- MMA: D = rows x B^T
+    // ---------------------------------------------------------------- MMA: D = rows x H^T (Q, K tiles)
     const uint32_t sa = smem_u32(sA), sb = smem_u32(sB);
+    int64_t mt = 0;  // MMA tiles issued (the TMEM buffer ring)
     for (int64_t it = 0; it < ntiles; ++it) {
-      const int s = (int)(it % STAGES), tb = (int)(it % TBUF);
       const TileInfo ti = tile_info((int)(it % tpb), nQ);
-      mbar_wait(&t_empty[tb], (uint32_t)((it / TBUF) & 1) ^ 1u);
+      if (ti.type == 2) continue;  // V: not rotated, the epilogue reads the stage directly
+      const int s = (int)(it % STAGES), tb = (int)(mt % TBUF);
+      mbar_wait(&t_empty[tb], (uint32_t)((mt / TBUF) & 1) ^ 1u);
       mbar_wait(&a_full[s], (uint32_t)((it / STAGES) & 1));
       tc_fence_after();
       const uint64_t a_desc = umma_desc_sw128(sa + (uint32_t)(s * TILE_BYTES));
-      const uint64_t b_desc = umma_desc_sw128(sb + (uint32_t)(ti.type == 2 ? TILE_BYTES : 0));
+      const uint64_t b_desc = umma_desc_sw128(sb);
       const uint32_t d_tmem = tmem_base + (uint32_t)(tb * HD);
       if (elect_one()) {
 #pragma unroll
@@ -251,10 +264,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint64_t koff = (uint64_t)((kk >> 2) * (16384 >> 4) + 2 * (kk & 3));
           mma_f16(d_tmem, a_desc + koff, b_desc + koff, IDESC, kk > 0 ? 1u : 0u);
         }
-        mma_commit(&a_empty[s]);
-        mma_commit(&t_full[tb]);
+        if (ti.type == 1) mma_commit(&a_empty[s]);  // K: the stage is free once read; Q: the
+        mma_commit(&t_full[tb]);                     // epilogue reuses it for the TMA store
       }
       __syncwarp();
+      ++mt;
     }
   } else if (warp < EPI_WARP0 + NUM_EPI) {
     // ---------------------------------------------------------------- epilogue: thread = row
@@ -262,8 +276,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t t_lane = tmem_base + ((uint32_t)(warp * 32) << 16);
     const double rnorm = rsqrt((double)HD);
     const float rn = (float)rnorm;
+    int64_t mt = 0;  // MMA tiles consumed (the TMEM buffer ring)
     for (int64_t it = 0; it < ntiles; ++it) {
-      const int tb = (int)(it % TBUF);
+      const int s = (int)(it % STAGES);
       const int64_t bi = it / tpb;
       const TileInfo ti = tile_info((int)(it % tpb), nQ);
       const int64_t t0 = ((int64_t)blockIdx.x + bi * gridDim.x) * BT;
@@ -272,13 +287,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int tl = rr / nh, h = rr - tl * nh;
       const int64_t t = t0 + tl;
       const bool ok = t < a.T;
-      mbar_wait_sleep(&t_full[tb], (uint32_t)((it / TBUF) & 1));
-      tc_fence_after();
-      const uint32_t tcol = t_lane + (uint32_t)(tb * HD);
-      // every lane runs the (warp-collective) TMEM loads; rows past T only skip their stores
+      const uint32_t stage = smem_u32(sA + s * TILE_BYTES);
       uint32_t u[HD / 2];  // one 64-column half of the row at a time (register budget)
-      if (ti.type == 0) {  // Q: rotated in place, rounded to fp16 (Eq. 13)
-        uint4* dst = reinterpret_cast<uint4*>(a.q + t * a.ld_q + h * HD);
+      if (ti.type == 0) {  // Q: rotated, rounded to fp16 (Eq. 13), TMA-stored back in place
+        const int tb = (int)(mt % TBUF);
+        mbar_wait_sleep(&t_full[tb], (uint32_t)((mt / TBUF) & 1));
+        tc_fence_after();
+        const uint32_t tcol = t_lane + (uint32_t)(tb * HD);
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf) {
           QR_TMEM_LD32(tcol + 64u * hf, u);
@@ -291,21 +306,63 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
             for (int e = 0; e < 4; ++e)
               hw[e] = __floats2half2_rn(__uint_as_float(u[8 * c + 2 * e]) * rn, __uint_as_float(u[8 * c + 2 * e + 1]) * rn);
-            if (ok) dst[8 * hf + c] = w;
+            sts_v4(stage + sw128(r, 64 * hf + 8 * c), w);  // the MMA has read the stage (t_full)
           }
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&t_empty[tb]);
+        ++mt;
+        fence_proxy_async_smem();  // the rows' generic stores -> the TMA store (async proxy)
+        bar_named(1, NUM_EPI * 32);
+        if (threadIdx.x == EPI_WARP0 * 32) {
+          const int tok = (int)(t0 + ti.row0 / nh);  // rows past T are clipped by the tensor map
+          tma_store_3d(&tmQ, 0, 0, tok, stage);
+          tma_store_3d(&tmQ, 64, 0, tok, stage + 16384);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem read: the stage is free
+          mbar_arrive(&a_empty[s]);
+        }
         continue;
       }
-      // K / V: asymmetric 4-bit quantization of the row (group = head_dim, reading Z14)
+      // K / V: asymmetric 4-bit quantization of the row (group = head_dim, reading Z14); K from
+      // TMEM (rotated), V straight from the stage (fp16 -> fp32 is exact, as the MMA with I was)
+      int tb = 0;
+      uint32_t tcol = 0;
+      if (ti.type == 1) {
+        tb = (int)(mt % TBUF);
+        mbar_wait_sleep(&t_full[tb], (uint32_t)((mt / TBUF) & 1));
+        tc_fence_after();
+        tcol = t_lane + (uint32_t)(tb * HD);
+      } else {
+        mbar_wait(&a_full[s], (uint32_t)((it / STAGES) & 1));  // landed (no RoPE on V)
+      }
+      auto load_half = [&](int hf) {
+        if (ti.type == 1) {
+          QR_TMEM_LD32(tcol + 64u * hf, u);
+          QR_TMEM_LD32(tcol + 64u * hf + 32u, (u + 32));
+          tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            uint4 w;
+            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+                         : "r"(stage + sw128(r, 64 * hf + 8 * c)));
+            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&ws[e]));
+              u[8 * c + 2 * e] = __float_as_uint(f.x);
+              u[8 * c + 2 * e + 1] = __float_as_uint(f.y);
+            }
+          }
+        }
+      };
       float mn4[4], mx4[4];
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
-        QR_TMEM_LD32(tcol + 64u * hf, u);
-        QR_TMEM_LD32(tcol + 64u * hf + 32u, (u + 32));
-        tmem_ld_wait();
+        load_half(hf);
         if (hf == 0) {
 #pragma unroll
           for (int j = 0; j < 4; ++j) mn4[j] = mx4[j] = __uint_as_float(u[j]);
@@ -335,10 +392,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint8_t* codes = (ti.type == 1 ? a.k_codes : a.v_codes) + gi * (HD / 2);
       const float zf = (float)z;
 #pragma unroll
-      for (int hf = 0; hf < 2; ++hf) {  // the first half is reloaded (TMEM reads are cheap)
-        QR_TMEM_LD32(tcol + 64u * hf, u);
-        QR_TMEM_LD32(tcol + 64u * hf + 32u, (u + 32));
-        tmem_ld_wait();
+      for (int hf = 0; hf < 2; ++hf) {  // the first half is reloaded (TMEM / smem reads are cheap)
+        load_half(hf);
         uint32_t w[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) w[j] = 0u;
@@ -361,14 +416,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             reinterpret_cast<uint4*>(codes)[2 * hf + c] = make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&t_empty[tb]);
+      if (ti.type == 1) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&t_empty[tb]);
+        ++mt;
+      } else {
+        bar_named(1, NUM_EPI * 32);  // every row of the V stage read: release it
+        if (threadIdx.x == EPI_WARP0 * 32) mbar_arrive(&a_empty[s]);
+      }
       if (ok) {
         (ti.type == 1 ? a.k_scale : a.v_scale)[gi] = sc;
         (ti.type == 1 ? a.k_zero : a.v_zero)[gi] = (uint8_t)z;
       }
     }
+    if (threadIdx.x == EPI_WARP0 * 32) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
@@ -382,11 +444,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
 namespace {
 
-// [H_128 | I_128] as K-major SWIZZLE_128B images (rows = output d', K = input d): two atoms of
+// H_128 as the K-major SWIZZLE_128B image (rows = output d', K = input d): two atoms of
 // 64 columns per matrix, 16-byte chunk c of row r at chunk c ^ (r & 7)
 std::vector<uint16_t> b_images() {
-  std::vector<uint16_t> img(2 * kvtc::TILE_BYTES / 2, 0);
-  for (int which = 0; which < 2; ++which)
+  std::vector<uint16_t> img(kvtc::TILE_BYTES / 2, 0);
+  for (int which = 0; which < 1; ++which)
     for (int r = 0; r < kvtc::HD; ++r)
       for (int k = 0; k < kvtc::HD; ++k) {
         const int v = which == 0 ? ((__builtin_popcount(r & k) & 1) ? -1 : 1) : (r == k ? 1 : 0);
@@ -401,7 +463,7 @@ std::vector<uint16_t> b_images() {
 std::mutex g_mu;
 void* g_bimg[64];
 // the constant B images live in static device memory (the library allocates none)
-__device__ uint4 g_kv_bimg[2 * kvtc::TILE_BYTES / 16];
+__device__ uint4 g_kv_bimg[kvtc::TILE_BYTES / 16];
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn_kv() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
