@@ -54,60 +54,95 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region.  An NVML polling thread
+    (every 10 ms, so even a 10 ms region gets samples) when pynvml is importable, else
+    nvidia-smi -lms 100.  The main thread sits in cudaEventSynchronize (GIL released)."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
         self.path = None
+        self.thread = None
+        self.samples = []  # (sm_mhz, max_mhz, {reasons})
+        self.source = None
+
+    def _nvml_loop(self, nv, h):
+        bits = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+                "sw_power_cap": 0x4}
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((float(sm), float(mx), {n for n, b in bits.items() if r & b}))
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.01)
 
     def __enter__(self):
+        try:
+            import threading
+
+            import pynvml as nv
+            nv.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            phys = int(vis.split(",")[self.index]) if vis and vis.split(",")[0].strip().isdigit() else self.index
+            h = nv.nvmlDeviceGetHandleByIndex(phys)
+            self._stop = threading.Event()
+            self.thread = threading.Thread(target=self._nvml_loop, args=(nv, h), daemon=True)
+            self.thread.start()
+            self.source = "nvml 10 ms"
+            return self
+        except Exception:  # noqa: BLE001
+            self.thread = None
         try:
             fd, self.path = tempfile.mkstemp(suffix=".csv")
             os.close(fd)
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=self.fh, stderr=subprocess.DEVNULL)
-        except Exception:
+            self.source = "nvidia-smi 100 ms"
+        except Exception:  # noqa: BLE001
             self.proc = None
         return self
 
     def __exit__(self, *a):
+        if self.thread is not None:
+            self._stop.set()
+            self.thread.join(timeout=5)
         if self.proc is not None:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
-            except Exception:
+            except Exception:  # noqa: BLE001
                 self.proc.kill()
             self.fh.close()
 
     def summary(self):
-        if not self.path or not os.path.exists(self.path):
+        if self.thread is None and self.path and os.path.exists(self.path):
+            with open(self.path) as f:
+                for line in f:
+                    parts = [p.strip() for p in line.split(",")]
+                    if len(parts) < 9:
+                        continue
+                    try:
+                        sm, mx = float(parts[1]), float(parts[2])
+                    except ValueError:
+                        continue
+                    self.samples.append((sm, mx, {n for n, v in zip(self.NAMES, parts[5:9])
+                                                  if v.lower().startswith("active")}))
+            os.unlink(self.path)
+        if not self.samples:
             return None
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        with open(self.path) as f:
-            for line in f:
-                parts = [p.strip() for p in line.split(",")]
-                if len(parts) < 9:
-                    continue
-                try:
-                    sm.append(float(parts[1]))
-                    mx = float(parts[2])
-                except ValueError:
-                    continue
-                for n, v in zip(names, parts[5:9]):
-                    if v.lower().startswith("active"):
-                        reasons.add(n)
-        os.unlink(self.path)
-        if not sm:
-            return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        reasons = set().union(*(s[2] for s in self.samples))
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples), "sm_max_mhz": self.samples[-1][1],
+                "reasons": sorted(reasons), "samples": len(self.samples), "source": self.source}
 
 
 CONFIGS = {  # BASELINE.json configs served by the bench: name -> (shapes, global batch, seq_len, workload)
@@ -522,6 +557,8 @@ def main():
                      "traffic": traffic.get("int4_gemm")},
         "roofline_hbm": {"bound": "hbm", "kernel": "hadamard_quant (4 launches/step)", "achieved": hq_gbs,
                          "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": hq_gbs / peaks["hbm_gbs"],
+                         "peak_source": ("measured (MEASURED_PEAKS.json hbm_gbs)" if peaks["source"] == "measured"
+                                         else "fallback: MEASURED_PEAKS.json absent, B200_PROFILING.md 6.65 TB/s"),
                          "traffic": traffic.get("hadamard_quant")},
         "kernels": kernels,
         "gpu_launches": step.LAUNCHES * args.steps,
