@@ -18,7 +18,7 @@
  *   quarot_kv_append        routine "Append": one new token per sequence into the cache
  *   quarot_kv_decode        routine "Decode": attention over the INT4 cache
  *   quarot_hadamard_quant8, quarot_int8_linear   A8W8 (8-bit RTN configuration)
- *   quarot_hadamard_quant_group(8), quarot_int4_linear_group   group-wise W4A4 (§8 f3)
+ *   quarot_hadamard_quant_group(8), quarot_int4_linear_group(8)   group-wise W4A4 (§8 f3)
  *
  * Conventions (all entry points)
  *  - Tensor pointers are CUDA DEVICE pointers owned by the caller.  The library never
@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define QUAROT_ABI_VERSION 1
+#define QUAROT_ABI_VERSION 2  /* 2: mode / head_dim in the group-wise quantizers */
 
 typedef enum {
   QUAROT_OK = 0,
@@ -196,46 +196,58 @@ quarot_status quarot_kv_quant_rope(const void* k, int64_t ld_k, const void* v, i
                                    float theta, uint8_t* k_codes, float* k_scale, uint8_t* k_zero,
                                    uint8_t* v_codes, float* v_scale, uint8_t* v_zero, void* stream);
 
-/* group-wise symmetric INT4 ("group-wise quantization", group size 128
- * in tab:group_wise_ablation), mode NONE (the global rotation is fused into W).
- * quarot_hadamard_quant_group: every run of `group` consecutive elements of a row is quantized
- *   by the rule of quarot_hadamard_quant (scale = fp32(clip * max|x_g| / 7), codes RNE, clamp
- *   [-7, 7]; zero group: scale 1, codes 0; non-finite group: scale NaN, codes 0).
+/* group-wise symmetric INT4 ("group-wise quantization", group sizes 256 / 128 /
+ * 64 in tab:group_wise_ablation P:392-416), after the online transform of `mode`.
+ * quarot_hadamard_quant_group: y = the transformed row exactly as quarot_hadamard_quant computes it
+ *   (mode NONE / FULL / ACROSS_HEADS, head_dim for ACROSS_HEADS; the normalized transform, reading
+ *   Z5); then every run of `group` consecutive elements of y (natural element order) is quantized by
+ *   the rule of quarot_hadamard_quant (scale = fp32(clip * max|y_g| / 7), codes RNE, clamp [-7, 7];
+ *   zero group: scale 1, codes 0; non-finite group: scale NaN, codes 0).
  *   x      fp16 [M][ld_x] device, K elements used per row
  *   q      uint8 [M][ld_q] device, K/2 packed bytes (low nibble = even element)
  *   scale  fp32 [M][ld_s] device, K/group scales per row (ld_s >= K/group)
- *   group  64, 128 or 256 (QUAROT_ERR_UNSUPPORTED_SIZE otherwise); K % group == 0 (QUAROT_ERR_DIM);
- *          M < 2^31, K <= 65535 * 1024
+ *   group  64, 128 or 256 (QUAROT_ERR_UNSUPPORTED_SIZE otherwise); K % group == 0 (QUAROT_ERR_DIM)
+ *   mode   NONE: M < 2^31, K <= 65535 * 1024.  FULL: K = 2^n m (n >= 1, m in {1, 20, 28, 108, 172}),
+ *          K <= 32768, K % 16 == 0.  ACROSS_HEADS: head_dim and n_h = K / head_dim >= 2 powers of two,
+ *          K <= 32768, K % 16 == 0 (QUAROT_ERR_UNSUPPORTED_SIZE / QUAROT_ERR_ALIGN otherwise).
+ *          RMSNORM / KPERM flags: QUAROT_ERR_ARG.
  * Errors as quarot_hadamard_quant; x and q 16-byte aligned, ld_x % 8 == 0, ld_q % 4 == 0.
  * quarot_hadamard_quant_group8: the same codes, one per int8 byte (q int8 [M][ld_q], ld_q >= K,
- *   ld_q % 8 == 0) — the operand format of quarot_int4_linear_group. */
-quarot_status quarot_hadamard_quant_group(const void* x, int64_t M, int64_t K, int64_t ld_x, int32_t group,
-                                         float clip_ratio, uint8_t* q, int64_t ld_q, float* scale, int64_t ld_s,
-                                         void* stream);
-quarot_status quarot_hadamard_quant_group8(const void* x, int64_t M, int64_t K, int64_t ld_x, int32_t group,
-                                          float clip_ratio, int8_t* q, int64_t ld_q, float* scale, int64_t ld_s,
-                                          void* stream);
-/* quarot_int4_linear_group: group-wise W4A4 linear (§8 f3), group 128:
- *   y[m][n] = fp16( sum_g x_scale[m][g] * w_scale_t[g][n] * sum_{k in g} xq[m][k] * wq[n][k] ),
+ *   ld_q % 8 == 0). */
+quarot_status quarot_hadamard_quant_group(const void* x, int64_t M, int64_t K, int64_t ld_x, int32_t mode,
+                                         int32_t head_dim, int32_t group, float clip_ratio, uint8_t* q, int64_t ld_q,
+                                         float* scale, int64_t ld_s, void* stream);
+quarot_status quarot_hadamard_quant_group8(const void* x, int64_t M, int64_t K, int64_t ld_x, int32_t mode,
+                                          int32_t head_dim, int32_t group, float clip_ratio, int8_t* q, int64_t ld_q,
+                                          float* scale, int64_t ld_s, void* stream);
+/* quarot_int4_linear_group: group-wise W4A4 linear (§8 f3), group G in {64, 128, 256}:
+ *   y[m][n] = fp16( sum_g x_scale[m][g] * w_scale_t[g][n] * sum_{k in g} cx[m][k] * cw[n][k] ),
  *   the per-group integer sums exact (int32 on the tensor cores), the scaled sum in fp32.
- *   xq int8 [M][ld_xq] and wq int8 [N][ld_wq]: INT4 codes in [-7, 7], one per byte (the 4-bit
- *   values take the native kind::i8 path); x_scale fp32 [M][ld_sx] (K/128 per row,
- *   as quarot_hadamard_quant_group8 writes them); w_scale_t fp32 [K/128][ld_sw] (transposed,
- *   prepared offline); y fp16 [M][ld_y].  K % 256 == 0, N % 8 == 0, ld_xq / ld_wq % 16 == 0,
- *   ld_y % 8 == 0, ld_sw % 4 == 0, 16-byte aligned xq / wq / y / w_scale_t (QUAROT_ERR_ALIGN); group != 128:
- *   QUAROT_ERR_UNSUPPORTED_SIZE. */
-quarot_status quarot_int4_linear_group(const int8_t* xq, const float* x_scale, int64_t ld_sx, int64_t M, int64_t K,
-                                       int64_t ld_xq, const int8_t* wq, const float* w_scale_t, int64_t ld_sw,
+ *   xq uint8 [M][ld_xq] and wq uint8 [N][ld_wq]: packed INT4 codes (the sub-byte format above,
+ *   K/2 bytes per row; activation codes in [-7, 7], weight codes in [-8, 7]); x_scale fp32
+ *   [M][ld_sx] (K/G per row, as quarot_hadamard_quant_group writes them); w_scale_t fp32
+ *   [K/G][ld_sw] (transposed, prepared offline); y fp16 [M][ld_y].  K % 256 == 0, N % 8 == 0,
+ *   ld_xq / ld_wq % 16 == 0, ld_y % 8 == 0, ld_sw % 4 == 0, 16-byte aligned xq / wq / y / w_scale_t
+ *   (QUAROT_ERR_ALIGN); other G: QUAROT_ERR_UNSUPPORTED_SIZE.
+ * quarot_int4_linear_group8: the same for G = 128 with the codes stored one per int8 byte
+ *   (xq int8 [M][ld_xq], wq int8 [N][ld_wq], ld >= K; the format quarot_hadamard_quant_group8
+ *   writes) on the native kind::i8 path without unpacking — the comparison point for the
+ *   on-chip widening. */
+quarot_status quarot_int4_linear_group(const uint8_t* xq, const float* x_scale, int64_t ld_sx, int64_t M, int64_t K,
+                                       int64_t ld_xq, const uint8_t* wq, const float* w_scale_t, int64_t ld_sw,
                                        int64_t N, int64_t ld_wq, int32_t group, void* y, int64_t ld_y, void* stream);
+quarot_status quarot_int4_linear_group8(const int8_t* xq, const float* x_scale, int64_t ld_sx, int64_t M, int64_t K,
+                                        int64_t ld_xq, const int8_t* wq, const float* w_scale_t, int64_t ld_sw,
+                                        int64_t N, int64_t ld_wq, int32_t group, void* y, int64_t ld_y, void* stream);
 
 /* A8W8 QuaRot ("lossless" 8-bit RTN, P:6, tab:rtn_results): the native
  * kind::i8 tensor path with no unpacking, the comparison point for the INT4 unpack cost.
  * quarot_hadamard_quant8: as quarot_hadamard_quant but codes are int8 in [-127, 127], one byte
  *   per element (q int8 [M][ld_q], ld_q >= K, % 8), scale = fp32(clip * amax / 127).  Modes:
- *   NONE (optionally | QUAROT_HAD_RMSNORM, any K <= 32768); FULL for K = 1024 x 28 (the 70B
- *   down_proj input); ACROSS_HEADS for head_dim 128 and 16, 32 or 64 heads.  Other FULL /
- *   ACROSS_HEADS widths return QUAROT_ERR_UNSUPPORTED_SIZE; RMSNORM with FULL / ACROSS_HEADS
- *   returns QUAROT_ERR_ARG.
+ *   NONE (optionally | QUAROT_HAD_RMSNORM), FULL for every K = 2^n m of quarot_hadamard_quant
+ *   (the tcgen05 kernels at 1024 x 28, 64 x 172, 128 x 108 and 256 x 20), ACROSS_HEADS for
+ *   power-of-two head_dim and n_h >= 2 (tcgen05 at head_dim 128 with 16-64 heads); K <= 32768.
+ *   RMSNORM with FULL / ACROSS_HEADS returns QUAROT_ERR_ARG.
  * quarot_int8_linear: y[m,n] = fp16_rn(fp32(acc) * x_scale[m] * w_scale[n]),
  *   acc = sum_k xq[m,k] * wq[n,k] (int8 x int8 -> exact int32).  xq int8 [M][ld_xq], wq int8
  *   [N][ld_wq] (nn.Linear layout), ld % 16 == 0, K % 128 == 0, K <= 131072, N % 8 == 0.

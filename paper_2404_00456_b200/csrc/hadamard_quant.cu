@@ -461,18 +461,64 @@ QR_DEVICE float fwht_pass_dyn(int r, float* Z, int P, int m, int sh) {
   }
 }
 
-template <int MB>
-__global__ void hq_full_kernel(const __half* __restrict__ x, int64_t ld_x, int P, float clip,
-                               uint8_t* __restrict__ q, int64_t ld_q, float* __restrict__ scale,
-                               const uint32_t* __restrict__ bfrag) {
+// OUT: the output format of the quantizer stage — 0 = INT4 packed, one scale per row (a3);
+// 1 = int8 codes, one scale per row (A8, §8 f4); 2 = INT4 packed, one scale per run of `group`
+// consecutive elements (group-wise, §8 f3); 3 = the same one code per int8 byte (the
+// group-wise GEMM's operand format).  MB == 1 with stride > 1 is ACROSS_HEADS: P = n_h heads of
+// `stride` = head_dim elements, y = (H_{n_h} (x) I) z (the FWHT along a at stride head_dim).
+template <int OUT>
+QR_DEVICE void quantize_groups(const float* __restrict__ Z, int K, int group, double norm, float clip,
+                               uint8_t* __restrict__ qr, float* __restrict__ sr) {
+  constexpr bool kQ8 = OUT == 3;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  const int per = group >> 5;  // 2, 4 or 8 elements per lane
+  for (int g = warp; g < K / group; g += nwarps) {
+    const int e0 = g * group + lane * per;
+    float v[8];
+    float am = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      v[j] = j < per ? Z[e0 + j] : 0.f;
+      am = fmax_nan(am, fabsf(v[j]));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) am = fmax_nan(am, __shfl_xor_sync(0xffffffffu, am, o));
+    float s, inv;
+    row_scale(am, norm, clip, s, inv);
+    if (lane == 0) sr[g] = s;
+    if constexpr (kQ8) {
+      uint32_t w[2] = {0u, 0u};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) w[j >> 2] |= ((uint32_t)code_of(v[j], inv) & 0xFFu) << (8 * (j & 3));
+      if (per == 8) *reinterpret_cast<uint2*>(qr + e0) = make_uint2(w[0], w[1]);
+      else if (per == 4) *reinterpret_cast<uint32_t*>(qr + e0) = w[0];
+      else *reinterpret_cast<uint16_t*>(qr + e0) = (uint16_t)w[0];
+    } else {
+      uint32_t packed = 0;
+#pragma unroll
+      for (int j = 0; j < 8; j += 2) packed |= (nib(code_of(v[j], inv)) | (nib(code_of(v[j + 1], inv)) << 4)) << (4 * j);
+      if (per == 8) *reinterpret_cast<uint32_t*>(qr + e0 / 2) = packed;
+      else if (per == 4) *reinterpret_cast<uint16_t*>(qr + e0 / 2) = (uint16_t)packed;
+      else qr[e0 / 2] = (uint8_t)packed;
+    }
+  }
+}
+
+template <int MB, int OUT = 0>
+__global__ void hq_full_kernel(const __half* __restrict__ x, int64_t ld_x, int P, int stride, float clip,
+                               uint8_t* __restrict__ q, int64_t ld_q, float* __restrict__ scale, int64_t ld_s,
+                               int group, const uint32_t* __restrict__ bfrag) {
   extern __shared__ __align__(16) uint8_t smem[];
-  const int m = MB;
+  const int m = MB > 1 ? MB : stride;
   const int K = P * m;
   float* Z = reinterpret_cast<float*>(smem);
   uint32_t* X32 = reinterpret_cast<uint32_t*>(smem + (size_t)K * 4);
   float* red = reinterpret_cast<float*>(smem + (size_t)K * 4 + (MB > 1 ? (size_t)K * 2 : 0));
   const int64_t row = blockIdx.x;
   const __half* xr = x + row * ld_x;
+  // 1/sqrt of the transform's order: K for FULL, n_h for ACROSS_HEADS (reading Z5)
+  const double norm = rsqrt((double)P * (double)MB);
 
   // 1) stage the row
   const int nvec = K >> 3;
@@ -505,10 +551,14 @@ __global__ void hq_full_kernel(const __half* __restrict__ x, int64_t ld_x, int P
   int sh = 0;
   for (int ps = 0; ps < npass; ++ps) {
     const int r = (nbits - sh + (npass - ps) - 1) / (npass - ps);  // balanced split
-    if (ps == npass - 1) amax = fwht_pass_dyn<true>(r, Z, P, m, sh);
+    if (ps == npass - 1 && OUT < 2) amax = fwht_pass_dyn<true>(r, Z, P, m, sh);
     else fwht_pass_dyn<false>(r, Z, P, m, sh);
     sh += r;
     __syncthreads();
+  }
+  if constexpr (OUT >= 2) {  // group-wise: the transformed row is complete in Z
+    quantize_groups<OUT>(Z, K, group, norm, clip, q + row * ld_q, scale + row * ld_s);
+    return;
   }
   if (npass == 0) {  // P == 1: amax over the base transform output
     for (int i = threadIdx.x; i < K; i += blockDim.x) amax = fmax_nan(amax, fabsf(Z[i]));
@@ -521,17 +571,25 @@ __global__ void hq_full_kernel(const __half* __restrict__ x, int64_t ld_x, int P
   amax = red[0];
   for (int w = 1; w < (int)(blockDim.x >> 5); ++w) amax = fmax_nan(amax, red[w]);
   float s, inv;
-  row_scale(amax, rsqrt((double)K), clip, s, inv);
+  row_scale(amax, norm, clip, s, inv, OUT == 1 ? 127.0 : 7.0);
   if (threadIdx.x == 0) scale[row] = s;
   uint8_t* qr = q + row * ld_q;
   for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
     const float4 f0 = reinterpret_cast<const float4*>(Z)[2 * i];
     const float4 f1 = reinterpret_cast<const float4*>(Z)[2 * i + 1];
-    const uint32_t packed = nib(code_of(f0.x, inv)) | (nib(code_of(f0.y, inv)) << 4) |
-                            (nib(code_of(f0.z, inv)) << 8) | (nib(code_of(f0.w, inv)) << 12) |
-                            (nib(code_of(f1.x, inv)) << 16) | (nib(code_of(f1.y, inv)) << 20) |
-                            (nib(code_of(f1.z, inv)) << 24) | (nib(code_of(f1.w, inv)) << 28);
-    *reinterpret_cast<uint32_t*>(qr + (int64_t)i * 4) = packed;
+    if constexpr (OUT == 1) {
+      const float f[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
+      uint32_t w[2] = {0u, 0u};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) w[j >> 2] |= ((uint32_t)code_of<127>(f[j], inv) & 0xFFu) << (8 * (j & 3));
+      *reinterpret_cast<uint2*>(qr + (int64_t)i * 8) = make_uint2(w[0], w[1]);
+    } else {
+      const uint32_t packed = nib(code_of(f0.x, inv)) | (nib(code_of(f0.y, inv)) << 4) |
+                              (nib(code_of(f0.z, inv)) << 8) | (nib(code_of(f0.w, inv)) << 12) |
+                              (nib(code_of(f1.x, inv)) << 16) | (nib(code_of(f1.y, inv)) << 20) |
+                              (nib(code_of(f1.z, inv)) << 24) | (nib(code_of(f1.w, inv)) << 28);
+      *reinterpret_cast<uint32_t*>(qr + (int64_t)i * 4) = packed;
+    }
   }
 }
 
@@ -881,26 +939,54 @@ cudaError_t launch_hq_heads(const void* x, int64_t M, int64_t K, int64_t ld_x, i
   return cudaPeekAtLastError();
 }
 
-cudaError_t launch_hq_full(const void* x, int64_t M, int64_t K, int64_t ld_x, int pow2, int m, float clip,
-                           uint8_t* q, int64_t ld_q, float* scale, cudaStream_t stream) {
-  const __half* xh = static_cast<const __half*>(x);
+// The smem kernel hq_full_kernel<MB, OUT> for one (MB, OUT): the row staged in shared memory,
+// H_m by mma.sync, the Sylvester factor by radix passes (every width 2^n m, and ACROSS_HEADS
+// when MB == 1 and stride = head_dim).
+template <int MB, int OUT>
+static cudaError_t launch_generic(const __half* xh, int64_t M, int64_t K, int64_t ld_x, int P, int stride, float clip,
+                                  uint8_t* q, int64_t ld_q, float* scale, int64_t ld_s, int group,
+                                  cudaStream_t stream) {
   const int threads = K >= 16384 ? 512 : 256;
-  const size_t smem = (size_t)K * 4 + (m > 1 ? (size_t)K * 2 : 0) + 32 * sizeof(float);
-  const dim3 grid((unsigned)M);
-  cudaError_t e;
-  if (m == 1) {
-    e = cudaFuncSetAttribute(hq::hq_full_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    hq::hq_full_kernel<1><<<grid, threads, smem, stream>>>(xh, ld_x, pow2, clip, q, ld_q, scale, nullptr);
-  } else if (m == 28 && pow2 == 1024 && g_hq_full_variant != 1) {
-    return launch_hq_full28_tc(x, M, ld_x, clip, q, ld_q, scale, stream);
-  } else if (m == 28 && pow2 == 1024) {
+  const size_t smem = (size_t)K * 4 + (MB > 1 ? (size_t)K * 2 : 0) + 32 * sizeof(float);
+  cudaError_t e = cudaFuncSetAttribute(hq::hq_full_kernel<MB, OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  hq::hq_full_kernel<MB, OUT><<<dim3((unsigned)M), threads, smem, stream>>>(
+      xh, ld_x, P, stride, clip, q, ld_q, scale, ld_s, group, MB > 1 ? device_bfrag_table(MB) : nullptr);
+  return cudaPeekAtLastError();
+}
+
+template <int OUT>
+static cudaError_t launch_generic_m(const __half* xh, int64_t M, int64_t K, int64_t ld_x, int P, int m, int stride,
+                                    float clip, uint8_t* q, int64_t ld_q, float* scale, int64_t ld_s, int group,
+                                    cudaStream_t stream) {
+  switch (m) {
+    case 1: return launch_generic<1, OUT>(xh, M, K, ld_x, P, stride, clip, q, ld_q, scale, ld_s, group, stream);
+    case 20: return launch_generic<20, OUT>(xh, M, K, ld_x, P, 20, clip, q, ld_q, scale, ld_s, group, stream);
+    case 28: return launch_generic<28, OUT>(xh, M, K, ld_x, P, 28, clip, q, ld_q, scale, ld_s, group, stream);
+    case 108: return launch_generic<108, OUT>(xh, M, K, ld_x, P, 108, clip, q, ld_q, scale, ld_s, group, stream);
+    case 172: return launch_generic<172, OUT>(xh, M, K, ld_x, P, 172, clip, q, ld_q, scale, ld_s, group, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_hq_full(const void* x, int64_t M, int64_t K, int64_t ld_x, int pow2, int m, float clip,
+                           uint8_t* q, int64_t ld_q, float* scale, cudaStream_t stream, int out, int group,
+                           int64_t ld_s) {
+  const __half* xh = static_cast<const __half*>(x);
+  const bool q8 = out == 1;
+  if (out <= 1 && g_hq_full_variant != 1) {  // the tcgen05 kernels of the model widths
+    if (m == 28 && pow2 == 1024) return launch_hq_full28_tc(x, M, ld_x, clip, q, ld_q, scale, stream, q8);
+    if (hq_full_small_tc_supported(pow2, m)) return launch_hq_full_small_tc(x, M, ld_x, pow2, m, clip, q, ld_q, scale, stream, q8);
+    if (m == 172 && pow2 == 64) return launch_hq_full172_tc(x, M, ld_x, clip, q, ld_q, scale, stream, q8);
+  }
+  if (out == 0 && m == 28 && pow2 == 1024) {  // debug variant 1: the mma.sync FULL-28 kernel
     static bool attr[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
     if (!attr[dev & 63]) {
-      e = cudaFuncSetAttribute(hq::hq_full28_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)hq::f28::SMEM);
+      cudaError_t e = cudaFuncSetAttribute(hq::hq_full28_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)hq::f28::SMEM);
       if (e != cudaSuccess) return e;
       attr[dev & 63] = true;
     }
@@ -909,27 +995,30 @@ cudaError_t launch_hq_full(const void* x, int64_t M, int64_t K, int64_t ld_x, in
     const int grid = (int)(M < nsm ? M : nsm);
     hq::hq_full28_kernel<<<grid, hq::f28::NT, hq::f28::SMEM, stream>>>(xh, M, ld_x, clip, q, ld_q, scale,
                                                                       device_afrag28());
-  } else if (m == 28) {
-    e = cudaFuncSetAttribute(hq::hq_full_kernel<28>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    hq::hq_full_kernel<28><<<grid, threads, smem, stream>>>(xh, ld_x, pow2, clip, q, ld_q, scale,
-                                                           device_bfrag_table(28));
-  } else if (hq_full_small_tc_supported(pow2, m) && g_hq_full_variant != 1) {  // 13B widths, tcgen05
-    return launch_hq_full_small_tc(x, M, ld_x, pow2, m, clip, q, ld_q, scale, stream);
-  } else if (m == 20 || m == 108) {  // other 2^n x {20, 108}: the smem kernel
-    auto kern = m == 20 ? hq::hq_full_kernel<20> : hq::hq_full_kernel<108>;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    kern<<<grid, threads, smem, stream>>>(xh, ld_x, pow2, clip, q, ld_q, scale, device_bfrag_table(m));
-  } else if (m == 172 && pow2 == 64 && g_hq_full_variant != 1) {
-    return launch_hq_full172_tc(x, M, ld_x, clip, q, ld_q, scale, stream);
-  } else {
-    e = cudaFuncSetAttribute(hq::hq_full_kernel<172>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    hq::hq_full_kernel<172><<<grid, threads, smem, stream>>>(xh, ld_x, pow2, clip, q, ld_q, scale,
-                                                            device_bfrag_table(172));
+    return cudaPeekAtLastError();
   }
-  return cudaPeekAtLastError();
+  switch (out) {
+    case 0: return launch_generic_m<0>(xh, M, K, ld_x, pow2, m, 1, clip, q, ld_q, scale, 1, 0, stream);
+    case 1: return launch_generic_m<1>(xh, M, K, ld_x, pow2, m, 1, clip, q, ld_q, scale, 1, 0, stream);
+    case 2: return launch_generic_m<2>(xh, M, K, ld_x, pow2, m, 1, clip, q, ld_q, scale, ld_s, group, stream);
+    case 3: return launch_generic_m<3>(xh, M, K, ld_x, pow2, m, 1, clip, q, ld_q, scale, ld_s, group, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_hq_heads_group(const void* x, int64_t M, int64_t K, int64_t ld_x, int head_dim, float clip,
+                                  uint8_t* q, int64_t ld_q, float* scale, int64_t ld_s, int group, bool q8,
+                                  cudaStream_t stream) {
+  const __half* xh = static_cast<const __half*>(x);
+  const int nh = (int)(K / head_dim);
+  return q8 ? launch_generic<1, 3>(xh, M, K, ld_x, nh, head_dim, clip, q, ld_q, scale, ld_s, group, stream)
+            : launch_generic<1, 2>(xh, M, K, ld_x, nh, head_dim, clip, q, ld_q, scale, ld_s, group, stream);
+}
+
+cudaError_t launch_hq_heads8(const void* x, int64_t M, int64_t K, int64_t ld_x, int head_dim, float clip, uint8_t* q,
+                             int64_t ld_q, float* scale, cudaStream_t stream) {
+  return launch_generic<1, 1>(static_cast<const __half*>(x), M, K, ld_x, (int)(K / head_dim), head_dim, clip, q, ld_q,
+                              scale, 1, 0, stream);
 }
 
 }  // namespace qr

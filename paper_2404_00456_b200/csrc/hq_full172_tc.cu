@@ -84,6 +84,7 @@ __host__ __device__ constexpr uint32_t sw128_off(int rows, int kc, int row, int 
   return (uint32_t)(kc * rows * 128 + (row >> 3) * 1024 + (row & 7) * 128 + ((c ^ (row & 7)) << 4));
 }
 
+template <bool kQ8>  // kQ8: int8 codes in [-127, 127], one byte per element (A8)
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     hq_full172_tc_kernel(const __half* __restrict__ x, int64_t M, int64_t ld_x, float clip, uint8_t* __restrict__ q,
                          int64_t ld_q, float* __restrict__ scale, const uint4* __restrict__ a_img) {
@@ -210,7 +211,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const bool odd = (lane & 1) != 0;
     const uint32_t t_lane = tmem_base + ((uint32_t)(qd * 32) << 16) + (uint32_t)(mh * P);
     const float norm_f = (float)rsqrt((double)K);
-    const float c0 = (float)((double)clip * rsqrt((double)K) / 7.0);
+    const float c0 = (float)((double)clip * rsqrt((double)K) / (kQ8 ? 127.0 : 7.0));
     const uint32_t sh_keep = odd ? 4u : 0u, sh_recv = odd ? 0u : 4u;
     const uint32_t keep_mask = odd ? 0xF0F0F0F0u : 0x0F0F0F0Fu;
     // byte (a, p = j'/2) at a * 86 + p; even lane writes a < 32, odd lane a >= 32
@@ -270,6 +271,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
         for (int c = 0; c < 32; ++c) v[c] = make_float2(0.f, 0.f);
       }
+      if constexpr (kQ8) {  // element (a, j') at byte a * MB + j': a warp store covers 32 bytes
+        if (lane_ok) {
+          int8_t* const q8 = reinterpret_cast<int8_t*>(q) + row * ld_q + jp;
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {  // v[c] = (a = 2c, 2c + 1)
+            const float2 mq = f2fma(v[c], make_float2(inv, inv), make_float2(12582912.f, 12582912.f));
+            const uint32_t w = __vmaxs2(__vmins2(__byte_perm(__float_as_uint(mq.x), __float_as_uint(mq.y), 0x5410),
+                                                 0x007F007Fu), 0xFF81FF81u);
+            q8[(int64_t)(2 * c) * MB] = (int8_t)(w & 0xFFu);
+            q8[(int64_t)(2 * c + 1) * MB] = (int8_t)((w >> 16) & 0xFFu);
+          }
+        }
+        continue;
+      }
       uint32_t out[8];
 #pragma unroll
       for (int m = 0; m < 8; ++m) {  // codes of a = 4m..4m+3 (even lane keeps) / 32 + 4m.. (odd)
@@ -327,7 +342,7 @@ __device__ uint4 g_a172_img[hq172::A_BYTES / 16];
 }  // namespace
 
 cudaError_t launch_hq_full172_tc(const void* x, int64_t M, int64_t ld_x, float clip, uint8_t* q, int64_t ld_q,
-                                 float* scale, cudaStream_t stream) {
+                                 float* scale, cudaStream_t stream, bool q8) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -345,7 +360,10 @@ cudaError_t launch_hq_full172_tc(const void* x, int64_t M, int64_t ld_x, float c
       if (e != cudaSuccess) return e;
       e = cudaDeviceSynchronize();  // one-time: the image is complete before any stream reads it
       if (e != cudaSuccess) return e;
-      e = cudaFuncSetAttribute(hq172::hq_full172_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      e = cudaFuncSetAttribute(hq172::hq_full172_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)hq172::SMEM);
+      if (e != cudaSuccess) return e;
+      e = cudaFuncSetAttribute(hq172::hq_full172_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)hq172::SMEM);
       if (e != cudaSuccess) return e;
       g_img172[dev & 63] = d;
@@ -355,7 +373,8 @@ cudaError_t launch_hq_full172_tc(const void* x, int64_t M, int64_t ld_x, float c
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)(M < nsm ? M : nsm);
-  hq172::hq_full172_tc_kernel<<<grid, hq172::NUM_THREADS, hq172::SMEM, stream>>>(
+  auto kern = q8 ? hq172::hq_full172_tc_kernel<true> : hq172::hq_full172_tc_kernel<false>;
+  kern<<<grid, hq172::NUM_THREADS, hq172::SMEM, stream>>>(
       static_cast<const __half*>(x), M, ld_x, clip, q, ld_q, scale, static_cast<const uint4*>(img));
   return cudaPeekAtLastError();
 }

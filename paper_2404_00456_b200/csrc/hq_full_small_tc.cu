@@ -81,7 +81,7 @@ QR_DEVICE uint32_t code_word(float2 a, float2 b, float inv) {
   return __byte_perm(lo, hi, 0x6420);
 }
 
-template <int MB, int LLO>
+template <int MB, int LLO, bool kQ8>  // kQ8: int8 codes in [-127, 127], one byte per element (§8 f4)
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     hq_full_small_tc_kernel(const __grid_constant__ CUtensorMap tmX, int64_t M, float clip, uint8_t* __restrict__ q,
                             int64_t ld_q, float* __restrict__ scale, const uint4* __restrict__ a_img) {
@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const bool odd = (lane & 1) != 0;
     const uint32_t t_lane = tmem_base + ((uint32_t)(qd * 32) << 16) + (uint32_t)(mh * NA);
     const float norm_f = (float)rsqrt((double)K);
-    const float c0 = (float)((double)clip * rsqrt((double)K) / 7.0);
+    const float c0 = (float)((double)clip * rsqrt((double)K) / (kQ8 ? 127.0 : 7.0));
     const uint32_t sh_keep = odd ? 4u : 0u, sh_recv = odd ? 0u : 4u;
     const uint32_t keep_mask = odd ? 0xF0F0F0F0u : 0x0F0F0F0Fu;
     // byte (a_hi, p = j'/2) at a_hi * J/2 + p; even lane writes a_hi < 32, odd lane a_hi >= 32
@@ -236,6 +236,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (inv == 0.f) {
 #pragma unroll
         for (int c = 0; c < 32; ++c) v[c] = make_float2(0.f, 0.f);
+      }
+      if constexpr (kQ8) {  // element (a, j') at byte a * J + j': a warp store covers 32 bytes
+        if (lane_ok) {
+          int8_t* const q8 = reinterpret_cast<int8_t*>(q) + row * ld_q + jp;
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {  // v[c] = (a = 2c, 2c + 1)
+            const float2 mq = f2fma(v[c], make_float2(inv, inv), make_float2(12582912.f, 12582912.f));
+            const uint32_t w = __vmaxs2(__vmins2(__byte_perm(__float_as_uint(mq.x), __float_as_uint(mq.y), 0x5410),
+                                                 0x007F007Fu), 0xFF81FF81u);
+            q8[(int64_t)(2 * c) * J] = (int8_t)(w & 0xFFu);
+            q8[(int64_t)(2 * c + 1) * J] = (int8_t)((w >> 16) & 0xFFu);
+          }
+        }
+        continue;
       }
       uint32_t out[8];
 #pragma unroll
@@ -314,7 +328,7 @@ __device__ uint4 g_small_img20[hqs::Cfg<20, 2>::A_BYTES / 16];
 
 template <int MB, int LLO>
 cudaError_t launch_small(const void* x, int64_t M, int64_t ld_x, float clip, uint8_t* q, int64_t ld_q, float* scale,
-                         cudaStream_t stream, int slot) {
+                         cudaStream_t stream, int slot, bool q8) {
   using C = hqs::Cfg<MB, LLO>;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -333,7 +347,10 @@ cudaError_t launch_small(const void* x, int64_t M, int64_t ld_x, float clip, uin
       if (e != cudaSuccess) return e;
       e = cudaDeviceSynchronize();  // one-time: the image is complete before any stream reads it
       if (e != cudaSuccess) return e;
-      e = cudaFuncSetAttribute(hqs::hq_full_small_tc_kernel<MB, LLO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      e = cudaFuncSetAttribute(hqs::hq_full_small_tc_kernel<MB, LLO, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)C::SMEM);
+      if (e != cudaSuccess) return e;
+      e = cudaFuncSetAttribute(hqs::hq_full_small_tc_kernel<MB, LLO, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)C::SMEM);
       if (e != cudaSuccess) return e;
       g_img_small[dev & 63][slot] = d;
@@ -354,7 +371,8 @@ cudaError_t launch_small(const void* x, int64_t M, int64_t ld_x, float clip, uin
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)(M < nsm ? M : nsm);
-  hqs::hq_full_small_tc_kernel<MB, LLO><<<grid, hqs::NUM_THREADS, C::SMEM, stream>>>(
+  auto kern = q8 ? hqs::hq_full_small_tc_kernel<MB, LLO, true> : hqs::hq_full_small_tc_kernel<MB, LLO, false>;
+  kern<<<grid, hqs::NUM_THREADS, C::SMEM, stream>>>(
       map, M, clip, q, ld_q, scale, static_cast<const uint4*>(img));
   return cudaPeekAtLastError();
 }
@@ -364,9 +382,9 @@ cudaError_t launch_small(const void* x, int64_t M, int64_t ld_x, float clip, uin
 bool hq_full_small_tc_supported(int64_t pow2, int m) { return (m == 108 && pow2 == 128) || (m == 20 && pow2 == 256); }
 
 cudaError_t launch_hq_full_small_tc(const void* x, int64_t M, int64_t ld_x, int64_t pow2, int m, float clip,
-                                    uint8_t* q, int64_t ld_q, float* scale, cudaStream_t stream) {
-  if (m == 108 && pow2 == 128) return launch_small<108, 1>(x, M, ld_x, clip, q, ld_q, scale, stream, 0);
-  if (m == 20 && pow2 == 256) return launch_small<20, 2>(x, M, ld_x, clip, q, ld_q, scale, stream, 1);
+                                    uint8_t* q, int64_t ld_q, float* scale, cudaStream_t stream, bool q8) {
+  if (m == 108 && pow2 == 128) return launch_small<108, 1>(x, M, ld_x, clip, q, ld_q, scale, stream, 0, q8);
+  if (m == 20 && pow2 == 256) return launch_small<20, 2>(x, M, ld_x, clip, q, ld_q, scale, stream, 1, q8);
   return cudaErrorInvalidValue;
 }
 

@@ -179,6 +179,13 @@ QR_DEVICE void mma_commit_pair(uint64_t* bar) {
       "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])                      \
       : "memory")
 
+// tcgen05.st of 8 registers into 8 consecutive columns of the warp's 32 lanes (STTM takes a
+// contiguous register range, so a constant fill keeps 8 registers, not 32, live)
+#define QR_TMEM_ST8(taddr, r)                                                                               \
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),        \
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])         \
+               : "memory")
+
 // Converts and stores one 32-column accumulator chunk of one row (columns n0 .. n0 + 31;
 // wsc = their 32 weight scales in smem).  fp16: y = fp16_rn(fp32(acc) * s_x * s_w); with a
 // residual, fp16_rn(fp32(y) + fp32(r)); s32: raw accumulators; SwiGLU: the chunk is
@@ -716,6 +723,7 @@ static_assert(SMEM_BYTES <= 232448, "227 KB dynamic smem");
 }  // namespace gq
 
 struct GParams {
+  uint32_t bias[8];        // int4_group_gemm_kernel: the TMEM accumulator bias (gq4::BIAS) x 8
   const float* x_scale;    // [M][ld_sx], K / G per row
   const float* w_scale_t;  // [K / G][ld_sw]
   __half* out;
@@ -914,6 +922,317 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(i8::NUM_THREADS, 1)
   tc_fence_before();
   cluster_sync();
   if (warp == i8::MMA_WARP) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+  }
+}
+
+
+// ============================================================ group-wise W4A4, packed INT4 (§8 f3)
+// The same computation as int8_group_gemm_kernel with the codes kept in the paper's 4-bit storage
+// (two per byte) and group sizes G = 64, 128, 256 (tab:group_wise_ablation):
+//  * TMA loads the PACKED A and B k-blocks (128 rows x 128 B each per CTA) into a 2-stage
+//    staging ring; two pairs of widen warps take alternate k-blocks and write the operands
+//    widened (the x16 nibble trick of int4_gemm_kernel, [16 lo | 16 hi] per 32-code chunk — the
+//    same permutation of k on both sides, inside one group) into a 2-stage SW128 int8 ring;
+//  * the MMA warp (leader CTA) runs G / 32 SS MMAs (cta_group::2, M256 N256 K32) per group into
+//    one of two 256-column TMEM buffers and commits the buffer to the epilogue;
+//  * the buffers hold the bias 0x4B400000 (the fp32 bits of 1.5 * 2^23) when a group starts and
+//    every MMA accumulates onto it, so the epilogue reads fp32(1.5 * 2^23 + 256 acc_g) directly
+//    (|256 acc_g| <= 256 * 49 * 256 < 2^22): one packed subtract recovers 256 acc_g exactly, one
+//    packed multiply forms s_x s_w / 256 and one packed FMA folds the group into the fp32 sums —
+//    1.5 issue slots per output element per group; the epilogue then rewrites the bias.
+namespace gq4 {
+constexpr int SSTAGES = 2, OSTAGES = 2;
+constexpr int SSTAGE_BYTES = SA_BYTES + SB_BYTES;  // 32 KB packed
+constexpr int OA_BYTES = BMC * BK, OB4_BYTES = BNC * BK;  // 32 KB + 32 KB widened
+constexpr int OSTAGE_BYTES = OA_BYTES + OB4_BYTES;
+// 16 warps = 512 threads: 0-7 epilogue (216 registers: the 128 fp32 sums + two 16-column chunks),
+// warpgroups 2-3 (40 registers) = 8 TMA, 9 MMA, 10-13 widen (two pairs on alternate k-blocks; in a
+// pair one warp widens A, the other B), 14-15 idle
+constexpr int EPI_WARPS = 8, TMA_WARP = 8, MMA_WARP = 9, W_WARP0 = 10, NUM_W = 4;
+constexpr int NUM_THREADS = 16 * 32;
+constexpr int WS_BYTES = EPI_WARPS * 2 * 128 * 4;  // per epilogue warp, per buffer: 128 column scales
+constexpr size_t SMEM_BYTES = 1024 + SSTAGES * SSTAGE_BYTES + OSTAGES * OSTAGE_BYTES + 512 + WS_BYTES;
+static_assert(SMEM_BYTES <= 232448, "227 KB dynamic smem");
+constexpr uint32_t BIAS = 0x4B400000u;
+}  // namespace gq4
+
+template <int G>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gq4::NUM_THREADS, 1)
+    int4_group_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                           const GParams p) {
+  static_assert(G == 64 || G == 128 || G == 256, "group size");
+  constexpr int GPK = BK / G;       // groups per k-block
+  constexpr int MPG = G / 32;       // MMAs per group
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* stage_smem = smem;                                        // [SSTAGES][A 16 KB | B 16 KB] packed
+  uint8_t* op_smem = smem + gq4::SSTAGES * gq4::SSTAGE_BYTES;         // [OSTAGES][A 32 KB | B 32 KB] int8 SW128
+  uint64_t* bars = reinterpret_cast<uint64_t*>(op_smem + gq4::OSTAGES * gq4::OSTAGE_BYTES);
+  uint64_t* st_full = bars;                         // [SSTAGES] TMA -> widen group
+  uint64_t* st_empty = st_full + gq4::SSTAGES;      // [SSTAGES] widen pair -> TMA
+  uint64_t* op_full = st_empty + gq4::SSTAGES;      // [OSTAGES] widen warps of both CTAs -> leader MMA
+  uint64_t* op_empty = op_full + gq4::OSTAGES;      // [OSTAGES] MMA commit -> widen warps
+  uint64_t* t_full = op_empty + gq4::OSTAGES;       // [2] MMA commit -> epilogue
+  uint64_t* t_empty = t_full + 2;                   // [2] epilogues of both CTAs -> leader MMA
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(t_empty + 2);
+  float* ws_smem = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 512);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int pair = (int)blockIdx.x >> 1;
+  const int num_pairs = (int)gridDim.x >> 1;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < gq4::SSTAGES; ++s) {
+      mbar_init(&st_full[s], 1);
+      mbar_init(&st_empty[s], 2);
+    }
+    for (int s = 0; s < gq4::OSTAGES; ++s) {
+      mbar_init(&op_full[s], 2 * 2);
+      mbar_init(&op_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&t_full[b], 1);
+      mbar_init(&t_empty[b], 2 * gq4::EPI_WARPS);
+    }
+    fence_barrier_init();
+  }
+  if (warp == gq4::MMA_WARP) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  if (warp == gq4::TMA_WARP && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  if (warp < gq4::EPI_WARPS) {  // both accumulator buffers start at the bias (this CTA's lanes)
+    const int quarter = warp & 3, chalf = warp >> 2;
+    uint32_t bias8[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) bias8[i] = gq4::BIAS;
+#pragma unroll 1
+    for (int c = 0; c < 32; ++c)
+      QR_TMEM_ST8(tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)((c >> 4) * BN + chalf * 128 + 8 * (c & 15)),
+                  bias8);
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const int my_tiles = (p.num_tiles > pair) ? (p.num_tiles - 1 - pair) / num_pairs + 1 : 0;
+  const int total = my_tiles * p.num_kb;
+  const int ngroups = (int)(p.K / G);
+
+  // register budgets per role (setmaxnreg is warpgroup-wide: warps 8-15 are warpgroups 2-3).  An
+  // increase draws only on what this CTA's decreases released: 256 x (128 - 40) = 256 x (216 - 128)
+  if (warp >= gq4::TMA_WARP) {
+    QR_SETMAXNREG_DEC(40);  // one instruction per warpgroup (.sync.aligned)
+  }
+  if (warp == gq4::TMA_WARP || warp == gq4::MMA_WARP) {
+    if (warp == gq4::TMA_WARP) {
+      if (lane == 0) {
+        for (int it = 0; it < total; ++it) {
+          const int tl = it / p.num_kb, kb = it - tl * p.num_kb;
+          int mb, nb;
+          gtile_coords(p, pair + tl * num_pairs, mb, nb);
+          const int s = it % gq4::SSTAGES;
+          mbar_wait_sleep(&st_empty[s], ((it / gq4::SSTAGES) & 1) ^ 1);
+          mbar_expect_tx(&st_full[s], gq4::SSTAGE_BYTES);
+          const uint32_t dst = smem_u32(stage_smem + s * gq4::SSTAGE_BYTES);
+          tma_load_2d(dst, &tmA, kb * BKP, mb * BM + (int)rank * BMC, &st_full[s]);
+          tma_load_2d(dst + SA_BYTES, &tmB, kb * BKP, nb * BN + (int)rank * BNC, &st_full[s]);
+        }
+      }
+    } else if (warp == gq4::MMA_WARP) {
+      if (rank == 0 && lane == 0) {
+        int it = 0, gc = 0;
+        for (int tl = 0; tl < my_tiles; ++tl) {
+          for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
+            const int o = it % gq4::OSTAGES;
+            mbar_wait_sleep(&op_full[o], (it / gq4::OSTAGES) & 1);
+            tc_fence_after();
+            const uint32_t base = smem_u32(op_smem + o * gq4::OSTAGE_BYTES);
+            const uint64_t a_desc = umma_desc_sw128(base), b_desc = umma_desc_sw128(base + gq4::OA_BYTES);
+#pragma unroll
+            for (int hg = 0; hg < GPK; ++hg, ++gc) {
+              const int ab = gc & 1;
+              mbar_wait_sleep(&t_empty[ab], ((gc >> 1) & 1) ^ 1);
+              tc_fence_after();
+              const uint32_t d_tmem = tmem_base + (uint32_t)(ab * BN);
+#pragma unroll
+              for (int k = MPG * hg; k < MPG * hg + MPG; ++k) {  // atom k/4 at +16 KB, 32 bytes along K within it
+                const uint64_t off = (uint64_t)((k >> 2) * (BMC * 128 / 16) + 2 * (k & 3));
+                mma_i8_ss_2sm(d_tmem, a_desc + off, b_desc + off, IDESC, 1u);  // onto the bias
+              }
+              mma_commit_pair(&t_full[ab]);
+            }
+            mma_commit_pair(&op_empty[o]);
+          }
+        }
+      }
+      __syncwarp();
+    }
+  } else if (warp >= gq4::W_WARP0 && warp < gq4::W_WARP0 + gq4::NUM_W) {
+    // ===================== widen A or B: packed smem -> int8 SW128 smem =====================
+    // lane t owns packed chunk qc = t % 8 of rows rr0 + 4 i (rr0 = t / 8 < 4, i < 32): the swizzle
+    // phase of row r = rr0 + 8 i2 + 4 h is rr0 + 4 h, and r / 8 = i2, so both variants are
+    // precomputed.  Widened: chunk qc -> K atom qc / 4, int8 chunks 2 (qc % 4) (lo nibbles) and +1
+    // (hi nibbles) of the row's 128-byte line; each 8-lane store phase covers all 8 chunk slots.
+    const int wi = (warp - gq4::W_WARP0) >> 1;    // the pair takes k-blocks it == wi (mod 2)
+    const int opnd = (warp - gq4::W_WARP0) & 1;   // 0: A, 1: B
+    const uint32_t t = (uint32_t)lane;
+    const uint32_t rr0 = t >> 3, qc = t & 7u;
+    const uint32_t atom = qc >> 2, qa = qc & 3u, odd = atom & 1u;
+    const uint32_t sh0 = odd ? 0u : 4u, sh1 = odd ? 4u : 0u;
+    uint32_t src_off[2], dst_off[2], d0[2], d1[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t swz = rr0 + 4u * h;
+      src_off[h] = swz * BKP + ((qc ^ swz) << 4);
+      dst_off[h] = atom * (BNC * 128u) + swz * 128u;
+      d0[h] = ((2u * qa + odd) ^ swz) << 4;
+      d1[h] = ((2u * qa + (odd ^ 1u)) ^ swz) << 4;
+    }
+    const uint32_t opfull_leader = map_to_rank(&op_full[0], 0);
+    for (int it = wi; it < total; it += 2) {
+      const int s = it % gq4::SSTAGES;
+      const int o = it % gq4::OSTAGES;
+      mbar_wait_sleep(&st_full[s], (it / gq4::SSTAGES) & 1);
+      QR_OPWAIT(&op_empty[o], ((it / gq4::OSTAGES) & 1) ^ 1);
+      {
+        const uint32_t src = smem_u32(stage_smem + s * gq4::SSTAGE_BYTES) + (opnd ? SA_BYTES : 0);
+        const uint32_t dst = smem_u32(op_smem + o * gq4::OSTAGE_BYTES) + (opnd ? gq4::OA_BYTES : 0);
+#pragma unroll 1
+        for (int i0 = 0; i0 < 16; i0 += 2) {  // row octets i0, i0 + 1 (two rows per lane each)
+          uint4 w[2][2];
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) w[i][h] = lds_v4(src + (uint32_t)(i0 + i) * 1024u + src_off[h]);
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const uint4 v = w[i][h];
+              const uint32_t base = dst + (uint32_t)(i0 + i) * 1024u + dst_off[h];
+              sts_v4(base + d0[h], make_uint4((v.x << sh0) & 0xF0F0F0F0u, (v.y << sh0) & 0xF0F0F0F0u,
+                                              (v.z << sh0) & 0xF0F0F0F0u, (v.w << sh0) & 0xF0F0F0F0u));
+              sts_v4(base + d1[h], make_uint4((v.x << sh1) & 0xF0F0F0F0u, (v.y << sh1) & 0xF0F0F0F0u,
+                                              (v.z << sh1) & 0xF0F0F0F0u, (v.w << sh1) & 0xF0F0F0F0u));
+            }
+        }
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&st_empty[s]);
+        mbar_arrive_cluster(opfull_leader + (uint32_t)o * 8u);
+      }
+    }
+  } else if (warp < gq4::EPI_WARPS) {
+    QR_SETMAXNREG_INC(216);
+    // ===================== epilogue warps 0..7: fold every group into fp32 sums =====================
+    const uint32_t tempty_leader = map_to_rank(&t_empty[0], 0);
+    const int quarter = warp & 3, chalf = warp >> 2;
+    const int row_in_tile = (int)rank * BMC + quarter * 32 + lane;
+    // the bias block is read from kernel parameters, so the compiler keeps it in one register
+    // block instead of re-materializing the constant before every store
+    uint32_t bias8[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) bias8[i] = p.bias[i];
+    int gc = 0;
+    for (int tl = 0; tl < my_tiles; ++tl) {
+      int mb, nb;
+      gtile_coords(p, pair + tl * num_pairs, mb, nb);
+      const int64_t m = (int64_t)mb * BM + row_in_tile;
+      const bool row_ok = m < p.M;
+      float2 acc[64];  // columns (2c, 2c + 1) of the thread's 128
+#pragma unroll
+      for (int c = 0; c < 64; ++c) acc[c] = make_float2(0.f, 0.f);
+      const int64_t n4 = (int64_t)nb * BN + chalf * 128 + 4 * lane;
+      auto ld_ws = [&](int g) {
+        return n4 < p.N ? __ldg(reinterpret_cast<const float4*>(p.w_scale_t + (int64_t)g * p.ld_sw + n4))
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+      };
+      float4 ws_next = ld_ws(0);
+      float sx_next = row_ok ? __ldg(p.x_scale + m * p.ld_sx) : 0.f;
+      for (int g = 0; g < ngroups; ++g, ++gc) {
+        const int ab = gc & 1;
+        float* wsw = ws_smem + (warp * 2 + ab) * 128;
+        reinterpret_cast<float4*>(wsw)[lane] = ws_next;
+        const float sx = sx_next * (1.f / 256.f);  // the x16 nibble scaling of both operands
+        if (g + 1 < ngroups) {
+          ws_next = ld_ws(g + 1);
+          sx_next = row_ok ? __ldg(p.x_scale + m * p.ld_sx + g + 1) : 0.f;
+        }
+        __syncwarp();
+        mbar_wait_sleep(&t_full[ab], (gc >> 1) & 1);  // sleeping, not spinning: the widen warps share these schedulers
+        tc_fence_after();
+        const uint32_t taddr =
+            tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(ab * BN) + (uint32_t)(chalf * 128);
+        const float2 sx2 = make_float2(sx, sx), mg = make_float2(-12582912.f, -12582912.f);
+        // 16-column chunks, software-pipelined: the load of chunk c + 1 is in flight while chunk c
+        // is folded (tcgen05.wait::ld waits for every outstanding load, so one wait per chunk)
+        uint32_t rc[2][16];
+        float4 wsc[2][4];  // the chunk's 16 column scales, loaded one chunk ahead
+        const uint32_t wsa = smem_u32(wsw);
+        auto ld_wsc = [&](int cc, float4(&w)[4]) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(w[i].x), "=f"(w[i].y), "=f"(w[i].z), "=f"(w[i].w)
+                         : "r"(wsa + (uint32_t)(64 * cc + 16 * i)));
+        };
+        ld_wsc(0, wsc[0]);
+        QR_TMEM_LD16(taddr, rc[0]);
+        tmem_ld_wait();
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc) {
+          uint32_t(&cur)[16] = rc[cc & 1];
+          const float4(&w)[4] = wsc[cc & 1];
+          QR_TMEM_ST8(taddr + 16u * cc, bias8);  // the next group of this buffer starts at the bias
+          QR_TMEM_ST8(taddr + 16u * cc + 8u, bias8);
+          if (cc + 1 < 8) {
+            QR_TMEM_LD16(taddr + 16u * (cc + 1), rc[(cc + 1) & 1]);
+            ld_wsc(cc + 1, wsc[(cc + 1) & 1]);
+          }
+#pragma unroll
+          for (int c = 0; c < 16; c += 4) {
+            const float4 w4 = w[c >> 2];
+            const float2 d0 = f2add(make_float2(__uint_as_float(cur[c]), __uint_as_float(cur[c + 1])), mg);
+            const float2 d1 = f2add(make_float2(__uint_as_float(cur[c + 2]), __uint_as_float(cur[c + 3])), mg);
+            const int j = (16 * cc + c) >> 1;
+            acc[j] = f2fma(d0, f2mul(sx2, make_float2(w4.x, w4.y)), acc[j]);
+            acc[j + 1] = f2fma(d1, f2mul(sx2, make_float2(w4.z, w4.w)), acc[j + 1]);
+          }
+          if (cc + 1 < 8) tmem_ld_wait();
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty_leader + (uint32_t)ab * 8u);
+      }
+      if (row_ok) {
+        __half* dst = p.out + m * p.ld_out + (int64_t)nb * BN + chalf * 128;
+        const int64_t n0 = (int64_t)nb * BN + chalf * 128;
+#pragma unroll
+        for (int c = 0; c < 128; c += 8) {
+          if (n0 + c < p.N)
+            *reinterpret_cast<uint4*>(dst + c) =
+                make_uint4(pack_half2(acc[c / 2].x, acc[c / 2].y), pack_half2(acc[c / 2 + 1].x, acc[c / 2 + 1].y),
+                           pack_half2(acc[c / 2 + 2].x, acc[c / 2 + 2].y), pack_half2(acc[c / 2 + 3].x, acc[c / 2 + 3].y));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == gq4::MMA_WARP) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
   }
@@ -1142,6 +1461,51 @@ cudaError_t launch_int8_group_gemm(const int8_t* xq, const float* xs, int64_t ld
   const int max_pairs = num_sms_current() / 2;
   const int pairs = p.num_tiles < max_pairs ? p.num_tiles : max_pairs;
   int8_group_gemm_kernel<<<2 * pairs, i8::NUM_THREADS, gq::SMEM_BYTES, stream>>>(ma, mb, p);
+  return cudaPeekAtLastError();
+}
+
+cudaError_t launch_int4_group_gemm(const uint8_t* xq, const float* xs, int64_t ld_sx, int64_t M, int64_t K,
+                                   int64_t ld_xq, const uint8_t* wq, const float* ws_t, int64_t ld_sw, int64_t N,
+                                   int64_t ld_wq, int group, void* y, int64_t ld_y, cudaStream_t stream) {
+  using namespace gemm;
+  auto kern = group == 64 ? int4_group_gemm_kernel<64> : group == 128 ? int4_group_gemm_kernel<128>
+                                                                       : int4_group_gemm_kernel<256>;
+  static bool attr_set[64][3] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int gi = group == 64 ? 0 : group == 128 ? 1 : 2;
+  if (!attr_set[dev & 63][gi]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gq4::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set[dev & 63][gi] = true;
+  }
+  CUtensorMap ma, mb;
+  if (!make_packed_map(&ma, xq, M, K / 2, ld_xq) || !make_packed_map(&mb, wq, N, K / 2, ld_wq))
+    return cudaErrorInvalidValue;
+  GParams p;
+  for (int i = 0; i < 8; ++i) p.bias[i] = gq4::BIAS;
+  p.x_scale = xs;
+  p.w_scale_t = ws_t;
+  p.out = static_cast<__half*>(y);
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.ld_out = ld_y;
+  p.ld_sx = ld_sx;
+  p.ld_sw = ld_sw;
+  p.num_m = (int)((M + BM - 1) / BM);
+  p.num_n = (int)((N + BN - 1) / BN);
+  p.num_kb = (int)(K / BK);
+  p.num_tiles = p.num_m * p.num_n;
+  {
+    const int64_t a_tile_bytes = (int64_t)BM * (K / 2);
+    int g = (int)((64ll << 20) / (a_tile_bytes > 0 ? a_tile_bytes : 1));
+    g = g < 8 ? 8 : (g > 32 ? 32 : g);
+    p.group_m = g > p.num_m ? p.num_m : g;
+  }
+  const int max_pairs = num_sms_current() / 2;
+  const int pairs = p.num_tiles < max_pairs ? p.num_tiles : max_pairs;
+  kern<<<2 * pairs, gq4::NUM_THREADS, gq4::SMEM_BYTES, stream>>>(ma, mb, p);
   return cudaPeekAtLastError();
 }
 

@@ -235,40 +235,83 @@ quarot_status quarot_int4_matmul_s32(const uint8_t* xq, int64_t M, int64_t K, in
   return QUAROT_OK;
 }
 
-// ---- A8W8
-static quarot_status hq_group_impl(const void* x, int64_t M, int64_t K, int64_t ld_x, int32_t group, float clip_ratio,
-                                   uint8_t* q, int64_t ld_q, float* scale, int64_t ld_s, void* stream, bool q8) {
+// ---- group-wise
+static quarot_status hq_group_impl(const void* x, int64_t M, int64_t K, int64_t ld_x, int32_t mode, int32_t head_dim,
+                                   int32_t group, float clip_ratio, uint8_t* q, int64_t ld_q, float* scale,
+                                   int64_t ld_s, void* stream, bool q8) {
   g_last_launches = 0;
+  if (mode < QUAROT_HAD_NONE || mode > QUAROT_HAD_ACROSS_HEADS) return QUAROT_ERR_ARG;
   if (!clip_ok(clip_ratio)) return QUAROT_ERR_ARG;
   if (!(group == 64 || group == 128 || group == 256)) return QUAROT_ERR_UNSUPPORTED_SIZE;
   if (M < 0 || K <= 0 || K % 2 || ld_x < K || ld_q < (q8 ? K : K / 2) || ld_s < K / group) return QUAROT_ERR_DIM;
   if (K % group) return QUAROT_ERR_DIM;
   if (M > 0x7fffffffLL) return QUAROT_ERR_DIM;              // rows on gridDim.x
-  if (K > 0xffffLL * 1024) return QUAROT_ERR_UNSUPPORTED_SIZE;  // 1024-element blocks on gridDim.y
+  int64_t p = 0;
+  int m = 0;
+  if (mode == QUAROT_HAD_NONE) {
+    if (K > 0xffffLL * 1024) return QUAROT_ERR_UNSUPPORTED_SIZE;  // 1024-element blocks on gridDim.y
+  } else if (mode == QUAROT_HAD_FULL) {
+    // the row is transformed in shared memory: K <= 32768, K = 2^n m
+    if (!factorize(K, p, m) || p < 2 || K > 32768 || (m > 1 && !qr::base_hadamard_host(m)))
+      return QUAROT_ERR_UNSUPPORTED_SIZE;
+  } else {
+    if (head_dim <= 0 || K % head_dim) return QUAROT_ERR_DIM;
+    if (!pow2(head_dim) || !pow2(K / head_dim) || K / head_dim < 2 || K > 32768) return QUAROT_ERR_UNSUPPORTED_SIZE;
+  }
   if (M == 0) return QUAROT_OK;
   if (!x || !q || !scale) return QUAROT_ERR_NULL;
-  if (!aligned16(x) || !aligned16(q) || (ld_x % 8) || (ld_q % (q8 ? 8 : 4))) return QUAROT_ERR_ALIGN;
-  cudaError_t e = qr::launch_hq_none_group(x, M, K, ld_x, group, clip_ratio, q, ld_q, scale, ld_s,
-                                           static_cast<cudaStream_t>(stream), q8);
+  if (!aligned16(x) || !aligned16(q) || (ld_x % 8) || (ld_q % (q8 ? 8 : 4)) || (mode != QUAROT_HAD_NONE && K % 16))
+    return QUAROT_ERR_ALIGN;
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  if (mode == QUAROT_HAD_NONE) {
+    e = qr::launch_hq_none_group(x, M, K, ld_x, group, clip_ratio, q, ld_q, scale, ld_s, st, q8);
+  } else if (mode == QUAROT_HAD_FULL) {
+    e = m > 1 ? qr::ensure_device_tables() : cudaSuccess;
+    if (e == cudaSuccess)
+      e = qr::launch_hq_full(x, M, K, ld_x, (int)p, m, clip_ratio, q, ld_q, scale, st, q8 ? 3 : 2, group, ld_s);
+  } else {
+    e = qr::launch_hq_heads_group(x, M, K, ld_x, head_dim, clip_ratio, q, ld_q, scale, ld_s, group, q8, st);
+  }
   if (e != cudaSuccess) return cuda_fail(e);
   g_last_launches = 1;
   return QUAROT_OK;
 }
 
-quarot_status quarot_hadamard_quant_group(const void* x, int64_t M, int64_t K, int64_t ld_x, int32_t group,
-                                         float clip_ratio, uint8_t* q, int64_t ld_q, float* scale, int64_t ld_s,
-                                         void* stream) {
-  return hq_group_impl(x, M, K, ld_x, group, clip_ratio, q, ld_q, scale, ld_s, stream, false);
+quarot_status quarot_hadamard_quant_group(const void* x, int64_t M, int64_t K, int64_t ld_x, int32_t mode,
+                                         int32_t head_dim, int32_t group, float clip_ratio, uint8_t* q, int64_t ld_q,
+                                         float* scale, int64_t ld_s, void* stream) {
+  return hq_group_impl(x, M, K, ld_x, mode, head_dim, group, clip_ratio, q, ld_q, scale, ld_s, stream, false);
 }
 
-quarot_status quarot_hadamard_quant_group8(const void* x, int64_t M, int64_t K, int64_t ld_x, int32_t group,
-                                          float clip_ratio, int8_t* q, int64_t ld_q, float* scale, int64_t ld_s,
-                                          void* stream) {
-  return hq_group_impl(x, M, K, ld_x, group, clip_ratio, reinterpret_cast<uint8_t*>(q), ld_q, scale, ld_s, stream,
-                       true);
+quarot_status quarot_hadamard_quant_group8(const void* x, int64_t M, int64_t K, int64_t ld_x, int32_t mode,
+                                          int32_t head_dim, int32_t group, float clip_ratio, int8_t* q, int64_t ld_q,
+                                          float* scale, int64_t ld_s, void* stream) {
+  return hq_group_impl(x, M, K, ld_x, mode, head_dim, group, clip_ratio, reinterpret_cast<uint8_t*>(q), ld_q, scale,
+                       ld_s, stream, true);
 }
 
-quarot_status quarot_int4_linear_group(const int8_t* xq, const float* x_scale, int64_t ld_sx, int64_t M, int64_t K,
+quarot_status quarot_int4_linear_group(const uint8_t* xq, const float* x_scale, int64_t ld_sx, int64_t M, int64_t K,
+                                       int64_t ld_xq, const uint8_t* wq, const float* w_scale_t, int64_t ld_sw,
+                                       int64_t N, int64_t ld_wq, int32_t group, void* y, int64_t ld_y, void* stream) {
+  g_last_launches = 0;
+  if (!(group == 64 || group == 128 || group == 256)) return QUAROT_ERR_UNSUPPORTED_SIZE;
+  if (M < 0 || N <= 0 || K <= 0 || ld_xq < K / 2 || ld_wq < K / 2 || ld_y < N || ld_sx < K / group || ld_sw < N)
+    return QUAROT_ERR_DIM;
+  if (M > 0x7fffffffLL || N > 0x7fffffffLL) return QUAROT_ERR_DIM;
+  if (M == 0) return QUAROT_OK;
+  if (!xq || !x_scale || !wq || !w_scale_t || !y) return QUAROT_ERR_NULL;
+  if (K % 256 || N % 8 || ld_xq % 16 || ld_wq % 16 || ld_y % 8 || ld_sw % 4 || !aligned16(xq) || !aligned16(wq) ||
+      !aligned16(y) || !aligned16(w_scale_t))
+    return QUAROT_ERR_ALIGN;
+  cudaError_t e = qr::launch_int4_group_gemm(xq, x_scale, ld_sx, M, K, ld_xq, wq, w_scale_t, ld_sw, N, ld_wq, group, y,
+                                             ld_y, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e);
+  g_last_launches = 1;
+  return QUAROT_OK;
+}
+
+quarot_status quarot_int4_linear_group8(const int8_t* xq, const float* x_scale, int64_t ld_sx, int64_t M, int64_t K,
                                        int64_t ld_xq, const int8_t* wq, const float* w_scale_t, int64_t ld_sw,
                                        int64_t N, int64_t ld_wq, int32_t group, void* y, int64_t ld_y, void* stream) {
   g_last_launches = 0;
@@ -298,10 +341,15 @@ quarot_status quarot_hadamard_quant8(const void* x, int64_t M, int64_t K, int64_
   if (!clip_ok(clip_ratio)) return QUAROT_ERR_ARG;
   if (M < 0 || K <= 0 || ld_x < K || ld_q < K) return QUAROT_ERR_DIM;
   if (M > 0x7fffffffLL) return QUAROT_ERR_DIM;
-  // 8-bit FULL / ACROSS_HEADS: the tcgen05 quantizers' widths (K = 1024 x 28; head_dim 128, n_h 16-64)
-  if (mode == QUAROT_HAD_FULL && K != 28672) return QUAROT_ERR_UNSUPPORTED_SIZE;
-  if (mode == QUAROT_HAD_ACROSS_HEADS && (head_dim <= 0 || K % head_dim || !qr::hq_heads_tc_supported(K, head_dim)))
+  int64_t p = 0;
+  int m = 0;
+  if (mode == QUAROT_HAD_FULL &&
+      (!factorize(K, p, m) || p < 2 || K > 32768 || (m > 1 && !qr::base_hadamard_host(m))))
     return QUAROT_ERR_UNSUPPORTED_SIZE;
+  if (mode == QUAROT_HAD_ACROSS_HEADS) {
+    if (head_dim <= 0 || K % head_dim) return QUAROT_ERR_DIM;
+    if (!pow2(head_dim) || !pow2(K / head_dim) || K / head_dim < 2) return QUAROT_ERR_UNSUPPORTED_SIZE;
+  }
   if (M == 0) return QUAROT_OK;
   if (!x || !q || !scale) return QUAROT_ERR_NULL;
   if (!aligned16(x) || !aligned16(q) || (ld_x % 8) || (ld_q % 8) || (K % 16)) return QUAROT_ERR_ALIGN;
@@ -314,9 +362,12 @@ quarot_status quarot_hadamard_quant8(const void* x, int64_t M, int64_t K, int64_
     e = qr::ensure_device_tables();
     if (e == cudaSuccess) {
       uint8_t* qb = reinterpret_cast<uint8_t*>(q);
-      e = mode == QUAROT_HAD_FULL ? qr::launch_hq_full28_tc(x, M, ld_x, clip_ratio, qb, ld_q, scale, st, true)
-                                  : qr::launch_hq_heads_tc(x, M, K, ld_x, head_dim, clip_ratio, qb, ld_q, scale, st,
-                                                           true);
+      if (mode == QUAROT_HAD_FULL)
+        e = qr::launch_hq_full(x, M, K, ld_x, (int)p, m, clip_ratio, qb, ld_q, scale, st, 1);
+      else if (qr::hq_heads_tc_supported(K, head_dim) && qr::g_hq_heads_variant != 1)
+        e = qr::launch_hq_heads_tc(x, M, K, ld_x, head_dim, clip_ratio, qb, ld_q, scale, st, true);
+      else
+        e = qr::launch_hq_heads8(x, M, K, ld_x, head_dim, clip_ratio, qb, ld_q, scale, st);
     }
   }
   if (e != cudaSuccess) return cuda_fail(e);

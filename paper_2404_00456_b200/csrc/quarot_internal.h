@@ -26,6 +26,10 @@ cudaError_t launch_hq_none_group(const void* x, int64_t M, int64_t K, int64_t ld
 cudaError_t launch_int8_group_gemm(const int8_t* xq, const float* xs, int64_t ld_sx, int64_t M, int64_t K,
                                    int64_t ld_xq, const int8_t* wq, const float* ws_t, int64_t ld_sw, int64_t N,
                                    int64_t ld_wq, void* y, int64_t ld_y, cudaStream_t stream);
+// group-wise W4A4 GEMM on packed INT4 codes (§8 f3), group in {64, 128, 256}
+cudaError_t launch_int4_group_gemm(const uint8_t* xq, const float* xs, int64_t ld_sx, int64_t M, int64_t K,
+                                   int64_t ld_xq, const uint8_t* wq, const float* ws_t, int64_t ld_sw, int64_t N,
+                                   int64_t ld_wq, int group, void* y, int64_t ld_y, cudaStream_t stream);
 cudaError_t launch_hq_none(const void* x, int64_t M, int64_t K, int64_t ld_x, float clip, uint8_t* q,
                            int64_t ld_q, float* scale, cudaStream_t stream, bool rmsnorm = false);
 cudaError_t launch_hq_heads(const void* x, int64_t M, int64_t K, int64_t ld_x, int head_dim, float clip,
@@ -38,16 +42,27 @@ extern int g_hq_full_variant;
 // hq_full_small_tc.cu: the Llama-2-13B widths K = 128 x 108 and 256 x 20 on the tcgen05 path
 bool hq_full_small_tc_supported(int64_t pow2, int m);
 cudaError_t launch_hq_full_small_tc(const void* x, int64_t M, int64_t ld_x, int64_t pow2, int m, float clip,
-                                    uint8_t* q, int64_t ld_q, float* scale, cudaStream_t stream);
+                                    uint8_t* q, int64_t ld_q, float* scale, cudaStream_t stream, bool q8 = false);
 // hq_full172_tc.cu: K = 64 x 172 on the tcgen05 path (the default for that width)
 cudaError_t launch_hq_full172_tc(const void* x, int64_t M, int64_t ld_x, float clip, uint8_t* q, int64_t ld_q,
-                                 float* scale, cudaStream_t stream);
+                                 float* scale, cudaStream_t stream, bool q8 = false);
 // hq_heads_tc.cu: ACROSS_HEADS on the tcgen05 path (head_dim 128, n_h in {16, 32, 64})
 bool hq_heads_tc_supported(int64_t K, int head_dim);
 cudaError_t launch_hq_heads_tc(const void* x, int64_t M, int64_t K, int64_t ld_x, int head_dim, float clip, uint8_t* q,
                                int64_t ld_q, float* scale, cudaStream_t stream, bool q8 = false);
+// FULL, K = pow2 * m.  out: 0 INT4 per row, 1 int8 per row (A8), 2 INT4 per group (scale [M][ld_s]),
+// 3 INT4 per group one code per byte.  The model widths take the tcgen05 kernels for out 0 / 1.
 cudaError_t launch_hq_full(const void* x, int64_t M, int64_t K, int64_t ld_x, int pow2, int m, float clip,
-                           uint8_t* q, int64_t ld_q, float* scale, cudaStream_t stream);
+                           uint8_t* q, int64_t ld_q, float* scale, cudaStream_t stream, int out = 0, int group = 0,
+                           int64_t ld_s = 0);
+// ACROSS_HEADS group-wise (§8 f3): y = (H_{n_h} (x) I) z, then per-group INT4 (q8: one code per byte)
+cudaError_t launch_hq_heads_group(const void* x, int64_t M, int64_t K, int64_t ld_x, int head_dim, float clip,
+                                  uint8_t* q, int64_t ld_q, float* scale, int64_t ld_s, int group, bool q8,
+                                  cudaStream_t stream);
+// ACROSS_HEADS 8-bit per row on the smem kernel (the shapes the tcgen05 kernel does not take)
+cudaError_t launch_hq_heads8(const void* x, int64_t M, int64_t K, int64_t ld_x, int head_dim, float clip, uint8_t* q,
+                             int64_t ld_q, float* scale, cudaStream_t stream);
+extern int g_hq_heads_variant;
 
 // kv_quant.cu
 cudaError_t launch_kv_quant(const void* k, int64_t ld_k, const void* v, int64_t ld_v, int64_t T, int n_kv,

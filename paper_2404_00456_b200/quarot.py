@@ -42,10 +42,14 @@ _SIGS = {
     "quarot_kv_decode": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_i64, _c_i32, _c_i32, _c_i32, _c_i64, _c_f32,
                          _vp, _vp, _c_i64, _vp],
     "quarot_kv_decode_workspace_bytes": [_c_i64, _c_i32, _c_i32, _c_i64],
-    "quarot_hadamard_quant_group": [_vp, _c_i64, _c_i64, _c_i64, _c_i32, _c_f32, _vp, _c_i64, _vp, _c_i64, _vp],
-    "quarot_hadamard_quant_group8": [_vp, _c_i64, _c_i64, _c_i64, _c_i32, _c_f32, _vp, _c_i64, _vp, _c_i64, _vp],
+    "quarot_hadamard_quant_group": [_vp, _c_i64, _c_i64, _c_i64, _c_i32, _c_i32, _c_i32, _c_f32, _vp, _c_i64, _vp,
+                                    _c_i64, _vp],
+    "quarot_hadamard_quant_group8": [_vp, _c_i64, _c_i64, _c_i64, _c_i32, _c_i32, _c_i32, _c_f32, _vp, _c_i64, _vp,
+                                     _c_i64, _vp],
     "quarot_int4_linear_group": [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _vp, _vp, _c_i64, _c_i64, _c_i64, _c_i32,
                                  _vp, _c_i64, _vp],
+    "quarot_int4_linear_group8": [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _vp, _vp, _c_i64, _c_i64, _c_i64, _c_i32,
+                                  _vp, _c_i64, _vp],
     "quarot_hadamard_quant8": [_vp, _c_i64, _c_i64, _c_i64, _c_i32, _c_i32, _c_f32, _vp, _c_i64, _vp, _vp],
     "quarot_int8_linear": [_vp, _vp, _c_i64, _c_i64, _c_i64, _vp, _vp, _c_i64, _c_i64, _vp, _c_i64, _vp],
     "quarot_int8_matmul_s32": [_vp, _c_i64, _c_i64, _c_i64, _vp, _c_i64, _c_i64, _vp, _c_i64, _vp],
@@ -291,24 +295,30 @@ def kv_quant(k: torch.Tensor, v: torch.Tensor, q: torch.Tensor | None = None, fl
 
 
 def hadamard_quant_group(x: torch.Tensor, group: int = 128, clip_ratio: float = 0.9, q: torch.Tensor | None = None,
-                         scale: torch.Tensor | None = None, stream=None):
-    """quarot_hadamard_quant_group (§8 f3, mode NONE): packed INT4 [M, K/2] and fp32 scales [M, K/group]."""
+                         scale: torch.Tensor | None = None, stream=None, mode="none", head_dim: int = 128):
+    """quarot_hadamard_quant_group (§8 f3; mode none / full / across_heads): packed INT4 [M, K/2]
+    and fp32 scales [M, K/group]."""
     M, K = x.shape
     q = torch.empty(M, K // 2, dtype=torch.uint8, device=x.device) if q is None else q
     scale = torch.empty(M, max(K // group, 1), dtype=torch.float32, device=x.device) if scale is None else scale
-    st = lib().quarot_hadamard_quant_group(_dev(x, "x", torch.float16), M, K, x.stride(0), group, clip_ratio,
+    mode_i = MODES[mode] if isinstance(mode, str) else int(mode)
+    st = lib().quarot_hadamard_quant_group(_dev(x, "x", torch.float16), M, K, x.stride(0), mode_i, head_dim, group,
+                                           clip_ratio,
                                            _dev(q, "q", torch.uint8), q.stride(0), _dev(scale, "scale", torch.float32),
                                            scale.stride(0), _stream(stream))
     _check("quarot_hadamard_quant_group", st)
     return q, scale
 
 
-def hadamard_quant_group8(x: torch.Tensor, group: int = 128, clip_ratio: float = 0.9, stream=None):
+def hadamard_quant_group8(x: torch.Tensor, group: int = 128, clip_ratio: float = 0.9, stream=None, mode="none",
+                          head_dim: int = 128):
     """quarot_hadamard_quant_group8 (§8 f3): int8 codes [M, K] (one per byte) and fp32 scales [M, K/group]."""
     M, K = x.shape
     q = torch.empty(M, K, dtype=torch.int8, device=x.device)
     scale = torch.empty(M, max(K // group, 1), dtype=torch.float32, device=x.device)
-    st = lib().quarot_hadamard_quant_group8(_dev(x, "x", torch.float16), M, K, x.stride(0), group, clip_ratio,
+    mode_i = MODES[mode] if isinstance(mode, str) else int(mode)
+    st = lib().quarot_hadamard_quant_group8(_dev(x, "x", torch.float16), M, K, x.stride(0), mode_i, head_dim, group,
+                                            clip_ratio,
                                             q.data_ptr(), q.stride(0), _dev(scale, "scale", torch.float32),
                                             scale.stride(0), _stream(stream))
     _check("quarot_hadamard_quant_group8", st)
@@ -316,24 +326,39 @@ def hadamard_quant_group8(x: torch.Tensor, group: int = 128, clip_ratio: float =
 
 
 def int4_linear_group(xq: torch.Tensor, x_scale: torch.Tensor, wq: torch.Tensor, w_scale_t: torch.Tensor,
-                      y: torch.Tensor | None = None, stream=None) -> torch.Tensor:
-    """quarot_int4_linear_group (§8 f3, group 128): int8-stored codes xq [M, K], wq [N, K];
+                      group: int = 128, y: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """quarot_int4_linear_group (§8 f3, group 64 / 128 / 256): packed INT4 codes xq [M, K/2], wq [N, K/2];
+    x_scale [M, K/group]; w_scale_t [K/group, N]; y fp16 [M, N]."""
+    M, K = xq.shape[0], 2 * xq.shape[1]
+    N = wq.shape[0]
+    y = torch.empty(M, N, dtype=torch.float16, device=xq.device) if y is None else y
+    st = lib().quarot_int4_linear_group(_dev(xq, "xq", torch.uint8), _dev(x_scale, "x_scale", torch.float32),
+                                        x_scale.stride(0), M, K, xq.stride(0), _dev(wq, "wq", torch.uint8),
+                                        _dev(w_scale_t, "w_scale_t", torch.float32), w_scale_t.stride(0), N,
+                                        wq.stride(0), group, _dev(y, "y", torch.float16), y.stride(0), _stream(stream))
+    _check("quarot_int4_linear_group", st)
+    return y
+
+
+def int4_linear_group8(xq: torch.Tensor, x_scale: torch.Tensor, wq: torch.Tensor, w_scale_t: torch.Tensor,
+                       y: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """quarot_int4_linear_group8 (§8 f3, group 128): int8-stored codes xq [M, K], wq [N, K];
     x_scale [M, K/128]; w_scale_t [K/128, N]; y fp16 [M, N]."""
     M, K = xq.shape
     N = wq.shape[0]
     y = torch.empty(M, N, dtype=torch.float16, device=xq.device) if y is None else y
-    st = lib().quarot_int4_linear_group(xq.data_ptr(), _dev(x_scale, "x_scale", torch.float32), x_scale.stride(0), M, K,
-                                        xq.stride(0), wq.data_ptr(), _dev(w_scale_t, "w_scale_t", torch.float32),
-                                        w_scale_t.stride(0), N, wq.stride(0), 128, _dev(y, "y", torch.float16),
-                                        y.stride(0), _stream(stream))
-    _check("quarot_int4_linear_group", st)
+    st = lib().quarot_int4_linear_group8(xq.data_ptr(), _dev(x_scale, "x_scale", torch.float32), x_scale.stride(0), M,
+                                         K, xq.stride(0), wq.data_ptr(), _dev(w_scale_t, "w_scale_t", torch.float32),
+                                         w_scale_t.stride(0), N, wq.stride(0), 128, _dev(y, "y", torch.float16),
+                                         y.stride(0), _stream(stream))
+    _check("quarot_int4_linear_group8", st)
     return y
 
 
 def hadamard_quant8(x: torch.Tensor, clip_ratio: float = 0.9, rmsnorm: bool = False, q: torch.Tensor | None = None,
                     scale: torch.Tensor | None = None, stream=None, mode="none", head_dim: int = 128):
     """quarot_hadamard_quant8 (A8W8, §8 f4): int8 codes [M, K] and fp32 scales [M]; mode NONE
-    (± RMSNorm), FULL (K = 28672) or ACROSS_HEADS (head_dim 128, 16-64 heads)."""
+    (± RMSNorm), FULL (every K = 2^n m) or ACROSS_HEADS (power-of-two head_dim and heads)."""
     M, K = x.shape
     if x.stride(1) != 1:
         raise ValueError("x rows must be contiguous")

@@ -23,7 +23,7 @@ def _peaks():
             p = json.load(f)
         return float(p["hbm_gbs"]), 2.0 * float(p.get("bf16_tflops_sustained", p["bf16_tflops"]))
     except (OSError, KeyError, ValueError):
-        return 6536.0, 2765.6
+        return 6650.0, 2800.0  # B200_PROFILING.md fallback (6.65 TB/s, 2 x 1.4 PF sustained bf16)
 
 
 HBM_GBS, INT8_TOPS = _peaks()
@@ -157,20 +157,30 @@ def main():
                 print(key, json.dumps(res[key]), flush=True)
                 del cache
     if "gemm_group" in a.what:
-        # group-wise (G = 128) W4A4 GEMM, codes one per int8 byte; same shapes
-        xq_big = torch.randint(-7, 8, (M, 28672), dtype=torch.int8, device=dev)
+        # group-wise W4A4 GEMM on packed INT4 codes (G = 64 / 128 / 256) and the
+        # int8-stored-codes variant (G = 128); the Llama-2-70B linear shapes
+        xq_big = torch.randint(0, 256, (M, 28672 // 2), dtype=torch.uint8, device=dev)
+        xq8_big = torch.randint(-7, 8, (M, 28672), dtype=torch.int8, device=dev)
         for name, N, K in (("qkv", 10240, 8192), ("o", 8192, 8192), ("gate_up", 57344, 8192), ("down", 8192, 28672)):
-            xq = xq_big[:, :K]
-            wq = torch.randint(-7, 8, (N, K), dtype=torch.int8, device=dev)
+            wq = torch.randint(0, 256, (N, K // 2), dtype=torch.uint8, device=dev)
+            y = torch.empty(M, N, dtype=torch.float16, device=dev)
+            for G in (64, 128, 256):
+                xs = torch.rand(M, K // G, device=dev) * 0.01 + 0.001
+                ws = torch.rand(K // G, N, device=dev) * 0.01 + 0.001
+                ms = timeit(lambda: q.int4_linear_group(xq_big[:, :K // 2], xs, wq, ws, group=G, y=y), a.iters)
+                tops = 2 * M * N * K / ms / 1e9
+                res[f"gemm_group{G}_{name}"] = {"ms": ms, "tops": tops, "frac_int8_2x_bf16_sustained": tops / INT8_TOPS}
+                print(f"group{G}", name, json.dumps(res[f"gemm_group{G}_{name}"]), flush=True)
+            del wq
+            wq8 = torch.randint(-7, 8, (N, K), dtype=torch.int8, device=dev)
             xs = torch.rand(M, K // 128, device=dev) * 0.01 + 0.001
             ws = torch.rand(K // 128, N, device=dev) * 0.01 + 0.001
-            y = torch.empty(M, N, dtype=torch.float16, device=dev)
-            ms = timeit(lambda: q.int4_linear_group(xq, xs, wq, ws, y=y), a.iters)
+            ms = timeit(lambda: q.int4_linear_group8(xq8_big[:, :K], xs, wq8, ws, y=y), a.iters)
             tops = 2 * M * N * K / ms / 1e9
-            res[f"gemm_group_{name}"] = {"ms": ms, "tops": tops, "frac_int8_2x_bf16_sustained": tops / INT8_TOPS}
-            print("group", name, json.dumps(res[f"gemm_group_{name}"]), flush=True)
-            del wq, y
-        del xq_big
+            res[f"gemm_group8_{name}"] = {"ms": ms, "tops": tops}
+            print("group8 (int8-stored)", name, json.dumps(res[f"gemm_group8_{name}"]), flush=True)
+            del wq8, y
+        del xq_big, xq8_big
     if "gemm8" in a.what:
         # A8W8: the native kind::i8 path, same shapes as the W4A4 bench; the
         # difference to "gemm" is the cost of unpacking INT4 on B200

@@ -43,7 +43,7 @@ def test_library_exports_every_declared_symbol(q):
 
 
 def test_abi_version_and_status_strings(q):
-    assert q.abi_version() == 1
+    assert q.abi_version() == 2
     for s in range(7):
         assert q.lib().quarot_status_string(s)
 
@@ -80,8 +80,8 @@ def test_hadamard_quant_validation_without_gpu(q):
     assert _hq(q, mode=2, K=256, hd=32) == 3                           # head_dim < 64
 
 
-def _hqg(q, x=16, M=4, K=256, ld_x=256, group=128, clip=0.9, qp=32, ld_q=128, sp=48, ld_s=2):
-    return q.lib().quarot_hadamard_quant_group(x, M, K, ld_x, group, clip, qp, ld_q, sp, ld_s, None)
+def _hqg(q, x=16, M=4, K=256, ld_x=256, group=128, clip=0.9, qp=32, ld_q=128, sp=48, ld_s=2, mode=0, hd=128):
+    return q.lib().quarot_hadamard_quant_group(x, M, K, ld_x, mode, hd, group, clip, qp, ld_q, sp, ld_s, None)
 
 
 def test_hadamard_quant_group_validation_without_gpu(q):
@@ -93,6 +93,12 @@ def test_hadamard_quant_group_validation_without_gpu(q):
     assert _hqg(q, M=0) == 0                                            # no-op
     assert _hqg(q, x=None) == 1 and _hqg(q, sp=None) == 1               # ERR_NULL
     assert _hqg(q, x=16 * 7 + 2) == 4                                   # misaligned pointer
+    assert _hqg(q, mode=3) == 5 and _hqg(q, mode=0x100) == 5            # bad mode / flags
+    assert _hqg(q, mode=1, K=192 * 4, ld_x=768, ld_q=384, ld_s=6) == 3  # 768 = 2^6 * 12: no H_12
+    assert _hqg(q, mode=1, K=65536, ld_x=65536, ld_q=32768, ld_s=512) == 3  # FULL: K <= 32768
+    assert _hqg(q, mode=2, hd=96) == 2                                  # K % head_dim
+    assert _hqg(q, mode=2, hd=256) == 3                                 # a single head
+    assert _hqg(q, mode=1, M=0) == 0 and _hqg(q, mode=2, M=0) == 0      # no-ops
 
 
 def _lin(q, M=128, K=256, N=256, ld_xq=128, ld_wq=128, ld_y=256, xp=16, wp=16, yp=16):
@@ -130,27 +136,37 @@ def test_kv_validation_without_gpu(q):
     assert f(*bad) == 4                                 # ld_k % 8
 
 
-def _lg(q, xp=16, sx=16, ld_sx=2, M=128, K=256, ld_xq=256, wp=16, sw=16, ld_sw=256, N=256, ld_wq=256, group=128,
-        yp=16, ld_y=256):
-    return q.lib().quarot_int4_linear_group(xp, sx, ld_sx, M, K, ld_xq, wp, sw, ld_sw, N, ld_wq, group, yp, ld_y, None)
+def _lg(q, xp=16, sx=16, ld_sx=2, M=4, K=256, ld_xq=128, wp=16, sw=16, ld_sw=256, N=256, ld_wq=128, group=128,
+        yp=16, ld_y=256, fn="quarot_int4_linear_group"):
+    return getattr(q.lib(), fn)(xp, sx, ld_sx, M, K, ld_xq, wp, sw, ld_sw, N, ld_wq, group, yp, ld_y, None)
 
 
 def test_int4_linear_group_validation_without_gpu(q):
-    # quarot_int4_linear_group (§8 f3): rejected before any CUDA call
-    assert _lg(q, group=64) == 3                                        # only group 128
-    assert _lg(q, K=384, ld_xq=384, ld_wq=384, ld_sx=3) == 4           # K % 256
+    # quarot_int4_linear_group (§8 f3, packed INT4, G = 64 / 128 / 256): rejected before any CUDA call
+    assert _lg(q, group=32) == 3 and _lg(q, group=512) == 3             # ERR_UNSUPPORTED_SIZE
+    assert _lg(q, K=384, ld_xq=192, ld_wq=192, ld_sx=3) == 4            # K % 256
     assert _lg(q, ld_sx=1) == 2 and _lg(q, ld_sw=100) == 2 and _lg(q, ld_y=100) == 2  # ERR_DIM
+    assert _lg(q, group=64, ld_sx=3) == 2                               # K / 64 scales per row
+    assert _lg(q, ld_xq=100) == 2                                       # ld_xq < K / 2
     assert _lg(q, N=260, ld_sw=260, ld_y=264) == 4                      # N % 8
     assert _lg(q, ld_sw=258) == 4                                       # ld_sw % 4
     assert _lg(q, M=0) == 0                                             # no-op
     assert _lg(q, xp=None) == 1 and _lg(q, sw=None) == 1                # ERR_NULL
+    # quarot_int4_linear_group8 (int8-stored codes, G = 128 only)
+    g8 = dict(fn="quarot_int4_linear_group8", ld_xq=256, ld_wq=256)
+    assert _lg(q, group=64, **g8) == 3
+    assert _lg(q, K=384, ld_sx=3, fn="quarot_int4_linear_group8", ld_xq=384, ld_wq=384) == 4
+    assert _lg(q, M=0, **g8) == 0
 
 
 def test_hadamard_quant8_validation_without_gpu(q):
     lib = q.lib()
     f = lambda mode, K, hd=128: lib.quarot_hadamard_quant8(16, 4, K, K, mode, hd, 0.9, 16, K, 16, None)
-    assert f(q.FULL, 8192) == 3                      # 8-bit FULL only for K = 1024 x 28
-    assert f(q.ACROSS_HEADS, 512) == 3               # 4 heads: not on the 8-bit path
+    assert f(q.FULL, 768) == 3                       # 768 = 2^6 x 12: no stored H_12
+    assert f(q.FULL, 65536) == 3                     # the smem kernels take K <= 32768
+    assert f(q.ACROSS_HEADS, 128) == 3               # a single head
+    assert f(q.ACROSS_HEADS, 384, hd=96) == 3        # head_dim not a power of two
+    assert f(q.ACROSS_HEADS, 500, hd=128) == 2       # K % head_dim
     assert f(q.FULL | q.RMSNORM, 28672) == 5         # RMSNorm only with mode NONE
 
 
@@ -237,7 +253,10 @@ def test_every_wrapper_passes_declared_arity_and_stream(monkeypatch):
     qq.kv_quant(k, v, qh, out=out, rope=(0, 2048, 1e4), stream=STREAM)
     qq.hadamard_quant_group(x, stream=STREAM)
     qq.hadamard_quant_group8(x, stream=STREAM)
-    qq.int4_linear_group(i8(4, 256), f32(4, 2), i8(16, 256), f32(2, 16), stream=STREAM)
+    qq.int4_linear_group(u8(4, 128), f32(4, 2), u8(16, 128), f32(2, 16), stream=STREAM)
+    qq.int4_linear_group8(i8(4, 256), f32(4, 2), i8(16, 256), f32(2, 16), stream=STREAM)
+    qq.hadamard_quant_group(x, mode="full", stream=STREAM)
+    qq.hadamard_quant8(x, mode="full", stream=STREAM)
     qq.hadamard_quant8(x, stream=STREAM)
     qq.int8_linear(i8(4, 256), f32(4), i8(16, 256), f32(16), stream=STREAM)
     qq.int8_matmul_s32(i8(4, 256), i8(16, 256), stream=STREAM)

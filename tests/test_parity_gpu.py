@@ -274,44 +274,93 @@ def test_hadamard_quant_group_parity(q, K, group):
     P.assert_scales(s[fin], ref_s[fin], f"group {group} K={K}")
 
 
-@pytest.mark.parametrize("M,N,K", [(300, 520, 512), (128, 256, 256), (513, 1032, 1024), (64, 256, 4096)])
-def test_int4_linear_group_parity(q, M, N, K):
-    """group-wise W4A4 GEMM (group 128) against the oracle's group_linear on the
-    same codes and scales: fp16 outputs within 1e-2 relative Frobenius and 2 fp16 ulp."""
-    from oracle import gemm as og
-    rng = np.random.default_rng(M + N + K)
+def _group_case(M, N, K, G, seed):
+    rng = np.random.default_rng(seed)
     cx = rng.integers(-7, 8, (M, K)).astype(np.int8)
-    cw = rng.integers(-7, 8, (N, K)).astype(np.int8)
-    sx = rng.uniform(0.001, 0.02, (M, K // 128)).astype(np.float32)
-    sw = rng.uniform(0.001, 0.02, (N, K // 128)).astype(np.float32)
-    y = q.int4_linear_group(torch.from_numpy(cx).to(DEV), torch.from_numpy(sx).to(DEV),
-                            torch.from_numpy(cw).to(DEV), torch.from_numpy(sw.T.copy()).to(DEV))
-    torch.cuda.synchronize()
-    ref = og.group_linear(cx, sx, cw, sw)
-    got = y.cpu().numpy()
+    cw = rng.integers(-8, 8, (N, K)).astype(np.int8)
+    sx = rng.uniform(0.001, 0.02, (M, K // G)).astype(np.float32)
+    sw = rng.uniform(0.001, 0.02, (N, K // G)).astype(np.float32)
+    return cx, cw, sx, sw
+
+
+def _assert_group_out(got, ref):
     assert P.frob_rel(got, ref) <= 1e-2
     ulp = np.abs(got.astype(np.float32) - ref.astype(np.float32)) / np.maximum(
         np.abs(np.spacing(ref.astype(np.float16))).astype(np.float32), 1e-30)
-    assert np.quantile(ulp, 0.999) <= 2.0
+    assert np.quantile(ulp, 0.999) <= 2.0 and ulp.max() <= 4.0
 
 
-def test_group_pipeline_quant8_then_linear(q):
-    """quarot_hadamard_quant_group8 -> quarot_int4_linear_group against the oracle pipeline
-    (quantize_sym_groups on x, group_linear), and quant8 codes equal the packed quantizer's."""
+@pytest.mark.parametrize("G", [64, 128, 256])
+@pytest.mark.parametrize("M,N,K", [(300, 520, 512), (128, 256, 256), (513, 1032, 1024), (64, 256, 4096),
+                                   (1100, 776, 2304)])
+def test_int4_linear_group_parity(q, M, N, K, G):
+    """group-wise W4A4 GEMM on PACKED INT4 codes (G = 64 / 128 / 256, weight codes
+    incl. -8) against the oracle's group_linear (fp64) on the same codes and scales: fp16 outputs
+    within 1e-2 relative Frobenius, 2 fp16 ulp at the 99.9th percentile (4 max).  Covers ragged M / N,
+    several tiles per CTA pair and K / 256 k-blocks of G / 32 MMAs per group."""
     from oracle import gemm as og
-    M, K, N = 200, 1024, 264
-    x = synth.activations(M, K, "outlier", seed=11, device=DEV)
-    xq8, xs = q.hadamard_quant_group8(x, 128)
-    xq4, xs4 = q.hadamard_quant_group(x, 128)
+    from oracle import quant as oq
+    cx, cw, sx, sw = _group_case(M, N, K, G, M + N + K + G)
+    xq = torch.from_numpy(oq.pack_int4(cx.astype(np.int64))).to(DEV)
+    wq = torch.from_numpy(oq.pack_int4(cw.astype(np.int64))).to(DEV)
+    y = q.int4_linear_group(xq, torch.from_numpy(sx).to(DEV), wq, torch.from_numpy(sw.T.copy()).to(DEV), group=G)
     torch.cuda.synchronize()
-    assert np.array_equal(P.unpack_signed(xq4.cpu().numpy()), xq8.cpu().numpy().astype(np.int64))
-    assert torch.equal(xs, xs4)
+    _assert_group_out(y.cpu().numpy(), og.group_linear(cx, sx, cw, sw))
+
+
+def test_int4_linear_group_extreme_codes(q):
+    """Largest per-group sums (|acc_g| = 7 * 8 * G at G = 256): the accumulator bias stays exact."""
+    from oracle import gemm as og
+    from oracle import quant as oq
+    M, N, K, G = 256, 256, 1024, 256
+    cx = np.full((M, K), 7, np.int8)
+    cx[1::2] = -7
+    cw = np.full((N, K), -8, np.int8)
+    cw[::3] = 7
+    sx = np.full((M, K // G), 1.0 / 1024, np.float32)
+    sw = np.full((N, K // G), 1.0 / 64, np.float32)
+    y = q.int4_linear_group(torch.from_numpy(oq.pack_int4(cx.astype(np.int64))).to(DEV), torch.from_numpy(sx).to(DEV),
+                            torch.from_numpy(oq.pack_int4(cw.astype(np.int64))).to(DEV),
+                            torch.from_numpy(sw.T.copy()).to(DEV), group=G)
+    ref = og.group_linear(cx, sx, cw, sw)
+    assert np.array_equal(y.cpu().numpy(), ref.astype(np.float16))
+
+
+@pytest.mark.parametrize("M,N,K", [(300, 520, 512), (513, 1032, 1024)])
+def test_int4_linear_group8_parity(q, M, N, K):
+    """quarot_int4_linear_group8: the int8-stored-codes variant (G = 128) on the same oracle."""
+    from oracle import gemm as og
+    cx, cw, sx, sw = _group_case(M, N, K, 128, M + N + K)
+    y = q.int4_linear_group8(torch.from_numpy(cx).to(DEV), torch.from_numpy(sx).to(DEV),
+                             torch.from_numpy(cw).to(DEV), torch.from_numpy(sw.T.copy()).to(DEV))
+    torch.cuda.synchronize()
+    _assert_group_out(y.cpu().numpy(), og.group_linear(cx, sx, cw, sw))
+
+
+@pytest.mark.parametrize("mode,G", [("none", 128), ("full", 64), ("across_heads", 256)])
+def test_group_pipeline_quant_then_linear(q, mode, G):
+    """quarot_hadamard_quant_group (packed) -> quarot_int4_linear_group against the oracle pipeline
+    (online transform, quantize_sym_groups, group_linear); the int8-stored quantizer agrees."""
+    from oracle import gemm as og
+    from oracle import layer as olayer
+    M, K, N = 200, 4096, 264
+    x = synth.activations(M, K, "outlier", seed=11, device=DEV)
+    xq4, xs4 = q.hadamard_quant_group(x, G, mode=mode)
+    xq8, xs8 = q.hadamard_quant_group8(x, G, mode=mode)
+    torch.cuda.synchronize()
+    got_c = P.unpack_signed(xq4.cpu().numpy())
+    assert np.array_equal(got_c, xq8.cpu().numpy().astype(np.int64))
+    assert torch.equal(xs4, xs8)
     rng = np.random.default_rng(12)
     cw = rng.integers(-7, 8, (N, K)).astype(np.int8)
-    sw = rng.uniform(0.001, 0.02, (N, K // 128)).astype(np.float32)
-    y = q.int4_linear_group(xq8, xs, torch.from_numpy(cw).to(DEV), torch.from_numpy(sw.T.copy()).to(DEV))
+    sw = rng.uniform(0.001, 0.02, (N, K // G)).astype(np.float32)
+    from oracle import quant as oq
+    wq = torch.from_numpy(oq.pack_int4(cw.astype(np.int64))).to(DEV)
+    y = q.int4_linear_group(xq4, xs4, wq, torch.from_numpy(sw.T.copy()).to(DEV), group=G)
     torch.cuda.synchronize()
-    rc, rs = oquant.quantize_sym_groups(x.float().cpu().numpy().astype(np.float64), 128)
-    P.assert_codes(xq8.cpu().numpy().astype(np.int64), rc, "group8 codes")
-    ref = og.group_linear(rc, rs, cw, sw)
-    assert P.frob_rel(y.cpu().numpy(), ref) <= 1e-2
+    rc, rs = oquant.quantize_sym_groups(olayer.online_transform(x.float().cpu().numpy().astype(np.float64), mode), G)
+    P.assert_codes(got_c, rc, f"group {G} {mode} codes")
+    # on the GPU's own codes and scales the GEMM matches group_linear to fp16 ulps; against the
+    # oracle's codes (<= 1e-4 flips) within the 1e-2 end-to-end bar
+    _assert_group_out(y.cpu().numpy(), og.group_linear(got_c.astype(np.int8), xs4.cpu().numpy(), cw, sw))
+    assert P.frob_rel(y.cpu().numpy(), og.group_linear(rc, rs, cw, sw)) <= 1e-2
