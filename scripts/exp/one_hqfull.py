@@ -1,6 +1,6 @@
 """One FULL hadamard_quant launch set (ncu target).  python scripts/one_hqfull.py M K variant"""
 import ctypes, os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch, synth
 import paper_2404_00456_b200 as q
 M, K = int(sys.argv[1]), int(sys.argv[2])
