@@ -287,6 +287,7 @@ quarot_status quarot_kv_append(const void* k, int64_t ld_k, const void* v, int64
  * [B][n_q][head_dim] contiguous (o is in V's space: V is not rotated online).
  * workspace fp32, quarot_kv_decode_workspace_bytes(B, n_q, head_dim, s_max) bytes, caller-owned.
  * Requirements: head_dim == 128; n_q / n_kv in {1, 2, 4, 8}; B, n_kv <= 65535 (ERR_DIM);
+ * B * s_max < 2^31 (ERR_UNSUPPORTED_SIZE: the cache rows are addressed by one TMA coordinate);
  * sm_scale finite (the standard
  * 1/sqrt(head_dim) is reading Z24); 16-B aligned pointers.  Two kernel launches. */
 quarot_status quarot_kv_decode(const void* q, const uint8_t* k_codes, const float* k_scale,

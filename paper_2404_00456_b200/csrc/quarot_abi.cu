@@ -510,6 +510,7 @@ quarot_status quarot_kv_decode(const void* q, const uint8_t* k_codes, const floa
   g_last_launches = 0;
   if (B < 0 || n_q <= 0 || n_kv <= 0 || head_dim <= 0 || s_max <= 0 || s_max > (1 << 30)) return QUAROT_ERR_DIM;
   if (B > 65535 || n_kv > 65535) return QUAROT_ERR_DIM;  // grid (split, n_kv, B)
+  if (B * s_max > 0x7fffffffLL) return QUAROT_ERR_UNSUPPORTED_SIZE;  // TMA row coordinate of the cache
   if (n_q % n_kv) return QUAROT_ERR_DIM;
   const int G = n_q / n_kv;
   if (head_dim != 128 || !(G == 1 || G == 2 || G == 4 || G == 8)) return QUAROT_ERR_UNSUPPORTED_SIZE;

@@ -1,6 +1,6 @@
 """One append + decode at a tab:QAttention_bench shape (ncu target).  n_q n_kv B [L]"""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch, synth
 import paper_2404_00456_b200 as q
 n_q, n_kv, B = (int(v) for v in sys.argv[1:4])
