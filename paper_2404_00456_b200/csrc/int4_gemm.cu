@@ -193,7 +193,14 @@ QR_DEVICE void mma_commit_pair(uint64_t* bar) {
 // values go to column n0 / 2, g and u the fp16 linear outputs (the FP16 model's ops, Z23).  The INT32 result is "immediately cast (and
 // scale[d]) to FP16" before any further op, so the fused epilogues equal the unfused
 // GEMM -> fp16 -> residual add / quarot_swiglu chain bit for bit.
-template <bool kS32, int kDbg, int kShift = 8>  // kShift: the x16 nibble scaling of both operands (A4W4)
+// kEpi: the epilogue variant as a compile-time choice (0 = read p.residual / p.swiglu at run time,
+// 1 = plain, 2 = + residual, 3 = SwiGLU): a specialized kernel keeps only its own code and registers
+template <int kEpi>
+QR_DEVICE bool epi_residual(const Params& p) { return kEpi == 0 ? p.residual != nullptr : kEpi == 2; }
+template <int kEpi>
+QR_DEVICE bool epi_swiglu(const Params& p) { return kEpi == 0 ? p.swiglu != 0 : kEpi == 3; }
+
+template <bool kS32, int kDbg, int kShift = 8, int kEpi = 0>  // kShift: the x16 nibble scaling of both operands (A4W4)
 QR_DEVICE void epi_chunk(const Params& p, const uint32_t (&rc)[32], int64_t m, bool row_ok, int64_t n0, float sx,
                          const float* wsc) {
   if (!row_ok) return;
@@ -205,7 +212,7 @@ QR_DEVICE void epi_chunk(const Params& p, const uint32_t (&rc)[32], int64_t m, b
         *reinterpret_cast<int4*>(dst + g * 4) =
             make_int4((int32_t)rc[4 * g] >> kShift, (int32_t)rc[4 * g + 1] >> kShift,
                       (int32_t)rc[4 * g + 2] >> kShift, (int32_t)rc[4 * g + 3] >> kShift);
-  } else if (p.swiglu) {
+  } else if (epi_swiglu<kEpi>(p)) {
 #pragma unroll
     for (int hgrp = 0; hgrp < 2; ++hgrp) {
       const int64_t nn = n0 + 16 * hgrp;
@@ -232,7 +239,7 @@ QR_DEVICE void epi_chunk(const Params& p, const uint32_t (&rc)[32], int64_t m, b
   } else {
     __half* dst = reinterpret_cast<__half*>(p.out) + m * p.ld_out + n0;
     uint4 rres0 = make_uint4(0, 0, 0, 0), rres1 = rres0, rres2 = rres0, rres3 = rres0;
-    if (p.residual) {  // all four loads in flight at once
+    if (epi_residual<kEpi>(p)) {  // all four loads in flight at once
       const __half* rrow = p.residual + m * p.ld_r + n0;
       if (n0 < p.N) rres0 = *reinterpret_cast<const uint4*>(rrow);
       if (n0 + 8 < p.N) rres1 = *reinterpret_cast<const uint4*>(rrow + 8);
@@ -252,7 +259,7 @@ QR_DEVICE void epi_chunk(const Params& p, const uint32_t (&rc)[32], int64_t m, b
         for (int e = 0; e < 4; ++e) {
           float v0 = ((float)((int32_t)rc[8 * g + 2 * e] >> kShift) * sx) * swv[2 * e];
           float v1 = ((float)((int32_t)rc[8 * g + 2 * e + 1] >> kShift) * sx) * swv[2 * e + 1];
-          if (p.residual) {  // the linear output is fp16 before the residual add
+          if (epi_residual<kEpi>(p)) {  // the linear output is fp16 before the residual add
             v0 = __half2float(__float2half_rn(v0)) + __half2float(__ushort_as_half((unsigned short)(rw[e] & 0xFFFFu)));
             v1 = __half2float(__float2half_rn(v1)) + __half2float(__ushort_as_half((unsigned short)(rw[e] >> 16)));
           }
@@ -265,7 +272,7 @@ QR_DEVICE void epi_chunk(const Params& p, const uint32_t (&rc)[32], int64_t m, b
   }
 }
 
-template <bool kS32, int kDbg = 0>  // kDbg: 0 normal; roofline probes: 1 MMA only, 2 no widening, 3 no TMA, 4 no fp16 stores
+template <bool kS32, int kDbg = 0, int kEpi = 0>  // kDbg: 0 normal; roofline probes: 1 MMA only, 2 no widening, 3 no TMA, 4 no fp16 stores
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     int4_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const Params p) {
@@ -491,7 +498,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         if (row_ok) sx = __ldg(p.x_scale + m);
         const int64_t n = (int64_t)nb * BN + et;
         ws_smem[et] = n < p.N ? __ldg(p.w_scale + n) : 0.f;
-        if (p.residual && row_ok) {
+        if (epi_residual<kEpi>(p) && row_ok) {
           const __half* rrow = p.residual + m * p.ld_r + ncol0;
           asm volatile("prefetch.global.L2 [%0];" ::"l"(rrow));
           asm volatile("prefetch.global.L2 [%0];" ::"l"(rrow + 64));
@@ -507,15 +514,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       QR_TMEM_LD32(taddr + 32u, rb);
       QR_TMEM_LD32(taddr + 64u, rc);
       tmem_ld_wait();
-      epi_chunk<kS32, kDbg>(p, ra, m, row_ok, ncol0, sx, ws_smem + chalf * 128);
+      epi_chunk<kS32, kDbg, 8, kEpi>(p, ra, m, row_ok, ncol0, sx, ws_smem + chalf * 128);
       QR_TMEM_LD32(taddr + 96u, ra);
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty_leader);
-      epi_chunk<kS32, kDbg>(p, rb, m, row_ok, ncol0 + 32, sx, ws_smem + chalf * 128 + 32);
-      epi_chunk<kS32, kDbg>(p, rc, m, row_ok, ncol0 + 64, sx, ws_smem + chalf * 128 + 64);
-      epi_chunk<kS32, kDbg>(p, ra, m, row_ok, ncol0 + 96, sx, ws_smem + chalf * 128 + 96);
+      epi_chunk<kS32, kDbg, 8, kEpi>(p, rb, m, row_ok, ncol0 + 32, sx, ws_smem + chalf * 128 + 32);
+      epi_chunk<kS32, kDbg, 8, kEpi>(p, rc, m, row_ok, ncol0 + 64, sx, ws_smem + chalf * 128 + 64);
+      epi_chunk<kS32, kDbg, 8, kEpi>(p, ra, m, row_ok, ncol0 + 96, sx, ws_smem + chalf * 128 + 96);
       if (!kS32) epi_bar_sync();  // every warp is done with ws_smem before the next tile's fill
     }
   }
@@ -1345,7 +1352,16 @@ static cudaError_t launch_gemm_impl(const uint8_t* xq, const float* xs, int64_t 
     if (e != cudaSuccess) return e;
     kern<<<2 * pairs, NUM_THREADS, SMEM_BYTES, stream>>>(ma, mb, p);
   } else {
-    int4_gemm_kernel<kS32><<<2 * pairs, NUM_THREADS, SMEM_BYTES, stream>>>(ma, mb, p);
+    const int epi = kS32 ? 0 : (swiglu ? 3 : (residual ? 2 : 1));
+    auto kern = epi == 1 ? int4_gemm_kernel<kS32, 0, 1> : epi == 2 ? int4_gemm_kernel<kS32, 0, 2>
+              : epi == 3 ? int4_gemm_kernel<kS32, 0, 3> : int4_gemm_kernel<kS32, 0, 0>;
+    static bool attr_epi[64][4] = {};
+    if (!attr_epi[dev & 63][epi]) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+      if (e != cudaSuccess) return e;
+      attr_epi[dev & 63][epi] = true;
+    }
+    kern<<<2 * pairs, NUM_THREADS, SMEM_BYTES, stream>>>(ma, mb, p);
   }
   return cudaPeekAtLastError();
 }
