@@ -272,14 +272,51 @@ QR_DEVICE void epi_chunk(const Params& p, const uint32_t (&rc)[32], int64_t m, b
   }
 }
 
+// The residual chunk from the warp's TMA-staged box (32 rows x 64 fp16, SWIZZLE_128B: 16-byte
+// chunk c of row r at r * 128 + ((c ^ (r & 7)) << 4)); half = which 32 columns of the box.
+// Same arithmetic as epi_chunk's residual path: y = fp16(fp16(acc * s_x * s_w) + r).
+QR_DEVICE void epi_chunk_res(const Params& p, const uint32_t (&rc)[32], int64_t m, bool row_ok, int64_t n0, float sx,
+                             const float* wsc, const uint8_t* box, int half) {
+  if (!row_ok) return;
+  const int r = threadIdx.x & 31;
+  const uint32_t rowb = smem_u32(box) + (uint32_t)r * 128u;
+  __half* dst = reinterpret_cast<__half*>(p.out) + m * p.ld_out + n0;
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    if (n0 + g * 8 < p.N) {
+      const uint4 rr = lds_v4(rowb + ((uint32_t)((4 * half + g) ^ (r & 7)) << 4));
+      const float4 s0 = *reinterpret_cast<const float4*>(wsc + g * 8);
+      const float4 s1 = *reinterpret_cast<const float4*>(wsc + g * 8 + 4);
+      const float swv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+      const uint32_t rw[4] = {rr.x, rr.y, rr.z, rr.w};
+      uint32_t h[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float v0 = ((float)((int32_t)rc[8 * g + 2 * e] >> 8) * sx) * swv[2 * e];
+        float v1 = ((float)((int32_t)rc[8 * g + 2 * e + 1] >> 8) * sx) * swv[2 * e + 1];
+        v0 = __half2float(__float2half_rn(v0)) + __half2float(__ushort_as_half((unsigned short)(rw[e] & 0xFFFFu)));
+        v1 = __half2float(__float2half_rn(v1)) + __half2float(__ushort_as_half((unsigned short)(rw[e] >> 16)));
+        h[e] = pack_half2(v0, v1);
+      }
+      *reinterpret_cast<uint4*>(dst + g * 8) = make_uint4(h[0], h[1], h[2], h[3]);
+    }
+  }
+}
+
 template <bool kS32, int kDbg = 0, int kEpi = 0>  // kDbg: 0 normal; roofline probes: 1 MMA only, 2 no widening, 3 no TMA, 4 no fp16 stores
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     int4_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const Params p) {
+                     const __grid_constant__ CUtensorMap tmR, const Params p) {
+  // the residual variant gives one operand stage to a per-warp residual staging area (8 x 4 KB,
+  // TMA-loaded [32 rows x 64 cols] boxes): the residual rows then reach the epilogue through the
+  // async proxy instead of 32-row uncoalesced loads on the L1 path the widening LDS/STS need
+  constexpr bool kResTma = kEpi == 2 && !kS32;
+  constexpr int kOst = kResTma ? OSTAGES - 1 : OSTAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stage_smem = smem;                                  // [SSTAGES][A 8 KB | B 8 KB]
-  uint8_t* opb_smem = smem + SSTAGES * SSTAGE_BYTES;           // [OSTAGES][16 KB]
+  uint8_t* opb_smem = smem + SSTAGES * SSTAGE_BYTES;           // [kOst][32 KB]
+  uint8_t* res_smem = opb_smem + kOst * OB_BYTES;              // kResTma: [8 warps][32 rows][128 B] SW128
   uint64_t* bars = reinterpret_cast<uint64_t*>(opb_smem + OSTAGES * OB_BYTES);
   uint64_t* st_full = bars;                          // [SSTAGES] TMA -> widen warps
   uint64_t* st_empty = st_full + SSTAGES;            // [SSTAGES] widen warps -> TMA (8 warps)
@@ -288,6 +325,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   uint64_t* t_full = op_empty + OSTAGES;             // MMA commit -> epilogue
   uint64_t* t_empty = t_full + 1;                    // epilogues of both CTAs -> leader MMA
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(t_empty + 1);
+  uint64_t* res_bar = bars + 24;                     // kResTma: [8 warps] residual box landed
   float* ws_smem = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 512);  // [BN] tile's w_scale
 
   const int warp = threadIdx.x >> 5;
@@ -301,12 +339,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&st_full[s], 1);
       mbar_init(&st_empty[s], 8);
     }
-    for (int s = 0; s < OSTAGES; ++s) {
+    for (int s = 0; s < kOst; ++s) {
       mbar_init(&op_full[s], 2 * 8);
       mbar_init(&op_empty[s], 1);
     }
     mbar_init(t_full, 1);
     mbar_init(t_empty, 2 * NUM_EPI_WARPS);
+    if (kResTma)
+      for (int w = 0; w < NUM_EPI_WARPS; ++w) mbar_init(&res_bar[w], 1);
     fence_barrier_init();
   }
   if (warp == MMA_WARP) {
@@ -317,6 +357,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   if (warp == TMA_WARP && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    if (kResTma) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmR)) : "memory");
   }
   tc_fence_before();
   cluster_sync();
@@ -359,8 +400,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           tc_fence_after();
           const uint32_t d_tmem = tmem_base + ACC_COL;
           for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
-            const int o = kMmaOnly ? 0 : it % OSTAGES;
-            if (!kMmaOnly) mbar_wait(&op_full[o], (it / OSTAGES) & 1);
+            const int o = kMmaOnly ? 0 : it % kOst;
+            if (!kMmaOnly) mbar_wait(&op_full[o], (it / kOst) & 1);
             tc_fence_after();
             const uint64_t b_desc = umma_desc_sw128(smem_u32(opb_smem + o * OB_BYTES));
             const uint32_t a_tmem = tmem_base + (uint32_t)(A_COL0 + A_COLS * o);
@@ -402,13 +443,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       const uint32_t opfull_leader = map_to_rank(&op_full[0], 0);
       for (int it = grp; it < total; it += 2) {
         const int s = it % SSTAGES;
-        const int o = it % OSTAGES;
+        const int o = it % kOst;
         mbar_wait_sleep(&st_full[s], (it / SSTAGES) & 1);
         const uint32_t src = smem_u32(stage_smem + s * SSTAGE_BYTES) + SA_BYTES + src_off;
         uint4 w[CPT_B];
   #pragma unroll
         for (int i = 0; i < CPT_B; ++i) w[i] = lds_v4(src + (uint32_t)i * (16u * BKP));
-        QR_OPWAIT(&op_empty[o], ((it / OSTAGES) & 1) ^ 1);
+        QR_OPWAIT(&op_empty[o], ((it / kOst) & 1) ^ 1);
         const uint32_t dst = smem_u32(opb_smem + o * OB_BYTES) + dst_row;
   #pragma unroll
         for (int i = 0; i < (kDbg == 2 ? 0 : CPT_B); ++i) {
@@ -437,13 +478,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       const uint32_t tlane = (uint32_t)((warp - A_WARP0) * 32) << 16;
       for (int it = 0; it < total; ++it) {
         const int s = it % SSTAGES;
-        const int o = it % OSTAGES;
+        const int o = it % kOst;
         mbar_wait_sleep(&st_full[s], (it / SSTAGES) & 1);
         const uint32_t src = smem_u32(stage_smem + s * SSTAGE_BYTES) + (uint32_t)row * BKP;
         uint4 w[CPR];
   #pragma unroll
         for (int c = 0; c < CPR; ++c) w[c] = lds_v4(src + (((uint32_t)c ^ sw) << 4));
-        QR_OPWAIT(&op_empty[o], ((it / OSTAGES) & 1) ^ 1);
+        QR_OPWAIT(&op_empty[o], ((it / kOst) & 1) ^ 1);
         tc_fence_after();
   #pragma unroll
         for (int half = 0; half < CPR / 4; ++half) {
@@ -485,6 +526,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     const int quarter = warp & 3, chalf = warp >> 2;
     const int row_in_tile = (int)rank * BMC + quarter * 32 + lane;
     const int et = threadIdx.x;  // 0..255: epilogue warps are warps 0..7
+    // kResTma: this warp's staging box and its TMA load (expect 4 KB on res_bar[warp])
+    uint8_t* res_w = res_smem + warp * 4096;
+    uint32_t res_par = 0u;
+    auto res_load = [&](int64_t col, int row) {
+      mbar_expect_tx(&res_bar[warp], 4096u);
+      tma_load_2d(smem_u32(res_w), &tmR, (int)col, row, &res_bar[warp]);
+    };
     for (int tl = 0; tl < my_tiles; ++tl) {
       int mb, nb;
       tile_coords(p, pair + tl * num_pairs, mb, nb);
@@ -498,7 +546,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         if (row_ok) sx = __ldg(p.x_scale + m);
         const int64_t n = (int64_t)nb * BN + et;
         ws_smem[et] = n < p.N ? __ldg(p.w_scale + n) : 0.f;
-        if (epi_residual<kEpi>(p) && row_ok) {
+        if (epi_residual<kEpi>(p) && !kResTma && row_ok) {
           const __half* rrow = p.residual + m * p.ld_r + ncol0;
           asm volatile("prefetch.global.L2 [%0];" ::"l"(rrow));
           asm volatile("prefetch.global.L2 [%0];" ::"l"(rrow + 64));
@@ -506,9 +554,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
         epi_bar_sync();
       }
+      if constexpr (kResTma) {  // residual box 0 (the warp's 32 rows x columns ncol0 .. +63)
+        if (lane == 0) res_load(ncol0, (int)(m - lane));
+      }
       mbar_wait_sleep(t_full, tl & 1);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + ACC_COL + (uint32_t)(chalf * 128);
+      if constexpr (kResTma) {
+        uint32_t ra[32], rb[32], rc[32];
+        const float* wsc = ws_smem + chalf * 128;
+        QR_TMEM_LD32(taddr, ra);
+        QR_TMEM_LD32(taddr + 32u, rb);
+        QR_TMEM_LD32(taddr + 64u, rc);
+        tmem_ld_wait();
+        mbar_wait(&res_bar[warp], res_par);
+        res_par ^= 1u;
+        epi_chunk_res(p, ra, m, row_ok, ncol0, sx, wsc, res_w, 0);
+        QR_TMEM_LD32(taddr + 96u, ra);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty_leader);
+        epi_chunk_res(p, rb, m, row_ok, ncol0 + 32, sx, wsc + 32, res_w, 1);
+        __syncwarp();  // every lane is done reading box 0
+        if (lane == 0) res_load(ncol0 + 64, (int)(m - lane));
+        mbar_wait(&res_bar[warp], res_par);
+        res_par ^= 1u;
+        epi_chunk_res(p, rc, m, row_ok, ncol0 + 64, sx, wsc + 64, res_w, 0);
+        epi_chunk_res(p, ra, m, row_ok, ncol0 + 96, sx, wsc + 96, res_w, 1);
+        __syncwarp();  // box 1 read by every lane before the next tile's box 0 lands
+        epi_bar_sync();
+        continue;
+      }
       uint32_t ra[32], rb[32], rc[32];
       QR_TMEM_LD32(taddr, ra);
       QR_TMEM_LD32(taddr + 32u, rb);
@@ -1292,6 +1369,21 @@ bool make_packed_map(CUtensorMap* map, const uint8_t* base, int64_t rows, int64_
   return r == CUDA_SUCCESS;
 }
 
+// residual fp16 [rows][ld] as a 2-D map, box 64 columns (128 B) x 32 rows, SWIZZLE_128B (the
+// residual epilogue's per-warp staging box); OOB rows / columns are zero-filled
+bool make_res_map(CUtensorMap* map, const __half* base, int64_t rows, int64_t cols, int64_t ld) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {64u, 32u};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 }  // namespace
 
 int g_gemm_debug_mode = 0;
@@ -1312,9 +1404,14 @@ static cudaError_t launch_gemm_impl(const uint8_t* xq, const float* xs, int64_t 
     if (e != cudaSuccess) return e;
     attr_set[dev & 63] = true;
   }
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, mr;
   if (!make_packed_map(&ma, xq, M, K / 2, ld_xq) || !make_packed_map(&mb, wq, N, K / 2, ld_wq))
     return cudaErrorInvalidValue;
+  if (residual && !kS32) {
+    if (!make_res_map(&mr, static_cast<const __half*>(residual), M, N, ld_r)) return cudaErrorInvalidValue;
+  } else {
+    mr = mb;  // unused
+  }
   Params p;
   p.x_scale = xs;
   p.w_scale = ws;
@@ -1350,7 +1447,7 @@ static cudaError_t launch_gemm_impl(const uint8_t* xq, const float* xs, int64_t 
                                          : int4_gemm_kernel<kS32, 4>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    kern<<<2 * pairs, NUM_THREADS, SMEM_BYTES, stream>>>(ma, mb, p);
+    kern<<<2 * pairs, NUM_THREADS, SMEM_BYTES, stream>>>(ma, mb, mr, p);
   } else {
     const int epi = kS32 ? 0 : (swiglu ? 3 : (residual ? 2 : 1));
     auto kern = epi == 1 ? int4_gemm_kernel<kS32, 0, 1> : epi == 2 ? int4_gemm_kernel<kS32, 0, 2>
@@ -1361,7 +1458,7 @@ static cudaError_t launch_gemm_impl(const uint8_t* xq, const float* xs, int64_t 
       if (e != cudaSuccess) return e;
       attr_epi[dev & 63][epi] = true;
     }
-    kern<<<2 * pairs, NUM_THREADS, SMEM_BYTES, stream>>>(ma, mb, p);
+    kern<<<2 * pairs, NUM_THREADS, SMEM_BYTES, stream>>>(ma, mb, mr, p);
   }
   return cudaPeekAtLastError();
 }

@@ -1,0 +1,31 @@
+"""GEMM roofline probes at the 70B QKV / O shapes (131072 tokens): mode 0 normal, 4 = no fp16
+stores (the epilogue still converts), 1 = MMA issue only.  Isolates the epilogue's store cost."""
+import ctypes, os, sys
+sys.path.insert(0, os.getcwd())
+import torch, synth
+import paper_2404_00456_b200 as q
+lib = q.lib()
+lib.quarot_debug_gemm_mode.argtypes = [ctypes.c_int]
+M = 131072
+def timeit(fn, iters=10):
+    for _ in range(3): fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(iters): fn()
+    b.record(); torch.cuda.synchronize()
+    return a.elapsed_time(b) / iters
+xq = synth.packed_weight_codes(M, 8192, 1, "cuda")
+for name, N in (("qkv", 10240), ("o", 8192)):
+    wq = synth.packed_weight_codes(N, 8192, 2, "cuda")
+    xs = torch.rand(M, device="cuda") + 0.5
+    ws = synth.weight_scales(N, 3, "cuda")
+    y = torch.empty(M, N, dtype=torch.float16, device="cuda")
+    r = torch.randn(M, N, device="cuda").half()
+    for mode in (0, 4, 1, 0):
+        lib.quarot_debug_gemm_mode(mode)
+        for res in (None, r):
+            ms = timeit(lambda: q.int4_linear(xq, xs, wq, ws, y=y, residual=res))
+            print(name, "mode", mode, "resid" if res is not None else "plain", round(ms, 3), "ms",
+                  round(2 * M * N * 8192 / ms / 1e9), "TOPS", flush=True)
+    lib.quarot_debug_gemm_mode(0)

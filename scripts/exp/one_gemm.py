@@ -1,6 +1,6 @@
 """Run one INT4 linear of a given shape a few times (ncu target).  M N K [reps]"""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch, synth
 import paper_2404_00456_b200 as q
 M, N, K = (int(v) for v in sys.argv[1:4])

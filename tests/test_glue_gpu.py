@@ -52,6 +52,24 @@ def test_linear_residual(q):
     assert torch.equal(y, y2)
 
 
+@pytest.mark.parametrize("M,N,K", [(300, 520, 4096), (1100, 776, 8192), (2085, 4120, 2048)])
+def test_linear_residual_tma_staging_repeated(q, M, N, K):
+    """The residual epilogue stages each warp's [32 rows x 64 cols] residual box through TMA
+    (DESIGN §5.2): ragged M / N, several tiles per CTA pair, separate and in-place residual,
+    repeated launches — bitwise equal to the unfused GEMM -> fp16 -> add chain every time."""
+    xq = synth.packed_weight_codes(M, K, 5, DEV)
+    wq = synth.packed_weight_codes(N, K, 6, DEV)
+    xs = torch.rand(M, device=DEV) * 0.01 + 0.001
+    ws = synth.weight_scales(N, 7, DEV)
+    r = synth.activations(M, N, "normal", 8, DEV)
+    ref = q.int4_linear(xq, xs, wq, ws) + r
+    for _ in range(5):
+        assert torch.equal(q.int4_linear(xq, xs, wq, ws, residual=r), ref)
+        y2 = r.clone()
+        q.int4_linear(xq, xs, wq, ws, y=y2, residual=y2)
+        assert torch.equal(y2, ref)
+
+
 @pytest.mark.parametrize("T,n,d,pos0", [(37, 9, 128, 0), (5, 3, 64, 2040), (4100, 2, 128, 0)])
 def test_rope(q, T, n, d, pos0):
     x = synth.activations(T, n * d + 64, "normal", seed=T, device=DEV)
