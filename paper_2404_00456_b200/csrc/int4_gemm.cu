@@ -57,6 +57,9 @@ constexpr int KATOMS = BK / 128;   // 128-byte K-major swizzle atoms per widened
 #ifndef QR_OPWAIT
 #define QR_OPWAIT mbar_wait_sleep
 #endif
+#ifndef QR_EPIWAIT  // the epilogue's wait for a finished accumulator (experiments: mbar_wait, mbar_wait_backoff<32>)
+#define QR_EPIWAIT mbar_wait_sleep
+#endif
 constexpr int SSTAGES = QR_GEMM_SSTAGES;  // packed staging ring (TMA destination)
 // the two B-widen groups take alternate k-blocks: with an even ring each staging slot is always
 // read by the same group, so no waiter can run two phases ahead of a slot (parity aliasing)
@@ -557,7 +560,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       if constexpr (kResTma) {  // residual box 0 (the warp's 32 rows x columns ncol0 .. +63)
         if (lane == 0) res_load(ncol0, (int)(m - lane));
       }
-      mbar_wait_sleep(t_full, tl & 1);
+      QR_EPIWAIT(t_full, tl & 1);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + ACC_COL + (uint32_t)(chalf * 128);
       if constexpr (kResTma) {
