@@ -427,6 +427,7 @@ def main():
     ap.add_argument("--no-verify", action="store_true", help="N > 1: skip the NCCL gather + bitwise check")
     ap.add_argument("--no-peak-probe", action="store_true", help="skip the in-process INT8 peak measurement")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-chunks", type=int, default=16, help="token chunks of the host pipeline (H2D / compute / D2H overlap)")
     ap.add_argument("--profile-steps", type=int, default=0, help="run N untimed steps and exit (ncu)")
     ap.add_argument("--step", default="chain", choices=["chain", "linears"],
                     help="chain: the decoder-layer chain (a1-a8, 9 launches); linears: a1-a7 on independent inputs")
@@ -573,7 +574,7 @@ def main():
             host_in = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in inputs.items()}
             for k in inputs:
                 host_in[k].copy_(inputs[k])
-            pipe = HostPipeline(step, host_in, chunks=8)
+            pipe = HostPipeline(step, host_in, chunks=args.e2e_chunks)
             pipe.run()
             torch.cuda.synchronize()
             barrier()
@@ -587,7 +588,7 @@ def main():
             e_ms = qd.max_over_ranks(e_ms, dev)
             line["e2e"] = {"value": job_tokens / (e_ms * 1e-3), "unit": UNIT,
                            "h2d_bytes_per_step": pipe.h2d_bytes(), "d2h_bytes_per_step": pipe.d2h_bytes(),
-                           "ms_per_step": e_ms, "chunks": 8, "steps": args.e2e_steps}
+                           "ms_per_step": e_ms, "chunks": args.e2e_chunks, "steps": args.e2e_steps}
             del pipe, host_in
         except Exception as exc:  # noqa: BLE001
             line["e2e"] = {"value": None, "unit": UNIT, "error": repr(exc)[:200]}
