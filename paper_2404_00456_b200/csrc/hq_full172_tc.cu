@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         float am[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int c = 0; c < 32; ++c) {  // a bit 0: within the register pair
-          v[c] = pair_bfly(v[c]);
+          v[c] = pair_bfly_bc(v[c]);
           am[c & 3] = fmax_nan(am[c & 3], fmax_nan(fabsf(v[c].x), fabsf(v[c].y)));
         }
         amax = lane_ok ? fmax_nan(fmax_nan(am[0], am[1]), fmax_nan(am[2], am[3])) : 0.f;

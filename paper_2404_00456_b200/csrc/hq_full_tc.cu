@@ -512,6 +512,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int64_t nrows = M > (int64_t)blockIdx.x ? (M - 1 - (int64_t)blockIdx.x) / gridDim.x + 1 : 0;
 
   if (warp < EPI_WARP0) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");  // 128 x 64 + 512 x 104 = 640 x 96
     if (warp == TMA_WARP) {
       if (lane == 0) {
         for (int64_t it = 0; it < nrows; ++it) {
@@ -554,6 +555,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 104;");
     const int e = warp - EPI_WARP0;   // 0..15
     const int b = e >> 3;             // row buffer (rows it % 2 == b)
     const int g = (e >> 2) & 1;       // half of the row this warp's pass A / quant own

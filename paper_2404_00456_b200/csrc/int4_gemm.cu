@@ -1029,6 +1029,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(i8::NUM_THREADS, 1)
 //    (|256 acc_g| <= 256 * 49 * 256 < 2^22): one packed subtract recovers 256 acc_g exactly, one
 //    packed multiply forms s_x s_w / 256 and one packed FMA folds the group into the fp32 sums —
 //    1.5 issue slots per output element per group; the epilogue then rewrites the bias.
+#ifndef QR_GQ_ABL  // timing ablations (scripts/exp/abbench_group.py); 0 = the product kernel
+#define QR_GQ_ABL 0
+#endif
+#ifndef QR_GQ_TWAIT  // the MMA warp's wait for a drained accumulator buffer
+#define QR_GQ_TWAIT mbar_wait_sleep
+#endif
+#ifndef QR_GQ_EWAIT  // the epilogue's wait for a finished group
+#define QR_GQ_EWAIT mbar_wait_sleep
+#endif
+#ifndef QR_GQ_OWAIT  // the MMA warp's wait for a widened operand stage
+#define QR_GQ_OWAIT mbar_wait_sleep
+#endif
 namespace gq4 {
 constexpr int SSTAGES = 2, OSTAGES = 2;
 constexpr int SSTAGE_BYTES = SA_BYTES + SB_BYTES;  // 32 KB packed
@@ -1142,14 +1154,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gq4::NUM_THREADS, 1)
         for (int tl = 0; tl < my_tiles; ++tl) {
           for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
             const int o = it % gq4::OSTAGES;
-            mbar_wait_sleep(&op_full[o], (it / gq4::OSTAGES) & 1);
+            QR_GQ_OWAIT(&op_full[o], (it / gq4::OSTAGES) & 1);
             tc_fence_after();
             const uint32_t base = smem_u32(op_smem + o * gq4::OSTAGE_BYTES);
             const uint64_t a_desc = umma_desc_sw128(base), b_desc = umma_desc_sw128(base + gq4::OA_BYTES);
 #pragma unroll
             for (int hg = 0; hg < GPK; ++hg, ++gc) {
               const int ab = gc & 1;
-              mbar_wait_sleep(&t_empty[ab], ((gc >> 1) & 1) ^ 1);
+              QR_GQ_TWAIT(&t_empty[ab], ((gc >> 1) & 1) ^ 1);
               tc_fence_after();
               const uint32_t d_tmem = tmem_base + (uint32_t)(ab * BN);
 #pragma unroll
@@ -1196,7 +1208,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gq4::NUM_THREADS, 1)
         const uint32_t src = smem_u32(stage_smem + s * gq4::SSTAGE_BYTES) + (opnd ? SA_BYTES : 0);
         const uint32_t dst = smem_u32(op_smem + o * gq4::OSTAGE_BYTES) + (opnd ? gq4::OA_BYTES : 0);
 #pragma unroll 1
-        for (int i0 = 0; i0 < 16; i0 += 2) {  // row octets i0, i0 + 1 (two rows per lane each)
+        for (int i0 = 0; i0 < ((QR_GQ_ABL & 4) ? 0 : 16); i0 += 2) {  // row octets i0, i0 + 1 (two rows per lane each)
           uint4 w[2][2];
 #pragma unroll
           for (int i = 0; i < 2; ++i)
@@ -1259,7 +1271,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gq4::NUM_THREADS, 1)
           sx_next = row_ok ? __ldg(p.x_scale + m * p.ld_sx + g + 1) : 0.f;
         }
         __syncwarp();
-        mbar_wait_sleep(&t_full[ab], (gc >> 1) & 1);  // sleeping, not spinning: the widen warps share these schedulers
+        QR_GQ_EWAIT(&t_full[ab], (gc >> 1) & 1);  // sleeping, not spinning: the widen warps share these schedulers
         tc_fence_after();
         const uint32_t taddr =
             tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(ab * BN) + (uint32_t)(chalf * 128);
@@ -1282,12 +1294,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gq4::NUM_THREADS, 1)
         for (int cc = 0; cc < 8; ++cc) {
           uint32_t(&cur)[16] = rc[cc & 1];
           const float4(&w)[4] = wsc[cc & 1];
-          QR_TMEM_ST8(taddr + 16u * cc, bias8);  // the next group of this buffer starts at the bias
-          QR_TMEM_ST8(taddr + 16u * cc + 8u, bias8);
+          if (!(QR_GQ_ABL & 2)) {
+            QR_TMEM_ST8(taddr + 16u * cc, bias8);  // the next group of this buffer starts at the bias
+            QR_TMEM_ST8(taddr + 16u * cc + 8u, bias8);
+          }
           if (cc + 1 < 8) {
             QR_TMEM_LD16(taddr + 16u * (cc + 1), rc[(cc + 1) & 1]);
-            ld_wsc(cc + 1, wsc[(cc + 1) & 1]);
+            if (!(QR_GQ_ABL & 8)) ld_wsc(cc + 1, wsc[(cc + 1) & 1]);
           }
+          if (QR_GQ_ABL & 1) {
+#pragma unroll
+            for (int c = 0; c < 16; ++c) acc[(16 * cc + c) >> 1].x += __uint_as_float(cur[c]);
+          } else
 #pragma unroll
           for (int c = 0; c < 16; c += 4) {
             const float4 w4 = w[c >> 2];
