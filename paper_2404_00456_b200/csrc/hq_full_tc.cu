@@ -108,13 +108,17 @@ QR_DEVICE void bfly(float2& u, float2& v) {
 // 4 codes (low nibble of each byte; the byte is the two's-complement code) of a.x, a.y, b.x, b.y:
 // RNE by the 1.5 * 2^23 magic add (|v * inv| <= 7 / 0.9 < 2^22), whose low 16 bits are the
 // integer; clamp to [-7, 7] on two 16-bit lanes at a time (VIMNMX), then gather the low bytes.
+// kClamp = false: the caller guarantees |v * inv| < 7.5 for every lane (RNE then lands in [-7, 7])
+template <bool kClamp = true>
 QR_DEVICE uint32_t code_word(float2 a, float2 b, float inv) {
   const float2 i2 = make_float2(inv, inv), mg = make_float2(12582912.f, 12582912.f);
   const float2 ma = f2add(f2mul(a, i2), mg), mb = f2add(f2mul(b, i2), mg);
   uint32_t lo = __byte_perm(__float_as_uint(ma.x), __float_as_uint(ma.y), 0x5410);
   uint32_t hi = __byte_perm(__float_as_uint(mb.x), __float_as_uint(mb.y), 0x5410);
-  lo = __vmaxs2(__vmins2(lo, 0x00070007u), 0xFFF9FFF9u);
-  hi = __vmaxs2(__vmins2(hi, 0x00070007u), 0xFFF9FFF9u);
+  if constexpr (kClamp) {
+    lo = __vmaxs2(__vmins2(lo, 0x00070007u), 0xFFF9FFF9u);
+    hi = __vmaxs2(__vmins2(hi, 0x00070007u), 0xFFF9FFF9u);
+  }
   return __byte_perm(lo, hi, 0x6420);
 }
 
@@ -470,6 +474,23 @@ QR_DEVICE uint32_t code_word8(float2 a, float2 b, float2 c, float2 d, float inv)
   return __byte_perm(w0, w1, 0x6420);
 }
 
+// code_word8 without the clamp, for threads none of whose elements can reach |v * inv| >= 7.5
+// (then RNE already lands in [-7, 7]): the low byte of each magic-added float is its
+// two's-complement code; gather the even / odd codes' low bytes (3 PRMT each) and merge the
+// nibbles with one shift and one bit-select LOP3 — 8 ALU instructions per 8 codes instead of 17.
+QR_DEVICE uint32_t code_word8_nc(float2 a, float2 b, float2 c, float2 d, float inv) {
+  const float2 i2 = make_float2(inv, inv), mg = make_float2(12582912.f, 12582912.f);
+  const float2 ma = f2fma(a, i2, mg), mb = f2fma(b, i2, mg), mc = f2fma(c, i2, mg), md = f2fma(d, i2, mg);
+  const uint32_t e = __byte_perm(__byte_perm(__float_as_uint(ma.x), __float_as_uint(mb.x), 0x0040),
+                                 __byte_perm(__float_as_uint(mc.x), __float_as_uint(md.x), 0x0040), 0x5410);
+  const uint32_t o = __byte_perm(__byte_perm(__float_as_uint(ma.y), __float_as_uint(mb.y), 0x0040),
+                                 __byte_perm(__float_as_uint(mc.y), __float_as_uint(md.y), 0x0040), 0x5410);
+  const uint32_t os = o << 4;
+  uint32_t w;  // (e & 0x0F0F0F0F) | (os & 0xF0F0F0F0): LUT 0xE4 = c ? a : b over (a = e, b = os, c = mask)
+  asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(w) : "r"(e), "r"(os), "r"(0x0F0F0F0Fu));
+  return w;
+}
+
 template <bool kPerm>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     hq_full28_wg_kernel(const __grid_constant__ CUtensorMap tmX, int64_t M, float clip, uint8_t* __restrict__ q,
@@ -495,7 +516,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int i = 0; i < 8; ++i) {
       mbar_init(&t_full[i], 1);
-      mbar_init(&t_empty[i], 4);
+      mbar_init(&t_empty[i], 8);  // the 4 lane-quarter warps of both halves
     }
     fence_barrier_init();
   }
@@ -565,22 +586,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const bool lane_ok = L < J;
     const bool odd = (lane & 1) != 0;
     const uint32_t t_lane = tmem_base + ((uint32_t)(qd * 32) << 16) + (uint32_t)(b * NA);
-    const uint32_t t_half = t_lane + (uint32_t)(g * NH);
     const int bar_lanes = 1 + 4 * b + qd, bar_row = 9 + b;  // named barriers (0 = __syncthreads)
     const float norm_f = (float)rsqrt((double)K);
     const float c0 = (float)((double)clip * rsqrt((double)K) / 7.0);  // scale = c0 * amax
     for (int64_t it = b; it < nrows; it += 2) {
       const uint32_t par = (uint32_t)((it >> 1) & 1);
       const int64_t row = (int64_t)blockIdx.x + it * gridDim.x;
-      // ---- pass A: this warp's half, one 64-column quarter at a time (as soon as its MMA landed),
+      // ---- pass A: quarters g and g + 2 (64 columns each, as soon as its MMA landed),
       //      bits 0-5 (pair i = columns 2i, 2i+1)
 #pragma unroll 1
       for (int k = 0; k < 2; ++k) {
-        mbar_wait(&t_full[4 * b + 2 * g + k], par);
+        const int qh = 2 * k + g;
+        mbar_wait(&t_full[4 * b + qh], par);
         tc_fence_after();
         uint32_t r[2][32];
-        QR_TMEM_LD32(t_half + 64u * k, r[0]);
-        QR_TMEM_LD32(t_half + 64u * k + 32u, r[1]);
+        QR_TMEM_LD32(t_lane + 64u * qh, r[0]);
+        QR_TMEM_LD32(t_lane + 64u * qh + 32u, r[1]);
         tmem_ld_wait();
         float2 P[32];
 #pragma unroll
@@ -597,8 +618,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           r[i >> 4][2 * (i & 15)] = __float_as_uint(P[i].x);
           r[i >> 4][2 * (i & 15) + 1] = __float_as_uint(P[i].y);
         }
-        QR_TMEM_ST32(t_half + 64u * k, r[0]);
-        QR_TMEM_ST32(t_half + 64u * k + 32u, r[1]);
+        QR_TMEM_ST32(t_lane + 64u * qh, r[0]);
+        QR_TMEM_ST32(t_lane + 64u * qh + 32u, r[1]);
       }
       hqtc::tmem_st_wait();
       tc_fence_before();
@@ -606,9 +627,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc_fence_after();
       // ---- pass B: bits 6, 7 over (c, c + 64, c + 128, c + 192), c in [32 g, 32 g + 32); amax
       float am = 0.f;
-#pragma unroll 1
-      for (int k = 0; k < 4; ++k) {
-        const uint32_t tc0 = t_lane + (uint32_t)(32 * g + 8 * k);
+      const uint32_t tB = t_lane + (uint32_t)(32 * g);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {  // unrolled: TMEM addresses are immediate offsets
+        const uint32_t tc0 = tB + (uint32_t)(8 * k);
         uint32_t u[4][8];
 #pragma unroll
         for (int i = 0; i < 4; ++i) QR_TMEM_LD8(tc0 + 64u * i, u[i]);
@@ -652,44 +674,57 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         inv = __fdiv_rn(norm_f, sc);
       }
       if (w8 == 0 && lane == 0) scale[row] = sc;
-      const bool zero = inv == 0.f;  // zero / non-finite row: all codes 0
+      const bool zero = !isfinite(amax);  // non-finite row: all codes 0 (a zero row has inv = 0: codes 0)
+      // am covers exactly the elements this thread quantizes below: if no lane of the warp can
+      // reach |v * inv| >= 7.5 (fp32 rounding is monotone and 7.5 is exact), RNE lands in
+      // [-7, 7] and the clamp is skipped (with clip 0.9 only the ~1-2 lanes of a row holding
+      // elements above 0.964 amax take the clamping path)
+      const bool clamp = __any_sync(0xffffffffu, am * inv >= 7.5f);
       uint8_t* const qrow = q + row * ld_q;
-      // ---- quant: this warp's half, 32 columns (a_hi = 128 g + 32 ch + r) at a time
-#pragma unroll 1
+      // KPERM: chunk cc of lane L at byte (cc * J * 32 + L * 32) / 2; cc = g + 2 ch
+      uint8_t* const qk = qrow + (int64_t)(g * J * 16 + L * 16);
+      // ---- quant: the columns pass B produced, 32 columns (chunk cc = g + 2 ch: a_hi = 32 cc + r)
+      //      at a time; each loaded chunk releases quarter ch of this warp's lanes to the MMA of row
+      //      it + 2 (8 arrivals: both halves of the 4 lane quarters)
+#pragma unroll
       for (int ch = 0; ch < 4; ++ch) {
+        const int cc = g + 2 * ch;
         uint32_t r[32];
-        QR_TMEM_LD32(t_half + 32u * ch, r);
+        QR_TMEM_LD32(t_lane + 32u * cc, r);
         tmem_ld_wait();
-        if (ch & 1) {  // quarter 2 g + ch / 2 fully loaded: release it to the MMA of row it + 2
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&t_empty[4 * b + 2 * g + (ch >> 1)]);
-        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&t_empty[4 * b + ch]);
         float2 V[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) V[i] = make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
         if constexpr (kPerm) {
           uint32_t w[4];
+          if (clamp) {
 #pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            w[t] = code_word8(V[4 * t], V[4 * t + 1], V[4 * t + 2], V[4 * t + 3], inv);
-            if (zero) w[t] = 0u;
+            for (int t = 0; t < 4; ++t) w[t] = code_word8(V[4 * t], V[4 * t + 1], V[4 * t + 2], V[4 * t + 3], inv);
+          } else {
+#pragma unroll
+            for (int t = 0; t < 4; ++t) w[t] = code_word8_nc(V[4 * t], V[4 * t + 1], V[4 * t + 2], V[4 * t + 3], inv);
           }
-          if (lane_ok) {
-            const int64_t byte = ((int64_t)(4 * g + ch) * (J * 32) + (int64_t)L * 32) >> 1;
-            *reinterpret_cast<uint4*>(qrow + byte) = make_uint4(w[0], w[1], w[2], w[3]);
-          }
+          if (zero) w[0] = w[1] = w[2] = w[3] = 0u;
+          if (lane_ok) *reinterpret_cast<uint4*>(qk + (int64_t)ch * (J * 32)) = make_uint4(w[0], w[1], w[2], w[3]);
         } else {
           // natural order: element (a_hi, j') at a_hi * 112 + j'; the byte of j' = 2p, 2p + 1 at
           // a_hi * 56 + p — even lanes keep words 0..3 (a_hi + 0..15), odd lanes 4..7 (+16..31)
           uint32_t w[8];
+          if (clamp) {
 #pragma unroll
-          for (int m = 0; m < 8; ++m) {
-            w[m] = hqtc::code_word(V[2 * m], V[2 * m + 1], inv);
-            if (zero) w[m] = 0u;
+            for (int m = 0; m < 8; ++m) w[m] = hqtc::code_word<true>(V[2 * m], V[2 * m + 1], inv);
+          } else {
+#pragma unroll
+            for (int m = 0; m < 8; ++m) w[m] = hqtc::code_word<false>(V[2 * m], V[2 * m + 1], inv);
           }
+#pragma unroll
+          for (int m = 0; m < 8; ++m)
+            if (zero) w[m] = 0u;
           const uint32_t keep_mask = odd ? 0xF0F0F0F0u : 0x0F0F0F0Fu;
-          uint8_t* const qb = qrow + (L >> 1) + (int64_t)(NH * g + 32 * ch + (odd ? 16 : 0)) * (J / 2);
+          uint8_t* const qb = qrow + (L >> 1) + (int64_t)(32 * cc + (odd ? 16 : 0)) * (J / 2);
 #pragma unroll
           for (int mm = 0; mm < 4; ++mm) {
             const uint32_t got = __shfl_xor_sync(0xffffffffu, odd ? w[mm] : w[mm + 4], 1);

@@ -39,8 +39,8 @@ def timeit(fn, iters=20):
 
 
 def run(name):
-    if name == "kperm":
-        lib.quarot_debug_hq_full_variant(0)
+    if name.startswith("kperm"):  # kperm[N]: variant N writing the transform-native order
+        lib.quarot_debug_hq_full_variant(int(name[5:] or 0))
         return lambda: q.hadamard_quant(x, "full", q=xq, scale=xs, kperm=True)
     lib.quarot_debug_hq_full_variant(int(name))
     return lambda: q.hadamard_quant(x, "full", q=xq, scale=xs)
