@@ -449,6 +449,12 @@ constexpr uint32_t TMEM_COLS = 512;
 #ifndef QR_WG_BACKOFF
 #define QR_WG_BACKOFF 64  // ns between the MMA warps' barrier polls (the next row's MMA is latency-critical)
 #endif
+#ifndef QR_WG_TMA_IN_MMA
+#define QR_WG_TMA_IN_MMA 1  // the MMA warps reload the stage their row freed (no polling TMA warp)
+#endif
+#ifndef QR_WG_MMA_SLEEP
+#define QR_WG_MMA_SLEEP 0  // 1: the MMA warps wait with try_wait's suspend hint instead of back-off polls
+#endif
 #ifndef QR_WG_TMA_BACKOFF
 #define QR_WG_TMA_BACKOFF 512  // ns between the TMA warp's polls (three stages of slack)
 #endif
@@ -534,19 +540,33 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   if (warp < EPI_WARP0) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");  // 128 x 64 + 512 x 104 = 640 x 96
+    auto issue_tma = [&](int64_t it) {  // local row it into stage it % STAGES (one thread)
+      const int s = (int)(it % STAGES);
+      hqtc::expect_tx(&full[s], STAGE_BYTES);
+      const int row = (int)((int64_t)blockIdx.x + it * gridDim.x);
+      const uint32_t dst = smem_u32(sB + s * STAGE_BYTES);
+      hqtc::tma_load_3d(dst, &tmX, 0, 0, row, &full[s]);
+      hqtc::tma_load_3d(dst + BOX_BYTES, &tmX, 64, 0, row, &full[s]);
+    };
+#if QR_WG_TMA_IN_MMA
+    // the MMA warps issue the TMA: after row it's last quarter the warp waits for its MMAs to
+    // complete (a few hundred cycles) and reloads the freed stage with row it + STAGES (a separate
+    // TMA warp polled the stage's mbarrier ~130 times per row: NANOSLEEP wakes early)
+    if (warp == TMA_WARP) {
+      if (lane == 0)
+        for (int64_t it = 0; it < nrows && it < STAGES; ++it) issue_tma(it);
+    } else
+#else
     if (warp == TMA_WARP) {
       if (lane == 0) {
         for (int64_t it = 0; it < nrows; ++it) {
-          const int s = (int)(it % STAGES);
-          mbar_wait_backoff<QR_WG_TMA_BACKOFF>(&empty[s], (uint32_t)((it / STAGES) & 1) ^ 1u);
-          hqtc::expect_tx(&full[s], STAGE_BYTES);
-          const int row = (int)((int64_t)blockIdx.x + it * gridDim.x);
-          const uint32_t dst = smem_u32(sB + s * STAGE_BYTES);
-          hqtc::tma_load_3d(dst, &tmX, 0, 0, row, &full[s]);
-          hqtc::tma_load_3d(dst + BOX_BYTES, &tmX, 64, 0, row, &full[s]);
+          mbar_wait_backoff<QR_WG_TMA_BACKOFF>(&empty[it % STAGES], (uint32_t)((it / STAGES) & 1) ^ 1u);
+          issue_tma(it);
         }
       }
-    } else if (warp < MMA_WARP0 + 2) {
+    } else
+#endif
+    if (warp < MMA_WARP0 + 2) {
       // MMA warp b issues the rows of buffer b (it % 2 == b)
       const int b = warp - MMA_WARP0;
       const uint64_t a_desc = umma_desc_sw128(smem_u32(sA));
@@ -557,7 +577,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         mbar_wait_backoff<QR_WG_BACKOFF>(&full[s], (uint32_t)((it / STAGES) & 1));
 #pragma unroll 1
         for (int h = 0; h < 4; ++h) {  // quarter h: a_hi 64 h .. 64 h + 63 (N = 64)
+#if QR_WG_MMA_SLEEP
+          mbar_wait_sleep(&t_empty[4 * b + h], n_par ^ 1u);
+#else
           mbar_wait_backoff<QR_WG_BACKOFF>(&t_empty[4 * b + h], n_par ^ 1u);
+#endif
           tc_fence_after();
           const uint64_t b_desc = umma_desc_sw128(sb + (uint32_t)(s * STAGE_BYTES + h * (NQ * 128)));
           const uint32_t d_tmem = tmem_base + (uint32_t)(b * NA + h * NQ);
@@ -573,6 +597,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           __syncwarp();
         }
+#if QR_WG_TMA_IN_MMA
+        if (it + STAGES < nrows) {
+          mbar_wait_backoff<32>(&empty[s], (uint32_t)((it / STAGES) & 1));
+          if (lane == 0) issue_tma(it + STAGES);
+          __syncwarp();
+        }
+#endif
       }
     }
   } else {

@@ -306,7 +306,8 @@ QR_DEVICE void epi_chunk_res(const Params& p, const uint32_t (&rc)[32], int64_t 
   }
 }
 
-template <bool kS32, int kDbg = 0, int kEpi = 0>  // kDbg: 0 normal; roofline probes: 1 MMA only, 2 no widening, 3 no TMA, 4 no fp16 stores
+template <bool kS32, int kDbg = 0, int kEpi = 0>  // kDbg: 0 normal; roofline probes: 1 MMA only, 2 no widening, 3 no TMA, 4 no fp16 stores,
+                                                   // 5 no B widening stores, 6 no A TMEM stores, 7 no epilogue work
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     int4_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmR, const Params p) {
@@ -455,7 +456,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         QR_OPWAIT(&op_empty[o], ((it / kOst) & 1) ^ 1);
         const uint32_t dst = smem_u32(opb_smem + o * OB_BYTES) + dst_row;
   #pragma unroll
-        for (int i = 0; i < (kDbg == 2 ? 0 : CPT_B); ++i) {
+        for (int i = 0; i < (kDbg == 2 || kDbg == 5 ? 0 : CPT_B); ++i) {
           const uint4 v = w[i];
           sts_v4(dst + (uint32_t)i * 2048u + d0,
                  make_uint4((v.x << sh0) & 0xF0F0F0F0u, (v.y << sh0) & 0xF0F0F0F0u, (v.z << sh0) & 0xF0F0F0F0u,
@@ -504,14 +505,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             r[8 * cc + 6] = hi_nib16(v.z);
             r[8 * cc + 7] = hi_nib16(v.w);
           }
-          if (kDbg != 2) QR_TMEM_ST32(tmem_base + tlane + (uint32_t)(A_COL0 + A_COLS * o + 32 * half), r);
+          if (kDbg != 2 && kDbg != 6) QR_TMEM_ST32(tmem_base + tlane + (uint32_t)(A_COL0 + A_COLS * o + 32 * half), r);
         }
         // the staging slot is released only once every lane has consumed its loads (the stores
         // above read the registers): an arrive does not wait for in-flight LDS, so releasing
         // right after issuing them lets the next TMA write overtake the reads
         __syncwarp();
         if (lane == 0) mbar_arrive(&st_empty[s]);
-        if (kDbg != 2) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        if (kDbg != 2 && kDbg != 6) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(opfull_leader + (uint32_t)o * 8u);
@@ -587,6 +588,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         epi_chunk_res(p, ra, m, row_ok, ncol0 + 96, sx, wsc + 96, res_w, 1);
         __syncwarp();  // box 1 read by every lane before the next tile's box 0 lands
         epi_bar_sync();
+        continue;
+      }
+      if constexpr (kDbg == 7) {  // probe: hand the accumulator straight back
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty_leader);
+        if (!kS32) epi_bar_sync();
         continue;
       }
       uint32_t ra[32], rb[32], rc[32];
@@ -1461,11 +1469,14 @@ static cudaError_t launch_gemm_impl(const uint8_t* xq, const float* xs, int64_t 
   }
   const int max_pairs = num_sms_current() / 2;
   const int pairs = p.num_tiles < max_pairs ? p.num_tiles : max_pairs;
-  if (g_gemm_debug_mode >= 1 && g_gemm_debug_mode <= 4) {
+  if (g_gemm_debug_mode >= 1 && g_gemm_debug_mode <= 7) {
     auto kern = g_gemm_debug_mode == 1   ? int4_gemm_kernel<kS32, 1>
                 : g_gemm_debug_mode == 2 ? int4_gemm_kernel<kS32, 2>
                 : g_gemm_debug_mode == 3 ? int4_gemm_kernel<kS32, 3>
-                                         : int4_gemm_kernel<kS32, 4>;
+                : g_gemm_debug_mode == 4 ? int4_gemm_kernel<kS32, 4>
+                : g_gemm_debug_mode == 5 ? int4_gemm_kernel<kS32, 5>
+                : g_gemm_debug_mode == 6 ? int4_gemm_kernel<kS32, 6>
+                                         : int4_gemm_kernel<kS32, 7>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
     if (e != cudaSuccess) return e;
     kern<<<2 * pairs, NUM_THREADS, SMEM_BYTES, stream>>>(ma, mb, mr, p);
