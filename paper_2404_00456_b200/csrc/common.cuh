@@ -65,6 +65,13 @@ QR_DEVICE void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// silu(g) = g / (1 + e^-g) in fp32 with the fast reciprocal division (MUFU.RCP + FMUL, <= 2 ulp;
+// the IEEE division was ~8 instructions and a slow-path branch per element of the SwiGLU epilogue).
+// The GEMM's fused SwiGLU epilogue and the standalone quarot_swiglu kernel both use this, so the
+// fused and unfused chains stay bitwise equal; fp16(silu) then rounds away the fp32 difference
+// except within ~2^-21 of an fp16 rounding boundary.
+QR_DEVICE float silu_f32(float g) { return __fdividef(g, 1.f + __expf(-g)); }
+
 // RoPE rotate-half of one pair with explicitly rounded fp32 products (no FMA
 // contraction), so the standalone RoPE kernel and the RoPE fused into the KV pass agree bitwise.
 QR_DEVICE float rope_first(float x1, float x2, float c, float s) { return __fsub_rn(__fmul_rn(x1, c), __fmul_rn(x2, s)); }

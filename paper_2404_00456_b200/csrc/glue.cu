@@ -67,8 +67,8 @@ __global__ void __launch_bounds__(256) swiglu_kernel(const __half* __restrict__ 
     for (int e = 0; e < 4; ++e) {
       const float2 g = __half22float2(g2[e]), u = __half22float2(u2[e]);
       // the FP16 model's ops (reading Z23): fp16(silu(g)), then fp16(that * u)
-      const float sx = __half2float(__float2half_rn(g.x / (1.f + __expf(-g.x))));
-      const float sy = __half2float(__float2half_rn(g.y / (1.f + __expf(-g.y))));
+      const float sx = __half2float(__float2half_rn(silu_f32(g.x)));
+      const float sy = __half2float(__float2half_rn(silu_f32(g.y)));
       o2[e] = __floats2half2_rn(sx * u.x, sy * u.y);
     }
     *reinterpret_cast<uint4*>(act + m * ld_act + c) = o;

@@ -231,7 +231,7 @@ QR_DEVICE void epi_chunk(const Params& p, const uint32_t (&rc)[32], int64_t m, b
             const float gv = __half2float(__float2half_rn(((float)((int32_t)rc[16 * hgrp + c] >> kShift) * sx) * sg[c]));
             const float uv =
                 __half2float(__float2half_rn(((float)((int32_t)rc[16 * hgrp + 8 + c] >> kShift) * sx) * sg[8 + c]));
-            a[j] = __half2float(__float2half_rn(gv / (1.f + __expf(-gv)))) * uv;  // fp16(silu(g)) * u
+            a[j] = __half2float(__float2half_rn(silu_f32(gv))) * uv;  // fp16(silu(g)) * u
           }
           h[e] = pack_half2(a[0], a[1]);
         }

@@ -1,6 +1,6 @@
 """One KV-cache Init (+RoPE) launch set at T tokens (ncu target).  python scripts/one_kv.py T [rope]"""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch, synth
 import paper_2404_00456_b200 as q
 T = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
