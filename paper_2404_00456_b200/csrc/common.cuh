@@ -70,7 +70,14 @@ QR_DEVICE void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
 // The GEMM's fused SwiGLU epilogue and the standalone quarot_swiglu kernel both use this, so the
 // fused and unfused chains stay bitwise equal; fp16(silu) then rounds away the fp32 difference
 // except within ~2^-21 of an fp16 rounding boundary.
-QR_DEVICE float silu_f32(float g) { return __fdividef(g, 1.f + __expf(-g)); }
+// e^-g as __expf(-g) computes it (ex2.approx of -g * log2(e) in fp32), with .ftz: only a subnormal
+// e^-g differs (flushed to 0), and 1 + subnormal == 1 in fp32, so silu is bitwise unchanged while
+// the non-ftz form's subnormal range fix-up (a compare and two predicated multiplies) disappears.
+QR_DEVICE float silu_f32(float g) {
+  float e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(g * -1.44269502162933349609375f));
+  return __fdividef(g, 1.f + e);
+}
 
 // RoPE rotate-half of one pair with explicitly rounded fp32 products (no FMA
 // contraction), so the standalone RoPE kernel and the RoPE fused into the KV pass agree bitwise.

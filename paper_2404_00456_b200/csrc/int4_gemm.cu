@@ -207,6 +207,11 @@ template <bool kS32, int kDbg, int kShift = 8, int kEpi = 0>  // kShift: the x16
 QR_DEVICE void epi_chunk(const Params& p, const uint32_t (&rc)[32], int64_t m, bool row_ok, int64_t n0, float sx,
                          const float* wsc) {
   if (!row_ok) return;
+  // the accumulator is 2^kShift x the integer dot product (exactly: both operands carry the x16
+  // nibble scaling), and |dot| < 2^24, so fp32(acc) * (s_x 2^-kShift) rounds exactly like
+  // fp32(acc >> kShift) * s_x (no shift per element; 2^-kShift s_x only loses bits when s_x <
+  // 2^-118, where every output rounds to fp16 zero either way)
+  const float sxs = sx * (1.f / (float)(1 << kShift));
   if constexpr (kS32) {
     int32_t* dst = reinterpret_cast<int32_t*>(p.out) + m * p.ld_out + n0;
 #pragma unroll
@@ -228,9 +233,9 @@ QR_DEVICE void epi_chunk(const Params& p, const uint32_t (&rc)[32], int64_t m, b
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
             const int c = 2 * e + j;
-            const float gv = __half2float(__float2half_rn(((float)((int32_t)rc[16 * hgrp + c] >> kShift) * sx) * sg[c]));
+            const float gv = __half2float(__float2half_rn(((float)(int32_t)rc[16 * hgrp + c] * sxs) * sg[c]));
             const float uv =
-                __half2float(__float2half_rn(((float)((int32_t)rc[16 * hgrp + 8 + c] >> kShift) * sx) * sg[8 + c]));
+                __half2float(__float2half_rn(((float)(int32_t)rc[16 * hgrp + 8 + c] * sxs) * sg[8 + c]));
             a[j] = __half2float(__float2half_rn(silu_f32(gv))) * uv;  // fp16(silu(g)) * u
           }
           h[e] = pack_half2(a[0], a[1]);
@@ -260,8 +265,8 @@ QR_DEVICE void epi_chunk(const Params& p, const uint32_t (&rc)[32], int64_t m, b
         uint32_t h[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          float v0 = ((float)((int32_t)rc[8 * g + 2 * e] >> kShift) * sx) * swv[2 * e];
-          float v1 = ((float)((int32_t)rc[8 * g + 2 * e + 1] >> kShift) * sx) * swv[2 * e + 1];
+          float v0 = ((float)(int32_t)rc[8 * g + 2 * e] * sxs) * swv[2 * e];
+          float v1 = ((float)(int32_t)rc[8 * g + 2 * e + 1] * sxs) * swv[2 * e + 1];
           if (epi_residual<kEpi>(p)) {  // the linear output is fp16 before the residual add
             v0 = __half2float(__float2half_rn(v0)) + __half2float(__ushort_as_half((unsigned short)(rw[e] & 0xFFFFu)));
             v1 = __half2float(__float2half_rn(v1)) + __half2float(__ushort_as_half((unsigned short)(rw[e] >> 16)));
@@ -283,6 +288,7 @@ QR_DEVICE void epi_chunk_res(const Params& p, const uint32_t (&rc)[32], int64_t 
   if (!row_ok) return;
   const int r = threadIdx.x & 31;
   const uint32_t rowb = smem_u32(box) + (uint32_t)r * 128u;
+  const float sxs = sx * (1.f / 256.f);  // as epi_chunk: fp32(acc) * s_x / 256 == fp32(acc >> 8) * s_x
   __half* dst = reinterpret_cast<__half*>(p.out) + m * p.ld_out + n0;
 #pragma unroll
   for (int g = 0; g < 4; ++g) {
@@ -295,8 +301,8 @@ QR_DEVICE void epi_chunk_res(const Params& p, const uint32_t (&rc)[32], int64_t 
       uint32_t h[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        float v0 = ((float)((int32_t)rc[8 * g + 2 * e] >> 8) * sx) * swv[2 * e];
-        float v1 = ((float)((int32_t)rc[8 * g + 2 * e + 1] >> 8) * sx) * swv[2 * e + 1];
+        float v0 = ((float)(int32_t)rc[8 * g + 2 * e] * sxs) * swv[2 * e];
+        float v1 = ((float)(int32_t)rc[8 * g + 2 * e + 1] * sxs) * swv[2 * e + 1];
         v0 = __half2float(__float2half_rn(v0)) + __half2float(__ushort_as_half((unsigned short)(rw[e] & 0xFFFFu)));
         v1 = __half2float(__float2half_rn(v1)) + __half2float(__ushort_as_half((unsigned short)(rw[e] >> 16)));
         h[e] = pack_half2(v0, v1);

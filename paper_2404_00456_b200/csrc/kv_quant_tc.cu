@@ -33,7 +33,10 @@ namespace kvtc {
 
 constexpr int HD = 128;
 constexpr int TILE_BYTES = 128 * HD * 2;  // 32 KB: 128 rows x 128 fp16, two SW128 atoms
-constexpr int STAGES = 4;
+#ifndef QR_KV_STAGES
+#define QR_KV_STAGES 5  // 5 x 32 KB stages: +1% with RoPE (the RoPE pass holds a stage longer)
+#endif
+constexpr int STAGES = QR_KV_STAGES;
 constexpr int NUM_EPI = 4, NUM_PROD = 8;  // two RoPE threads per tile row
 constexpr int EPI_WARP0 = 0, PROD_WARP0 = 4, MMA_WARP = 12, TMA_WARP = 13, TAB_WARP0 = 14, NUM_TAB = 2;
 constexpr int NUM_THREADS = 16 * 32;
