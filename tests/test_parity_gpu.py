@@ -364,3 +364,25 @@ def test_group_pipeline_quant_then_linear(q, mode, G):
     # oracle's codes (<= 1e-4 flips) within the 1e-2 end-to-end bar
     _assert_group_out(y.cpu().numpy(), og.group_linear(got_c.astype(np.int8), xs4.cpu().numpy(), cw, sw))
     assert P.frob_rel(y.cpu().numpy(), og.group_linear(rc, rs, cw, sw)) <= 1e-2
+
+
+@pytest.mark.parametrize("clip", [0.9, 1.0, 0.5])
+def test_full28_kperm_vs_oracle_clamp_paths(q, clip):
+    """The KPERM FULL K = 1024 x 28 kernel (the chain's down_proj quantizer) against the oracle,
+    un-permuted: its clamp-free packing (warps none of whose lanes can reach |v * inv| >= 7.5)
+    and its clamping path.  Gaussian-like rows take mostly the clamp-free path, the adversarial
+    rows (a spike: every transformed element at amax, so every warp clamps; ties; extremes) the
+    clamping one, and clip 0.5 saturates many codes in every row."""
+    K = 28672
+    x = synth.activations(40, K, "swiglu", seed=11, device=DEV)
+    x = torch.cat([x, torch.from_numpy(_adversarial_rows(K)).to(DEV)], 0).contiguous()
+    xq, xs = q.hadamard_quant(x, "full", clip_ratio=clip, kperm=True)
+    perm = q.full_kperm(K)
+    inv = torch.empty_like(perm)
+    inv[perm] = torch.arange(K)
+    nat = q.permute_k_packed(xq, inv)
+    ref_codes, _, ref_scale = olayer.hadamard_quant(x.float().cpu().numpy().astype(np.float64), "full", 128, clip)
+    got = P.unpack_signed(nat.cpu().numpy())
+    P.assert_codes(got, ref_codes, f"full-28 kperm clip={clip}")
+    P.assert_scales(xs.cpu().numpy(), ref_scale, f"full-28 kperm clip={clip}")
+    assert not np.any(got == -8) and np.abs(got).max() == 7
