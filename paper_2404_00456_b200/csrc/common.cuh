@@ -79,10 +79,13 @@ QR_DEVICE float silu_f32(float g) {
   return __fdividef(g, 1.f + e);
 }
 
-// RoPE rotate-half of one pair with explicitly rounded fp32 products (no FMA
-// contraction), so the standalone RoPE kernel and the RoPE fused into the KV pass agree bitwise.
-QR_DEVICE float rope_first(float x1, float x2, float c, float s) { return __fsub_rn(__fmul_rn(x1, c), __fmul_rn(x2, s)); }
-QR_DEVICE float rope_second(float x1, float x2, float c, float s) { return __fadd_rn(__fmul_rn(x2, c), __fmul_rn(x1, s)); }
+// RoPE rotate-half of one pair in fp32 with one fixed rounding sequence, so every
+// kernel that applies it (the standalone RoPE kernel and the RoPE fused into the KV passes) agrees
+// bitwise: x1 c - x2 s = fma(x1, c, -rn(x2 s)) and x2 c + x1 s = fma(x2, c, rn(x1 s)).  (The
+// fma form, because ptxas contracts packed mul.rn.f32x2 + sub.rn.f32x2 into FFMA2 even with the
+// explicit rounding modifier; the packed forms below state the same arithmetic explicitly.)
+QR_DEVICE float rope_first(float x1, float x2, float c, float s) { return __fmaf_rn(x1, c, -__fmul_rn(x2, s)); }
+QR_DEVICE float rope_second(float x1, float x2, float c, float s) { return __fmaf_rn(x2, c, __fmul_rn(x1, s)); }
 
 // ---------------------------------------------------------------- proxy fences
 // generic-proxy st.shared -> async-proxy (tcgen05.mma operand) visibility
@@ -215,6 +218,12 @@ QR_DEVICE float2 f2mul(float2 a, float2 b) {
       : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
   return r;
 }
+// rope_first / rope_second on two pairs at once (packed fp32x2, the same roundings)
+QR_DEVICE float2 rope_first2(float2 x1, float2 x2, float2 c, float2 sn) {
+  const float2 t = f2mul(x2, sn);
+  return f2fma(x1, c, make_float2(-t.x, -t.y));
+}
+QR_DEVICE float2 rope_second2(float2 x1, float2 x2, float2 c, float2 sn) { return f2fma(x2, c, f2mul(x1, sn)); }
 // (x + y, x - y) of the pair held in one float2: ONE FFMA2, p * (1, -1) + swap(p) — SASS
 // `FFMA2 d, p, UR.F32x2, p.F32x2.LO_HI`, the constant read from a uniform register pair (the
 // broadcast form y * (1, -1) + x made ptxas re-materialise the 1.0 before every FFMA2: +1 MOV

@@ -215,8 +215,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
                            : "=f"(c2.x), "=f"(c2.y), "=f"(c2.z), "=f"(c2.w)
                            : "r"(cs + (uint32_t)((8 * c + 2 * e) * 8)));
-              lo[e] = __floats2half2_rn(rope_first(x1.x, x2.x, c2.x, c2.y), rope_first(x1.y, x2.y, c2.z, c2.w));
-              hi[e] = __floats2half2_rn(rope_second(x1.x, x2.x, c2.x, c2.y), rope_second(x1.y, x2.y, c2.z, c2.w));
+              // pairs i, i + 1 at once: c2 = (cos_i, cos_i+1, sin_i, sin_i+1); the packed forms are
+              // rope_first / rope_second elementwise, bitwise quarot_rope's
+              const float2 cv = make_float2(c2.x, c2.y), sv = make_float2(c2.z, c2.w);
+              const float2 f = rope_first2(x1, x2, cv, sv);
+              const float2 g = rope_second2(x1, x2, cv, sv);
+              lo[e] = __floats2half2_rn(f.x, f.y);
+              hi[e] = __floats2half2_rn(g.x, g.y);
             }
             sts_v4(plo, lo4);
             sts_v4(phi, hi4);
@@ -241,7 +246,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int64_t pos = (a.pos0 + t0 + tt) % a.seq_len;
           double sn, cn;
           sincos((double)pos * inv_freq[ii], &sn, &cn);  // == quarot_rope's table
-          btab[i] = make_float2((float)cn, (float)sn);
+          // layout per two pairs (2k, 2k + 1): (cos_2k, cos_2k+1, sin_2k, sin_2k+1) — the RoPE warps'
+          // packed fp32x2 operands
+          reinterpret_cast<float*>(btab)[tt * HD + (ii & ~1) * 2 + (ii & 1)] = (float)cn;
+          reinterpret_cast<float*>(btab)[tt * HD + (ii & ~1) * 2 + 2 + (ii & 1)] = (float)sn;
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&tab_full[bi & 1]);
