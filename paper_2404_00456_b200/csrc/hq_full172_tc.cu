@@ -205,9 +205,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int g = e >> 3;            // row group
     const int qd = warp & 3;         // TMEM lane quarter
     const int mh = (e >> 2) & 1;     // M-half
-    const int jp = mh * 128 + qd * 32 + lane;  // output j'
-    const bool warp_ok = mh * 128 + qd * 32 < MB;
-    const bool lane_ok = jp < MB;
+    // M-half 1 holds H_172's rows 128..171 twice (A image rows 0..43 and 64..107): row group 0
+    // reads lanes 0..43 (warps of lane quarters 0, 1), row group 1 lanes 64..107 (quarters 2, 3),
+    // so each scheduler carries 3 busy warps over the two groups instead of 4, 4, 2, 2
+    const int off = mh ? 64 * g : 0;
+    const int jp = mh * 128 + qd * 32 + lane - off;  // output j'
+    const bool warp_ok = mh ? (qd * 32 + 31 >= off && qd * 32 < off + (MB - 128)) : true;
+    const bool lane_ok = mh ? (jp >= 128 && jp < MB) : true;
     const bool odd = (lane & 1) != 0;
     const uint32_t t_lane = tmem_base + ((uint32_t)(qd * 32) << 16) + (uint32_t)(mh * P);
     const float norm_f = (float)rsqrt((double)K);
@@ -326,8 +330,11 @@ std::vector<uint16_t> a_image_172(const int8_t* h) {
   std::vector<uint16_t> img(hq172::A_BYTES / 2, 0);
   for (int m = 0; m < 256; ++m)
     for (int k = 0; k < hq172::KP; ++k) {
-      int v = (m < 172 && k < 172) ? h[m * 172 + k] : 0;
       const int mh = m >> 7, r = m & 127, kc = k / 64, c = (k % 64) / 8, within = k % 8;
+      // output row j' of image row (mh, r): half 1 carries rows 128..171 at r < 44 and again at
+      // 64 <= r < 108 (one copy per epilogue row group)
+      const int jr = mh == 0 ? r : (r < 44 ? 128 + r : (r >= 64 && r < 108 ? 128 + r - 64 : -1));
+      int v = (jr >= 0 && k < 172) ? h[jr * 172 + k] : 0;
       const size_t off = (size_t)mh * 3 * 16384 + hq172::sw128_off(128, kc, r, c) + (size_t)within * 2;
       img[off / 2] = v > 0 ? 0x3C00 : (v < 0 ? 0xBC00 : 0);
     }
