@@ -31,6 +31,10 @@
 #include "common.cuh"
 #include "quarot_internal.h"
 
+#ifndef QR_DEC_CTAS_PER_SM
+#define QR_DEC_CTAS_PER_SM 4  // target CTAs per SM of the split-sequence grid
+#endif
+
 namespace qr {
 namespace kvd {
 
@@ -490,7 +494,7 @@ cudaError_t launch_kv_decode(const void* q, const uint8_t* k_codes, const float*
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int64_t pairs = (int64_t)B * n_kv;
-  int per = (int)((4 * nsm + pairs - 1) / pairs);
+  int per = (int)((QR_DEC_CTAS_PER_SM * nsm + pairs - 1) / pairs);
   per = per < 1 ? 1 : (per > nchunks ? nchunks : per);
   a.chunks_per_cta = (nchunks + per - 1) / per;
   a.nsplit = (nchunks + a.chunks_per_cta - 1) / a.chunks_per_cta;
