@@ -321,6 +321,13 @@ quarot_status quarot_base_hadamard(int32_t m, int8_t* out);
  * index whose code sits at position p (perm: int64 [K], caller-owned).  K = 1024 x 28 only
  * (QUAROT_ERR_UNSUPPORTED_SIZE otherwise). */
 quarot_status quarot_full_kperm(int64_t K, int64_t* perm);
+/* One-time setup for the current device: uploads the library's constant operand images and
+ * Hadamard tables (static __device__ memory) and sets the kernels' shared-memory attributes,
+ * synchronously (it ends with a device synchronization).  Optional — every entry point does the
+ * same lazily on first use — but calling it once before CUDA-graph capture or before a timed
+ * region keeps the first real call free of host synchronization.  Idempotent; errors:
+ * QUAROT_ERR_CUDA. */
+quarot_status quarot_prepare(void);
 /* Number of kernels the last successful entry point on this host thread enqueued. */
 int32_t quarot_last_launch_count(void);
 /* "cudaErrorName: description" of the last call on this host thread that returned

@@ -9,4 +9,5 @@ from .quarot import (  # noqa: F401
     last_launch_count, lib, quarot_linear, rope, swiglu, interleave_gate_up, int4_linear_swiglu,
     kv_append, kv_decode, kv_cache_empty, hadamard_quant8, int8_linear, int8_matmul_s32,
     hadamard_quant_group, hadamard_quant_group8, int4_linear_group, int4_linear_group8, full_kperm, permute_k_packed,
+    prepare,
 )

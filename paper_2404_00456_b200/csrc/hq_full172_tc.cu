@@ -377,6 +377,7 @@ cudaError_t launch_hq_full172_tc(const void* x, int64_t M, int64_t ld_x, float c
     }
     img = g_img172[dev & 63];
   }
+  if (M == 0) return cudaSuccess;  // quarot_prepare: one-time setup only
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)(M < nsm ? M : nsm);

@@ -883,6 +883,7 @@ cudaError_t launch_hq_full28_tc(const void* x, int64_t M, int64_t ld_x, float cl
   const void* img = nullptr;
   cudaError_t e = a28_image(&img);
   if (e != cudaSuccess) return e;
+  if (M == 0) return cudaSuccess;  // quarot_prepare: one-time setup only
   CUtensorMap map;
   e = x_map_28(x, M, ld_x, &map);
   if (e != cudaSuccess) return e;

@@ -364,6 +364,7 @@ cudaError_t launch_hq_heads_tc(const void* x, int64_t M, int64_t K, int64_t ld_x
     }
     img = g_img[dev & 63][slot];
   }
+  if (M == 0) return cudaSuccess;  // quarot_prepare: one-time setup only
   if (q8) {
     if (nh == 16) return launch_nh<16, true>(x, M, ld_x, clip, q, ld_q, scale, stream, dev, img);
     if (nh == 32) return launch_nh<32, true>(x, M, ld_x, clip, q, ld_q, scale, stream, dev, img);

@@ -1,5 +1,6 @@
 // quarot_abi.cu — the extern "C" boundary (include/quarot.h): argument validation and
-// dispatch to the sm_100a kernels.  No torch types, no allocation, no host synchronization.
+// dispatch to the sm_100a kernels.  No torch types, no allocation, no host synchronization (except
+// the one-time constant uploads, quarot_prepare).
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -66,6 +67,22 @@ quarot_status quarot_full_kperm(int64_t K, int64_t* perm) {
   for (int64_t a = 0; a < 256; ++a)
     for (int64_t j = 0; j < J; ++j) perm[(a >> 5) * 32 * J + 32 * j + (a & 31)] = a * J + j;
   return QUAROT_OK;
+}
+
+quarot_status quarot_prepare(void) {
+  // every lazily initialised launcher, called with zero rows: one-time setup only, no launch
+  cudaError_t e = qr::ensure_device_tables();
+  if (e == cudaSuccess) e = qr::launch_hq_full28_tc(nullptr, 0, 0, 0.9f, nullptr, 0, nullptr, nullptr);
+  if (e == cudaSuccess) e = qr::launch_hq_full172_tc(nullptr, 0, 0, 0.9f, nullptr, 0, nullptr, nullptr);
+  if (e == cudaSuccess) e = qr::launch_hq_full_small_tc(nullptr, 0, 0, 128, 108, 0.9f, nullptr, 0, nullptr, nullptr);
+  if (e == cudaSuccess) e = qr::launch_hq_full_small_tc(nullptr, 0, 0, 256, 20, 0.9f, nullptr, 0, nullptr, nullptr);
+  for (int nh = 16; e == cudaSuccess && nh <= 64; nh *= 2)
+    e = qr::launch_hq_heads_tc(nullptr, 0, (int64_t)nh * 128, 0, 128, 0.9f, nullptr, 0, nullptr, nullptr);
+  if (e == cudaSuccess)
+    e = qr::launch_kv_tc(nullptr, 0, nullptr, 0, 0, 8, nullptr, 0, 64, 0.95f, false, 0, 2048, 10000.f, nullptr,
+                         nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  return e == cudaSuccess ? QUAROT_OK : cuda_fail(e);
 }
 
 quarot_status quarot_base_hadamard(int32_t m, int8_t* out) {

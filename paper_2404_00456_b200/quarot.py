@@ -57,6 +57,7 @@ _SIGS = {
     "quarot_abi_version": [],
     "quarot_base_hadamard": [_c_i32, _vp],
     "quarot_full_kperm": [_c_i64, _vp],
+    "quarot_prepare": [],
     "quarot_last_launch_count": [],
     "quarot_last_cuda_error": [],
     "quarot_debug_gemm_mode": [_c_i32],
@@ -154,6 +155,12 @@ def hadamard_quant(x: torch.Tensor, mode="none", head_dim: int = 128, clip_ratio
                                      _dev(scale, "scale", torch.float32), _stream(stream))
     _check("quarot_hadamard_quant", st)
     return q, scale
+
+
+def prepare() -> None:
+    """quarot_prepare: one-time setup (constant images, tables, kernel attributes) on the current
+    CUDA device, so no later call synchronizes the host (e.g. before CUDA-graph capture)."""
+    _check("quarot_prepare", lib().quarot_prepare())
 
 
 def full_kperm(K: int) -> torch.Tensor:

@@ -227,6 +227,8 @@ class DecoderLayerStep:
             "v_scale": torch.empty(tokens, L.n_kv, dtype=torch.float32, device=device),
             "v_zero": torch.empty(tokens, L.n_kv, dtype=torch.uint8, device=device),
         }
+        with torch.cuda.device(self.device):
+            q.prepare()  # one-time constant uploads now, not inside a timed region or a graph capture
 
     INPUTS = ("x", "attn_out")
 

@@ -65,3 +65,46 @@ def test_side_stream_ordering(q):
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
         assert torch.equal(y, ref)
+
+
+def test_prepare_then_first_call_inside_graph_capture():
+    """quarot_prepare (one-time constant uploads) in a fresh process, then the FIRST quantizer and
+    KV calls of that process inside a CUDA-graph capture on a side stream: no host
+    synchronization happens during capture (it would invalidate it), and the replay equals an
+    eager run bitwise."""
+    import subprocess
+    import sys
+    code = r'''
+import sys, torch
+sys.path.insert(0, ".")
+import synth
+import paper_2404_00456_b200 as q
+q.prepare()
+x = synth.activations(300, 28672, "swiglu", 3, "cuda")
+k, v, qq = synth.kv_inputs(64, 8, 64, 128, seed=2, device="cuda")
+xq = torch.empty(300, 14336, dtype=torch.uint8, device="cuda")
+xs = torch.empty(300, dtype=torch.float32, device="cuda")
+out = {"k_codes": torch.empty(64, 8, 64, dtype=torch.uint8, device="cuda"),
+       "k_scale": torch.empty(64, 8, dtype=torch.float32, device="cuda"),
+       "k_zero": torch.empty(64, 8, dtype=torch.uint8, device="cuda"),
+       "v_codes": torch.empty(64, 8, 64, dtype=torch.uint8, device="cuda"),
+       "v_scale": torch.empty(64, 8, dtype=torch.float32, device="cuda"),
+       "v_zero": torch.empty(64, 8, dtype=torch.uint8, device="cuda")}
+qc = qq.clone()
+side = torch.cuda.Stream()
+g = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g, stream=side):
+    q.hadamard_quant(x, "full", q=xq, scale=xs, kperm=True, stream=side)
+    q.kv_quant(k, v, qc, out=out, rope=(0, 2048, 10000.0), stream=side)
+g.replay()
+torch.cuda.synchronize()
+xq2, xs2 = q.hadamard_quant(x, "full", kperm=True)
+qc2 = qq.clone()
+out2 = q.kv_quant(k, v, qc2, rope=(0, 2048, 10000.0))
+torch.cuda.synchronize()
+assert torch.equal(xq, xq2) and torch.equal(xs, xs2)
+assert torch.equal(qc, qc2) and all(torch.equal(out[n], out2[n]) for n in out)
+print("OK")
+'''
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
