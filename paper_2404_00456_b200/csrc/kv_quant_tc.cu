@@ -336,8 +336,70 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         continue;
       }
-      // K / V: asymmetric 4-bit quantization of the row (group = head_dim, reading Z14); K from
-      // TMEM (rotated), V straight from the stage (fp16 -> fp32 is exact, as the MMA with I was)
+      if (ti.type == 2) {
+        // V: the row (128 fp16) is copied to registers as 64 packed half2 and the stage released
+        // at once — the MHA shapes quantize two of every three tiles, and holding the V stage
+        // through the whole quantization starved the TMA ring.  Asymmetric 4-bit quantization of
+        // the row exactly as for K below (fp16 -> fp32 is exact), with norm = 1 (V not rotated).
+        mbar_wait(&a_full[s], (uint32_t)((it / STAGES) & 1));  // landed (no RoPE on V)
+        uint32_t hv[HD / 2];
+#pragma unroll
+        for (int c = 0; c < HD / 8; ++c)
+          asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(hv[4 * c]), "=r"(hv[4 * c + 1]), "=r"(hv[4 * c + 2]), "=r"(hv[4 * c + 3])
+                       : "r"(stage + sw128(r, 8 * c)));
+        bar_named(1, NUM_EPI * 32);  // every row of the V stage is in registers: release it
+        if (threadIdx.x == EPI_WARP0 * 32) mbar_arrive(&a_empty[s]);
+        auto h2 = [&](int k) { return *reinterpret_cast<const __half2*>(&hv[k]); };
+        __half2 mn2[4] = {h2(0), h2(1), h2(2), h2(3)}, mx2[4] = {h2(0), h2(1), h2(2), h2(3)};
+#pragma unroll
+        for (int k = 4; k < HD / 2; ++k) {
+          mn2[k & 3] = __hmin2_nan(mn2[k & 3], h2(k));
+          mx2[k & 3] = __hmax2_nan(mx2[k & 3], h2(k));
+        }
+        const __half2 mnh = __hmin2_nan(__hmin2_nan(mn2[0], mn2[1]), __hmin2_nan(mn2[2], mn2[3]));
+        const __half2 mxh = __hmax2_nan(__hmax2_nan(mx2[0], mx2[1]), __hmax2_nan(mx2[2], mx2[3]));
+        const float mn = fmin_nan(__low2float(mnh), __high2float(mnh));
+        const float mx = fmax_nan(__low2float(mxh), __high2float(mxh));
+        const double lo = (double)a.clip * (double)fminf(mn, 0.f);
+        const double hi = (double)a.clip * (double)fmaxf(mx, 0.f);
+        float sc = 1.f, inv = 0.f;
+        int z = 0;
+        if (!(isfinite(mn) && isfinite(mx))) {
+          sc = __int_as_float(0x7fc00000);
+        } else if (hi != lo) {
+          sc = (float)((hi - lo) / 15.0);
+          const double zr = rint(-lo / (double)sc);
+          z = (int)(zr < 0.0 ? 0.0 : (zr > 15.0 ? 15.0 : zr));
+          inv = (float)(1.0 / (double)sc);
+        }
+        const int64_t gi = t * a.n_kv + h;
+        const float zf = (float)z;
+        uint32_t w[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) w[j] = 0u;
+        if (inv != 0.f) {
+#pragma unroll
+          for (int k = 0; k < HD / 2; ++k) {  // elements 2k, 2k + 1: one code byte
+            float2 m = f2fma(__half22float2(h2(k)), make_float2(inv, inv), make_float2(zf, zf));
+            m.x = fminf(fmaxf(m.x, 0.f), 15.f);
+            m.y = fminf(fmaxf(m.y, 0.f), 15.f);
+            m = f2add(m, make_float2(12582912.f, 12582912.f));
+            const uint32_t byte = (__float_as_uint(m.x) & 0xFu) | ((__float_as_uint(m.y) & 0xFu) << 4);
+            w[k >> 2] |= byte << (8 * (k & 3));
+          }
+        }
+        if (ok) {
+          uint4* codes = reinterpret_cast<uint4*>(a.v_codes + gi * (HD / 2));
+#pragma unroll
+          for (int c = 0; c < 4; ++c) codes[c] = make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
+          a.v_scale[gi] = sc;
+          a.v_zero[gi] = (uint8_t)z;
+        }
+        continue;
+      }
+      // K: asymmetric 4-bit quantization of the row (group = head_dim, reading Z14) from TMEM
+      // (rotated); the V branches below are no longer taken (V is handled above)
       int tb = 0;
       uint32_t tcol = 0;
       if (ti.type == 1) {
