@@ -386,3 +386,46 @@ def test_full28_kperm_vs_oracle_clamp_paths(q, clip):
     P.assert_codes(got, ref_codes, f"full-28 kperm clip={clip}")
     P.assert_scales(xs.cpu().numpy(), ref_scale, f"full-28 kperm clip={clip}")
     assert not np.any(got == -8) and np.abs(got).max() == 7
+
+
+@pytest.mark.parametrize("n_kv,n_q", [(8, 64), (32, 32)])
+def test_kv_tc_value_rows_edge_cases(q, n_kv, n_q):
+    """KV Init's V rows (tcgen05 kernel: copied to registers, fp16 min / max) on edge rows —
+    zero, constant, +-0 mixes, a NaN, an inf, fp16 extremes, a single spike — against the
+    oracle's kv_init and bitwise against the CUDA-core kernel (quarot_debug_kv_variant 1), an
+    independent implementation of the same arithmetic."""
+    T, d = 64, 128
+    k, v, qq = synth.kv_inputs(T, n_kv, n_q, d, seed=21, device=DEV)
+    v[0, 0] = 0
+    v[1, 0] = 0.75
+    v[2, 0, ::2] = 0.0
+    v[2, 0, 1::2] = -0.0
+    v[3, 0, 5] = float("nan")
+    v[4, 0, 7] = float("inf")
+    v[5, 0, ::2] = 65504.0
+    v[5, 0, 1::2] = -65504.0
+    v[6, 0] = 0
+    v[6, 0, 17] = -3.0
+    outs = []
+    for variant in (0, 1):
+        q.lib().quarot_debug_kv_variant(variant)
+        try:
+            qc = qq.clone()
+            outs.append(q.kv_quant(k, v, qc))
+        finally:
+            q.lib().quarot_debug_kv_variant(0)
+    torch.cuda.synchronize()
+    # V is not rotated: both kernels do exactly the same arithmetic (K goes through H_128 on the
+    # tensor core in one and in butterflies in the other, so its fp32 sums may round differently)
+    for key in ("v_codes", "v_zero"):
+        assert torch.equal(outs[0][key], outs[1][key]), key
+    assert torch.equal(outs[0]["v_scale"].view(torch.int32), outs[1]["v_scale"].view(torch.int32))  # NaNs bitwise
+    sv = outs[0]["v_scale"].cpu().numpy()
+    assert np.isnan(sv[3, 0]) and np.isnan(sv[4, 0]) and sv[0, 0] == 1.0
+    vc = P.unpack_unsigned(outs[0]["v_codes"].cpu().numpy())
+    assert np.all(vc[3, 0] == 0) and np.all(vc[4, 0] == 0)
+    fin = np.ones(T, bool)
+    fin[[3, 4]] = False
+    ref = okv.kv_init(k.cpu().numpy()[fin], v.cpu().numpy()[fin], None if qq is None else qq.cpu().numpy()[fin])
+    P.assert_codes(vc[fin], P.unpack_unsigned(ref["v_codes"]), "v codes")
+    P.assert_scales(sv[fin], ref["v_scale"], "v scale")
