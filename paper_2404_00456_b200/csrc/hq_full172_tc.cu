@@ -35,7 +35,13 @@ constexpr int KP = 192;                       // contraction padded to 3 SW128 a
 constexpr int RAW_BYTES = K * 2;              // 22016 (a multiple of 16)
 constexpr int B_BYTES = P * KP * 2;           // 24 KB: [3 atoms][64 rows][128 B]
 constexpr int A_BYTES = 2 * 3 * 16384;        // 96 KB: [M-half][atom][128 rows][128 B]
-constexpr int RSTAGES = 2, BSTAGES = 3;
+#ifndef QR_172_RSTAGES
+#define QR_172_RSTAGES 2
+#endif
+#ifndef QR_172_BSTAGES
+#define QR_172_BSTAGES 3
+#endif
+constexpr int RSTAGES = QR_172_RSTAGES, BSTAGES = QR_172_BSTAGES;  // raw-row TMA ring, relayouted operand ring
 constexpr int NG = 2, NUM_EPI = 8 * NG;
 constexpr int TMA_WARP = 0, MMA_WARP = 1, RL_WARP0 = 2, NUM_RL = 2, EPI_WARP0 = 4;
 constexpr int NUM_THREADS = (EPI_WARP0 + NUM_EPI) * 32;  // 640
