@@ -43,8 +43,16 @@ constexpr int A_BYTES = 2 * 3 * 16384;        // 96 KB: [M-half][atom][128 rows]
 #endif
 constexpr int RSTAGES = QR_172_RSTAGES, BSTAGES = QR_172_BSTAGES;  // raw-row TMA ring, relayouted operand ring
 constexpr int NG = 2, NUM_EPI = 8 * NG;
-constexpr int TMA_WARP = 0, MMA_WARP = 1, RL_WARP0 = 2, NUM_RL = 2, EPI_WARP0 = 4;
-constexpr int NUM_THREADS = (EPI_WARP0 + NUM_EPI) * 32;  // 640
+// The producer roles (TMA, MMA, the two relayout warps) take the HIGHEST warp ids: the schedulers
+// pick the highest-id eligible warp first, so the relayout of the next row is not starved of
+// issue slots by the 16 epilogue warps (with the producers at warps 0-3 the epilogue waited on
+// the next row's MMA ~300 polls per row)
+#ifndef QR_172_PROD_HIGH
+#define QR_172_PROD_HIGH 1
+#endif
+constexpr int EPI_WARP0 = QR_172_PROD_HIGH ? 0 : 4, CTL_WARP0 = QR_172_PROD_HIGH ? 16 : 0;
+constexpr int TMA_WARP = CTL_WARP0, MMA_WARP = CTL_WARP0 + 1, RL_WARP0 = CTL_WARP0 + 2, NUM_RL = 2;
+constexpr int NUM_THREADS = (4 + NUM_EPI) * 32;  // 640
 constexpr int TBUF = 4;                                   // TMEM row buffers of 128 columns
 constexpr uint32_t TMEM_COLS = 512;
 constexpr size_t SMEM = 1024 + A_BYTES + (size_t)BSTAGES * B_BYTES + (size_t)RSTAGES * RAW_BYTES + 512;
@@ -140,7 +148,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const uint32_t tmem_base = *tmem_holder;
   const int64_t nrows = M > (int64_t)blockIdx.x ? (M - 1 - (int64_t)blockIdx.x) / gridDim.x + 1 : 0;
 
-  if (warp < EPI_WARP0) {
+  if (warp >= CTL_WARP0 && warp < CTL_WARP0 + 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");  // 128 x 64 + 512 x 104 = 640 x 96
     if (warp == TMA_WARP) {
       if (lane == 0) {
