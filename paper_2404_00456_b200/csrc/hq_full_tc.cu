@@ -481,8 +481,9 @@ QR_DEVICE uint32_t code_word8(float2 a, float2 b, float2 c, float2 d, float inv)
   o0 = __vmaxs2(__vmins2(o0, 0x00070007u), 0xFFF9FFF9u);
   e1 = __vmaxs2(__vmins2(e1, 0x00070007u), 0xFFF9FFF9u);
   o1 = __vmaxs2(__vmins2(o1, 0x00070007u), 0xFFF9FFF9u);
-  const uint32_t w0 = (e0 & 0x000F000Fu) | ((o0 & 0x000F000Fu) << 4);  // bytes at bits 0-7, 16-23
-  const uint32_t w1 = (e1 & 0x000F000Fu) | ((o1 & 0x000F000Fu) << 4);
+  // bytes at bits 0-7, 16-23 (the shifts as SHF: ALU pipe rather than IMAD.SHL on the FMA pipe)
+  const uint32_t w0 = (e0 & 0x000F000Fu) | __funnelshift_l(0u, o0 & 0x000F000Fu, 4);
+  const uint32_t w1 = (e1 & 0x000F000Fu) | __funnelshift_l(0u, o1 & 0x000F000Fu, 4);
   return __byte_perm(w0, w1, 0x6420);
 }
 
@@ -497,7 +498,7 @@ QR_DEVICE uint32_t code_word8_nc(float2 a, float2 b, float2 c, float2 d, float i
                                  __byte_perm(__float_as_uint(mc.x), __float_as_uint(md.x), 0x0040), 0x5410);
   const uint32_t o = __byte_perm(__byte_perm(__float_as_uint(ma.y), __float_as_uint(mb.y), 0x0040),
                                  __byte_perm(__float_as_uint(mc.y), __float_as_uint(md.y), 0x0040), 0x5410);
-  const uint32_t os = o << 4;
+  const uint32_t os = __funnelshift_l(0u, o, 4);  // o << 4 as SHF (ALU pipe; a plain shift became IMAD.SHL on the busier FMA pipe)
   uint32_t w;  // (e & 0x0F0F0F0F) | (os & 0xF0F0F0F0): LUT 0xE4 = c ? a : b over (a = e, b = os, c = mask)
   asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(w) : "r"(e), "r"(os), "r"(0x0F0F0F0Fu));
   return w;
