@@ -338,7 +338,8 @@ const char* quarot_last_cuda_error(void);
  * (not thread-safe; 0 restores the default).  quarot_debug_gemm_mode: 1 = the INT4 GEMM with its
  * producers idled (MMA issue only: the tensor-pipe probe bench.py reports as the INT8 peak), 2 =
  * no widening stores, 3 = no TMA, 4 = no output stores, 5 = no B widening stores, 6 = no A TMEM
- * stores, 7 = no epilogue work — probes 1-7 compute garbage.
+ * stores, 7 = no epilogue work, 8 = the MMA skips the wait for the accumulator drain — probes 1-8
+ * compute garbage.
  * quarot_debug_gemm_group_m: raster group override (pair-rows).  quarot_debug_hq_full_variant:
  * 1 = the mma.sync FULL-28 kernel, 2 / 3 = the 16-warps-per-row tcgen05 kernel (spin / sleep
  * waits).  quarot_debug_hq_heads_variant: 1 = the CUDA-core ACROSS_HEADS kernel for every width.

@@ -313,7 +313,8 @@ QR_DEVICE void epi_chunk_res(const Params& p, const uint32_t (&rc)[32], int64_t 
 }
 
 template <bool kS32, int kDbg = 0, int kEpi = 0>  // kDbg: 0 normal; roofline probes: 1 MMA only, 2 no widening, 3 no TMA, 4 no fp16 stores,
-                                                   // 5 no B widening stores, 6 no A TMEM stores, 7 no epilogue work
+                                                   // 5 no B widening stores, 6 no A TMEM stores, 7 no epilogue work,
+                                                   // 8 the MMA does not wait for the accumulator drain
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     int4_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmR, const Params p) {
@@ -406,7 +407,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       if (rank == 0 && lane == 0) {
         int it = 0;
         for (int tl = 0; tl < my_tiles; ++tl) {
-          mbar_wait(t_empty, (tl & 1) ^ 1);
+          if (kDbg != 8) mbar_wait(t_empty, (tl & 1) ^ 1);  // probe 8: no wait for the drain
           tc_fence_after();
           const uint32_t d_tmem = tmem_base + ACC_COL;
           for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
@@ -1475,14 +1476,15 @@ static cudaError_t launch_gemm_impl(const uint8_t* xq, const float* xs, int64_t 
   }
   const int max_pairs = num_sms_current() / 2;
   const int pairs = p.num_tiles < max_pairs ? p.num_tiles : max_pairs;
-  if (g_gemm_debug_mode >= 1 && g_gemm_debug_mode <= 7) {
+  if (g_gemm_debug_mode >= 1 && g_gemm_debug_mode <= 8) {
     auto kern = g_gemm_debug_mode == 1   ? int4_gemm_kernel<kS32, 1>
                 : g_gemm_debug_mode == 2 ? int4_gemm_kernel<kS32, 2>
                 : g_gemm_debug_mode == 3 ? int4_gemm_kernel<kS32, 3>
                 : g_gemm_debug_mode == 4 ? int4_gemm_kernel<kS32, 4>
                 : g_gemm_debug_mode == 5 ? int4_gemm_kernel<kS32, 5>
                 : g_gemm_debug_mode == 6 ? int4_gemm_kernel<kS32, 6>
-                                         : int4_gemm_kernel<kS32, 7>;
+                : g_gemm_debug_mode == 7 ? int4_gemm_kernel<kS32, 7>
+                                         : int4_gemm_kernel<kS32, 8>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
     if (e != cudaSuccess) return e;
     kern<<<2 * pairs, NUM_THREADS, SMEM_BYTES, stream>>>(ma, mb, mr, p);
