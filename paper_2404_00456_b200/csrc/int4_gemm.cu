@@ -228,17 +228,18 @@ QR_DEVICE void epi_chunk(const Params& p, const uint32_t (&rc)[32], int64_t m, b
         const float* sg = wsc + 16 * hgrp;
         uint32_t h[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          float a[2];
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            const int c = 2 * e + j;
-            const float gv = __half2float(__float2half_rn(((float)(int32_t)rc[16 * hgrp + c] * sxs) * sg[c]));
-            const float uv =
-                __half2float(__float2half_rn(((float)(int32_t)rc[16 * hgrp + 8 + c] * sxs) * sg[8 + c]));
-            a[j] = __half2float(__float2half_rn(silu_f32(gv))) * uv;  // fp16(silu(g)) * u
-          }
-          h[e] = pack_half2(a[0], a[1]);
+        for (int e = 0; e < 4; ++e) {  // two act outputs (columns c, c + 1) per packed half2
+          const int c = 2 * e;
+          const __half2 gh = __floats2half2_rn(((float)(int32_t)rc[16 * hgrp + c] * sxs) * sg[c],
+                                               ((float)(int32_t)rc[16 * hgrp + c + 1] * sxs) * sg[c + 1]);
+          const __half2 uh = __floats2half2_rn(((float)(int32_t)rc[16 * hgrp + 8 + c] * sxs) * sg[8 + c],
+                                               ((float)(int32_t)rc[16 * hgrp + 9 + c] * sxs) * sg[9 + c]);
+          const float2 gf = __half22float2(gh);
+          const __half2 sh = __floats2half2_rn(silu_f32(gf.x), silu_f32(gf.y));  // fp16(silu(g))
+          // fp16(fp16(silu(g)) * u): the product of two fp16 values is exact in fp32, so one
+          // fp16 multiply (RN) gives the same bits as the fp32 multiply rounded to fp16
+          const __half2 act = __hmul2(sh, uh);
+          h[e] = *reinterpret_cast<const uint32_t*>(&act);
         }
         *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(p.out) + m * p.ld_out + (nn >> 1)) =
             make_uint4(h[0], h[1], h[2], h[3]);
