@@ -419,16 +419,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // hardware named barriers (no mbarrier polling) for the two intra-row dependencies.  Round-1
 // ncu: the 16-warps-share-every-row design spent ~1.9 instructions per element polling
 // mbarriers.  Per row, thread (lane L = j', g = its warpgroup within the pair):
-//   pass A: its half (a_hi bit 7 = g) in two 64-column chunks, bits 0-5 in registers;
+//   pass A: quarters g and g + 2 (64 columns each), bits 0-5 in registers;
 //   [named barrier, the 2 warps sharing the lanes]
 //   pass B: bits 6 and 7 over the 4-tuples (c, c + 64, c + 128, c + 192), c in [32 g, 32 g + 32),
 //           + amax; parked in TMEM;
 //   [named barrier, the 8 warps: the row's amax]
-//   quant:  its half, 32 columns at a time; the half is released to the MMA after its last load.
+//   quant:  exactly pass B's columns, 32 at a time (so the thread's pass-B amax tells the warp
+//           whether the clamp can be skipped); each loaded chunk releases one quarter (8 arrivals).
 // The MMA runs per 64-column quarter (N = 64), one MMA warp per buffer, so a quarter of the next
-// row is multiplied as soon as its warpgroup's quant loaded it and pass A of the next row starts
-// on it while the rest of the quant runs.  Bit 0 (within a register pair) uses one FFMA2
-// with scalar-broadcast operands (pair_bfly), so all 8 stages cost 0.5 instructions / element.
+// row is multiplied as soon as all 8 warps' quant loaded it; the MMA warp also reloads the stage
+// its row freed (TMA of row it + 3).  The producer warps have the highest warp ids (the
+// schedulers prefer them).  Bit 0 (within a register pair) uses one FFMA2 (pair_bfly), so all 8
+// stages cost 0.5 instructions / element.
 // kPerm: codes in the transform-native K order (quarot.h QUAROT_HAD_KPERM): position
 //   p = (a_hi >> 5) * 3584 + j' * 32 + (a_hi & 31) — 32 consecutive a_hi of a lane are 16
 //   contiguous bytes (one 16-byte store; a warp writes 512 contiguous bytes); otherwise the
