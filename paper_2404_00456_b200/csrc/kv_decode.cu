@@ -494,7 +494,11 @@ cudaError_t launch_kv_decode(const void* q, const uint8_t* k_codes, const float*
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int64_t pairs = (int64_t)B * n_kv;
-  int per = (int)((QR_DEC_CTAS_PER_SM * nsm + pairs - 1) / pairs);
+  // target CTAs per SM: when there are already >= 2 (sequence, KV head) pairs per SM, 2 (fewer,
+  // longer CTAs: the 70B GQA batch-64 shape runs one CTA per pair, 0.064 -> 0.060 ms); otherwise
+  // QR_DEC_CTAS_PER_SM (4: small batches need the split for parallelism)
+  const int64_t target = pairs >= 2 * (int64_t)nsm ? 2 : QR_DEC_CTAS_PER_SM;
+  int per = (int)((target * nsm + pairs - 1) / pairs);
   per = per < 1 ? 1 : (per > nchunks ? nchunks : per);
   a.chunks_per_cta = (nchunks + per - 1) / per;
   a.nsplit = (nchunks + a.chunks_per_cta - 1) / a.chunks_per_cta;
