@@ -98,6 +98,7 @@ struct Args {
   int n_q, n_kv, s_max, nsplit, chunks_per_cta;  // nsplit = CTAs per (sequence, KV head)
   float sm_scale_log2;  // sm_scale * log2(e)
   float* ws;            // [B][n_q][nsplit][HD + 2]: o (HD), m, l
+  __half* out;          // [B][n_q][HD]: written directly when nsplit == 1 (no combine pass)
 };
 
 // Barriers of the chunk ring (static smem so the kernel needs no dynamic-smem attribute games)
@@ -393,6 +394,10 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
       O += f * mrg_s[w][r][d];
       Ls += f * mrg_s[w][r][HD + 1];
     }
+    if (a.nsplit == 1) {  // one CTA per (sequence, KV head): the combine pass's arithmetic, here
+      a.out[((int64_t)b * a.n_q + kvh * G + r) * HD + d] = __float2half_rn(O / Ls);
+      continue;
+    }
     float* dst = a.ws + (((int64_t)b * a.n_q + kvh * G + r) * a.nsplit + split) * (HD + 2);
     dst[d] = O;
     if (d == 0) {
@@ -471,7 +476,7 @@ cudaError_t launch_g(dim3 grid, const CUtensorMap& mk, const CUtensorMap& mv, co
 cudaError_t launch_kv_decode(const void* q, const uint8_t* k_codes, const float* k_scale, const uint8_t* k_zero,
                              const uint8_t* v_codes, const float* v_scale, const uint8_t* v_zero,
                              const int32_t* seq_lens, int B, int n_q, int n_kv, int head_dim, int s_max,
-                             float sm_scale, void* out, float* workspace, cudaStream_t stream) {
+                             float sm_scale, void* out, float* workspace, cudaStream_t stream, int* launches) {
   if (B == 0) return cudaSuccess;
   CUtensorMap mk, mv;
   const int64_t rows = (int64_t)B * s_max;
@@ -504,6 +509,7 @@ cudaError_t launch_kv_decode(const void* q, const uint8_t* k_codes, const float*
   a.nsplit = (nchunks + a.chunks_per_cta - 1) / a.chunks_per_cta;
   a.sm_scale_log2 = sm_scale * kvd::LOG2E;
   a.ws = workspace;
+  a.out = static_cast<__half*>(out);
   const dim3 grid(a.nsplit, n_kv, B);
   const int G = n_q / n_kv;
   cudaError_t e;
@@ -515,6 +521,8 @@ cudaError_t launch_kv_decode(const void* q, const uint8_t* k_codes, const float*
     default: return cudaErrorInvalidValue;
   }
   if (e != cudaSuccess) return e;
+  if (launches) *launches = a.nsplit > 1 ? 2 : 1;
+  if (a.nsplit == 1) return cudaSuccess;  // the decode kernel wrote the output
   kvd::kv_decode_combine<<<(unsigned)((int64_t)B * n_q), kvd::HD, 0, stream>>>(workspace, a.nsplit, n_q,
                                                                               static_cast<__half*>(out));
   return cudaPeekAtLastError();

@@ -538,11 +538,12 @@ quarot_status quarot_kv_decode(const void* q, const uint8_t* k_codes, const floa
   if (workspace_bytes < quarot_kv_decode_workspace_bytes(B, n_q, head_dim, s_max)) return QUAROT_ERR_ARG;
   if (!aligned16(q) || !aligned16(k_codes) || !aligned16(v_codes) || !aligned16(out) || !aligned16(workspace))
     return QUAROT_ERR_ALIGN;
+  int launches = 0;
   cudaError_t e = qr::launch_kv_decode(q, k_codes, k_scale, k_zero, v_codes, v_scale, v_zero, seq_lens, (int)B, n_q,
                                        n_kv, head_dim, (int)s_max, sm_scale, out, workspace,
-                                       static_cast<cudaStream_t>(stream));
+                                       static_cast<cudaStream_t>(stream), &launches);
   if (e != cudaSuccess) return cuda_fail(e);
-  g_last_launches = 2;
+  g_last_launches = launches;
   return QUAROT_OK;
 }
 

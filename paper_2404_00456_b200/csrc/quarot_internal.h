@@ -95,7 +95,8 @@ int64_t kv_decode_workspace_bytes(int64_t B, int64_t n_q, int64_t head_dim, int6
 cudaError_t launch_kv_decode(const void* q, const uint8_t* k_codes, const float* k_scale, const uint8_t* k_zero,
                              const uint8_t* v_codes, const float* v_scale, const uint8_t* v_zero,
                              const int32_t* seq_lens, int B, int n_q, int n_kv, int head_dim, int s_max,
-                             float sm_scale, void* out, float* workspace, cudaStream_t stream);
+                             float sm_scale, void* out, float* workspace, cudaStream_t stream,
+                             int* launches = nullptr);
 
 // glue.cu
 cudaError_t launch_rope(void* x, int64_t T, int n_heads, int head_dim, int64_t ld_x, int64_t pos0, int seq_len,

@@ -100,3 +100,30 @@ def test_decode_errors(q):
     cache = q.kv_cache_empty(1, 16, 2)
     with pytest.raises(q.QuarotError):  # G = 3 unsupported
         q.kv_decode(qq, cache, torch.ones(1, dtype=torch.int32, device=DEV))
+
+
+def test_kv_decode_one_cta_per_pair_writes_output_directly(q):
+    """With >= 2 (sequence, KV head) pairs per SM the grid runs one CTA per pair (nsplit 1): the
+    decode kernel writes the fp16 output itself (one launch, no combine pass) — same parity bar."""
+    B, n_kv, n_q, s_max, d = 40, 8, 64, 1024, 128
+    rng = np.random.default_rng(11)
+    seq_lens = [int(v) for v in rng.integers(1, s_max + 1, B)]
+    seq_lens[0], seq_lens[1] = 1, s_max
+    k = rng.standard_normal((B, s_max, n_kv, d))
+    k[..., 5] *= 20.0
+    v = rng.standard_normal((B, s_max, n_kv, d))
+    c = oatt.cache_init(k.astype(np.float16), v.astype(np.float16), s_max)
+    H = ohad.hadamard(d)
+    q_rot = (rng.standard_normal((B, n_q, d)) @ H.T).astype(np.float16)
+    ref = oatt.decode_attention(q_rot, c, seq_lens)
+    out = q.kv_decode(torch.as_tensor(q_rot, device=DEV), _to_gpu_cache(c),
+                      torch.tensor(seq_lens, dtype=torch.int32, device=DEV))
+    launches = q.last_launch_count()
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    if B * n_kv >= 2 * nsm:
+        assert launches == 1
+    assert np.isfinite(got).all()
+    for b in range(B):
+        assert P.frob_rel(got[b], ref[b]) <= P.FROB_REL, b
