@@ -32,8 +32,13 @@ constexpr int STAGES = 6;
 constexpr int STAGE_BYTES = 2 * 64 * MAXH * 2;  // two 64-d boxes of n_h rows x 128 B
 constexpr int B_BYTES = MAXH * 128;         // H_{n_h}: n_h rows x (n_h fp16 <= 128 B), SW128 K-major
 constexpr int NG = 4, NUM_EPI = 4 * NG;
-constexpr int TMA_WARP = 0, MMA_WARP = 1, EPI_WARP0 = 4;
-constexpr int NUM_THREADS = (EPI_WARP0 + NUM_EPI) * 32;  // 640
+// producer warps at the highest ids (the schedulers prefer them), as in the FULL kernels
+#ifndef QR_HH_PROD_HIGH
+#define QR_HH_PROD_HIGH 1
+#endif
+constexpr int EPI_WARP0 = QR_HH_PROD_HIGH ? 0 : 4, CTL_WARP0 = QR_HH_PROD_HIGH ? NUM_EPI : 0;
+constexpr int TMA_WARP = CTL_WARP0, MMA_WARP = CTL_WARP0 + 1;
+constexpr int NUM_THREADS = (4 + NUM_EPI) * 32;  // 640
 constexpr uint32_t TMEM_COLS = 512;
 constexpr size_t SMEM = 1024 + B_BYTES + (size_t)STAGES * STAGE_BYTES + 512;
 static_assert(SMEM <= 232448, "227 KB dynamic smem");
@@ -135,7 +140,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const uint32_t tmem_base = *tmem_holder;
   const int64_t nrows = M > (int64_t)blockIdx.x ? (M - 1 - (int64_t)blockIdx.x) / gridDim.x + 1 : 0;
 
-  if (warp < EPI_WARP0) {
+  if (warp >= CTL_WARP0 && warp < CTL_WARP0 + 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 32;");  // 128 x 32 + 512 x 112 = 640 x 96
     if (warp == TMA_WARP) {
       if (lane == 0) {
