@@ -22,8 +22,13 @@ namespace qr {
 namespace hqs {
 
 constexpr int NA = 64;  // a_hi columns
-constexpr int TMA_WARP = 0, MMA_WARP = 1, EPI_WARP0 = 4, NUM_EPI = 16;
-constexpr int NUM_THREADS = (EPI_WARP0 + NUM_EPI) * 32;  // 640
+// producer warps at the highest ids (the schedulers prefer them), as in the other FULL kernels
+#ifndef QR_SMALL_PROD_HIGH
+#define QR_SMALL_PROD_HIGH 1
+#endif
+constexpr int NUM_EPI = 16, EPI_WARP0 = QR_SMALL_PROD_HIGH ? 0 : 4, CTL_WARP0 = QR_SMALL_PROD_HIGH ? 16 : 0;
+constexpr int TMA_WARP = CTL_WARP0, MMA_WARP = CTL_WARP0 + 1;
+constexpr int NUM_THREADS = (4 + NUM_EPI) * 32;  // 640
 constexpr uint32_t TMEM_COLS = 512;
 
 template <int MB, int LLO>
@@ -123,7 +128,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const uint32_t tmem_base = *tmem_holder;
   const int64_t nrows = M > (int64_t)blockIdx.x ? (M - 1 - (int64_t)blockIdx.x) / gridDim.x + 1 : 0;
 
-  if (warp < EPI_WARP0) {
+  if (warp >= CTL_WARP0 && warp < CTL_WARP0 + 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");  // 128 x 56 + 512 x 104 <= 640 x 96
     if (warp == TMA_WARP) {
       if (lane == 0) {
